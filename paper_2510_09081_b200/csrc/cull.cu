@@ -1,0 +1,189 @@
+// cull.cu -- voxel camera-visibility culling.  Replaces lv/culling.py:112-127 (erode),
+// 143-200 (_march_blocked, _visibility_kernel), 130-140 (dilate_bits), 103-109 (or_mips).
+//
+// Only `eroded >= THETA_BLOCK (0.999)` is ever consumed (lv/culling.py:186), and level-0
+// occupancy is min(occ_q,4096)/4096, so erode+threshold collapses to the integer predicate
+// "occ_q >= 4092 for the voxel and its 6 neighbours" (4092/4096 = 0.99902 >= 0.999 > 4091/4096).
+// It is stored as a 1-bit mask (res^3/8 bytes: 2 MiB at 256^3, L1/L2 resident for the march).
+#include "lvx_device.cuh"
+
+namespace lvx {
+
+#define LVX_SOLID_Q 4092u
+
+__device__ __forceinline__ bool q_solid(const uint32_t *__restrict__ base, int res, int x, int y, int z) {
+    if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) return false;   // outside counts as 0
+    return (base[x + (int64_t)res * (y + (int64_t)res * z)] & 0xFFFFu) >= LVX_SOLID_Q;
+}
+
+__global__ void __launch_bounds__(256)
+k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restrict__ solid,
+        uint64_t *__restrict__ stats) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool s = false, occ = false;
+    if (idx < V) {
+        const uint32_t w = base[idx];
+        occ = (w >> 16) != 0;
+        if ((w & 0xFFFFu) >= LVX_SOLID_Q) {
+            const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
+            s = q_solid(base, res, x - 1, y, z) && q_solid(base, res, x + 1, y, z) &&
+                q_solid(base, res, x, y - 1, z) && q_solid(base, res, x, y + 1, z) &&
+                q_solid(base, res, x, y, z - 1) && q_solid(base, res, x, y, z + 1);
+        }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, s);
+    const uint32_t mo = __ballot_sync(0xffffffffu, occ);
+    if ((threadIdx.x & 31) == 0 && idx < V) {
+        solid[idx >> 5] = m;
+        if (m) atomicAdd((unsigned long long *)&stats[LVX_ST_SOLID], (unsigned long long)__popc(m));
+        if (mo) atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)__popc(mo));
+    }
+}
+
+// lv/culling.py:143-188, literally: Amanatides-Woo from the voxel centre to the camera point.
+__device__ __forceinline__ bool march_blocked(const uint32_t *__restrict__ solid, int res, int x, int y, int z,
+                                              double cx, double cy, double cz) {
+    const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
+    const double dx = cx - ox, dy = cy - oy, dz = cz - oz;
+    const int ex = (int)floor(cx), ey = (int)floor(cy), ez = (int)floor(cz);
+    const int sx = dx > 0 ? 1 : -1, sy = dy > 0 ? 1 : -1, sz = dz > 0 ? 1 : -1;
+    const double big = 1e30;
+    double tmx = dx != 0.0 ? ((double)(x + (sx > 0 ? 1 : 0)) - ox) / dx : big;
+    double tmy = dy != 0.0 ? ((double)(y + (sy > 0 ? 1 : 0)) - oy) / dy : big;
+    double tmz = dz != 0.0 ? ((double)(z + (sz > 0 ? 1 : 0)) - oz) / dz : big;
+    const double tdx = dx != 0.0 ? fabs(1.0 / dx) : big;
+    const double tdy = dy != 0.0 ? fabs(1.0 / dy) : big;
+    const double tdz = dz != 0.0 ? fabs(1.0 / dz) : big;
+    for (;;) {
+        double t;
+        if (tmx <= tmy && tmx <= tmz) { x += sx; t = tmx; tmx += tdx; }
+        else if (tmy <= tmz) { y += sy; t = tmy; tmy += tdy; }
+        else { z += sz; t = tmz; tmz += tdz; }
+        if (t >= 1.0) return false;                                               // reached the camera
+        if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) return false;  // left the grid
+        if (x == ex && y == ey && z == ez) return false;                          // camera's own voxel
+        const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
+        if ((solid[idx >> 5] >> (idx & 31)) & 1u) return true;
+    }
+}
+
+// lv/culling.py:191-200.  When the frame has no solid voxel at all nothing can block, so every
+// occupied voxel is visible and the march is skipped (decided on the device, no host sync).
+__global__ void __launch_bounds__(128)
+k_visibility(const uint32_t *__restrict__ base, const uint32_t *__restrict__ solid, int res, int64_t V,
+             double cx, double cy, double cz, const uint64_t *__restrict__ stats, uint8_t *__restrict__ vis) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= V) return;
+    uint8_t v = 0;
+    if ((base[idx] >> 16) != 0) {
+        if (stats[LVX_ST_SOLID] == 0) v = 1;
+        else {
+            const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
+            v = march_blocked(solid, res, x, y, z, cx, cy, cz) ? 0 : 1;
+        }
+    }
+    vis[idx] = v;
+}
+
+// lv/culling.py:130-140 dilate_bits, then `& occ_bits` (224)
+__global__ void __launch_bounds__(256)
+k_dilate(const uint32_t *__restrict__ base, const uint8_t *__restrict__ vis, int res, int64_t V,
+         uint8_t *__restrict__ out, uint64_t *__restrict__ stats) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool v = false;
+    if (idx < V && (base[idx] >> 16) != 0) {
+        v = vis[idx] != 0;
+        if (!v && stats[LVX_ST_SOLID] != 0) {
+            const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
+            for (int dz = -1; dz <= 1 && !v; dz++) {
+                const int Z = z + dz;
+                if (Z < 0 || Z >= res) continue;
+                for (int dy = -1; dy <= 1 && !v; dy++) {
+                    const int Y = y + dy;
+                    if (Y < 0 || Y >= res) continue;
+                    for (int dx = -1; dx <= 1; dx++) {
+                        const int X = x + dx;
+                        if (X < 0 || X >= res) continue;
+                        if (vis[X + (int64_t)res * (Y + (int64_t)res * Z)]) { v = true; break; }
+                    }
+                }
+            }
+        }
+    }
+    if (idx < V) out[idx] = v ? 1 : 0;
+    const uint32_t m = __ballot_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && m)
+        atomicAdd((unsigned long long *)&stats[LVX_ST_VISIBLE], (unsigned long long)__popc(m));
+}
+
+__global__ void __launch_bounds__(256)
+k_occupied(const uint32_t *__restrict__ base, int64_t V, uint8_t *__restrict__ out, uint64_t *__restrict__ stats) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool v = idx < V && (base[idx] >> 16) != 0;
+    if (idx < V) out[idx] = v ? 1 : 0;
+    const uint32_t m = __ballot_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && m) {
+        atomicAdd((unsigned long long *)&stats[LVX_ST_VISIBLE], (unsigned long long)__popc(m));
+        atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)__popc(m));
+    }
+}
+
+// lv/culling.py:103-109: parent = OR of its 8 children
+__global__ void __launch_bounds__(256)
+k_ormip(const uint8_t *__restrict__ src, int rsrc, uint8_t *__restrict__ out) {
+    const int rl = rsrc >> 1;
+    const int64_t n = (int64_t)rl * rl * rl;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int x = (int)(i % rl), y = (int)((i / rl) % rl), z = (int)(i / ((int64_t)rl * rl));
+    uint32_t m = 0;
+#pragma unroll
+    for (int dz = 0; dz < 2; dz++)
+#pragma unroll
+        for (int dy = 0; dy < 2; dy++) {
+            const uchar2 w = *reinterpret_cast<const uchar2 *>(
+                src + (2 * x + (int64_t)rsrc * ((2 * y + dy) + (int64_t)rsrc * (2 * z + dz))));
+            m |= w.x | w.y;
+        }
+    out[i] = m ? 1 : 0;
+}
+
+static int or_mips(uint8_t *flat, int res, cudaStream_t s) {
+    const LevelOffsets L = make_level_offsets(res);
+    for (int l = 1; l < L.n_levels; l++) {
+        const int rsrc = res >> (l - 1), rl = res >> l;
+        k_ormip<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(flat + L.off[l - 1], rsrc, flat + L.off[l]);
+    }
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+}  // namespace lvx
+
+using namespace lvx;
+
+extern "C" {
+
+int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32_t *solid_bits,
+             uint8_t *vis_tmp, uint8_t *cull_flat, uint64_t *stats, void *stream) {
+    if (!pow2(res)) return LVX_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t V = (int64_t)res * res * res;
+    k_solid<<<blocks_for(V, 256), 256, 0, s>>>(base, res, V, solid_bits, stats);
+    k_visibility<<<blocks_for(V, 128), 128, 0, s>>>(base, solid_bits, res, V, cam_voxel_host[0],
+                                                    cam_voxel_host[1], cam_voxel_host[2], stats, vis_tmp);
+    k_dilate<<<blocks_for(V, 256), 256, 0, s>>>(base, vis_tmp, res, V, cull_flat, stats);
+    LVX_LAUNCH_CHECK();
+    return or_mips(cull_flat, res, s);
+}
+
+int lvx_occupied_pyramid(const uint32_t *base, int res, uint8_t *cull_flat, uint64_t *stats, void *stream) {
+    if (!pow2(res)) return LVX_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t V = (int64_t)res * res * res;
+    k_occupied<<<blocks_for(V, 256), 256, 0, s>>>(base, V, cull_flat, stats);
+    LVX_LAUNCH_CHECK();
+    return or_mips(cull_flat, res, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,221 @@
+// lvx_device.cuh -- device-side building blocks shared by the sm_100a kernels.
+//
+// Everything that decides voxel membership runs in IEEE f64 and is compiled with
+// -fmad=false, in the reference's operation order, so integer outputs are
+// bit-identical to the numba reference.  Reference citations: lv/ = pkg/src/linevox/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdint.h>
+
+#include "../../include/lvx.h"
+
+namespace lvx {
+
+// ----------------------------------------------------------------------------- host helpers
+extern thread_local char g_err[256];
+int cuda_fail(cudaError_t e, const char *where);
+#define LVX_CUDA(call)                                         \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return lvx::cuda_fail(e_, #call); \
+    } while (0)
+#define LVX_LAUNCH_CHECK() LVX_CUDA(cudaGetLastError())
+
+static inline bool pow2(int r) { return r >= 2 && (r & (r - 1)) == 0; }
+static inline unsigned blocks_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+// ----------------------------------------------------------------------------- small math
+struct d3 { double x, y, z; };
+__device__ __forceinline__ double sel(const d3 &v, int a) { return a == 0 ? v.x : (a == 1 ? v.y : v.z); }
+__device__ __forceinline__ d3 ld3(const double *p) { return d3{p[0], p[1], p[2]}; }
+
+// lv/voxelizer.py:89-106 _rank3: major axis first, ties keep x before y before z
+__device__ __forceinline__ void rank3(double ax, double ay, double az, int &a0, int &a1, int &a2) {
+    int m = 0, r1, r2;
+    if (ay > ax && ay >= az) m = 1;
+    else if (az > ax && az > ay) m = 2;
+    if (m == 0) { r1 = 1; r2 = 2; }
+    else if (m == 1) { r1 = 0; r2 = 2; }
+    else { r1 = 0; r2 = 1; }
+    double vr2 = (r2 == 1) ? ay : az;
+    double vr1 = (r1 == 0) ? ax : ay;
+    a0 = m;
+    if (vr2 > vr1) { a1 = r2; a2 = r1; } else { a1 = r1; a2 = r2; }
+}
+
+// ----------------------------------------------------------------------------- traversal
+// Calls f(x, y, z) for every IN-GRID cell of the segment's traversal, each exactly once.
+// Nothing is materialised: slabs are enumerated arithmetically (the reference builds a heap
+// list per segment, lv/voxelizer.py:180-206).  Out-of-grid cells are skipped by clamping the
+// loop bounds, which is what the callers' `continue` does (lv/voxelizer.py:321-322).
+
+template <class F>
+__device__ __forceinline__ void cells_aabb(const d3 &v0, const d3 &v1, double r, int res, F &&f) {
+    // lv/voxelizer.py:116-140
+    int x0 = (int)floor(fmin(v0.x, v1.x) - r), x1 = (int)floor(fmax(v0.x, v1.x) + r);
+    int y0 = (int)floor(fmin(v0.y, v1.y) - r), y1 = (int)floor(fmax(v0.y, v1.y) + r);
+    int z0 = (int)floor(fmin(v0.z, v1.z) - r), z1 = (int)floor(fmax(v0.z, v1.z) + r);
+    x0 = max(x0, 0); y0 = max(y0, 0); z0 = max(z0, 0);
+    x1 = min(x1, res - 1); y1 = min(y1, res - 1); z1 = min(z1, res - 1);
+    for (int z = z0; z <= z1; z++)
+        for (int y = y0; y <= y1; y++)
+            for (int x = x0; x <= x1; x++) f(x, y, z);
+}
+
+template <class F>
+__device__ __forceinline__ void cells_capsule(const d3 &a, const d3 &b, double r, int res, F &&f) {
+    // lv/voxelizer.py:143-206 (Algorithm 1 of the paper)
+    d3 d{b.x - a.x, b.y - a.y, b.z - a.z};
+    if (d.x == 0.0 && d.y == 0.0 && d.z == 0.0) { cells_aabb(a, b, r, res, f); return; }
+    int a0, a1, a2;
+    rank3(fabs(d.x), fabs(d.y), fabs(d.z), a0, a1, a2);
+    double d0 = sel(d, a0), d1 = sel(d, a1), d2 = sel(d, a2);
+    // v0 = start in the +major direction
+    double v0_0 = sel(a, a0), v0_1 = sel(a, a1), v0_2 = sel(a, a2);
+    double v1_0 = sel(b, a0), v1_1 = sel(b, a1), v1_2 = sel(b, a2);
+    if (d0 < 0.0) {
+        double t;
+        t = v0_0; v0_0 = v1_0; v1_0 = t;
+        t = v0_1; v0_1 = v1_1; v1_1 = t;
+        t = v0_2; v0_2 = v1_2; v1_2 = t;
+        d0 = -d0; d1 = -d1; d2 = -d2;
+    }
+    const double s1 = d1 / d0, s2 = d2 / d0;      // s[a0] == 1 exactly
+    const double t_min = v0_0 - 1.0 * r;          // v0e[a0] = v0 - s*r with s = d0/d0 = 1
+    const double t_max = v1_0 + 1.0 * r;
+    const double e1 = v0_1 - s1 * r, e2 = v0_2 - s2 * r;  // v0e minor components
+    const double r1 = r * sqrt(1.0 + s1 * s1);
+    const double r2 = r * sqrt(1.0 + s2 * s2);
+    int lo_j = (int)floor(fmin(v0_1, v1_1) - r), hi_j = (int)floor(fmax(v0_1, v1_1) + r);
+    int lo_k = (int)floor(fmin(v0_2, v1_2) - r), hi_k = (int)floor(fmax(v0_2, v1_2) + r);
+    lo_j = max(lo_j, 0); lo_k = max(lo_k, 0);
+    hi_j = min(hi_j, res - 1); hi_k = min(hi_k, res - 1);
+    double t0 = t_min, p0_1 = e1, p0_2 = e2;
+    while (t0 < t_max) {
+        const double t1 = fmin(t_max, floor(t0 + 1.0));
+        const double dt = t1 - t_min;
+        const double p1_1 = e1 + s1 * dt, p1_2 = e2 + s2 * dt;
+        const int ci = (int)floor(t0);
+        if (ci >= 0 && ci < res) {
+            int j_min = max((int)floor(fmin(p0_1, p1_1) - r1), lo_j);
+            int j_max = min((int)floor(fmax(p0_1, p1_1) + r1), hi_j);
+            int k_min = max((int)floor(fmin(p0_2, p1_2) - r2), lo_k);
+            int k_max = min((int)floor(fmax(p0_2, p1_2) + r2), hi_k);
+            for (int j = j_min; j <= j_max; j++)
+                for (int k = k_min; k <= k_max; k++) {
+                    int x = a0 == 0 ? ci : (a1 == 0 ? j : k);
+                    int y = a0 == 1 ? ci : (a1 == 1 ? j : k);
+                    int z = a0 == 2 ? ci : (a1 == 2 ? j : k);
+                    f(x, y, z);
+                }
+        }
+        t0 = t1; p0_1 = p1_1; p0_2 = p1_2;
+    }
+}
+
+template <class F>
+__device__ __forceinline__ void cells_dda(const d3 &v0, const d3 &v1, int res, F &&f) {
+    // lv/voxelizer.py:209-251
+    int x = (int)floor(v0.x), y = (int)floor(v0.y), z = (int)floor(v0.z);
+    const int ex = (int)floor(v1.x), ey = (int)floor(v1.y), ez = (int)floor(v1.z);
+    const int steps = abs(ex - x) + abs(ey - y) + abs(ez - z);
+    auto emit = [&](int X, int Y, int Z) {
+        if (X >= 0 && Y >= 0 && Z >= 0 && X < res && Y < res && Z < res) f(X, Y, Z);
+    };
+    emit(x, y, z);
+    if (steps == 0) return;
+    const double dx = v1.x - v0.x, dy = v1.y - v0.y, dz = v1.z - v0.z;
+    const int sx = dx > 0 ? 1 : -1, sy = dy > 0 ? 1 : -1, sz = dz > 0 ? 1 : -1;
+    const double big = 1e30;
+    double tmx = dx != 0.0 ? ((double)(x + (sx > 0 ? 1 : 0)) - v0.x) / dx : big;
+    double tmy = dy != 0.0 ? ((double)(y + (sy > 0 ? 1 : 0)) - v0.y) / dy : big;
+    double tmz = dz != 0.0 ? ((double)(z + (sz > 0 ? 1 : 0)) - v0.z) / dz : big;
+    const double tdx = dx != 0.0 ? fabs(1.0 / dx) : big;
+    const double tdy = dy != 0.0 ? fabs(1.0 / dy) : big;
+    const double tdz = dz != 0.0 ? fabs(1.0 / dz) : big;
+    for (int i = 1; i <= steps; i++) {
+        if (tmx <= tmy && tmx <= tmz) { x += sx; tmx += tdx; }
+        else if (tmy <= tmz) { y += sy; tmy += tdy; }
+        else { z += sz; tmz += tdz; }
+        emit(x, y, z);
+    }
+}
+
+template <class F>
+__device__ __forceinline__ void for_each_cell(int method, const d3 &a, const d3 &b, double rt, int res, F &&f) {
+    if (method == 1) cells_capsule(a, b, rt, res, f);
+    else if (method == 0) cells_dda(a, b, res, f);
+    else cells_aabb(a, b, rt, res, f);
+}
+
+// ----------------------------------------------------------------------------- capsule
+struct Capsule {
+    d3 a, b, n0, n1;
+    double r;
+    bool clip;
+};
+
+// lv/voxelizer.py:254-283 _sdf
+__device__ __forceinline__ double capsule_sdf(double px, double py, double pz, const Capsule &c, double r) {
+    const double dx = c.b.x - c.a.x, dy = c.b.y - c.a.y, dz = c.b.z - c.a.z;
+    const double p0x = px - c.a.x, p0y = py - c.a.y, p0z = pz - c.a.z;
+    const double dd = dx * dx + dy * dy + dz * dz;
+    double h = 0.0;
+    if (dd > 0.0) {
+        h = (p0x * dx + p0y * dy + p0z * dz) / dd;
+        if (h < 0.0) h = 0.0; else if (h > 1.0) h = 1.0;
+    }
+    const double qx = p0x - dx * h, qy = p0y - dy * h, qz = p0z - dz * h;
+    double sdf = sqrt(qx * qx + qy * qy + qz * qz) - r;
+    if (c.clip) {
+        const double s0 = -(p0x * c.n0.x + p0y * c.n0.y + p0z * c.n0.z);
+        const double s1 = (px - c.b.x) * c.n1.x + (py - c.b.y) * c.n1.y + (pz - c.b.z) * c.n1.z;
+        if (s0 > sdf) sdf = s0;
+        if (s1 > sdf) sdf = s1;
+    }
+    return sdf;
+}
+
+// lv/voxelizer.py:286-298 _occupancy followed by q = int(round(occ * 4096)) (328)
+__device__ __forceinline__ uint32_t occupancy_q(double px, double py, double pz, const Capsule &c,
+                                                double rc, double corr) {
+    const double sdf = capsule_sdf(px, py, pz, c, rc);
+    double occ = 0.5 - sdf;
+    if (occ < 0.0) occ = 0.0; else if (occ > 1.0) occ = 1.0;
+    return (uint32_t)(int)rint(occ * corr * 4096.0);   // rint = round-half-even, like python round()
+}
+
+__device__ __forceinline__ Capsule load_capsule(const double *__restrict__ verts, const double *__restrict__ normals,
+                                                int64_t i, double r, bool clip) {
+    Capsule c;
+    c.a = ld3(verts + 3 * i);
+    c.b = ld3(verts + 3 * i + 3);
+    if (clip) { c.n0 = ld3(normals + 3 * i); c.n1 = ld3(normals + 3 * i + 3); }
+    else { c.n0 = d3{0, 0, 0}; c.n1 = d3{0, 0, 0}; }
+    c.r = r;
+    c.clip = clip;
+    return c;
+}
+
+// pyramid level offsets (elements), level 0 first
+struct LevelOffsets {
+    int64_t off[16];
+    int n_levels;
+};
+static inline LevelOffsets make_level_offsets(int res) {
+    LevelOffsets L;
+    int n = 0;
+    int64_t o = 0;
+    for (int r = res; r >= 1; r >>= 1) { L.off[n++] = o; o += (int64_t)r * r * r; }
+    L.off[n] = o;
+    L.n_levels = n;
+    return L;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace lvx

@@ -1,0 +1,177 @@
+// upload.cu -- line-set upload: voxel-unit vertices, segment ids, clip normals, AABB.
+// Replaces lv/voxelizer.py:435-447 (segment_arrays), lv/lineset.py:74-79, 81-82, 213-242.
+#include "lvx_device.cuh"
+
+namespace lvx {
+
+thread_local char g_err[256] = {0};
+int cuda_fail(cudaError_t e, const char *where) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return LVX_E_CUDA;
+}
+
+// polyline containing vertex i: largest p with off[p] <= i
+__device__ __forceinline__ int64_t find_polyline(const int64_t *__restrict__ off, int64_t n_poly, int64_t i) {
+    int64_t lo = 0, hi = n_poly;  // invariant off[lo] <= i < off[hi]
+    while (hi - lo > 1) {
+        int64_t mid = (lo + hi) >> 1;
+        if (off[mid] <= i) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ d3 wv(const float *__restrict__ v, int64_t i) {
+    return d3{(double)v[3 * i], (double)v[3 * i + 1], (double)v[3 * i + 2]};
+}
+__device__ __forceinline__ d3 sub(const d3 &a, const d3 &b) { return d3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double len3(const d3 &d) { return sqrt(d.x * d.x + d.y * d.y + d.z * d.z); }
+
+// One thread per vertex.  Uniform polylines (the common case: off[p] = p*L) skip the search.
+__global__ void __launch_bounds__(256)
+k_upload(const float *__restrict__ v32, const int64_t *__restrict__ off, int64_t n_verts, int64_t n_poly,
+         double wx, double wy, double wz, double vs, int64_t uniform_len,
+         double *__restrict__ verts, double *__restrict__ normals, int32_t *__restrict__ segs,
+         uint64_t *__restrict__ stats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_verts) return;
+    const d3 w = wv(v32, i);
+    // lv/voxelizer.py:438
+    verts[3 * i] = (w.x - wx) / vs;
+    verts[3 * i + 1] = (w.y - wy) / vs;
+    verts[3 * i + 2] = (w.z - wz) / vs;
+    const int64_t p = uniform_len > 0 ? i / uniform_len : find_polyline(off, n_poly, i);
+    const int64_t s = off[p], e = off[p + 1];
+    // lv/lineset.py:74-79: vertex i starts segment number i - p unless it ends its polyline
+    if (i != e - 1) segs[i - p] = (int32_t)i;
+    if (normals == nullptr) return;
+    // lv/lineset.py:222-242
+    d3 d;
+    if (i == s) d = sub(wv(v32, s + 1), w);
+    else if (i == e - 1) d = sub(w, wv(v32, e - 2));
+    else d = sub(wv(v32, i + 1), wv(v32, i - 1));
+    double len = len3(d);
+    if (len == 0.0) {
+        const int64_t m = e - s, li = i - s;
+        const int64_t k = li < m - 2 ? li : m - 2;
+        d = sub(wv(v32, s + k + 1), wv(v32, s + k));
+        len = len3(d);
+        if (len == 0.0) {
+            bool found = false;
+            for (int64_t j = 0; j < m - 1 && !found; j++) {
+                d = sub(wv(v32, s + j + 1), wv(v32, s + j));
+                len = len3(d);
+                found = len > 0.0;
+            }
+            if (!found) {
+                atomicMax((unsigned long long *)&stats[LVX_ST_DEGENERATE], (unsigned long long)(p + 1));
+                d = d3{0, 0, 0};
+                len = 1.0;
+            }
+        }
+    }
+    normals[3 * i] = d.x / len;
+    normals[3 * i + 1] = d.y / len;
+    normals[3 * i + 2] = d.z / len;
+}
+
+// order-preserving float <-> uint mapping so that min/max can use integer atomics
+__device__ __forceinline__ uint32_t f2o(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float o2f(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__global__ void k_aabb_init(uint32_t *acc) {
+    if (threadIdx.x < 3) acc[threadIdx.x] = 0xffffffffu;
+    else if (threadIdx.x < 6) acc[threadIdx.x] = 0u;
+}
+
+__global__ void __launch_bounds__(256)
+k_aabb(const float *__restrict__ v, int64_t n_verts, uint32_t *__restrict__ acc) {
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_verts;
+         i += (int64_t)gridDim.x * blockDim.x)
+        for (int a = 0; a < 3; a++) {
+            float f = v[3 * i + a];
+            mn[a] = fminf(mn[a], f);
+            mx[a] = fmaxf(mx[a], f);
+        }
+    for (int a = 0; a < 3; a++)
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
+            mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
+        }
+    if ((threadIdx.x & 31) == 0)
+        for (int a = 0; a < 3; a++) {
+            atomicMin(&acc[a], f2o(mn[a]));
+            atomicMax(&acc[3 + a], f2o(mx[a]));
+        }
+}
+
+__global__ void k_aabb_finish(uint32_t *acc) {
+    if (threadIdx.x < 6) ((float *)acc)[threadIdx.x] = o2f(acc[threadIdx.x]);
+}
+
+__global__ void k_stats_reset(uint64_t *stats) {
+    if (threadIdx.x < LVX_STATS_WORDS) stats[threadIdx.x] = 0;
+}
+
+}  // namespace lvx
+
+using namespace lvx;
+
+extern "C" {
+
+const char *lvx_last_cuda_error(void) { return g_err; }
+int lvx_version(void) { return 100; }
+
+int lvx_num_levels(int res) {
+    if (!pow2(res)) return LVX_E_ARG;
+    return make_level_offsets(res).n_levels;
+}
+int64_t lvx_pyramid_elems(int res) {
+    if (!pow2(res)) return LVX_E_ARG;
+    LevelOffsets L = make_level_offsets(res);
+    return L.off[L.n_levels];
+}
+
+int lvx_stats_reset(uint64_t *stats, void *stream) {
+    k_stats_reset<<<1, 32, 0, (cudaStream_t)stream>>>(stats);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_clear(void *ptr, int64_t bytes, void *stream) {
+    LVX_CUDA(cudaMemsetAsync(ptr, 0, (size_t)bytes, (cudaStream_t)stream));
+    return LVX_OK;
+}
+
+int lvx_upload(const float *verts_f32, const int64_t *poly_off, int64_t n_verts, int64_t n_poly,
+               const double *world_min_host, double voxel_size, double *verts, double *normals,
+               int32_t *segs, uint64_t *stats, void *stream) {
+    if (n_verts < 2 || n_poly < 1 || !(voxel_size > 0) || n_verts > 0x7fffffffLL) return LVX_E_ARG;
+    // uniform-length hint: valid only if n_verts divides evenly; the kernel still reads off[p], so
+    // a wrong hint cannot happen silently -- the host wrapper passes it only when verified.
+    int64_t uniform = 0;
+    k_upload<<<blocks_for(n_verts, 256), 256, 0, (cudaStream_t)stream>>>(
+        verts_f32, poly_off, n_verts, n_poly, world_min_host[0], world_min_host[1], world_min_host[2],
+        voxel_size, uniform, verts, normals, segs, stats);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_aabb(const float *verts_f32, int64_t n_verts, float *out6, void *stream) {
+    if (n_verts < 1) return LVX_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    k_aabb_init<<<1, 32, 0, s>>>((uint32_t *)out6);
+    unsigned nb = blocks_for(n_verts, 256);
+    if (nb > 148 * 8) nb = 148 * 8;
+    k_aabb<<<nb, 256, 0, s>>>(verts_f32, n_verts, (uint32_t *)out6);
+    k_aabb_finish<<<1, 32, 0, s>>>((uint32_t *)out6);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,227 @@
+// voxelize.cu -- conservative capsule voxelization into the packed (count<<16 | occ_q) grid,
+// and the occupancy pyramid.  Replaces lv/voxelizer.py:301-340 (_voxelize_kernel), the
+// saturating merge at 490-495 and build_mips at 422-432.
+//
+// Accumulation.  The reference result per voxel is
+//   (min(sum 1, 0xFFFF) << 16) | min(sum q, 0xFFFF).
+// Fast path: ONE 32-bit atomicAdd of (1<<16)+q per incidence.  The add returns the old word, so
+// the single thread whose add carries out of the low field sees it ((old&0xFFFF)+q > 0xFFFF),
+// takes the carry back out of the count field and flags the voxel in a 1-bit "occupancy
+// saturated" mask; lvx_finalize_base then writes 0xFFFF into flagged low fields.  A wrap of the
+// whole word (>= 65536 segments in one voxel) raises LVX_ST_NEED_WIDE and the caller re-runs
+// the exact 64-bit path (lvx_voxelize_wide + lvx_pack_wide).  The grid stays 4 B/voxel, so a
+// 256^3 grid (64 MiB) is L2-resident on B200 while the atomics run.
+#include "lvx_device.cuh"
+
+namespace lvx {
+
+template <bool WIDE>
+__global__ void __launch_bounds__(128)
+k_voxelize(const double *__restrict__ verts, const double *__restrict__ normals,
+           const int32_t *__restrict__ segs, int64_t seg_begin, int64_t seg_end, int use_clip,
+           double r, double rt, double r_min, int res, int method,
+           uint32_t *__restrict__ base, uint32_t *__restrict__ occ_sat,
+           unsigned long long *__restrict__ wide, uint64_t *__restrict__ stats) {
+    const int64_t si = seg_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t visited = 0;
+    if (si < seg_end) {
+        const int64_t i = segs[si];
+        const Capsule c = load_capsule(verts, normals, i, r, use_clip != 0);
+        const double rc = r > r_min ? r : r_min;     // lv/voxelizer.py:289-290
+        const double ratio = r / rc;
+        const double corr = ratio * ratio;
+        const int64_t res64 = res;
+        for_each_cell(method, c.a, c.b, rt, res, [&](int x, int y, int z) {
+            const uint32_t q = occupancy_q(x + 0.5, y + 0.5, z + 0.5, c, rc, corr);
+            const int64_t idx = x + res64 * (y + res64 * z);
+            visited++;
+            if (WIDE) {
+                atomicAdd(&wide[idx], (1ull << 32) | (unsigned long long)q);
+            } else {
+                const uint32_t inc = 0x10000u + q;
+                const uint32_t old = atomicAdd(&base[idx], inc);
+                if (old + inc < old) stats[LVX_ST_NEED_WIDE] = 1;   // count field wrapped
+                if ((old & 0xFFFFu) + q > 0xFFFFu) {
+                    atomicSub(&base[idx], 0x10000u);                  // undo the carry into count
+                    atomicOr(&occ_sat[idx >> 5], 1u << (idx & 31));
+                }
+            }
+        });
+    }
+    visited = warp_sum_u64(visited);
+    if ((threadIdx.x & 31) == 0 && visited)
+        atomicAdd((unsigned long long *)&stats[LVX_ST_VISITED], (unsigned long long)visited);
+}
+
+__global__ void __launch_bounds__(256)
+k_finalize_base(uint32_t *__restrict__ base, const uint32_t *__restrict__ occ_sat, int64_t n_words,
+                uint64_t *__restrict__ stats) {
+    // one thread per 32-voxel mask word; flagged voxels are rare
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= n_words) return;
+    uint32_t m = occ_sat[w];
+    if (!m) return;
+    atomicAdd((unsigned long long *)&stats[LVX_ST_OCC_SAT], (unsigned long long)__popc(m));
+    while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        base[w * 32 + b] |= 0xFFFFu;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_widen(const uint32_t *__restrict__ base, const uint32_t *__restrict__ occ_sat, int64_t n,
+        unsigned long long *__restrict__ wide) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t w = base[i];
+    uint32_t lo = w & 0xFFFFu;
+    if (occ_sat && ((occ_sat[i >> 5] >> (i & 31)) & 1u)) lo = 0xFFFFu;
+    wide[i] = ((unsigned long long)(w >> 16) << 32) | lo;
+}
+
+__global__ void __launch_bounds__(256)
+k_pack_wide(const unsigned long long *__restrict__ wide, int64_t n, uint32_t *__restrict__ base,
+            uint64_t *__restrict__ stats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t sat = 0;
+    if (i < n) {
+        const unsigned long long w = wide[i];
+        uint64_t c = w >> 32, o = w & 0xFFFFFFFFull;
+        if (c > 0xFFFF) { sat = c - 0xFFFF; c = 0xFFFF; }   // lv/voxelizer.py:333-336, 493
+        if (o > 0xFFFF) o = 0xFFFF;                          // lv/voxelizer.py:494
+        base[i] = (uint32_t)((c << 16) | o);
+    }
+    sat = warp_sum_u64(sat);
+    if ((threadIdx.x & 31) == 0 && sat)
+        atomicAdd((unsigned long long *)&stats[LVX_ST_SATURATED], (unsigned long long)sat);
+}
+
+// ----------------------------------------------------------------------------- mips
+// Level sums are exact dyadic rationals (multiples of 2^-(12+3l) below 2^53 ulps), so any
+// summation order gives the reference's bits.
+
+__device__ __forceinline__ double occ0(uint32_t w) {
+    const uint32_t q = min(w & 0xFFFFu, 4096u);      // lv/voxelizer.py:496
+    return (double)q * (1.0 / 4096.0);
+}
+
+// level 1 from the packed base: one thread per parent, 8-byte loads of x-adjacent children
+__global__ void __launch_bounds__(256)
+k_mip1(const uint32_t *__restrict__ base, int res, double *__restrict__ out) {
+    const int rl = res >> 1;
+    const int64_t n = (int64_t)rl * rl * rl;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int x = (int)(i % rl), y = (int)((i / rl) % rl), z = (int)(i / ((int64_t)rl * rl));
+    uint32_t s = 0;
+#pragma unroll
+    for (int dz = 0; dz < 2; dz++)
+#pragma unroll
+        for (int dy = 0; dy < 2; dy++) {
+            const uint2 w = *reinterpret_cast<const uint2 *>(
+                base + (2 * x + (int64_t)res * ((2 * y + dy) + (int64_t)res * (2 * z + dz))));
+            s += min(w.x & 0xFFFFu, 4096u) + min(w.y & 0xFFFFu, 4096u);
+        }
+    out[i] = (double)s * (1.0 / 32768.0);   // (sum / 4096) / 8, exact
+}
+
+__global__ void __launch_bounds__(256)
+k_mip_next(const double *__restrict__ src, int rsrc, double *__restrict__ out) {
+    const int rl = rsrc >> 1;
+    const int64_t n = (int64_t)rl * rl * rl;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int x = (int)(i % rl), y = (int)((i / rl) % rl), z = (int)(i / ((int64_t)rl * rl));
+    double s = 0.0;
+#pragma unroll
+    for (int dz = 0; dz < 2; dz++)
+#pragma unroll
+        for (int dy = 0; dy < 2; dy++) {
+            const double2 w = *reinterpret_cast<const double2 *>(
+                src + (2 * x + (int64_t)rsrc * ((2 * y + dy) + (int64_t)rsrc * (2 * z + dz))));
+            s += w.x + w.y;
+        }
+    out[i] = s * 0.125;
+}
+
+}  // namespace lvx
+
+using namespace lvx;
+
+extern "C" {
+
+static int voxelize_common(bool wide_path, const double *verts, const double *normals, const int32_t *segs,
+                           int64_t seg_begin, int64_t seg_end, int use_clip, double r, double rt,
+                           double r_min, int res, int method, uint32_t *base, uint32_t *occ_sat,
+                           uint64_t *wide, uint64_t *stats, void *stream) {
+    if (!pow2(res) || res > 1024 || method < 0 || method > 2 || !(r_min > 0) || seg_end < seg_begin)
+        return LVX_E_ARG;
+    const int64_t n = seg_end - seg_begin;
+    if (n == 0) return LVX_OK;
+    const unsigned nb = blocks_for(n, 128);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (wide_path)
+        k_voxelize<true><<<nb, 128, 0, s>>>(verts, normals, segs, seg_begin, seg_end, use_clip, r, rt, r_min,
+                                            res, method, nullptr, nullptr, (unsigned long long *)wide, stats);
+    else
+        k_voxelize<false><<<nb, 128, 0, s>>>(verts, normals, segs, seg_begin, seg_end, use_clip, r, rt, r_min,
+                                             res, method, base, occ_sat, nullptr, stats);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_voxelize(const double *verts, const double *normals, const int32_t *segs, int64_t seg_begin,
+                 int64_t seg_end, int use_clip, double r, double rt, double r_min, int res, int method,
+                 uint32_t *base, uint32_t *occ_sat, uint64_t *stats, void *stream) {
+    return voxelize_common(false, verts, normals, segs, seg_begin, seg_end, use_clip, r, rt, r_min, res,
+                           method, base, occ_sat, nullptr, stats, stream);
+}
+
+int lvx_voxelize_wide(const double *verts, const double *normals, const int32_t *segs, int64_t seg_begin,
+                      int64_t seg_end, int use_clip, double r, double rt, double r_min, int res, int method,
+                      uint64_t *wide, uint64_t *stats, void *stream) {
+    return voxelize_common(true, verts, normals, segs, seg_begin, seg_end, use_clip, r, rt, r_min, res,
+                           method, nullptr, nullptr, wide, stats, stream);
+}
+
+int lvx_widen(const uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, uint64_t *wide, void *stream) {
+    k_widen<<<blocks_for(n_voxels, 256), 256, 0, (cudaStream_t)stream>>>(base, occ_sat, n_voxels,
+                                                                        (unsigned long long *)wide);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_pack_wide(const uint64_t *wide, int64_t n_voxels, uint32_t *base, uint64_t *stats, void *stream) {
+    k_pack_wide<<<blocks_for(n_voxels, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const unsigned long long *)wide, n_voxels, base, stats);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_finalize_base(uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, uint64_t *stats, void *stream) {
+    const int64_t n_words = (n_voxels + 31) / 32;
+    k_finalize_base<<<blocks_for(n_words, 256), 256, 0, (cudaStream_t)stream>>>(base, occ_sat, n_words, stats);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_build_mips(const uint32_t *base, int res, double *mips, void *stream) {
+    if (!pow2(res)) return LVX_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const LevelOffsets L = make_level_offsets(res);
+    const int64_t V = L.off[1];
+    {
+        const int rl = res >> 1;
+        k_mip1<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(base, res, mips);
+    }
+    for (int l = 2; l < L.n_levels; l++) {
+        const int rsrc = res >> (l - 1), rl = res >> l;
+        k_mip_next<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(mips + (L.off[l - 1] - V), rsrc,
+                                                                        mips + (L.off[l] - V));
+    }
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,237 @@
+"""FrameEngine: the device-resident, sync-free executor of one frame
+(upload -> voxelize -> mips -> cull -> scan -> scatter/order -> shade -> trace).
+
+It is what `ScenePipeline` and `bench.py` run.  All buffers are allocated once and reused;
+every stage is enqueued on the current CUDA stream with a CUDA event between stages; the only
+host synchronisation is the read-back of the 128-byte stats block (and of the image, when the
+caller asks for it) at the end of the frame.  The fragment buffer is sized from the previous
+frame's total with head-room; if a frame overflows it (or trips the 16-bit count fallback) the
+affected stages are re-run -- exactness is never traded for the fast path.
+
+Stage order and semantics follow lv/pipeline.py:68-136.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from . import ops
+from .abuffer import ABufferError
+from .grid import GridDesc, fit_grid
+from .raytracer import RenderSettings, make_params
+from .shading import AO_HALF_ANGLE, SHADOW_HALF_ANGLE, cone_directions
+
+STAGES = ("upload", "voxelize", "mips", "cull", "scan", "scatter", "shade", "trace")
+
+
+class FrameResult:
+    def __init__(self, engine):
+        self._e = engine
+        self.stats = {}
+        self.stage_ms = {}
+
+    @property
+    def srgb_dev(self):
+        return self._e.srgb
+
+    @property
+    def hit_id_dev(self):
+        return self._e.hit_id
+
+    @property
+    def rgb_dev(self):
+        return self._e.rgb
+
+
+class FrameEngine:
+    def __init__(self, res: int, width: int, height: int, strategy="vcsv", mode="opaque", alpha=1.0, k=8,
+                 method="capsule", r_min=0.5, light=(-0.5, -0.3, -0.8), clip=True, keep_rgb=False,
+                 early_termination=True, background=(0.1, 0.1, 0.12), device=None, frag_capacity=0):
+        torch = N.require_cuda()
+        if strategy not in ("vsv", "vcsv"):
+            raise ValueError("strategy must be vsv or vcsv")
+        if method not in ops.METHODS:
+            raise ValueError(f"unknown voxelization method {method!r}")
+        self.torch = torch
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.res, self.w, self.h = int(res), int(width), int(height)
+        self.strategy, self.method, self.r_min, self.clip = strategy, method, float(r_min), bool(clip)
+        self.settings = RenderSettings(mode=mode, alpha=alpha, k=k, background=tuple(background),
+                                       early_termination=early_termination)
+        l = np.asarray(light, dtype=np.float64)
+        self.light = l / np.linalg.norm(l)
+        self.light = self.light / np.linalg.norm(self.light)      # lv/shading.py:175 normalises again
+        self.dirs = cone_directions()
+        V = self.V = self.res ** 3
+        d, t = self.dev, torch
+        n_pyr = int(ops.level_offsets(self.res)[-1])
+        self.stats = ops.new_stats(d)
+        self.base = t.empty(V, dtype=t.int32, device=d)
+        self.occ_sat = t.empty(max(V // 32, 1), dtype=t.int32, device=d)
+        self.mips = t.empty(max(n_pyr - V, 1), dtype=t.float64, device=d)
+        self.solid = t.empty(max(V // 32, 1), dtype=t.int32, device=d)
+        self.vis_tmp = t.empty(V, dtype=t.uint8, device=d)
+        self.cull_flat = t.empty(n_pyr, dtype=t.uint8, device=d)
+        self.offsets = t.empty(V + 1, dtype=t.int32, device=d)
+        self.cursor = t.empty(V, dtype=t.int32, device=d)
+        self.scan_scratch = t.empty(ops.scan_scratch_bytes(V), dtype=t.uint8, device=d)
+        self.shade_scratch = t.empty(ops.shade_scratch_bytes(V), dtype=t.uint8, device=d)
+        self.ao = t.empty(V, dtype=t.float32, device=d)
+        self.shadow = t.empty(V, dtype=t.float32, device=d)
+        self.rgb = t.empty((self.h, self.w, 3), dtype=t.float64, device=d) if keep_rgb else None
+        self.srgb = t.empty((self.h, self.w, 3), dtype=t.uint8, device=d)
+        self.hit_id = t.empty((self.h, self.w), dtype=t.int32, device=d)
+        self.frags = t.empty(max(int(frag_capacity), 1), dtype=t.int32, device=d)
+        self.wide = None
+        self.use_wide = False
+        self.lines = None
+        self.grid = None
+        self._verts32 = self._poly_off = None
+        self._ev = [t.cuda.Event(enable_timing=True) for _ in range(len(STAGES) + 1)]
+        self.launches_per_frame = 0
+
+    # ------------------------------------------------------------------ line set
+    def set_topology(self, polyline_offsets: np.ndarray, n_vertices: int):
+        """Polyline structure is fixed across an animation; only vertex positions stream in."""
+        t = self.torch
+        self._poly_off = t.from_numpy(np.ascontiguousarray(polyline_offsets, dtype=np.int64)).to(self.dev)
+        self._verts32 = t.empty((int(n_vertices), 3), dtype=t.float32, device=self.dev)
+        self._verts64 = t.empty((int(n_vertices), 3), dtype=t.float64, device=self.dev)
+        self._normals = t.empty((int(n_vertices), 3), dtype=t.float64, device=self.dev) if self.clip else None
+        self._segs = t.empty(int(n_vertices) - (len(polyline_offsets) - 1), dtype=t.int32, device=self.dev)
+
+    def load_vertices(self, verts):
+        """verts: (N,3) f32 -- pinned host tensor / numpy (H2D on the current stream) or cuda tensor."""
+        t = self.torch
+        if not t.is_tensor(verts):
+            verts = t.from_numpy(np.ascontiguousarray(verts, dtype=np.float32))
+        self._verts32.copy_(verts, non_blocking=True)
+
+    def fit(self, radius_voxels=None, radius_world=None):
+        """fit_grid with the AABB reduced on the GPU (one 24-byte read-back)."""
+        lo, hi = ops.aabb(self._verts32)
+
+        class _L:
+            radius = radius_world if radius_world is not None else 1.0
+        return fit_grid(_L, self.res, radius_voxels=radius_voxels, aabb=(lo, hi))
+
+    # ------------------------------------------------------------------ stages
+    def _stage_upload(self, grid: GridDesc, r_world: float):
+        import ctypes as C
+        wm = np.ascontiguousarray(grid.world_min, dtype=np.float64)
+        N.check(N.lib().lvx_upload(ops._ptr(self._verts32), ops._ptr(self._poly_off),
+                                   int(self._verts32.shape[0]), int(self._poly_off.shape[0]) - 1,
+                                   wm.ctypes.data_as(C.c_void_p), float(grid.voxel_size),
+                                   ops._ptr(self._verts64), ops._ptr(self._normals), ops._ptr(self._segs),
+                                   ops._ptr(self.stats), ops._stream()), "lvx_upload")
+        self.lines = ops.DeviceLines(self._verts32, self._poly_off, self._verts64, self._normals, self._segs,
+                                     int(self._verts32.shape[0]), int(self._poly_off.shape[0]) - 1,
+                                     float(r_world) / float(grid.voxel_size), grid, float(r_world))
+        self.grid = grid
+
+    def _stage_voxelize(self, seg_range=None):
+        b, e = (0, self.lines.n_segments) if seg_range is None else seg_range
+        if self.use_wide:
+            if self.wide is None:
+                self.wide = self.torch.empty(self.V, dtype=self.torch.int64, device=self.dev)
+            ops.clear(self.wide)
+            ops.voxelize_wide(self.lines, self.res, self.r_min, self.method, self.wide, self.stats, b, e)
+            ops.pack_wide(self.wide, self.base, self.stats)
+        else:
+            ops.clear(self.base)
+            ops.clear(self.occ_sat)
+            ops.voxelize(self.lines, self.res, self.r_min, self.method, self.base, self.occ_sat, self.stats, b, e)
+            ops.finalize_base(self.base, self.occ_sat, self.stats)
+
+    def _stage_mips(self):
+        ops.build_mips(self.base, self.res, self.mips)
+
+    def _stage_cull(self, cam):
+        if self.strategy == "vcsv":
+            ops.cull(self.base, self.res, self.grid.to_voxel(cam.position), self.solid, self.vis_tmp,
+                     self.cull_flat, self.stats)
+        else:
+            ops.occupied_pyramid(self.base, self.res, self.cull_flat, self.stats)
+
+    def _stage_scan(self):
+        cull_base = self.cull_flat[:self.V] if self.strategy == "vcsv" else None
+        ops.scan(self.base, cull_base, self.offsets, self.scan_scratch, self.stats)
+
+    def _stage_scatter(self):
+        rt = ops.footprint_radius(self.lines.r, self.r_min)
+        ops.scatter(self.lines, rt, self.res, self.method,
+                    self.cull_flat if self.strategy == "vcsv" else None,
+                    self.offsets, self.cursor, self.frags, self.stats)
+
+    def _stage_shade(self):
+        ops.shade(self.base, self.mips, self.res, self.cull_flat[:self.V], self.dirs, np.tan(AO_HALF_ANGLE),
+                  self.light, np.tan(SHADOW_HALF_ANGLE), self.ao, self.shadow, self.shade_scratch)
+
+    def _stage_trace(self, cam, tile=None):
+        p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
+        ops.render(self.lines, self.offsets, self.frags, self.cull_flat, self.res, self.ao, self.shadow,
+                   ops.make_camera_struct(cam, self.grid), p, self.rgb, self.srgb, self.hit_id, self.stats)
+
+    # ------------------------------------------------------------------ frame
+    def _ensure_capacity(self, need: int):
+        if need > self.frags.numel():
+            cap = int(need * 1.25) + 1024
+            if cap >= 2 ** 32:
+                cap = need
+            self.frags = self.torch.empty(cap, dtype=self.torch.int32, device=self.dev)
+
+    def run(self, cam, grid: GridDesc, r_world: float, tile=None, seg_range=None, after_voxelize=None):
+        """One frame on the already loaded vertices.  `after_voxelize(engine)` is the hook where the
+        multi-GPU path all-reduces the occupancy grid (distributed.py).  Returns FrameResult."""
+        if cam.width != self.w or cam.height != self.h:
+            raise ValueError("camera size does not match the engine's image size")
+        ev = self._ev
+        first = self.frags.numel() <= 1
+        for attempt in range(4):
+            ops.stats_reset(self.stats)
+            ev[0].record()
+            self._stage_upload(grid, r_world); ev[1].record()
+            self._stage_voxelize(seg_range)
+            if after_voxelize is not None:
+                after_voxelize(self)
+            ev[2].record()
+            self._stage_mips(); ev[3].record()
+            self._stage_cull(cam); ev[4].record()
+            self._stage_scan(); ev[5].record()
+            if first:     # size the fragment buffer once; later frames reuse it with head-room
+                self._ensure_capacity(int(self.stats[N.ST_FRAG_TOTAL].item()))
+                first = False
+            self._stage_scatter(); ev[6].record()
+            self._stage_shade(); ev[7].record()
+            self._stage_trace(cam, tile); ev[8].record()
+            st = self.stats.cpu().numpy()          # the frame's only mandatory sync
+            if st[N.ST_NEED_WIDE] and not self.use_wide:
+                self.use_wide = True               # a 16-bit count wrapped: exact 64-bit path from now on
+                continue
+            total = int(st[N.ST_FRAG_TOTAL])
+            if total >= 2 ** 32:
+                raise ABufferError(f"fragment total {total} exceeds the 32-bit offset range")
+            if total > self.frags.numel():
+                self._ensure_capacity(total)
+                continue
+            break
+        else:
+            raise RuntimeError("frame did not converge")
+        if st[N.ST_DEGENERATE]:
+            from .lineset import LineSetError
+            raise LineSetError(f"degenerate polyline {int(st[N.ST_DEGENERATE]) - 1}: all vertices coincide")
+        if st[N.ST_MISMATCH] and st[N.ST_SATURATED] == 0:
+            raise ABufferError("fragment count mismatch between passes (nondeterministic traversal?)")
+        out = FrameResult(self)
+        out.stage_ms = {s: ev[i].elapsed_time(ev[i + 1]) for i, s in enumerate(STAGES)}
+        occ = int(st[N.ST_OCCUPIED])
+        out.stats = {
+            "segments": self.lines.n_segments, "vertices": self.lines.n_vertices, "resolution": self.res,
+            "voxels_visited": int(st[N.ST_VISITED]), "saturated": int(st[N.ST_SATURATED]),
+            "fragments": total, "fragment_touches": 2 * total, "solid_voxels": int(st[N.ST_SOLID]),
+            "occupied_voxels": occ, "visible_voxels": int(st[N.ST_VISIBLE]),
+            "culled_fraction": (1.0 - int(st[N.ST_VISIBLE]) / occ) if (self.strategy == "vcsv" and occ) else 0.0,
+            "ray_capsule_tests": int(st[N.ST_RAY_TESTS]), "long_lists": int(st[N.ST_LONG_LISTS]),
+            "occ_saturated_voxels": int(st[N.ST_OCC_SAT]), "wide_path": bool(self.use_wide),
+        }
+        return out

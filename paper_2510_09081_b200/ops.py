@@ -1,0 +1,204 @@
+"""Thin, allocation-explicit Python layer over the C ABI (``include/lvx.h``).
+
+Every function takes torch CUDA tensors (device memory is PyTorch's job), enqueues one C-ABI
+call on the current CUDA stream and returns without synchronising.  The reference-shaped API
+(`voxelizer.py`, `culling.py`, ...) and the per-frame executor (`frame.py`) are built on these.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from ._native import check, lib
+
+METHODS = {"dda": 0, "capsule": 1, "aabb": 2}          # lv/voxelizer.py:47
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dbl3(v):
+    a = np.ascontiguousarray(v, dtype=np.float64)
+    assert a.shape == (3,)
+    return a, a.ctypes.data_as(C.c_void_p)
+
+
+def num_levels(res: int) -> int:
+    return int(res).bit_length()
+
+
+def level_offsets(res: int) -> np.ndarray:
+    sizes = [(res >> l) ** 3 for l in range(num_levels(res))]
+    return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+
+def new_stats(device):
+    import torch
+    return torch.zeros(N.STATS_WORDS, dtype=torch.int64, device=device)
+
+
+def stats_reset(stats):
+    check(lib().lvx_stats_reset(_ptr(stats), _stream()), "lvx_stats_reset")
+
+
+@dataclass
+class DeviceLines:
+    """A line set resident in HBM in the layout the kernels consume
+    (lv/voxelizer.py:435-447 segment_arrays)."""
+    verts32: "object"     # (Nv,3) f32 world
+    poly_off: "object"    # (P+1,) i64
+    verts: "object"       # (Nv,3) f64 voxel units
+    normals: "object"     # (Nv,3) f64 unit tangents, or None
+    segs: "object"        # (N,) i32 ascending start-vertex ids
+    n_vertices: int
+    n_polylines: int
+    r: float              # capsule radius, voxel units
+    grid: "object"
+    r_world: float
+
+    @property
+    def n_segments(self) -> int:
+        return self.n_vertices - self.n_polylines
+
+    @property
+    def use_clip(self) -> bool:
+        return self.normals is not None
+
+
+def upload(verts32, poly_off, grid, r_world, stats, with_normals=True, normals=None) -> DeviceLines:
+    """lvx_upload.  verts32: cuda f32 (Nv,3); poly_off: cuda i64 (P+1,).  `normals`, when
+    given (cuda f64 (Nv,3)), is used instead of computing tangents on the device."""
+    import torch
+    nv, npoly = int(verts32.shape[0]), int(poly_off.shape[0]) - 1
+    dev = verts32.device
+    verts = torch.empty((nv, 3), dtype=torch.float64, device=dev)
+    segs = torch.empty(nv - npoly, dtype=torch.int32, device=dev)
+    out_n = None
+    if with_normals and normals is None:
+        out_n = torch.empty((nv, 3), dtype=torch.float64, device=dev)
+    wm, wm_p = _dbl3(grid.world_min)
+    check(lib().lvx_upload(_ptr(verts32), _ptr(poly_off), nv, npoly, wm_p, float(grid.voxel_size),
+                           _ptr(verts), _ptr(out_n), _ptr(segs), _ptr(stats), _stream()), "lvx_upload")
+    if normals is not None:
+        out_n = normals
+    return DeviceLines(verts32, poly_off, verts, out_n if with_normals else None, segs, nv, npoly,
+                       float(r_world) / float(grid.voxel_size), grid, float(r_world))
+
+
+def aabb(verts32):
+    """LineSet.aabb() on the device -> (lo, hi) float64 numpy (synchronises)."""
+    import torch
+    out = torch.empty(6, dtype=torch.float32, device=verts32.device)
+    check(lib().lvx_aabb(_ptr(verts32), int(verts32.shape[0]), _ptr(out), _stream()), "lvx_aabb")
+    h = out.cpu().numpy().astype(np.float64)
+    return h[:3], h[3:]
+
+
+def footprint_radius(r: float, r_min: float = 0.5) -> float:
+    """lv/voxelizer.py:450-458"""
+    return max(r, r_min) + 0.5
+
+
+def clear(t):
+    check(lib().lvx_clear(_ptr(t), t.numel() * t.element_size(), _stream()), "lvx_clear")
+
+
+def voxelize(lines: DeviceLines, res, r_min, method, base, occ_sat, stats, seg_begin=0, seg_end=None):
+    """lvx_voxelize into zeroed `base` (V i32) / `occ_sat` (V/32 i32)."""
+    seg_end = lines.n_segments if seg_end is None else seg_end
+    r = lines.r
+    check(lib().lvx_voxelize(_ptr(lines.verts), _ptr(lines.normals), _ptr(lines.segs), seg_begin, seg_end,
+                             int(lines.use_clip), r, footprint_radius(r, r_min), float(r_min), res,
+                             METHODS[method], _ptr(base), _ptr(occ_sat), _ptr(stats), _stream()),
+          "lvx_voxelize")
+
+
+def voxelize_wide(lines: DeviceLines, res, r_min, method, wide, stats, seg_begin=0, seg_end=None):
+    seg_end = lines.n_segments if seg_end is None else seg_end
+    r = lines.r
+    check(lib().lvx_voxelize_wide(_ptr(lines.verts), _ptr(lines.normals), _ptr(lines.segs), seg_begin,
+                                  seg_end, int(lines.use_clip), r, footprint_radius(r, r_min), float(r_min),
+                                  res, METHODS[method], _ptr(wide), _ptr(stats), _stream()),
+          "lvx_voxelize_wide")
+
+
+def widen(base, occ_sat, wide):
+    check(lib().lvx_widen(_ptr(base), _ptr(occ_sat), base.numel(), _ptr(wide), _stream()), "lvx_widen")
+
+
+def pack_wide(wide, base, stats):
+    check(lib().lvx_pack_wide(_ptr(wide), wide.numel(), _ptr(base), _ptr(stats), _stream()), "lvx_pack_wide")
+
+
+def finalize_base(base, occ_sat, stats):
+    check(lib().lvx_finalize_base(_ptr(base), _ptr(occ_sat), base.numel(), _ptr(stats), _stream()),
+          "lvx_finalize_base")
+
+
+def build_mips(base, res, mips):
+    check(lib().lvx_build_mips(_ptr(base), res, _ptr(mips), _stream()), "lvx_build_mips")
+
+
+def cull(base, res, cam_voxel, solid_bits, vis_tmp, cull_flat, stats):
+    cv, cv_p = _dbl3(cam_voxel)
+    check(lib().lvx_cull(_ptr(base), res, cv_p, _ptr(solid_bits), _ptr(vis_tmp), _ptr(cull_flat),
+                         _ptr(stats), _stream()), "lvx_cull")
+
+
+def occupied_pyramid(base, res, cull_flat, stats):
+    check(lib().lvx_occupied_pyramid(_ptr(base), res, _ptr(cull_flat), _ptr(stats), _stream()),
+          "lvx_occupied_pyramid")
+
+
+def scan_scratch_bytes(n_voxels: int) -> int:
+    return int(lib().lvx_scan_scratch_bytes(n_voxels))
+
+
+def scan(base, cull_base, offsets, scratch, stats):
+    check(lib().lvx_scan(_ptr(base), _ptr(cull_base), base.numel(), _ptr(offsets), _ptr(scratch),
+                         _ptr(stats), _stream()), "lvx_scan")
+
+
+def scatter(lines: DeviceLines, rt, res, method, cull_flat, offsets, cursor, frags, stats):
+    check(lib().lvx_scatter(_ptr(lines.verts), _ptr(lines.segs), lines.n_segments, float(rt), res,
+                            METHODS[method], _ptr(cull_flat), _ptr(offsets), _ptr(cursor), None,
+                            _ptr(frags), frags.numel(), _ptr(stats), _stream()), "lvx_scatter")
+
+
+def shade_scratch_bytes(n_voxels: int) -> int:
+    return int(lib().lvx_shade_scratch_bytes(n_voxels))
+
+
+def shade(base, mips, res, visible, dirs, tan_ao, light, tan_shadow, ao, shadow, scratch):
+    d = np.ascontiguousarray(dirs, dtype=np.float64)
+    l, l_p = _dbl3(light)
+    check(lib().lvx_shade(_ptr(base), _ptr(mips), res, _ptr(visible), d.ctypes.data_as(C.c_void_p),
+                          int(d.shape[0]), float(tan_ao), l_p, float(tan_shadow), _ptr(ao), _ptr(shadow),
+                          _ptr(scratch), _stream()), "lvx_shade")
+
+
+def make_camera_struct(cam, grid) -> N.lvx_camera:
+    c = N.lvx_camera()
+    c.pos[:] = [float(x) for x in grid.to_voxel(cam.position)]       # lv/raytracer.py:690
+    c.fwd[:] = [float(x) for x in cam.forward]
+    c.right[:] = [float(x) for x in cam.right]
+    c.up[:] = [float(x) for x in cam.up]
+    c.tan_half_fov = float(np.tan(cam.fov / 2.0))                     # lv/raytracer.py:695
+    c.width, c.height = int(cam.width), int(cam.height)
+    return c
+
+
+def render(lines: DeviceLines, offsets, frags, bits_flat, res, ao, shadow, cam_struct, params, rgb, srgb,
+           hit_id, stats):
+    check(lib().lvx_render(_ptr(lines.verts), _ptr(lines.normals), _ptr(offsets), _ptr(frags), _ptr(bits_flat),
+                           res, _ptr(ao), _ptr(shadow), C.byref(cam_struct), C.byref(params), _ptr(rgb),
+                           _ptr(srgb), _ptr(hit_id), _ptr(stats), _stream()), "lvx_render")

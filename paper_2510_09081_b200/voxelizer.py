@@ -1,0 +1,172 @@
+"""GPU voxelization and the occupancy pyramid, with the reference's call surface
+(lv/voxelizer.py:435-498: ``segment_arrays``, ``footprint_radius``, ``voxelize``,
+``OccupancyPyramid``).  Arrays live in HBM; the numpy views the reference exposes
+(``base``, ``occ_levels``, ``counts()``...) are materialised on demand.
+"""
+from __future__ import annotations
+
+import struct
+from pathlib import Path
+
+import numpy as np
+
+from . import _native as N
+from . import ops
+from .grid import GridDesc
+from .lineset import LineSet
+
+__all__ = ["OccupancyPyramid", "voxelize", "segment_arrays", "footprint_radius", "upload_lineset",
+           "compute_clip_normals", "OCC_SCALE", "DEFAULT_R_MIN", "METHODS"]
+
+OCC_SCALE = 4096
+DEFAULT_R_MIN = 0.5
+METHODS = ops.METHODS
+footprint_radius = ops.footprint_radius
+
+
+def _device():
+    torch = N.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def upload_lineset(ls: LineSet, g: GridDesc, r_world=None, cn="device", stats=None) -> ops.DeviceLines:
+    """Host LineSet -> DeviceLines (cached on the LineSet per grid/radius/normal mode).
+
+    cn: "device" computes clip normals on the GPU (lv/lineset.py:213-242); None disables
+    clipping (lv/voxelizer.py:440-442); an (N,3) array (numpy or cuda tensor) is used as given.
+    """
+    torch = N.require_cuda()
+    dev = _device()
+    r_world = float(ls.radius if r_world is None else r_world)
+    mode = "device" if isinstance(cn, str) else ("none" if cn is None else id(cn))
+    key = (dev.index, g.resolution, g.voxel_size, tuple(float(x) for x in g.world_min), r_world, mode)
+    cache = ls.__dict__.setdefault("_lvx_device_cache", {})
+    if key in cache:
+        return cache[key]
+    v32 = torch.from_numpy(ls.vertices).to(dev, non_blocking=True)
+    off = torch.from_numpy(ls.polyline_offsets).to(dev, non_blocking=True)
+    normals = None
+    if not isinstance(cn, str) and cn is not None:
+        normals = cn if torch.is_tensor(cn) else torch.from_numpy(np.ascontiguousarray(cn, dtype=np.float64))
+        normals = normals.to(dev, dtype=torch.float64).contiguous()
+        if tuple(normals.shape) != (ls.n_vertices, 3):
+            raise ValueError("clip normals must have shape (n_vertices, 3)")
+    own_stats = stats is None
+    if own_stats:
+        stats = ops.new_stats(dev)
+    lines = ops.upload(v32, off, g, r_world, stats, with_normals=cn is not None, normals=normals)
+    if own_stats and isinstance(cn, str):
+        bad = int(stats[N.ST_DEGENERATE].item())
+        if bad:
+            from .lineset import LineSetError
+            raise LineSetError(f"degenerate polyline {bad - 1}: all vertices coincide")
+    cache.clear()          # one entry: a LineSet is re-gridded rarely and the arrays are big
+    cache[key] = lines
+    return lines
+
+
+def compute_clip_normals(ls: LineSet):
+    """Per-vertex unit tangents on the GPU -> cuda f64 (N,3) (lv/lineset.py:213-242).  The
+    result is grid independent; it can be passed as `cn` to every stage."""
+    g = GridDesc(2, np.zeros(3), 1.0)
+    return upload_lineset(ls, g, cn="device").normals
+
+
+def segment_arrays(ls: LineSet, cn, g: GridDesc, r_world=None):
+    """lv/voxelizer.py:435-447, device edition: (verts f64 cuda, segs i32 cuda, normals, use_clip, r)."""
+    d = upload_lineset(ls, g, r_world, cn)
+    return d.verts, d.segs, d.normals, d.use_clip, d.r
+
+
+class OccupancyPyramid:
+    """lv/voxelizer.py:391-419.  `base_dev` (V,) int32 bits of the packed u32 words and
+    `mips_dev` (levels >= 1, f64, flat) stay on the GPU."""
+
+    def __init__(self, base_dev, mips_dev, grid: GridDesc, r_min: float, saturated=0, visited=0):
+        self.base_dev, self.mips_dev, self.grid, self.r_min = base_dev, mips_dev, grid, r_min
+        self.saturated, self.visited = int(saturated), int(visited)
+        self._base = self._levels = None
+
+    @property
+    def resolution(self) -> int:
+        return self.grid.resolution
+
+    @property
+    def base(self) -> np.ndarray:
+        if self._base is None:
+            r = self.resolution
+            self._base = self.base_dev.cpu().numpy().view(np.uint32).reshape(r, r, r)
+        return self._base
+
+    @property
+    def occ_levels(self) -> list:
+        if self._levels is None:
+            r = self.resolution
+            lv = [np.minimum(self.base & np.uint32(0xFFFF), OCC_SCALE).astype(np.float64) / OCC_SCALE]
+            flat = self.mips_dev.cpu().numpy()
+            offs = ops.level_offsets(r) - r ** 3
+            for l in range(1, len(offs) - 1):
+                rl = r >> l
+                lv.append(flat[offs[l]:offs[l + 1]].reshape(rl, rl, rl))
+            self._levels = lv
+        return self._levels
+
+    def counts(self) -> np.ndarray:
+        return (self.base >> np.uint32(16)).astype(np.int64)
+
+    def occupancy(self) -> np.ndarray:
+        return (self.base & np.uint32(0xFFFF)).astype(np.float64) / OCC_SCALE
+
+    def total_occupancy(self) -> float:
+        return float(self.occupancy().sum())
+
+    def dump(self, path) -> None:
+        """VOXP dump, byte-compatible with lv/voxelizer.py:414-419."""
+        parts = [b"VOXP", struct.pack("<I", self.resolution), self.base.astype("<u4").tobytes()]
+        parts += [l.astype("<f4").tobytes() for l in self.occ_levels[1:]]
+        Path(path).write_bytes(b"".join(parts))
+
+
+def voxelize_device(lines: ops.DeviceLines, res, r_min, method, stats, seg_range=None):
+    """Enqueue clear + voxelize + finalize; returns (base, occ_sat).  No sync."""
+    torch = N.require_cuda()
+    V = res ** 3
+    dev = lines.verts.device
+    base = torch.empty(V, dtype=torch.int32, device=dev)
+    occ_sat = torch.empty(max(V // 32, 1), dtype=torch.int32, device=dev)
+    ops.clear(base)
+    ops.clear(occ_sat)
+    b, e = (0, lines.n_segments) if seg_range is None else seg_range
+    ops.voxelize(lines, res, r_min, method, base, occ_sat, stats, b, e)
+    return base, occ_sat
+
+
+def voxelize(ls: LineSet, cn, g: GridDesc, method: str = "capsule", r_min: float = DEFAULT_R_MIN,
+             workers=None, r_world=None) -> OccupancyPyramid:
+    """lv/voxelizer.py:466-498.  `workers` is accepted and ignored (results never depended on it).
+    `cn` may be None, an (N,3) array, a cuda tensor, or "device"."""
+    if method not in METHODS:
+        raise ValueError(f"unknown voxelization method {method!r}")
+    if not r_min > 0:
+        raise ValueError("r_min must be positive")
+    torch = N.require_cuda()
+    res = g.resolution
+    lines = upload_lineset(ls, g, r_world, cn)
+    stats = ops.new_stats(lines.verts.device)
+    base, occ_sat = voxelize_device(lines, res, r_min, method, stats)
+    st = stats.cpu().numpy()
+    if st[N.ST_NEED_WIDE]:
+        # a 16-bit count wrapped: redo with exact 64-bit accumulators (include/lvx.h)
+        stats.zero_()
+        wide = torch.zeros(res ** 3, dtype=torch.int64, device=base.device)
+        ops.voxelize_wide(lines, res, r_min, method, wide, stats)
+        ops.pack_wide(wide, base, stats)
+        del wide
+        st = stats.cpu().numpy()
+    else:
+        ops.finalize_base(base, occ_sat, stats)
+    mips = torch.empty(max(int(ops.level_offsets(res)[-1]) - res ** 3, 1), dtype=torch.float64,
+                       device=base.device)
+    ops.build_mips(base, res, mips)
+    return OccupancyPyramid(base, mips, g, r_min, saturated=int(st[N.ST_SATURATED]),
+                            visited=int(st[N.ST_VISITED]))

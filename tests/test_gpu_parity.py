@@ -1,0 +1,218 @@
+"""GPU parity tests (run on the B200 box): the CUDA path, called through the C ABI, against the
+CPU oracle on the same seeded inputs and against the committed golden fixtures.
+
+Bars (BASELINE.json north_star): bit-exact counts, culling masks, offsets, fragment lists;
+occupancy max-abs <= 1e-4 (in practice bit-exact); pixels <= 1/255 on >= 99.9 % of pixels.
+"""
+import numpy as np
+import pytest
+
+from helpers import SCENES, Scene, h
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lvx():
+    import paper_2510_09081_b200 as m
+    return m
+
+
+def gpu_frame(lvx, sc, method="capsule"):
+    cn = lvx.compute_clip_normals(sc.ls)
+    pyr = lvx.voxelize(sc.ls, cn, sc.g, method=method, r_min=sc.r_min, r_world=sc.r_world)
+    culling = None
+    if sc.strategy == "vcsv":
+        culling = lvx.compute_visibility(lvx.erode(pyr), sc.g, sc.cam)
+        abuf = lvx.build_vcsv(sc.ls, cn, sc.g, pyr, culling, method=method, r_world=sc.r_world)
+    else:
+        abuf = lvx.build_vsv(sc.ls, cn, sc.g, pyr, method=method, r_world=sc.r_world)
+    scene = lvx.RenderScene(sc.ls, cn, sc.g, pyr, abuf, None, culling=culling, r_world=sc.r_world)
+    scene.shading = lvx.compute_shading(pyr, scene.march_bits(), sc.g, sc.light)
+    img = lvx.render(scene, sc.cam, lvx.RenderSettings(mode=sc.mode, alpha=sc.alpha, k=sc.k))
+    return cn, pyr, culling, abuf, scene, img
+
+
+@pytest.fixture(scope="module", params=SCENES)
+def both(request, lvx, oracle):
+    sc = Scene(request.param)
+    ref = oracle.run_frame(sc.ls, sc.g, sc.r_world, sc.cam, sc.light, strategy=sc.strategy, mode=sc.mode,
+                           alpha=sc.alpha, k=sc.k, r_min=sc.r_min)
+    return sc, ref, gpu_frame(lvx, sc)
+
+
+def test_upload(both, lvx):
+    sc, ref, (cn, *_rest) = both
+    verts, segs, normals, use_clip, r = lvx.segment_arrays(sc.ls, cn, sc.g, sc.r_world)
+    assert h(verts.cpu().numpy()) == sc.hash["verts_voxel_f64"]
+    assert h(normals.cpu().numpy()) == sc.hash["normals_f64"]
+    assert h(segs.cpu().numpy().astype(np.int64)) == sc.hash["segs_i64"]
+    assert float(r).hex() == sc.meta["r_voxel"] and use_clip
+
+
+def test_base_bit_exact(both):
+    sc, ref, (_, pyr, *_r) = both
+    assert np.array_equal(pyr.base, ref.pyramid.base)
+    assert h(pyr.base) == sc.hash["base_u32"]
+    assert pyr.visited == sc.stats["visited"] and pyr.saturated == sc.stats["saturated"]
+    # stated tolerance on occupancy: max-abs <= 1e-4 (holds trivially when the words are equal)
+    assert np.abs(pyr.occupancy() - (ref.pyramid.base & 0xFFFF) / 4096.0).max() <= 1e-4
+
+
+def test_mips(both):
+    sc, ref, (_, pyr, *_r) = both
+    assert [h(l) for l in pyr.occ_levels] == sc.hash["occ_levels_f64"]
+
+
+def test_culling_masks(both):
+    sc, ref, (_, _p, culling, *_r) = both
+    if culling is None:
+        pytest.skip("vsv")
+    assert [h(l) for l in culling.levels] == sc.hash["cull_levels_u8"]
+    assert np.array_equal(np.packbits(culling.base.ravel(), bitorder="little"), sc.arr["cull_base_bits"])
+
+
+def test_abuffer_bit_exact(both):
+    sc, ref, (_, _p, _c, abuf, *_r) = both
+    assert abuf.total == sc.stats["fragments"]
+    assert np.array_equal(abuf.table.offsets, ref.abuf.table.offsets)
+    assert np.array_equal(abuf.table.counts, ref.abuf.table.counts)
+    assert np.array_equal(abuf.fragments, ref.abuf.fragments)
+    assert h(abuf.table.offsets) == sc.hash["offsets_i64"]
+    assert h(abuf.table.counts) == sc.hash["counts_i64"]
+    assert h(abuf.fragments) == sc.hash["fragments_u32"]
+
+
+def test_shading(both):
+    sc, ref, (*_a, scene, _img) = both
+    assert np.array_equal(scene.shading.ao, ref.shading.ao)
+    assert np.array_equal(scene.shading.shadow, ref.shading.shadow)
+    assert h(scene.shading.ao) == sc.hash["ao_f32"] and h(scene.shading.shadow) == sc.hash["shadow_f32"]
+
+
+def test_image(both):
+    sc, ref, (*_a, img) = both
+    assert img.stats["ray_capsule_tests"] == sc.stats["ray_capsule_tests"]
+    assert np.array_equal(img.hit_id, sc.arr["hit_id"])
+    srgb = np.frombuffer(img.srgb_bytes(), np.uint8).reshape(sc.arr["srgb"].shape)
+    d = np.abs(srgb.astype(int) - sc.arr["srgb"].astype(int))
+    assert (d <= 1).all(axis=2).mean() >= 0.999      # <= 1/255 per channel on >= 99.9 % of pixels
+    assert d.max() <= 1
+    assert np.abs(img.rgb - ref.image.rgb).max() <= 1e-12
+    assert h(img.rgb) == sc.hash["rgb_f64"]          # f64 path without FMA: bit-identical in practice
+
+
+@pytest.mark.parametrize("method", ["dda", "aabb"])
+def test_other_traversals(lvx, oracle, method):
+    sc = Scene("walk32_inside_cam")
+    cn = oracle.compute_clip_normals(sc.ls)
+    rp = oracle.voxelize(sc.ls, cn, sc.g, method=method, r_min=sc.r_min, r_world=sc.r_world)
+    ra = oracle.build_vsv(sc.ls, cn, sc.g, rp, method=method, r_world=sc.r_world)
+    gp = lvx.voxelize(sc.ls, cn, sc.g, method=method, r_min=sc.r_min, r_world=sc.r_world)
+    ga = lvx.build_vsv(sc.ls, cn, sc.g, gp, method=method, r_world=sc.r_world)
+    assert np.array_equal(gp.base, rp.base) and gp.visited == rp.visited
+    assert np.array_equal(ga.fragments, ra.fragments)
+    assert np.array_equal(ga.table.offsets, ra.table.offsets)
+
+
+def test_no_clip_normals(lvx, oracle):
+    sc = Scene("helix32_vsv")
+    rp = oracle.voxelize(sc.ls, None, sc.g, r_min=sc.r_min, r_world=sc.r_world)
+    gp = lvx.voxelize(sc.ls, None, sc.g, r_min=sc.r_min, r_world=sc.r_world)
+    assert np.array_equal(gp.base, rp.base)
+
+
+@pytest.mark.parametrize("seed,res,r", [(1, 16, 0.2), (2, 32, 0.7), (5, 64, 0.2), (7, 64, 1.1), (11, 128, 0.3)])
+def test_random_scenes_vs_oracle(lvx, oracle, seed, res, r):
+    ls = lvx.generate("random_streamlines", seed=seed, polylines=60, verts_per_line=40)
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=r)
+    cfg = lvx.PipelineConfig(res=res, width=96, height=80, strategy="vcsv", cam_azimuth=10.0 * seed)
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vcsv")
+    eng = lvx.FrameEngine(res, 96, 80, strategy="vcsv", keep_rgb=True)
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    eng.load_vertices(ls.vertices)
+    out = eng.run(cam, g, r_world)
+    assert np.array_equal(eng.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
+    assert np.array_equal(eng.cull_flat.cpu().numpy(), ref.culling.flat)
+    n = out.stats["fragments"]
+    assert n == ref.abuf.total
+    assert np.array_equal(eng.offsets.cpu().numpy().view(np.uint32)[:-1].astype(np.int64), ref.abuf.table.offsets)
+    assert np.array_equal(eng.frags[:n].cpu().numpy().view(np.uint32), ref.abuf.fragments)
+    assert np.array_equal(eng.ao.cpu().numpy().reshape(res, res, res), ref.shading.ao)
+    assert np.array_equal(eng.shadow.cpu().numpy().reshape(res, res, res), ref.shading.shadow)
+    assert np.array_equal(eng.hit_id.cpu().numpy(), ref.image.hit_id)
+    assert np.array_equal(eng.rgb.cpu().numpy(), ref.image.rgb)
+    assert out.stats["ray_capsule_tests"] == ref.image.stats["ray_capsule_tests"]
+    assert out.stats["voxels_visited"] == ref.pyramid.visited
+
+
+def test_transparent_engine_vs_oracle(lvx, oracle):
+    ls = lvx.generate("random_streamlines", seed=4, polylines=80, verts_per_line=30)
+    g, r_world = lvx.fit_grid(ls, 32, radius_voxels=0.5)
+    cfg = lvx.PipelineConfig(res=32, width=80, height=64, strategy="vsv", mode="transparent", alpha=0.25, k=3)
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vsv", mode="transparent",
+                           alpha=0.25, k=3)
+    eng = lvx.FrameEngine(32, 80, 64, strategy="vsv", mode="transparent", alpha=0.25, k=3, keep_rgb=True)
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    eng.load_vertices(ls.vertices)
+    out = eng.run(cam, g, r_world)
+    assert np.array_equal(eng.hit_id.cpu().numpy(), ref.image.hit_id)
+    assert np.array_equal(eng.rgb.cpu().numpy(), ref.image.rgb)
+    assert out.stats["ray_capsule_tests"] == ref.image.stats["ray_capsule_tests"]
+
+
+def test_count_overflow_takes_wide_path(lvx, oracle):
+    """> 65535 segments through one voxel: the 16-bit count saturates (lv/voxelizer.py:333-336)."""
+    n = 70000
+    rng = np.random.default_rng(0)
+    a = 3.5 + 0.2 * rng.uniform(-1, 1, size=(n, 3))
+    v = np.empty((2 * n, 3), np.float32)
+    v[0::2] = a
+    v[1::2] = a + 0.05
+    ls = lvx.LineSet(v, np.arange(n + 1, dtype=np.int64) * 2, 0.1)
+    g = lvx.GridDesc(8, np.zeros(3), 1.0)
+    rp = oracle.voxelize(ls, None, g, r_world=0.1)
+    gp = lvx.voxelize(ls, None, g, r_world=0.1)
+    assert rp.saturated > 0
+    assert np.array_equal(gp.base, rp.base)
+    assert gp.visited == rp.visited and gp.saturated == rp.saturated
+
+
+def test_empty_and_tiny_inputs(lvx, oracle):
+    # a single 2-vertex polyline, zero-length segment included
+    v = np.array([[1.5, 1.5, 1.5], [1.5, 1.5, 1.5], [2.5, 2.0, 1.0]], np.float32)
+    ls = lvx.LineSet(v, np.array([0, 3]), 0.3)
+    g = lvx.GridDesc(4, np.zeros(3), 1.0)
+    cn = oracle.compute_clip_normals(ls)
+    rp = oracle.voxelize(ls, cn, g)
+    gp = lvx.voxelize(ls, cn, g)
+    assert np.array_equal(gp.base, rp.base)
+    ra = oracle.build_vsv(ls, cn, g, rp)
+    ga = lvx.build_vsv(ls, cn, g, gp)
+    assert np.array_equal(ga.fragments, ra.fragments)
+    # geometry entirely outside the grid -> empty structures
+    g2 = lvx.GridDesc(4, np.array([100.0, 100.0, 100.0]), 1.0)
+    gp2 = lvx.voxelize(ls, cn, g2)
+    assert gp2.visited == 0 and not gp2.base.any()
+    ga2 = lvx.build_vsv(ls, cn, g2, gp2)
+    assert ga2.total == 0
+
+
+def test_long_lists_sorted(lvx, oracle):
+    """Lists longer than the per-lane insertion-sort limit go through the warp bitonic sort."""
+    n = 3000
+    rng = np.random.default_rng(1)
+    a = 2.0 + 4.0 * rng.uniform(0, 1, size=(n, 3))
+    v = np.empty((2 * n, 3), np.float32)
+    v[0::2] = a
+    v[1::2] = a + rng.normal(scale=0.6, size=(n, 3))
+    ls = lvx.LineSet(v, np.arange(n + 1, dtype=np.int64) * 2, 0.3)
+    g = lvx.GridDesc(8, np.zeros(3), 1.0)
+    rp = oracle.voxelize(ls, None, g)
+    ra = oracle.build_vsv(ls, None, g, rp)
+    gp = lvx.voxelize(ls, None, g)
+    ga = lvx.build_vsv(ls, None, g, gp)
+    assert ga.stats["long_lists"] > 0
+    assert np.array_equal(ga.fragments, ra.fragments)
