@@ -119,8 +119,9 @@ int lvx_build_mips(const uint32_t *base, int res, double *mips, void *stream);
 
 /* ---- culling: lv/culling.py:112-127 erode, 143-200 _march_blocked/_visibility_kernel,
  * 130-140 dilate_bits, 103-109 or_mips.  cull_flat (lvx_pyramid_elems(res) bytes) receives the
- * u8 visibility pyramid (CullingPyramid.packed()).  solid_bits: V/32 u32 scratch; vis_tmp: V
- * bytes scratch.  cam_voxel_host = GridDesc.to_voxel(cam.position). */
+ * u8 visibility pyramid (CullingPyramid.packed()).  solid_bits: lvx_cull_scratch_words(res) u32
+ * of scratch (per-voxel solid bits + coarse brick flags); vis_tmp: V bytes scratch.  cam_voxel_host = GridDesc.to_voxel(cam.position). */
+int64_t lvx_cull_scratch_words(int res);
 int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host,
              uint32_t *solid_bits, uint8_t *vis_tmp, uint8_t *cull_flat, uint64_t *stats, void *stream);
 /* march bits for the un-culled strategy: CullingPyramid.from_bits(counts > 0)

@@ -140,7 +140,6 @@ k_scatter(const double *__restrict__ verts, const int32_t *__restrict__ segs, in
 }
 
 // ----------------------------------------------------------------------------- ordering
-constexpr int SORT_SMALL = 24;
 
 // all-ascending bitonic network on f[0..n) executed by one warp; indices >= n act as +inf
 __device__ void warp_bitonic(uint32_t *f, uint32_t n, int lane) {
@@ -171,13 +170,37 @@ __device__ void warp_bitonic(uint32_t *f, uint32_t n, int lane) {
     }
 }
 
-// One lane per voxel for short lists (insertion sort; the scatter order is already nearly
-// ascending because low segment ids run in early blocks), whole warp per long list.
-__global__ void __launch_bounds__(256)
+// Ordering pass.  A warp owns 32 consecutive voxels and walks their lists one at a time:
+//   n <= 32 : one coalesced 128-byte load, a 15-step bitonic network in registers (warp
+//             shuffles), one coalesced store -- skipped entirely when the list is already
+//             ascending (a ballot), which is common because low segment ids are scattered first;
+//   n  > 32 : staged through shared memory (or sorted in place when it exceeds the stage) with
+//             the all-ascending bitonic network above.
+// HBM traffic is <= 8 B per fragment, every access coalesced.
+constexpr int ORDER_WARPS = 8;
+constexpr int ORDER_CAP = 1024;   // fragments staged per warp for long lists (4 KiB)
+
+__device__ __forceinline__ uint32_t warp_sort32(uint32_t v, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+            const bool up = ((lane & k) == 0);            // ascending block?
+            const bool lower = ((lane & j) == 0);
+            const uint32_t mn = min(v, o), mx = max(v, o);
+            v = (lower == up) ? mn : mx;
+        }
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(ORDER_WARPS * 32)
 k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ cursor, int64_t V,
         uint32_t *__restrict__ frags, int64_t cap, uint64_t *__restrict__ stats) {
+    __shared__ uint32_t stage[ORDER_WARPS][ORDER_CAP];
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t b = 0, n = 0;
     if (v < V) {
         b = offsets[v];
@@ -186,28 +209,31 @@ k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ curso
         if (cursor[v] != e) stats[LVX_ST_MISMATCH] = 1;   // lv/abuffer.py:310-311
         if ((int64_t)e > cap) n = 0;                      // never touch memory past the buffer
     }
-    if (n > 1 && n <= SORT_SMALL) {
-        uint32_t *f = frags + b;
-        for (uint32_t i = 1; i < n; i++) {
-            const uint32_t key = f[i];
-            uint32_t j = i;
-            while (j > 0) {
-                const uint32_t p = f[j - 1];
-                if (p <= key) break;
-                f[j] = p;
-                j--;
-            }
-            if (j != i) f[j] = key;
-        }
-    }
-    uint32_t longs = __ballot_sync(0xffffffffu, n > SORT_SMALL);
+    uint32_t work = __ballot_sync(0xffffffffu, n > 1);
+    const uint32_t longs = __ballot_sync(0xffffffffu, n > 32);
     if (longs && lane == 0)
         atomicAdd((unsigned long long *)&stats[LVX_ST_LONG_LISTS], (unsigned long long)__popc(longs));
-    while (longs) {
-        const int src = __ffs(longs) - 1;
-        longs &= longs - 1;
+    while (work) {
+        const int src = __ffs(work) - 1;
+        work &= work - 1;
         const uint32_t bb = __shfl_sync(0xffffffffu, b, src), nn = __shfl_sync(0xffffffffu, n, src);
-        warp_bitonic(frags + bb, nn, lane);
+        uint32_t *f = frags + bb;
+        if (nn <= 32) {
+            uint32_t val = lane < nn ? f[lane] : 0xffffffffu;
+            const uint32_t next = __shfl_down_sync(0xffffffffu, val, 1);
+            if (__ballot_sync(0xffffffffu, lane + 1 < nn && val > next) == 0) continue;   // already ascending
+            val = warp_sort32(val, lane);
+            if (lane < nn) f[lane] = val;
+        } else if (nn <= ORDER_CAP) {
+            uint32_t *buf = stage[warp];
+            for (uint32_t i = lane; i < nn; i += 32) buf[i] = f[i];
+            __syncwarp();
+            warp_bitonic(buf, nn, lane);
+            for (uint32_t i = lane; i < nn; i += 32) f[i] = buf[i];
+            __syncwarp();
+        } else {
+            warp_bitonic(f, nn, lane);
+        }
     }
 }
 
@@ -252,7 +278,7 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
     if (n_seg > 0)
         k_scatter<<<blocks_for(n_seg, 128), 128, 0, s>>>(verts, segs, n_seg, rt, res, method, cull_flat, cursor,
                                                         frags, frag_capacity);
-    k_order<<<blocks_for(V, 256), 256, 0, s>>>(offsets, cursor, V, frags, frag_capacity, stats);
+    k_order<<<blocks_for(V, ORDER_WARPS * 32), ORDER_WARPS * 32, 0, s>>>(offsets, cursor, V, frags, frag_capacity, stats);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -10,6 +10,13 @@
 namespace lvx {
 
 #define LVX_SOLID_Q 4092u
+#define LVX_BRICK 8        // coarse "may contain a blocker" bricks for the visibility march
+#define LVX_SUPER 32       // and a coarser level above them
+
+__host__ __device__ inline int64_t brick_words(int res, int B) {
+    const int64_t rb = (res + B - 1) / B;
+    return (rb * rb * rb + 31) / 32;
+}
 
 __device__ __forceinline__ bool q_solid(const uint32_t *__restrict__ base, int res, int x, int y, int z) {
     if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) return false;   // outside counts as 0
@@ -18,7 +25,7 @@ __device__ __forceinline__ bool q_solid(const uint32_t *__restrict__ base, int r
 
 __global__ void __launch_bounds__(256)
 k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restrict__ solid,
-        uint64_t *__restrict__ stats) {
+        uint32_t *__restrict__ bricks, uint64_t *__restrict__ stats) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool s = false, occ = false;
     if (idx < V) {
@@ -33,6 +40,26 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
     }
     const uint32_t m = __ballot_sync(0xffffffffu, s);
     const uint32_t mo = __ballot_sync(0xffffffffu, occ);
+    if (s) {
+        // flag every brick that overlaps this solid voxel dilated by one voxel, at both brick sizes
+        const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
+        uint32_t *bits = bricks;
+#pragma unroll
+        for (int lvl = 0; lvl < 2; lvl++) {
+            const int B = lvl == 0 ? LVX_BRICK : LVX_SUPER;
+            const int rb = (res + B - 1) / B;
+            const int bx0 = max(x - 1, 0) / B, bx1 = min(x + 1, res - 1) / B;
+            const int by0 = max(y - 1, 0) / B, by1 = min(y + 1, res - 1) / B;
+            const int bz0 = max(z - 1, 0) / B, bz1 = min(z + 1, res - 1) / B;
+            for (int bz = bz0; bz <= bz1; bz++)
+                for (int by = by0; by <= by1; by++)
+                    for (int bx = bx0; bx <= bx1; bx++) {
+                        const int bi = bx + rb * (by + rb * bz);
+                        atomicOr(&bits[bi >> 5], 1u << (bi & 31));
+                    }
+            bits += brick_words(res, B);
+        }
+    }
     if ((threadIdx.x & 31) == 0 && idx < V) {
         solid[idx >> 5] = m;
         if (m) atomicAdd((unsigned long long *)&stats[LVX_ST_SOLID], (unsigned long long)__popc(m));
@@ -67,10 +94,54 @@ __device__ __forceinline__ bool march_blocked(const uint32_t *__restrict__ solid
     }
 }
 
+// Conservative coarse walk: Amanatides-Woo over bricks of `brick` voxels along the segment
+// o -> c (clipped to the grid); true if a flagged brick is visited.  A brick is flagged when it
+// overlaps a solid voxel dilated by a whole voxel, so if the fine march would reach a solid voxel,
+// at least 2 voxels of the segment lie strictly inside a flagged region and the coarse walk
+// (whose rounding errors are ~1e-13) must visit a flagged brick.
+__device__ __forceinline__ bool coarse_may_hit(const uint32_t *__restrict__ bits, int rb, int brick,
+                                               double ox, double oy, double oz, double cx, double cy, double cz) {
+    const double inv = 1.0 / brick;
+    const double o[3] = {ox * inv, oy * inv, oz * inv};
+    const double d[3] = {(cx - ox) * inv, (cy - oy) * inv, (cz - oz) * inv};
+    double t0 = 0.0, t1 = 1.0;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        if (d[a] == 0.0) { if (o[a] < 0.0 || o[a] > (double)rb) return false; }
+        else {
+            double ta = (0.0 - o[a]) / d[a], tb = ((double)rb - o[a]) / d[a];
+            if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
+            t0 = fmax(t0, ta); t1 = fmin(t1, tb);
+        }
+    }
+    if (t0 > t1) return false;
+    int c[3], st[3];
+    double tm[3], td[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const double p = o[a] + d[a] * t0;
+        c[a] = min(max((int)floor(p), 0), rb - 1);
+        st[a] = d[a] > 0 ? 1 : -1;
+        tm[a] = d[a] != 0.0 ? ((double)(c[a] + (d[a] > 0 ? 1 : 0)) - o[a]) / d[a] : 1e30;
+        td[a] = d[a] != 0.0 ? fabs(1.0 / d[a]) : 1e30;
+    }
+    for (;;) {
+        const int bi = c[0] + rb * (c[1] + rb * c[2]);
+        if ((bits[bi >> 5] >> (bi & 31)) & 1u) return true;
+        double t;
+        if (tm[0] <= tm[1] && tm[0] <= tm[2]) { c[0] += st[0]; t = tm[0]; tm[0] += td[0]; }
+        else if (tm[1] <= tm[2]) { c[1] += st[1]; t = tm[1]; tm[1] += td[1]; }
+        else { c[2] += st[2]; t = tm[2]; tm[2] += td[2]; }
+        if (t > t1) return false;
+        if (c[0] < 0 || c[1] < 0 || c[2] < 0 || c[0] >= rb || c[1] >= rb || c[2] >= rb) return false;
+    }
+}
+
 // lv/culling.py:191-200.  When the frame has no solid voxel at all nothing can block, so every
 // occupied voxel is visible and the march is skipped (decided on the device, no host sync).
 __global__ void __launch_bounds__(128)
-k_visibility(const uint32_t *__restrict__ base, const uint32_t *__restrict__ solid, int res, int64_t V,
+k_visibility(const uint32_t *__restrict__ base, const uint32_t *__restrict__ solid,
+             const uint32_t *__restrict__ bricks, int res, int64_t V,
              double cx, double cy, double cz, const uint64_t *__restrict__ stats, uint8_t *__restrict__ vis) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= V) return;
@@ -79,7 +150,15 @@ k_visibility(const uint32_t *__restrict__ base, const uint32_t *__restrict__ sol
         if (stats[LVX_ST_SOLID] == 0) v = 1;
         else {
             const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
-            v = march_blocked(solid, res, x, y, z, cx, cy, cz) ? 0 : 1;
+            // Only a solid voxel can block.  Walk the segment centre->camera through the 32^3-voxel
+            // super-bricks, then the 8^3 bricks; only if both touch a flagged cell does the literal
+            // fine march (which decides) run.
+            const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
+            bool may_hit = coarse_may_hit(bricks + brick_words(res, LVX_BRICK), (res + LVX_SUPER - 1) / LVX_SUPER,
+                                          LVX_SUPER, ox, oy, oz, cx, cy, cz);
+            if (may_hit)
+                may_hit = coarse_may_hit(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz, cx, cy, cz);
+            v = (may_hit && march_blocked(solid, res, x, y, z, cx, cy, cz)) ? 0 : 1;
         }
     }
     vis[idx] = v;
@@ -164,13 +243,22 @@ using namespace lvx;
 
 extern "C" {
 
+int64_t lvx_cull_scratch_words(int res) {
+    if (!pow2(res)) return LVX_E_ARG;
+    const int64_t V = (int64_t)res * res * res;
+    return (V + 31) / 32 + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER);
+}
+
 int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32_t *solid_bits,
              uint8_t *vis_tmp, uint8_t *cull_flat, uint64_t *stats, void *stream) {
     if (!pow2(res)) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
-    k_solid<<<blocks_for(V, 256), 256, 0, s>>>(base, res, V, solid_bits, stats);
-    k_visibility<<<blocks_for(V, 128), 128, 0, s>>>(base, solid_bits, res, V, cam_voxel_host[0],
+    // solid_bits scratch layout: [V/32 words of per-voxel solid bits][8^3-brick flags][32^3-brick flags]
+    uint32_t *bricks = solid_bits + (V + 31) / 32;
+    LVX_CUDA(cudaMemsetAsync(bricks, 0, (size_t)(brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER)) * 4, s));
+    k_solid<<<blocks_for(V, 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, stats);
+    k_visibility<<<blocks_for(V, 128), 128, 0, s>>>(base, solid_bits, bricks, res, V, cam_voxel_host[0],
                                                     cam_voxel_host[1], cam_voxel_host[2], stats, vis_tmp);
     k_dilate<<<blocks_for(V, 256), 256, 0, s>>>(base, vis_tmp, res, V, cull_flat, stats);
     LVX_LAUNCH_CHECK();

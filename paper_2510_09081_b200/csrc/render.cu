@@ -29,6 +29,33 @@ __device__ __forceinline__ bool clip_ok(const Capsule &c, double px, double py, 
     return true;
 }
 
+// Conservative miss test: every surface _ray_capsule can return a point on (cylinder body, end
+// spheres, clip disks incl. their 1e-9 slacks) lies within r + ~1e-9/r of the segment's axis
+// LINE, so a ray whose line-to-line distance from the axis exceeds r + 1e-4 cannot hit and the
+// full f64 routine would return -1.  ~25 flops, no division or square root; it removes most of
+// the tests (lists hold every segment within the 1-voxel traversal footprint, the capsule
+// itself is much thinner).  Near-parallel and degenerate cases are never rejected here.
+__device__ __forceinline__ bool surely_misses(double ox, double oy, double oz, double dx, double dy, double dz,
+                                              const d3 &a, const d3 &b, double r) {
+    const double bax = b.x - a.x, bay = b.y - a.y, baz = b.z - a.z;
+    const double baba = bax * bax + bay * bay + baz * baz;
+    const double nx = dy * baz - dz * bay, ny = dz * bax - dx * baz, nz = dx * bay - dy * bax;
+    const double nn = nx * nx + ny * ny + nz * nz;
+    if (!(baba > 1e-12) || !(nn > 1e-6 * baba)) return false;
+    const double h = (ox - a.x) * nx + (oy - a.y) * ny + (oz - a.z) * nz;
+    const double R = r + 1e-4;
+    return h * h > R * R * nn;
+}
+
+__device__ __forceinline__ Capsule load_capsule_lazy(const double *__restrict__ normals, int64_t i, const d3 &a,
+                                                     const d3 &b, double r, bool clip) {
+    Capsule c;
+    c.a = a; c.b = b; c.r = r; c.clip = clip;
+    if (clip) { c.n0 = ld3(normals + 3 * i); c.n1 = ld3(normals + 3 * i + 3); }
+    else { c.n0 = d3{0, 0, 0}; c.n1 = d3{0, 0, 0}; }
+    return c;
+}
+
 // lv/raytracer.py:113-222: smallest t >= 0 on the clipped capsule surface, or -1
 __device__ double ray_capsule(double ox, double oy, double oz, double dx, double dy, double dz, const Capsule &c) {
     const double ax = c.a.x, ay = c.a.y, az = c.a.z, bx = c.b.x, by = c.b.y, bz = c.b.z, r = c.r;
@@ -254,9 +281,11 @@ k_render(const RenderArgs A) {
                         const uint32_t fo = A.offsets[idx], fe = A.offsets[idx + 1];
                         for (uint32_t s = fo; s < fe; s++) {
                             const int64_t i = A.frags[s];
-                            const Capsule c = load_capsule(A.verts, A.normals, i, r, clip);
-                            const double tt = ray_capsule(ox, oy, oz, dx, dy, dz, c);
                             n_tests++;
+                            const d3 va = ld3(A.verts + 3 * i), vb = ld3(A.verts + 3 * i + 3);
+                            if (surely_misses(ox, oy, oz, dx, dy, dz, va, vb, r)) continue;
+                            const Capsule c = load_capsule_lazy(A.normals, i, va, vb, r, clip);
+                            const double tt = ray_capsule(ox, oy, oz, dx, dy, dz, c);
                             if (tt < 0.0) continue;
                             const int hx = (int)floor(ox + dx * tt), hy = (int)floor(oy + dy * tt), hz = (int)floor(oz + dz * tt);
                             if (hx != x || hy != y || hz != z) continue;   // belongs to another voxel's list
@@ -312,9 +341,11 @@ k_render(const RenderArgs A) {
                         uint32_t accepted = 0;
                         for (uint32_t s = 0; s < fn; s++) {
                             const int64_t i = A.frags[fo + s];
-                            const Capsule c = load_capsule(A.verts, A.normals, i, r, clip);
-                            const double tt = ray_capsule(ox, oy, oz, dx, dy, dz, c);
                             n_tests++;
+                            const d3 va = ld3(A.verts + 3 * i), vb = ld3(A.verts + 3 * i + 3);
+                            if (surely_misses(ox, oy, oz, dx, dy, dz, va, vb, r)) continue;
+                            const Capsule c = load_capsule_lazy(A.normals, i, va, vb, r, clip);
+                            const double tt = ray_capsule(ox, oy, oz, dx, dy, dz, c);
                             if (tt < 0.0) continue;
                             const int hx = (int)floor(ox + dx * tt), hy = (int)floor(oy + dy * tt), hz = (int)floor(oz + dz * tt);
                             if (hx != x || hy != y || hz != z) continue;

@@ -2,9 +2,8 @@
 // pyramid.  Replaces lv/shading.py:72-109 (_trilinear), 112-132 (_cone_trace), 135-155
 // (_shading_kernel) and the clip/f32 store of compute_shading (170-185).
 //
-// Work layout: visible voxels are compacted first; then 16 lanes cooperate on one voxel --
-// lanes 0..n_dirs-1 march one AO cone each, lane n_dirs the shadow cone -- and the partial
-// results are folded on lane 0 in cone order so the f64 sum has the reference's rounding.
+// Work layout: visible voxels are compacted first, then one thread per visible voxel marches
+// the 12 AO cones and the shadow cone (see k_shade for why that is the coalesced mapping).
 #include "lvx_device.cuh"
 
 namespace lvx {
@@ -88,43 +87,32 @@ k_shade_prepare(const uint8_t *__restrict__ visible, int64_t V, float *__restric
     if (v) list[b + __popc(m & ((1u << lane) - 1u))] = (uint32_t)idx;
 }
 
+// One thread per visible voxel; a warp holds 32 consecutive entries of the compacted list, i.e.
+// (mostly) x-adjacent voxels.  All lanes march the SAME cone direction in lock step: t, step and
+// the mip level depend only on t, so the loop is convergent and the 8 trilinear taps of the 32
+// lanes fall on consecutive addresses (or the same address at coarse levels) -- a few L1
+// wavefronts per load instead of one per lane.  The 12 AO cones are folded in cone order in a
+// register (lv/shading.py:150-152), so the f64 sum has the reference's rounding.
 __global__ void __launch_bounds__(128)
 k_shade(const uint32_t *__restrict__ base, const double *__restrict__ mips, const ShadeParams P,
         const uint32_t *__restrict__ list, const unsigned long long *__restrict__ list_n,
         float *__restrict__ ao, float *__restrict__ shadow) {
     const int64_t n = (int64_t)*list_n;
-    const int sub = threadIdx.x & 15;                       // lane within the 16-lane group
-    const int64_t group = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
-    const int64_t n_groups = ((int64_t)gridDim.x * blockDim.x) >> 4;
-    const int64_t n_iter = (n + n_groups - 1) / n_groups;   // uniform trip count keeps shuffles converged
-    for (int64_t it = 0; it < n_iter; it++) {
-        const int64_t e = it * n_groups + group;
-        const bool live = e < n;
-        double val = 0.0;
-        int64_t idx = 0;
-        if (live) {
-            idx = list[e];
-            const int x = (int)(idx % P.res), y = (int)((idx / P.res) % P.res), z = (int)(idx / ((int64_t)P.res * P.res));
-            const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
-            if (sub < P.n_dirs)
-                val = cone_trace(base, mips, P, ox, oy, oz, P.dirs[sub][0], P.dirs[sub][1], P.dirs[sub][2], P.tan_ao);
-            else if (sub == P.n_dirs)
-                val = cone_trace(base, mips, P, ox, oy, oz, P.shadow_dir[0], P.shadow_dir[1], P.shadow_dir[2],
-                                 P.tan_shadow);
-        }
-        // fold on the group's lane 0, cone order 0..n_dirs-1 (lv/shading.py:150-152)
-        double acc = 0.0, sh = 0.0;
-        for (int c = 0; c <= P.n_dirs; c++) {
-            const double vc = __shfl_sync(0xffffffffu, val, (threadIdx.x & 16) + c);
-            if (c < P.n_dirs) acc += P.w * vc; else sh = vc;
-        }
-        if (live && sub == 0) {
-            double a = 1.0 - acc, s = 1.0 - sh;
-            a = a < 0.0 ? 0.0 : (a > 1.0 ? 1.0 : a);     // lv/shading.py:183-184
-            s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
-            ao[idx] = (float)a;                          // lv/shading.py:185
-            shadow[idx] = (float)s;
-        }
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+        const int64_t idx = list[e];
+        const int x = (int)(idx % P.res), y = (int)((idx / P.res) % P.res), z = (int)(idx / ((int64_t)P.res * P.res));
+        const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
+        double acc = 0.0;
+        for (int c = 0; c < P.n_dirs; c++)
+            acc += P.w * cone_trace(base, mips, P, ox, oy, oz, P.dirs[c][0], P.dirs[c][1], P.dirs[c][2], P.tan_ao);
+        const double sh = cone_trace(base, mips, P, ox, oy, oz, P.shadow_dir[0], P.shadow_dir[1], P.shadow_dir[2],
+                                     P.tan_shadow);
+        double a = 1.0 - acc, s = 1.0 - sh;
+        a = a < 0.0 ? 0.0 : (a > 1.0 ? 1.0 : a);     // lv/shading.py:183-184
+        s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
+        ao[idx] = (float)a;                          // lv/shading.py:185
+        shadow[idx] = (float)s;
     }
 }
 
@@ -154,9 +142,9 @@ int lvx_shade(const uint32_t *base, const double *mips, int res, const uint8_t *
     uint32_t *list = (uint32_t *)((char *)scratch + 64);
     LVX_CUDA(cudaMemsetAsync(list_n, 0, 8, s));
     k_shade_prepare<<<blocks_for(V, 256), 256, 0, s>>>(visible, V, ao, shadow, list, list_n);
-    // persistent grid: 148 SMs x 16 CTAs of 128 threads (8 voxel groups per CTA)
+    // persistent grid-stride launch: 148 SMs x 16 CTAs of 128 threads
     unsigned nb = 148 * 16;
-    const unsigned need = blocks_for(V * 16, 128);
+    const unsigned need = blocks_for(V, 128);
     if (nb > need) nb = need;
     k_shade<<<nb, 128, 0, s>>>(base, mips, P, list, list_n, ao, shadow);
     LVX_LAUNCH_CHECK();

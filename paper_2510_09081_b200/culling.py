@@ -126,7 +126,7 @@ def compute_visibility(eroded, g: GridDesc, cam: Camera, occupied=None) -> Culli
         base = (base & 0xFFFF) | (occ << 16)
     V = res ** 3
     stats = ops.new_stats(dev)
-    solid = torch.empty(max(V // 32, 1), dtype=torch.int32, device=dev)
+    solid = torch.empty(ops.cull_scratch_words(res), dtype=torch.int32, device=dev)
     vis = torch.empty(V, dtype=torch.uint8, device=dev)
     flat = torch.empty(int(ops.level_offsets(res)[-1]), dtype=torch.uint8, device=dev)
     ops.cull(base, res, g.to_voxel(cam.position), solid, vis, flat, stats)

@@ -69,7 +69,7 @@ class FrameEngine:
         self.base = t.empty(V, dtype=t.int32, device=d)
         self.occ_sat = t.empty(max(V // 32, 1), dtype=t.int32, device=d)
         self.mips = t.empty(max(n_pyr - V, 1), dtype=t.float64, device=d)
-        self.solid = t.empty(max(V // 32, 1), dtype=t.int32, device=d)
+        self.solid = t.empty(ops.cull_scratch_words(self.res), dtype=t.int32, device=d)
         self.vis_tmp = t.empty(V, dtype=t.uint8, device=d)
         self.cull_flat = t.empty(n_pyr, dtype=t.uint8, device=d)
         self.offsets = t.empty(V + 1, dtype=t.int32, device=d)

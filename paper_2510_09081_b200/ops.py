@@ -148,6 +148,10 @@ def build_mips(base, res, mips):
     check(lib().lvx_build_mips(_ptr(base), res, _ptr(mips), _stream()), "lvx_build_mips")
 
 
+def cull_scratch_words(res: int) -> int:
+    return int(lib().lvx_cull_scratch_words(res))
+
+
 def cull(base, res, cam_voxel, solid_bits, vis_tmp, cull_flat, stats):
     cv, cv_p = _dbl3(cam_voxel)
     check(lib().lvx_cull(_ptr(base), res, cv_p, _ptr(solid_bits), _ptr(vis_tmp), _ptr(cull_flat),
