@@ -143,13 +143,13 @@ k_scatter(const double *__restrict__ verts, const int32_t *__restrict__ segs, in
 
 // all-ascending bitonic network on f[0..n) executed by one warp; indices >= n act as +inf
 __device__ void warp_bitonic(uint32_t *f, uint32_t n, int lane) {
-    uint32_t np2 = 1;
-    while (np2 < n) np2 <<= 1;
-    const uint32_t half = np2 >> 1;
-    for (uint32_t k = 2; k <= np2; k <<= 1) {
-        const uint32_t hk = k >> 1;
-        for (uint32_t t = lane; t < half; t += 32) {   // flip
-            const uint32_t blk = (t / hk) * k, o = t % hk;
+    int lg = 1;
+    while ((1u << lg) < n) lg++;
+    const uint32_t half = 1u << (lg - 1);
+    for (int lk = 1; lk <= lg; lk++) {                 // merge size k = 2^lk
+        const uint32_t k = 1u << lk, hk = k >> 1;
+        for (uint32_t t = lane; t < half; t += 32) {   // flip: i <-> mirror inside the k-block
+            const uint32_t blk = (t >> (lk - 1)) << lk, o = t & (hk - 1);
             const uint32_t i = blk + o, l = blk + k - 1 - o;
             if (l < n) {
                 const uint32_t a = f[i], b = f[l];
@@ -157,9 +157,10 @@ __device__ void warp_bitonic(uint32_t *f, uint32_t n, int lane) {
             }
         }
         __syncwarp();
-        for (uint32_t j = hk >> 1; j > 0; j >>= 1) {   // disperse
+        for (int lj = lk - 2; lj >= 0; lj--) {         // disperse: i <-> i + 2^lj
+            const uint32_t j = 1u << lj;
             for (uint32_t t = lane; t < half; t += 32) {
-                const uint32_t i = (t / j) * 2 * j + (t % j), l = i + j;
+                const uint32_t i = ((t >> lj) << (lj + 1)) + (t & (j - 1)), l = i + j;
                 if (l < n) {
                     const uint32_t a = f[i], b = f[l];
                     if (a > b) { f[i] = b; f[l] = a; }
@@ -180,16 +181,18 @@ __device__ void warp_bitonic(uint32_t *f, uint32_t n, int lane) {
 constexpr int ORDER_WARPS = 8;
 constexpr int ORDER_CAP = 1024;   // fragments staged per warp for long lists (4 KiB)
 
-__device__ __forceinline__ uint32_t warp_sort32(uint32_t v, int lane) {
+// bitonic sort of one value per lane (ascending by lane), network truncated to LG stages:
+// sorts the first 2^LG lanes when the rest hold +inf
+template <int LG>
+__device__ __forceinline__ uint32_t warp_sort(uint32_t v, int lane) {
 #pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
+    for (int lk = 1; lk <= LG; lk++) {
 #pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
-            const bool up = ((lane & k) == 0);            // ascending block?
-            const bool lower = ((lane & j) == 0);
-            const uint32_t mn = min(v, o), mx = max(v, o);
-            v = (lower == up) ? mn : mx;
+        for (int lj = lk - 1; lj >= 0; lj--) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, v, 1 << lj);
+            // keep the smaller value on the lower lane of an ascending block
+            const bool keep_min = (((lane >> lk) ^ (lane >> lj)) & 1) == 0;
+            v = keep_min ? min(v, o) : max(v, o);
         }
     }
     return v;
@@ -222,7 +225,10 @@ k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ curso
             uint32_t val = lane < nn ? f[lane] : 0xffffffffu;
             const uint32_t next = __shfl_down_sync(0xffffffffu, val, 1);
             if (__ballot_sync(0xffffffffu, lane + 1 < nn && val > next) == 0) continue;   // already ascending
-            val = warp_sort32(val, lane);
+            if (nn <= 4) val = warp_sort<2>(val, lane);
+            else if (nn <= 8) val = warp_sort<3>(val, lane);
+            else if (nn <= 16) val = warp_sort<4>(val, lane);
+            else val = warp_sort<5>(val, lane);
             if (lane < nn) f[lane] = val;
         } else if (nn <= ORDER_CAP) {
             uint32_t *buf = stage[warp];

@@ -400,6 +400,222 @@ k_render(const RenderArgs A) {
         atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)tests);
 }
 
+// ----------------------------------------------------------------------------- opaque, warp-cooperative
+// The per-pixel loop above spends most of its instructions in the heavy f64 intersection with 2-3
+// of 32 lanes active (ncu: profiles/r01c).  This kernel keeps the reference's per-ray semantics
+// (lv/raytracer.py:459-515) but shares the work of a warp's 8x4 pixel tile:
+//   1. every unfinished ray marches (hierarchical skip) to its next occupied voxel;
+//   2. the (ray, fragment) pairs of all 32 rays are flattened with a warp prefix sum and dealt
+//      round-robin to the lanes -> the cheap conservative reject runs fully converged, fragment
+//      ids are read coalesced;
+//   3. pairs that survive the reject are compacted into a shared-memory queue; whenever 32 are
+//      queued the full clipped ray-capsule routine runs on all 32 lanes at once;
+//   4. hits are folded on the owning lane by (t, slot) -- "min t, first slot wins ties" (453) --
+//      and rays without a hit step to the voxel exit.
+// Shading runs once, after the loop, for all hit rays together.
+constexpr int RC_WARPS = 4;
+
+struct WarpShared {
+    double dir[3][32];
+    int vox[3][32];
+    uint32_t fo[32];
+    uint32_t prefix[33];
+    uint32_t q_i[64];
+    uint32_t q_rs[64];
+    double hit_t[32];
+    uint32_t hit_s[32], hit_i[32];
+};
+
+__global__ void __launch_bounds__(RC_WARPS * 32)
+k_render_opaque_coop(const RenderArgs A) {
+    __shared__ WarpShared sh_all[RC_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpShared &S = sh_all[warp];
+    // block = 4 warps side by side: 32 x 4 pixels, each warp an 8x4 tile
+    const int px = A.p.tile_x0 + blockIdx.x * (8 * RC_WARPS) + warp * 8 + (lane & 7);
+    const int py = A.p.tile_y0 + blockIdx.y * 4 + (lane >> 3);
+    const bool live = px < A.p.tile_x1 && py < A.p.tile_y1;
+    const int w = A.cam.width, h = A.cam.height, res = A.res;
+    const double ox = A.cam.pos[0], oy = A.cam.pos[1], oz = A.cam.pos[2];
+    const bool clip = A.p.use_clip != 0;
+    const double r = A.p.radius;
+    double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
+    bool active = false;
+    if (live) {
+        // lv/raytracer.py:414-423
+        const double aspect = (double)w / (double)h;
+        const double u = (2.0 * (px + 0.5) / w - 1.0) * aspect * A.cam.tan_half_fov;
+        const double v = (1.0 - 2.0 * (py + 0.5) / h) * A.cam.tan_half_fov;
+        dx = A.cam.fwd[0] + u * A.cam.right[0] + v * A.cam.up[0];
+        dy = A.cam.fwd[1] + u * A.cam.right[1] + v * A.cam.up[1];
+        dz = A.cam.fwd[2] + u * A.cam.right[2] + v * A.cam.up[2];
+        const double dn = sqrt(dx * dx + dy * dy + dz * dz);
+        dx = dx / dn; dy = dy / dn; dz = dz / dn;
+        // lv/raytracer.py:272-291
+        double t0 = 0.0;
+        t1 = 1e30;
+        const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            if (d[a] == 0.0) {
+                if (o[a] < 0.0 || o[a] > (double)res) { t0 = 1.0; t1 = -1.0; break; }
+            } else {
+                double ta = (0.0 - o[a]) / d[a], tb = ((double)res - o[a]) / d[a];
+                if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
+                if (ta > t0) t0 = ta;
+                if (tb < t1) t1 = tb;
+            }
+        }
+        active = t1 >= t0;
+        t = t0 > 0.0 ? t0 : 0.0;
+    }
+    S.dir[0][lane] = dx; S.dir[1][lane] = dy; S.dir[2][lane] = dz;
+    double best_t = -1.0;      // final hit of this lane's ray
+    int64_t best_i = -1;
+    uint64_t n_tests = 0;
+    __syncwarp();
+
+    for (;;) {
+        // ---- 1. march to the next occupied voxel (lv/raytracer.py:475-482, 506-509)
+        uint32_t n = 0;
+        double te = 0.0;
+        int x = 0, y = 0, z = 0;
+        if (active) {
+            for (;;) {
+                if (!(t < t1)) { active = false; break; }
+                const double tm = t + 1e-6;
+                x = (int)floor(ox + dx * tm); y = (int)floor(oy + dy * tm); z = (int)floor(oz + dz * tm);
+                if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) { active = false; break; }
+                const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
+                if (A.bits[idx] != 0) {
+                    const uint32_t fo = A.offsets[idx];
+                    n = A.offsets[idx + 1] - fo;
+                    S.fo[lane] = fo;
+                    te = voxel_exit(ox, oy, oz, dx, dy, dz, x, y, z, 0);
+                    break;
+                }
+                const int l = empty_level(A, x, y, z);
+                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, x, y, z, l);
+                t = tl > t ? tl : t + 1e-6;
+            }
+        }
+        if (__ballot_sync(0xffffffffu, active) == 0) break;
+        S.vox[0][lane] = x; S.vox[1][lane] = y; S.vox[2][lane] = z;
+        // ---- 2. flatten (ray, fragment) pairs
+        uint32_t inc = active ? n : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        S.prefix[lane + 1] = inc;
+        if (lane == 0) S.prefix[0] = 0;
+        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane == 0) n_tests += T;
+        double cur_t = -1.0;           // best hit of this lane's ray in this voxel
+        uint32_t cur_s = 0xffffffffu, cur_i = 0;
+        uint32_t qn = 0;
+        __syncwarp();
+        for (uint32_t p0 = 0; p0 < T || qn > 0; p0 += 32) {
+            const uint32_t p = p0 + lane;
+            bool pass = false;
+            uint32_t rr = 0, ss = 0, ii = 0;
+            if (p < T) {
+                // owner ray: largest rr with prefix[rr] <= p
+                uint32_t lo = 0, hi = 32;
+#pragma unroll
+                for (int it = 0; it < 5; it++) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (S.prefix[mid] <= p) lo = mid; else hi = mid;
+                }
+                rr = lo;
+                ss = p - S.prefix[rr];
+                ii = A.frags[S.fo[rr] + ss];
+                const d3 va = ld3(A.verts + 3 * (int64_t)ii), vb = ld3(A.verts + 3 * (int64_t)ii + 3);
+                pass = !surely_misses(ox, oy, oz, S.dir[0][rr], S.dir[1][rr], S.dir[2][rr], va, vb, r);
+            }
+            // ---- 3. compact survivors into the queue
+            const uint32_t m = __ballot_sync(0xffffffffu, pass);
+            if (pass) {
+                const uint32_t pos = qn + __popc(m & ((1u << lane) - 1u));
+                S.q_i[pos] = ii;
+                S.q_rs[pos] = (rr << 16) | ss;
+            }
+            qn += __popc(m);
+            __syncwarp();
+            const bool flush = p0 + 32 >= T;          // last batch of pairs: drain what is left
+            if (qn >= 32 || (flush && qn > 0)) {
+                const uint32_t take = qn < 32 ? qn : 32;
+                bool hit = false;
+                double ht = 0.0;
+                uint32_t hr = 0, hs = 0, hi_ = 0;
+                if (lane < take) {
+                    hi_ = S.q_i[lane];
+                    const uint32_t rs = S.q_rs[lane];
+                    hr = rs >> 16; hs = rs & 0xFFFFu;
+                    const double ddx = S.dir[0][hr], ddy = S.dir[1][hr], ddz = S.dir[2][hr];
+                    const Capsule c = load_capsule(A.verts, A.normals, (int64_t)hi_, r, clip);
+                    ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
+                    if (ht >= 0.0) {   // lv/raytracer.py:446-452: the hit must lie in the ray's current voxel
+                        const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
+                        hit = hx == S.vox[0][hr] && hy == S.vox[1][hr] && hz == S.vox[2][hr];
+                    }
+                }
+                __syncwarp();
+                // move the queue tail down
+                uint32_t mv_i = 0, mv_rs = 0;
+                const bool mv = lane + 32 < qn;
+                if (mv) { mv_i = S.q_i[lane + 32]; mv_rs = S.q_rs[lane + 32]; }
+                __syncwarp();
+                if (mv) { S.q_i[lane] = mv_i; S.q_rs[lane] = mv_rs; }
+                qn -= take;
+                // ---- 4. fold hits on the owning lanes: min t, then lowest slot (lv/raytracer.py:453)
+                uint32_t hm = __ballot_sync(0xffffffffu, hit);
+                if (hit) { S.hit_t[lane] = ht; S.hit_s[lane] = hs; S.hit_i[lane] = hi_; }
+                __syncwarp();
+                while (hm) {
+                    const int src = __ffs(hm) - 1;
+                    hm &= hm - 1;
+                    const uint32_t owner = __shfl_sync(0xffffffffu, hr, src);
+                    if ((uint32_t)lane == owner) {
+                        const double tt = S.hit_t[src];
+                        const uint32_t s2 = S.hit_s[src];
+                        if (cur_t < 0.0 || tt < cur_t || (tt == cur_t && s2 < cur_s)) {
+                            cur_t = tt; cur_s = s2; cur_i = S.hit_i[src];
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            if (flush && qn == 0) break;
+        }
+        if (active) {
+            if (cur_t >= 0.0) { best_t = cur_t; best_i = cur_i; active = false; }
+            else t = te > t ? te : t + 1e-6;
+        }
+        __syncwarp();
+    }
+
+    if (live) {
+        double out_r = A.p.background[0], out_g = A.p.background[1], out_b = A.p.background[2];
+        int32_t out_id = -1;
+        if (best_t >= 0.0) {
+            const double hx = ox + dx * best_t, hy = oy + dy * best_t, hz = oz + dz * best_t;
+            const Capsule c = load_capsule(A.verts, A.normals, best_i, r, clip);
+            double nx, ny, nz;
+            capsule_normal(hx, hy, hz, c, nx, ny, nz);
+            shade(A, c, nx, ny, nz, hx, hy, hz, out_r, out_g, out_b);
+            out_id = (int32_t)best_i;
+        }
+        const int64_t pix = (int64_t)py * w + px;
+        if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
+        if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
+        A.hit_id[pix] = out_id;
+    }
+    if (lane == 0 && n_tests)
+        atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)n_tests);
+}
+
 }  // namespace lvx
 
 using namespace lvx;
@@ -426,7 +642,10 @@ int lvx_render(const double *verts, const double *normals, const uint32_t *offse
     A.res = res; A.n_levels = L.n_levels; A.cam = *cam_host; A.p = p;
     A.rgb = rgb; A.srgb = srgb; A.hit_id = hit_id; A.stats = stats;
     const dim3 grid((tw + 7) / 8, (th + 15) / 16);
-    if (p.mode == 0) k_render<0><<<grid, 128, 0, (cudaStream_t)stream>>>(A);
+    if (p.mode == 0) {
+        const dim3 cgrid((tw + 8 * RC_WARPS - 1) / (8 * RC_WARPS), (th + 3) / 4);
+        k_render_opaque_coop<<<cgrid, RC_WARPS * 32, 0, (cudaStream_t)stream>>>(A);
+    }
     else k_render<1><<<grid, 128, 0, (cudaStream_t)stream>>>(A);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
