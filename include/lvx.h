@@ -123,10 +123,16 @@ int lvx_build_mips(const uint32_t *base, int res, double *mips, void *stream);
  * of scratch (per-voxel solid bits + coarse brick flags); vis_tmp: V bytes scratch.  cam_voxel_host = GridDesc.to_voxel(cam.position). */
 int64_t lvx_cull_scratch_words(int res);
 int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host,
-             uint32_t *solid_bits, uint8_t *vis_tmp, uint8_t *cull_flat, uint64_t *stats, void *stream);
+             uint32_t *solid_bits, uint8_t *vis_tmp, uint8_t *cull_flat, uint32_t *vis_list,
+             uint64_t *stats, void *stream);
 /* march bits for the un-culled strategy: CullingPyramid.from_bits(counts > 0)
  * (lv/raytracer.py:665-668, lv/pipeline.py:115-116) */
-int lvx_occupied_pyramid(const uint32_t *base, int res, uint8_t *cull_flat, uint64_t *stats, void *stream);
+int lvx_occupied_pyramid(const uint32_t *base, int res, uint8_t *cull_flat, uint32_t *vis_list,
+                         uint64_t *stats, void *stream);
+/* Both calls also emit `vis_list`: lvx_list_words(V) u32 words -- word 0..1 = number of set base
+ * bits (u64), entries (flat voxel indices, unordered) from word 16.  The A-buffer ordering pass
+ * and the shading kernel iterate this list instead of the whole volume. */
+int64_t lvx_list_words(int64_t n_voxels);
 
 /* ---- A-buffer: lv/abuffer.py:104-114 scan_offsets; 195-255 _chunk_count_kernel/_write_kernel.
  * offsets has V+1 entries (u32): offsets[i] = exclusive scan of the culling-masked counts,
@@ -137,18 +143,18 @@ int lvx_scan(const uint32_t *base, const uint8_t *cull_base, int64_t n_voxels,
              uint32_t *offsets, void *scratch, uint64_t *stats, void *stream);
 /* second traversal: cursor (V u32 scratch) is initialised from offsets; fragments of each
  * voxel end up in ascending segment order (lv/abuffer.py:313-317 semantics) after the
- * in-kernel ordering pass.  worklist: V/8+64 u32 scratch for long lists. */
+ * ordering pass, which walks vis_list (the voxels that own fragments). */
 int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double rt, int res, int method,
-                const uint8_t *cull_flat /* NULL = no culling */, const uint32_t *offsets,
-                uint32_t *cursor, uint32_t *worklist, uint32_t *frags, int64_t frag_capacity,
+                const uint8_t *cull_flat /* NULL = no culling */, const uint32_t *vis_list,
+                const uint32_t *offsets, uint32_t *cursor, uint32_t *frags, int64_t frag_capacity,
                 uint64_t *stats, void *stream);
 
 /* ---- shading: lv/shading.py:72-155 _trilinear/_cone_trace/_shading_kernel, 170-185.
  * dirs_host: n_dirs*3 unit vectors (lv/shading.py:32-40); light_host: unit light direction.
  * ao/shadow: V f32, 1.0 where not visible.  n_dirs <= 15.  scratch: lvx_shade_scratch_bytes(V)
- * (compacted list of visible voxels). */
+ * (per-level non-empty masks). */
 int64_t lvx_shade_scratch_bytes(int64_t n_voxels);
-int lvx_shade(const uint32_t *base, const double *mips, int res, const uint8_t *visible,
+int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t *vis_list,
               const double *dirs_host, int n_dirs, double tan_ao, const double *light_host,
               double tan_shadow, float *ao, float *shadow, void *scratch, void *stream);
 

@@ -51,8 +51,9 @@ SIGNATURES = {
     "lvx_finalize_base": (_I, [_P, _P, _L, _P, _P]),
     "lvx_build_mips": (_I, [_P, _I, _P, _P]),
     "lvx_cull_scratch_words": (_L, [_I]),
-    "lvx_cull": (_I, [_P, _I, _P, _P, _P, _P, _P, _P]),
-    "lvx_occupied_pyramid": (_I, [_P, _I, _P, _P, _P]),
+    "lvx_cull": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "lvx_occupied_pyramid": (_I, [_P, _I, _P, _P, _P, _P]),
+    "lvx_list_words": (_L, [_L]),
     "lvx_scan_scratch_bytes": (_L, [_L]),
     "lvx_scan": (_I, [_P, _P, _L, _P, _P, _P, _P]),
     "lvx_scatter": (_I, [_P, _P, _L, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P]),

@@ -9,6 +9,7 @@ import numpy as np
 
 from . import _native as N
 from . import ops
+from .culling import occupied_bits
 from .voxelizer import METHODS, upload_lineset
 
 __all__ = ["OffsetTable", "ABuffer", "ABufferError", "scan_offsets", "build_vsv", "build_vcsv"]
@@ -103,7 +104,8 @@ def _second_pass(ls, cn, g, pyramid, culling, method, r_world):
     rt = ops.footprint_radius(lines.r, pyramid.r_min)
     frags = torch.empty(max(table.total, 1), dtype=torch.int32, device=dev)
     cursor = torch.empty(res ** 3, dtype=torch.int32, device=dev)
-    ops.scatter(lines, rt, res, method, None if culling is None else culling.flat_dev,
+    owners = culling if culling is not None else occupied_bits(pyramid)   # voxels that own fragments
+    ops.scatter(lines, rt, res, method, None if culling is None else culling.flat_dev, owners.list_dev,
                 table.offsets_dev, cursor, frags, stats)
     st = stats.cpu().numpy()
     if pyramid.saturated == 0 and st[N.ST_MISMATCH]:

@@ -171,15 +171,16 @@ __device__ void warp_bitonic(uint32_t *f, uint32_t n, int lane) {
     }
 }
 
-// Ordering pass.  A warp owns 32 consecutive voxels and walks their lists one at a time:
-//   n <= 32 : one coalesced 128-byte load, a 15-step bitonic network in registers (warp
-//             shuffles), one coalesced store -- skipped entirely when the list is already
-//             ascending (a ballot), which is common because low segment ids are scattered first;
+// Ordering pass over the compacted list of visible voxels (the only voxels that own fragments).
+// One warp sorts one list at a time, two lists in flight per iteration for memory-level
+// parallelism:
+//   n <= 32 : one coalesced 128-byte load, a bitonic network in registers (warp shuffles, depth
+//             chosen from n), one coalesced store -- skipped when the list is already ascending;
 //   n  > 32 : staged through shared memory (or sorted in place when it exceeds the stage) with
 //             the all-ascending bitonic network above.
 // HBM traffic is <= 8 B per fragment, every access coalesced.
 constexpr int ORDER_WARPS = 8;
-constexpr int ORDER_CAP = 1024;   // fragments staged per warp for long lists (4 KiB)
+constexpr int ORDER_CAP = 512;   // fragments staged per warp for long lists (2 KiB)
 
 // bitonic sort of one value per lane (ascending by lane), network truncated to LG stages:
 // sorts the first 2^LG lanes when the rest hold +inf
@@ -198,49 +199,72 @@ __device__ __forceinline__ uint32_t warp_sort(uint32_t v, int lane) {
     return v;
 }
 
+__device__ __forceinline__ void sort_short(uint32_t *f, uint32_t nn, uint32_t val, int lane) {
+    const uint32_t next = __shfl_down_sync(0xffffffffu, val, 1);
+    if (__ballot_sync(0xffffffffu, lane + 1 < nn && val > next) == 0) return;   // already ascending
+    if (nn <= 4) val = warp_sort<2>(val, lane);
+    else if (nn <= 8) val = warp_sort<3>(val, lane);
+    else if (nn <= 16) val = warp_sort<4>(val, lane);
+    else val = warp_sort<5>(val, lane);
+    if (lane < nn) f[lane] = val;
+}
+
 __global__ void __launch_bounds__(ORDER_WARPS * 32)
-k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ cursor, int64_t V,
-        uint32_t *__restrict__ frags, int64_t cap, uint64_t *__restrict__ stats) {
+k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ cursor,
+        const uint32_t *__restrict__ vis_list, uint32_t *__restrict__ frags, int64_t cap,
+        uint64_t *__restrict__ stats) {
     __shared__ uint32_t stage[ORDER_WARPS][ORDER_CAP];
-    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t b = 0, n = 0;
-    if (v < V) {
-        b = offsets[v];
-        const uint32_t e = offsets[v + 1];
-        n = e - b;
-        if (cursor[v] != e) stats[LVX_ST_MISMATCH] = 1;   // lv/abuffer.py:310-311
-        if ((int64_t)e > cap) n = 0;                      // never touch memory past the buffer
-    }
-    uint32_t work = __ballot_sync(0xffffffffu, n > 1);
-    const uint32_t longs = __ballot_sync(0xffffffffu, n > 32);
-    if (longs && lane == 0)
-        atomicAdd((unsigned long long *)&stats[LVX_ST_LONG_LISTS], (unsigned long long)__popc(longs));
-    while (work) {
-        const int src = __ffs(work) - 1;
-        work &= work - 1;
-        const uint32_t bb = __shfl_sync(0xffffffffu, b, src), nn = __shfl_sync(0xffffffffu, n, src);
-        uint32_t *f = frags + bb;
-        if (nn <= 32) {
-            uint32_t val = lane < nn ? f[lane] : 0xffffffffu;
-            const uint32_t next = __shfl_down_sync(0xffffffffu, val, 1);
-            if (__ballot_sync(0xffffffffu, lane + 1 < nn && val > next) == 0) continue;   // already ascending
-            if (nn <= 4) val = warp_sort<2>(val, lane);
-            else if (nn <= 8) val = warp_sort<3>(val, lane);
-            else if (nn <= 16) val = warp_sort<4>(val, lane);
-            else val = warp_sort<5>(val, lane);
-            if (lane < nn) f[lane] = val;
-        } else if (nn <= ORDER_CAP) {
-            uint32_t *buf = stage[warp];
-            for (uint32_t i = lane; i < nn; i += 32) buf[i] = f[i];
-            __syncwarp();
-            warp_bitonic(buf, nn, lane);
-            for (uint32_t i = lane; i < nn; i += 32) f[i] = buf[i];
-            __syncwarp();
-        } else {
-            warp_bitonic(f, nn, lane);
+    const int64_t n_lists = (int64_t)*reinterpret_cast<const unsigned long long *>(vis_list);
+    const int64_t warp_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t n_long = 0;
+    // each warp takes a contiguous chunk of 32 list entries per step: lane k reads entry k's bounds
+    for (int64_t e0 = warp_id * 32; e0 < n_lists; e0 += n_warps * 32) {
+        uint32_t b = 0, n = 0;
+        if (e0 + lane < n_lists) {
+            const uint32_t v = vis_list[LVX_LIST_HDR + e0 + lane];
+            b = offsets[v];
+            const uint32_t e = offsets[v + 1];
+            n = e - b;
+            if (cursor[v] != e) stats[LVX_ST_MISMATCH] = 1;   // lv/abuffer.py:310-311
+            if ((int64_t)e > cap) n = 0;                      // never touch memory past the buffer
+        }
+        uint32_t work = __ballot_sync(0xffffffffu, n > 1);
+        n_long += __popc(__ballot_sync(0xffffffffu, n > 32));
+        while (work) {
+            // two lists per iteration: both loads are issued before either sort
+            const int s0 = __ffs(work) - 1;
+            work &= work - 1;
+            const int s1 = work ? __ffs(work) - 1 : -1;
+            if (s1 >= 0) work &= work - 1;
+            const uint32_t b0 = __shfl_sync(0xffffffffu, b, s0), n0 = __shfl_sync(0xffffffffu, n, s0);
+            const uint32_t b1 = __shfl_sync(0xffffffffu, b, s1 < 0 ? 0 : s1);
+            const uint32_t n1 = s1 < 0 ? 0 : __shfl_sync(0xffffffffu, n, s1 < 0 ? 0 : s1);
+            uint32_t v0 = 0xffffffffu, v1 = 0xffffffffu;
+            if (n0 <= 32 && lane < n0) v0 = frags[b0 + lane];
+            if (n1 <= 32 && lane < n1) v1 = frags[b1 + lane];
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                const uint32_t bb = k ? b1 : b0, nn = k ? n1 : n0;
+                if (nn < 2) continue;
+                uint32_t *f = frags + bb;
+                if (nn <= 32) sort_short(f, nn, k ? v1 : v0, lane);
+                else if (nn <= ORDER_CAP) {
+                    uint32_t *buf = stage[warp];
+                    for (uint32_t i = lane; i < nn; i += 32) buf[i] = f[i];
+                    __syncwarp();
+                    warp_bitonic(buf, nn, lane);
+                    for (uint32_t i = lane; i < nn; i += 32) f[i] = buf[i];
+                    __syncwarp();
+                } else {
+                    warp_bitonic(f, nn, lane);
+                }
+            }
         }
     }
+    if (lane == 0 && n_long)
+        atomicAdd((unsigned long long *)&stats[LVX_ST_LONG_LISTS], (unsigned long long)n_long);
 }
 
 __global__ void __launch_bounds__(256)
@@ -274,9 +298,9 @@ int lvx_scan(const uint32_t *base, const uint8_t *cull_base, int64_t n_voxels, u
 }
 
 int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double rt, int res, int method,
-                const uint8_t *cull_flat, const uint32_t *offsets, uint32_t *cursor, uint32_t *worklist,
+                const uint8_t *cull_flat, const uint32_t *vis_list, const uint32_t *offsets, uint32_t *cursor,
                 uint32_t *frags, int64_t frag_capacity, uint64_t *stats, void *stream) {
-    (void)worklist;
+    if (!vis_list) return LVX_E_ARG;
     if (!pow2(res) || method < 0 || method > 2) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
@@ -284,7 +308,12 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
     if (n_seg > 0)
         k_scatter<<<blocks_for(n_seg, 128), 128, 0, s>>>(verts, segs, n_seg, rt, res, method, cull_flat, cursor,
                                                         frags, frag_capacity);
-    k_order<<<blocks_for(V, ORDER_WARPS * 32), ORDER_WARPS * 32, 0, s>>>(offsets, cursor, V, frags, frag_capacity, stats);
+    {
+        unsigned nb = 148 * 8;   // persistent: 148 SMs x 8 CTAs of 8 warps
+        const unsigned need = blocks_for((V + 31) / 32, ORDER_WARPS);
+        if (nb > need) nb = need;
+        k_order<<<nb, ORDER_WARPS * 32, 0, s>>>(offsets, cursor, vis_list, frags, frag_capacity, stats);
+    }
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

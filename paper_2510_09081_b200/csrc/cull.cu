@@ -25,7 +25,8 @@ __device__ __forceinline__ bool q_solid(const uint32_t *__restrict__ base, int r
 
 __global__ void __launch_bounds__(256)
 k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restrict__ solid,
-        uint32_t *__restrict__ bricks, uint64_t *__restrict__ stats) {
+        uint32_t *__restrict__ bricks, uint32_t *__restrict__ occ_list, uint8_t *__restrict__ vis,
+        uint64_t *__restrict__ stats) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool s = false, occ = false;
     if (idx < V) {
@@ -60,10 +61,18 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
             bits += brick_words(res, B);
         }
     }
-    if ((threadIdx.x & 31) == 0 && idx < V) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long slot = 0;
+    if (lane == 0 && idx < V) {
         solid[idx >> 5] = m;
         if (m) atomicAdd((unsigned long long *)&stats[LVX_ST_SOLID], (unsigned long long)__popc(m));
-        if (mo) atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)__popc(mo));
+        // compacted list of occupied voxels: the march kernel then runs on dense warps
+        if (mo) slot = atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)__popc(mo));
+    }
+    if (idx < V) vis[idx] = 0;
+    if (mo) {
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (occ) occ_list[slot + __popc(mo & ((1u << lane) - 1u))] = (uint32_t)idx;
     }
 }
 
@@ -139,35 +148,55 @@ __device__ __forceinline__ bool coarse_may_hit(const uint32_t *__restrict__ bits
 
 // lv/culling.py:191-200.  When the frame has no solid voxel at all nothing can block, so every
 // occupied voxel is visible and the march is skipped (decided on the device, no host sync).
+// Phase A over the compacted occupied voxels: coarse walks only.  Voxels that may be blocked are
+// appended to `march_list`; everything else is visible.
 __global__ void __launch_bounds__(128)
-k_visibility(const uint32_t *__restrict__ base, const uint32_t *__restrict__ solid,
-             const uint32_t *__restrict__ bricks, int res, int64_t V,
-             double cx, double cy, double cz, const uint64_t *__restrict__ stats, uint8_t *__restrict__ vis) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= V) return;
-    uint8_t v = 0;
-    if ((base[idx] >> 16) != 0) {
-        if (stats[LVX_ST_SOLID] == 0) v = 1;
-        else {
-            const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
-            // Only a solid voxel can block.  Walk the segment centre->camera through the 32^3-voxel
-            // super-bricks, then the 8^3 bricks; only if both touch a flagged cell does the literal
-            // fine march (which decides) run.
-            const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
-            bool may_hit = coarse_may_hit(bricks + brick_words(res, LVX_BRICK), (res + LVX_SUPER - 1) / LVX_SUPER,
-                                          LVX_SUPER, ox, oy, oz, cx, cy, cz);
-            if (may_hit)
-                may_hit = coarse_may_hit(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz, cx, cy, cz);
-            v = (may_hit && march_blocked(solid, res, x, y, z, cx, cy, cz)) ? 0 : 1;
+k_visibility(const uint32_t *__restrict__ bricks, const uint32_t *__restrict__ occ_list, int res,
+             double cx, double cy, double cz, const uint64_t *__restrict__ stats,
+             uint8_t *__restrict__ vis, uint32_t *__restrict__ march_list) {
+    const int64_t n = (int64_t)stats[LVX_ST_OCCUPIED];
+    const bool any_solid = stats[LVX_ST_SOLID] != 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_iter = (n + stride - 1) / stride;
+    for (int64_t it = 0; it < n_iter; it++) {
+        const int64_t e = it * stride + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        bool may_hit = false;
+        uint32_t idx = 0;
+        if (e < n) {
+            idx = occ_list[e];
+            if (any_solid) {
+                const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
+                // Only a solid voxel can block.  Walk the segment centre->camera through the
+                // 32^3-voxel super-bricks, then the 8^3 bricks.
+                const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
+                may_hit = coarse_may_hit(bricks + brick_words(res, LVX_BRICK), (res + LVX_SUPER - 1) / LVX_SUPER,
+                                         LVX_SUPER, ox, oy, oz, cx, cy, cz);
+                if (may_hit)
+                    may_hit = coarse_may_hit(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz, cx, cy, cz);
+            }
+            if (!may_hit) vis[idx] = 1;
         }
+        list_append_warp(march_list, may_hit, idx);
     }
-    vis[idx] = v;
+}
+
+// Phase B: the literal fine march (lv/culling.py:143-188) decides for the remaining candidates.
+__global__ void __launch_bounds__(128)
+k_march(const uint32_t *__restrict__ solid, const uint32_t *__restrict__ march_list, int res,
+        double cx, double cy, double cz, uint8_t *__restrict__ vis) {
+    const int64_t n = (int64_t)*reinterpret_cast<const unsigned long long *>(march_list);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+        const uint32_t idx = march_list[LVX_LIST_HDR + e];
+        const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
+        vis[idx] = march_blocked(solid, res, x, y, z, cx, cy, cz) ? 0 : 1;
+    }
 }
 
 // lv/culling.py:130-140 dilate_bits, then `& occ_bits` (224)
 __global__ void __launch_bounds__(256)
 k_dilate(const uint32_t *__restrict__ base, const uint8_t *__restrict__ vis, int res, int64_t V,
-         uint8_t *__restrict__ out, uint64_t *__restrict__ stats) {
+         uint8_t *__restrict__ out, uint32_t *__restrict__ vis_list, uint64_t *__restrict__ stats) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool v = false;
     if (idx < V && (base[idx] >> 16) != 0) {
@@ -193,10 +222,12 @@ k_dilate(const uint32_t *__restrict__ base, const uint8_t *__restrict__ vis, int
     const uint32_t m = __ballot_sync(0xffffffffu, v);
     if ((threadIdx.x & 31) == 0 && m)
         atomicAdd((unsigned long long *)&stats[LVX_ST_VISIBLE], (unsigned long long)__popc(m));
+    list_append_warp(vis_list, v, (uint32_t)idx);
 }
 
 __global__ void __launch_bounds__(256)
-k_occupied(const uint32_t *__restrict__ base, int64_t V, uint8_t *__restrict__ out, uint64_t *__restrict__ stats) {
+k_occupied(const uint32_t *__restrict__ base, int64_t V, uint8_t *__restrict__ out, uint32_t *__restrict__ vis_list,
+           uint64_t *__restrict__ stats) {
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool v = idx < V && (base[idx] >> 16) != 0;
     if (idx < V) out[idx] = v ? 1 : 0;
@@ -205,6 +236,7 @@ k_occupied(const uint32_t *__restrict__ base, int64_t V, uint8_t *__restrict__ o
         atomicAdd((unsigned long long *)&stats[LVX_ST_VISIBLE], (unsigned long long)__popc(m));
         atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)__popc(m));
     }
+    list_append_warp(vis_list, v, (uint32_t)idx);
 }
 
 // lv/culling.py:103-109: parent = OR of its 8 children
@@ -246,32 +278,44 @@ extern "C" {
 int64_t lvx_cull_scratch_words(int res) {
     if (!pow2(res)) return LVX_E_ARG;
     const int64_t V = (int64_t)res * res * res;
-    return (V + 31) / 32 + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER);
+    return (V + 31) / 32 + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER) + V;   // + occupied-voxel list
 }
 
 int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32_t *solid_bits,
-             uint8_t *vis_tmp, uint8_t *cull_flat, uint64_t *stats, void *stream) {
+             uint8_t *vis_tmp, uint8_t *cull_flat, uint32_t *vis_list, uint64_t *stats, void *stream) {
     if (!pow2(res)) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
-    // solid_bits scratch layout: [V/32 words of per-voxel solid bits][8^3-brick flags][32^3-brick flags]
+    // solid_bits scratch layout: [V/32 words of solid bits][8^3-brick flags][32^3-brick flags][V: occupied list]
     uint32_t *bricks = solid_bits + (V + 31) / 32;
     LVX_CUDA(cudaMemsetAsync(bricks, 0, (size_t)(brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER)) * 4, s));
-    k_solid<<<blocks_for(V, 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, stats);
-    k_visibility<<<blocks_for(V, 128), 128, 0, s>>>(base, solid_bits, bricks, res, V, cam_voxel_host[0],
-                                                    cam_voxel_host[1], cam_voxel_host[2], stats, vis_tmp);
-    k_dilate<<<blocks_for(V, 256), 256, 0, s>>>(base, vis_tmp, res, V, cull_flat, stats);
+    uint32_t *occ_list = bricks + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER);
+    k_solid<<<blocks_for(V, 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, occ_list, vis_tmp, stats);
+    unsigned nb = 148 * 16;
+    if (nb > blocks_for(V, 128)) nb = blocks_for(V, 128);
+    // vis_list doubles as the "needs the fine march" list until k_dilate refills it
+    LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
+    k_visibility<<<nb, 128, 0, s>>>(bricks, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
+                                    cam_voxel_host[2], stats, vis_tmp, vis_list);
+    k_march<<<nb, 128, 0, s>>>(solid_bits, vis_list, res, cam_voxel_host[0], cam_voxel_host[1],
+                               cam_voxel_host[2], vis_tmp);
+    LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
+    k_dilate<<<blocks_for(V, 256), 256, 0, s>>>(base, vis_tmp, res, V, cull_flat, vis_list, stats);
     LVX_LAUNCH_CHECK();
     return or_mips(cull_flat, res, s);
 }
 
-int lvx_occupied_pyramid(const uint32_t *base, int res, uint8_t *cull_flat, uint64_t *stats, void *stream) {
+int lvx_occupied_pyramid(const uint32_t *base, int res, uint8_t *cull_flat, uint32_t *vis_list, uint64_t *stats,
+                         void *stream) {
     if (!pow2(res)) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
-    k_occupied<<<blocks_for(V, 256), 256, 0, s>>>(base, V, cull_flat, stats);
+    LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
+    k_occupied<<<blocks_for(V, 256), 256, 0, s>>>(base, V, cull_flat, vis_list, stats);
     LVX_LAUNCH_CHECK();
     return or_mips(cull_flat, res, s);
 }
+
+int64_t lvx_list_words(int64_t n_voxels) { return n_voxels + LVX_LIST_HDR; }
 
 }  // extern "C"

@@ -213,6 +213,19 @@ static inline LevelOffsets make_level_offsets(int res) {
     return L;
 }
 
+// List buffers: word 0..1 hold the entry count (u64), entries start at word LVX_LIST_HDR.
+#define LVX_LIST_HDR 16
+
+__device__ __forceinline__ void list_append_warp(uint32_t *list, bool pred, uint32_t value) {
+    const uint32_t m = __ballot_sync(0xffffffffu, pred);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    unsigned long long b = 0;
+    if (lane == __ffs(m) - 1) b = atomicAdd(reinterpret_cast<unsigned long long *>(list), (unsigned long long)__popc(m));
+    b = __shfl_sync(0xffffffffu, b, __ffs(m) - 1);
+    if (pred) list[LVX_LIST_HDR + b + __popc(m & ((1u << lane) - 1u))] = value;
+}
+
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     return v;

@@ -12,7 +12,7 @@ struct RenderArgs {
     const uint32_t *offsets, *frags;
     const uint8_t *bits;
     const float *ao, *sh;
-    int64_t bits_off[16];
+    uint32_t bits_off[16];
     int res, n_levels;
     lvx_camera cam;
     lvx_render_params p;
@@ -154,27 +154,50 @@ __device__ void capsule_normal(double px, double py, double pz, const Capsule &c
     ox = nx / nn; oy = ny / nn; oz = nz / nn;
 }
 
-// lv/raytracer.py:294-313
+// lv/raytracer.py:294-313.  The reference takes the minimum of up to three quotients.  Here the
+// quotients are first estimated with precomputed reciprocals (error < 3e-16 relative); only axes
+// whose estimate is within 1e-13 of the smallest can own the exact minimum, so the exact IEEE
+// division is evaluated for those (almost always one) and the result is bit-identical.
+struct RayInv { double ix, iy, iz; };
+__device__ __forceinline__ RayInv make_inv(double dx, double dy, double dz) {
+    return RayInv{dx != 0.0 ? 1.0 / dx : 0.0, dy != 0.0 ? 1.0 / dy : 0.0, dz != 0.0 ? 1.0 / dz : 0.0};
+}
 __device__ __forceinline__ double voxel_exit(double ox, double oy, double oz, double dx, double dy, double dz,
-                                             int x, int y, int z, int lvl) {
+                                             const RayInv &inv, int x, int y, int z, int lvl) {
     const int size = 1 << lvl;
     const int bx = (x >> lvl) << lvl, by = (y >> lvl) << lvl, bz = (z >> lvl) << lvl;
-    double t = 1e30;
-    if (dx > 0.0) t = fmin(t, ((double)(bx + size) - ox) / dx); else if (dx < 0.0) t = fmin(t, ((double)bx - ox) / dx);
-    if (dy > 0.0) t = fmin(t, ((double)(by + size) - oy) / dy); else if (dy < 0.0) t = fmin(t, ((double)by - oy) / dy);
-    if (dz > 0.0) t = fmin(t, ((double)(bz + size) - oz) / dz); else if (dz < 0.0) t = fmin(t, ((double)bz - oz) / dz);
+    const double big = 1e30;
+    const double nx = (double)(dx > 0.0 ? bx + size : bx) - ox;
+    const double ny = (double)(dy > 0.0 ? by + size : by) - oy;
+    const double nz = (double)(dz > 0.0 ? bz + size : bz) - oz;
+    const double ax = dx != 0.0 ? nx * inv.ix : big;
+    const double ay = dy != 0.0 ? ny * inv.iy : big;
+    const double az = dz != 0.0 ? nz * inv.iz : big;
+    const double m = fmin(ax, fmin(ay, az));
+    const double lim = m + fabs(m) * 1e-13 + 1e-290;
+    double t = big;
+    if (ax <= lim) t = fmin(t, nx / dx);
+    if (ay <= lim) t = fmin(t, ny / dy);
+    if (az <= lim) t = fmin(t, nz / dz);
     return t;
 }
 
-// lv/raytracer.py:316-326
-__device__ __forceinline__ int empty_level(const RenderArgs &A, int x, int y, int z) {
-    int l = 0;
-    while (l < A.n_levels - 1) {
-        const int nl = l + 1;
-        const int64_t rl = A.res >> nl;
-        if (A.bits[A.bits_off[nl] + (x >> nl) + rl * ((y >> nl) + rl * (z >> nl))] != 0) break;
-        l = nl;
+// lv/raytracer.py:316-326: largest level whose node containing (x,y,z) is clear.  A parent is the OR
+// of its children, so "clear" is monotone in the level and the answer can be found from any
+// starting level (`hint`, normally the previous step's answer) instead of always climbing from 1.
+__device__ __forceinline__ bool node_clear(const RenderArgs &A, int l, int x, int y, int z) {
+    const uint32_t rl = (uint32_t)A.res >> l;
+    return A.bits[A.bits_off[l] + ((uint32_t)x >> l) + rl * (((uint32_t)y >> l) + rl * ((uint32_t)z >> l))] == 0;
+}
+__device__ __forceinline__ int empty_level(const RenderArgs &A, int x, int y, int z, int hint) {
+    const int top = A.n_levels - 1;
+    int l = hint < 1 ? 1 : (hint > top ? top : hint);
+    if (top < 1) return 0;
+    if (node_clear(A, l, x, y, z)) {
+        while (l < top && node_clear(A, l + 1, x, y, z)) l++;
+        return l;
     }
+    do { l--; } while (l >= 1 && !node_clear(A, l, x, y, z));
     return l;
 }
 
@@ -261,6 +284,8 @@ k_render(const RenderArgs A) {
         }
         const bool clip = A.p.use_clip != 0;
         const double r = A.p.radius;
+        const RayInv inv = make_inv(dx, dy, dz);
+        int lvl_hint = 1;
         double out_r, out_g, out_b;
         int32_t out_id;
         if (MODE == 0) {
@@ -300,10 +325,10 @@ k_render(const RenderArgs A) {
                             out_id = (int32_t)best_i;
                             break;
                         }
-                        te = voxel_exit(ox, oy, oz, dx, dy, dz, x, y, z, 0);
+                        te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
                     } else {
-                        const int l = empty_level(A, x, y, z);
-                        te = voxel_exit(ox, oy, oz, dx, dy, dz, x, y, z, l);
+                        const int l = lvl_hint = empty_level(A, x, y, z, lvl_hint);
+                        te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, l);
                     }
                     t = te > t ? te : t + 1e-6;
                 }
@@ -326,12 +351,12 @@ k_render(const RenderArgs A) {
                     if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) break;
                     const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
                     if (A.bits[idx] == 0) {
-                        const int l = empty_level(A, x, y, z);
-                        const double te = voxel_exit(ox, oy, oz, dx, dy, dz, x, y, z, l);
+                        const int l = lvl_hint = empty_level(A, x, y, z, lvl_hint);
+                        const double te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, l);
                         t = te > t ? te : t + 1e-6;
                         continue;
                     }
-                    const double te = voxel_exit(ox, oy, oz, dx, dy, dz, x, y, z, 0);
+                    const double te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
                     const double t_enter = t, span = te - t_enter;
                     const double inv_span = span > 0.0 ? 65535.0 / span : 0.0;
                     const uint32_t fo = A.offsets[idx], fn = A.offsets[idx + 1] - fo;
@@ -470,6 +495,8 @@ k_render_opaque_coop(const RenderArgs A) {
         t = t0 > 0.0 ? t0 : 0.0;
     }
     S.dir[0][lane] = dx; S.dir[1][lane] = dy; S.dir[2][lane] = dz;
+    const RayInv inv = make_inv(dx, dy, dz);
+    int lvl_hint = 1;
     double best_t = -1.0;      // final hit of this lane's ray
     int64_t best_i = -1;
     uint64_t n_tests = 0;
@@ -491,11 +518,11 @@ k_render_opaque_coop(const RenderArgs A) {
                     const uint32_t fo = A.offsets[idx];
                     n = A.offsets[idx + 1] - fo;
                     S.fo[lane] = fo;
-                    te = voxel_exit(ox, oy, oz, dx, dy, dz, x, y, z, 0);
+                    te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
                     break;
                 }
-                const int l = empty_level(A, x, y, z);
-                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, x, y, z, l);
+                const int l = lvl_hint = empty_level(A, x, y, z, lvl_hint);
+                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, l);
                 t = tl > t ? tl : t + 1e-6;
             }
         }
@@ -638,7 +665,7 @@ int lvx_render(const double *verts, const double *normals, const uint32_t *offse
     A.verts = verts; A.normals = normals; A.offsets = offsets; A.frags = frags; A.bits = bits_flat;
     A.ao = ao; A.sh = shadow;
     const LevelOffsets L = make_level_offsets(res);
-    for (int l = 0; l < 16; l++) A.bits_off[l] = l < L.n_levels ? L.off[l] : 0;
+    for (int l = 0; l < 16; l++) A.bits_off[l] = l < L.n_levels ? (uint32_t)L.off[l] : 0;
     A.res = res; A.n_levels = L.n_levels; A.cam = *cam_host; A.p = p;
     A.rgb = rgb; A.srgb = srgb; A.hit_id = hit_id; A.stats = stats;
     const dim3 grid((tw + 7) / 8, (th + 15) / 16);

@@ -12,33 +12,59 @@ struct ShadeParams {
     double dirs[15][3];
     double shadow_dir[3];   // -light
     double tan_ao, tan_shadow, w;
-    int64_t mip_off[16];    // element offset of level l (l >= 1) inside `mips`
+    uint32_t mip_off[16];   // element offset of level l (l >= 1) inside `mips`
+    uint32_t mask_off[16];  // word offset of level l inside the non-empty masks
     int n_dirs, res, n_levels;
 };
 
+// Non-empty masks.  Bit (ix,iy,iz) of level l says "some tap of the trilinear footprint
+// [ix,ix+1]x[iy,iy+1]x[iz,iz+1] of level l is non-zero" (always set on the last row/column/slice,
+// where the footprint is clamped).  A cleared bit means the sample is exactly 0.0, and
+// occ + (1-occ)*0.0 == occ bit for bit, so the eight loads and ~30 f64 operations of that sample
+// can be skipped without changing the result.  One bit per cell, x fastest: the 32 lanes of a
+// warp (x-adjacent voxels, same cone) read the same word.
+__device__ __forceinline__ bool cell_nonzero(const uint32_t *__restrict__ base, const double *__restrict__ lvl,
+                                             int l, uint32_t idx) {
+    return l == 0 ? (base[idx] & 0xFFFFu) != 0 : lvl[idx] != 0.0;
+}
+
+__global__ void __launch_bounds__(256)
+k_nzmask(const uint32_t *__restrict__ base, const double *__restrict__ lvl, int l, int rl,
+         uint32_t *__restrict__ mask) {
+    const uint32_t n = (uint32_t)rl * rl * rl;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool any = false;
+    if (i < n) {
+        const int x = i % rl, y = (i / rl) % rl, z = i / (rl * rl);
+        if (x == rl - 1 || y == rl - 1 || z == rl - 1) any = true;
+        else {
+#pragma unroll
+            for (int k = 0; k < 8 && !any; k++)
+                any = cell_nonzero(base, lvl, l, (x + (k & 1)) + (uint32_t)rl * ((y + ((k >> 1) & 1)) + (uint32_t)rl * (z + (k >> 2))));
+        }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, any);
+    if ((threadIdx.x & 31) == 0 && i < n) mask[i >> 5] = m;
+}
+
 // lv/shading.py:72-109; level 0 is read straight from the packed base words
-__device__ __forceinline__ double trilinear(const uint32_t *__restrict__ base, const double *__restrict__ mips,
-                                            const ShadeParams &P, int l, double px, double py, double pz) {
-    const int rl = P.res >> l;
-    const double scale = 1.0 / (double)(1 << l);
-    const double ux = px * scale - 0.5, uy = py * scale - 0.5, uz = pz * scale - 0.5;
-    const int ix = (int)floor(ux), iy = (int)floor(uy), iz = (int)floor(uz);
-    const double fx = ux - ix, fy = uy - iy, fz = uz - iz;
-    const double *lvl = mips + P.mip_off[l];
+template <bool CLAMP>
+__device__ __forceinline__ double trilinear(const uint32_t *__restrict__ base, const double *__restrict__ lvl,
+                                            int l, int rl, int ix, int iy, int iz, double fx, double fy, double fz) {
     double acc = 0.0;
 #pragma unroll
     for (int dz = 0; dz < 2; dz++) {
-        const int z = min(max(iz + dz, 0), rl - 1);
+        const int z = CLAMP ? min(max(iz + dz, 0), rl - 1) : iz + dz;
         const double wz = dz ? fz : 1.0 - fz;
 #pragma unroll
         for (int dy = 0; dy < 2; dy++) {
-            const int y = min(max(iy + dy, 0), rl - 1);
+            const int y = CLAMP ? min(max(iy + dy, 0), rl - 1) : iy + dy;
             const double wy = dy ? fy : 1.0 - fy;
 #pragma unroll
             for (int dx = 0; dx < 2; dx++) {
-                const int x = min(max(ix + dx, 0), rl - 1);
+                const int x = CLAMP ? min(max(ix + dx, 0), rl - 1) : ix + dx;
                 const double wx = dx ? fx : 1.0 - fx;
-                const int64_t idx = x + (int64_t)rl * (y + (int64_t)rl * z);
+                const uint32_t idx = (uint32_t)x + (uint32_t)rl * ((uint32_t)y + (uint32_t)rl * (uint32_t)z);
                 double val;
                 if (l == 0) val = (double)min(base[idx] & 0xFFFFu, 4096u) * (1.0 / 4096.0);
                 else val = lvl[idx];
@@ -51,40 +77,57 @@ __device__ __forceinline__ double trilinear(const uint32_t *__restrict__ base, c
 
 // lv/shading.py:112-132
 __device__ __forceinline__ double cone_trace(const uint32_t *__restrict__ base, const double *__restrict__ mips,
-                                             const ShadeParams &P, double ox, double oy, double oz,
+                                             const uint32_t *__restrict__ masks, const ShadeParams &P,
+                                             double ox, double oy, double oz,
                                              double dx, double dy, double dz, double tan_half) {
     const double R = (double)P.res;
     if (ox < 0.0 || oy < 0.0 || oz < 0.0 || ox > R || oy > R || oz > R) return 0.0;
+    // while t <= t_safe the sample point is inside [1e-3, R-1e-3]^3 for certain, so the exact
+    // six-way bounds test (line 122 of the reference) cannot fire and is not evaluated
+    double t_safe = 1e30;
+    {
+        const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            if (d[a] > 0.0) t_safe = fmin(t_safe, (R - 1e-3 - o[a]) / d[a]);
+            else if (d[a] < 0.0) t_safe = fmin(t_safe, (1e-3 - o[a]) / d[a]);
+        }
+    }
     double occ = 0.0, t = 1.0;
     while (occ < 0.99) {
         const double px = ox + dx * t, py = oy + dy * t, pz = oz + dz * t;
-        if (px < 0.0 || py < 0.0 || pz < 0.0 || px > R || py > R || pz > R) break;
+        if (t > t_safe && (px < 0.0 || py < 0.0 || pz < 0.0 || px > R || py > R || pz > R)) break;
         const double diam = 2.0 * t * tan_half;
         const double step = diam > 1.0 ? diam : 1.0;
         // floor(log2(step)), step >= 1: the unbiased exponent
         int l = (int)((__double_as_longlong(step) >> 52) & 0x7ff) - 1023;
         if (l > P.n_levels - 1) l = P.n_levels - 1;
-        const double s = trilinear(base, mips, P, l, px, py, pz);
-        occ = occ + (1.0 - occ) * s;
+        const int rl = P.res >> l;
+        const double scale = __longlong_as_double((long long)(1023 - l) << 52);   // 1.0 / (1 << l), exact
+        const double ux = px * scale - 0.5, uy = py * scale - 0.5, uz = pz * scale - 0.5;
+        const int ix = (int)floor(ux), iy = (int)floor(uy), iz = (int)floor(uz);
+        const double *lvl = mips + P.mip_off[l];
+        const bool interior = ix >= 0 && iy >= 0 && iz >= 0 && ix < rl - 1 && iy < rl - 1 && iz < rl - 1;
+        if (interior) {
+            const uint32_t cell = (uint32_t)ix + (uint32_t)rl * ((uint32_t)iy + (uint32_t)rl * (uint32_t)iz);
+            if ((masks[P.mask_off[l] + (cell >> 5)] >> (cell & 31)) & 1u) {
+                const double s = trilinear<false>(base, lvl, l, rl, ix, iy, iz, ux - ix, uy - iy, uz - iz);
+                occ = occ + (1.0 - occ) * s;
+            }   // else: s == 0.0 exactly and occ is unchanged
+        } else {
+            const double s = trilinear<true>(base, lvl, l, rl, ix, iy, iz, ux - ix, uy - iy, uz - iz);
+            occ = occ + (1.0 - occ) * s;
+        }
         t += step;
     }
     return occ < 1.0 ? occ : 1.0;
 }
 
-// ao = shadow = 1 everywhere (lv/shading.py:177-178) + compaction of the visible voxels
+// ao = shadow = 1 everywhere (lv/shading.py:177-178)
 __global__ void __launch_bounds__(256)
-k_shade_prepare(const uint8_t *__restrict__ visible, int64_t V, float *__restrict__ ao, float *__restrict__ shadow,
-                uint32_t *__restrict__ list, unsigned long long *__restrict__ list_n) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane = threadIdx.x & 31;
-    const bool v = idx < V && visible[idx] != 0;
-    if (idx < V) { ao[idx] = 1.0f; shadow[idx] = 1.0f; }
-    const uint32_t m = __ballot_sync(0xffffffffu, v);
-    if (!m) return;
-    unsigned long long b = 0;
-    if (lane == 0) b = atomicAdd(list_n, (unsigned long long)__popc(m));
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (v) list[b + __popc(m & ((1u << lane) - 1u))] = (uint32_t)idx;
+k_shade_fill(int64_t n4, float4 *__restrict__ ao, float4 *__restrict__ shadow) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n4) { ao[i] = make_float4(1.f, 1.f, 1.f, 1.f); shadow[i] = make_float4(1.f, 1.f, 1.f, 1.f); }
 }
 
 // One thread per visible voxel; a warp holds 32 consecutive entries of the compacted list, i.e.
@@ -94,10 +137,11 @@ k_shade_prepare(const uint8_t *__restrict__ visible, int64_t V, float *__restric
 // wavefronts per load instead of one per lane.  The 12 AO cones are folded in cone order in a
 // register (lv/shading.py:150-152), so the f64 sum has the reference's rounding.
 __global__ void __launch_bounds__(128)
-k_shade(const uint32_t *__restrict__ base, const double *__restrict__ mips, const ShadeParams P,
-        const uint32_t *__restrict__ list, const unsigned long long *__restrict__ list_n,
+k_shade(const uint32_t *__restrict__ base, const double *__restrict__ mips,
+        const uint32_t *__restrict__ masks, const ShadeParams P, const uint32_t *__restrict__ vis_list,
         float *__restrict__ ao, float *__restrict__ shadow) {
-    const int64_t n = (int64_t)*list_n;
+    const int64_t n = (int64_t)*reinterpret_cast<const unsigned long long *>(vis_list);
+    const uint32_t *__restrict__ list = vis_list + LVX_LIST_HDR;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
         const int64_t idx = list[e];
@@ -105,8 +149,8 @@ k_shade(const uint32_t *__restrict__ base, const double *__restrict__ mips, cons
         const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
         double acc = 0.0;
         for (int c = 0; c < P.n_dirs; c++)
-            acc += P.w * cone_trace(base, mips, P, ox, oy, oz, P.dirs[c][0], P.dirs[c][1], P.dirs[c][2], P.tan_ao);
-        const double sh = cone_trace(base, mips, P, ox, oy, oz, P.shadow_dir[0], P.shadow_dir[1], P.shadow_dir[2],
+            acc += P.w * cone_trace(base, mips, masks, P, ox, oy, oz, P.dirs[c][0], P.dirs[c][1], P.dirs[c][2], P.tan_ao);
+        const double sh = cone_trace(base, mips, masks, P, ox, oy, oz, P.shadow_dir[0], P.shadow_dir[1], P.shadow_dir[2],
                                      P.tan_shadow);
         double a = 1.0 - acc, s = 1.0 - sh;
         a = a < 0.0 ? 0.0 : (a > 1.0 ? 1.0 : a);     // lv/shading.py:183-184
@@ -122,9 +166,14 @@ using namespace lvx;
 
 extern "C" {
 
-int64_t lvx_shade_scratch_bytes(int64_t n_voxels) { return 4 * n_voxels + 64; }
+// scratch: the non-empty masks of all levels
+int64_t lvx_shade_scratch_bytes(int64_t n_voxels) {
+    int64_t words = 0;
+    for (int64_t n = n_voxels; n >= 1; n /= 8) words += (n + 31) / 32;
+    return 4 * words + 64;
+}
 
-int lvx_shade(const uint32_t *base, const double *mips, int res, const uint8_t *visible,
+int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t *vis_list,
               const double *dirs_host, int n_dirs, double tan_ao, const double *light_host, double tan_shadow,
               float *ao, float *shadow, void *scratch, void *stream) {
     if (!pow2(res) || n_dirs < 1 || n_dirs > 15) return LVX_E_ARG;
@@ -136,17 +185,26 @@ int lvx_shade(const uint32_t *base, const double *mips, int res, const uint8_t *
     for (int a = 0; a < 3; a++) P.shadow_dir[a] = -light_host[a];   // lv/shading.py:154-155
     P.tan_ao = tan_ao; P.tan_shadow = tan_shadow; P.w = 1.0 / n_dirs;
     const LevelOffsets L = make_level_offsets(res);
-    for (int l = 0; l < 16; l++) P.mip_off[l] = (l >= 1 && l < L.n_levels) ? L.off[l] - L.off[1] : 0;
+    uint32_t mw = 0;
+    for (int l = 0; l < 16; l++) {
+        P.mip_off[l] = (l >= 1 && l < L.n_levels) ? (uint32_t)(L.off[l] - L.off[1]) : 0;
+        P.mask_off[l] = mw;
+        if (l < L.n_levels) mw += (uint32_t)((L.off[l + 1] - L.off[l] + 31) / 32);
+    }
     P.n_dirs = n_dirs; P.res = res; P.n_levels = L.n_levels;
-    unsigned long long *list_n = (unsigned long long *)scratch;
-    uint32_t *list = (uint32_t *)((char *)scratch + 64);
-    LVX_CUDA(cudaMemsetAsync(list_n, 0, 8, s));
-    k_shade_prepare<<<blocks_for(V, 256), 256, 0, s>>>(visible, V, ao, shadow, list, list_n);
+    if (!vis_list || V < 4) return LVX_E_ARG;
+    uint32_t *masks = (uint32_t *)scratch;
+    for (int l = 0; l < L.n_levels; l++) {
+        const int rl = res >> l;
+        k_nzmask<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(base, mips + P.mip_off[l], l, rl,
+                                                                       masks + P.mask_off[l]);
+    }
+    k_shade_fill<<<blocks_for(V / 4, 256), 256, 0, s>>>(V / 4, (float4 *)ao, (float4 *)shadow);
     // persistent grid-stride launch: 148 SMs x 16 CTAs of 128 threads
     unsigned nb = 148 * 16;
     const unsigned need = blocks_for(V, 128);
     if (nb > need) nb = need;
-    k_shade<<<nb, 128, 0, s>>>(base, mips, P, list, list_n, ao, shadow);
+    k_shade<<<nb, 128, 0, s>>>(base, mips, masks, P, vis_list, ao, shadow);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

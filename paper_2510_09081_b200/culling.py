@@ -20,7 +20,7 @@ from . import ops
 from .camera import Camera
 from .grid import GridDesc
 
-__all__ = ["Camera", "CullingPyramid", "erode", "compute_visibility", "or_mips", "THETA_BLOCK"]
+__all__ = ["Camera", "CullingPyramid", "erode", "compute_visibility", "or_mips", "occupied_bits", "THETA_BLOCK"]
 
 THETA_BLOCK = 0.999   # lv/culling.py:27 (compiled into csrc/cull.cu as occ_q >= 4092)
 
@@ -28,9 +28,9 @@ THETA_BLOCK = 0.999   # lv/culling.py:27 (compiled into csrc/cull.cu as occ_q >=
 class CullingPyramid:
     """lv/culling.py:70-100.  `flat_dev`: all levels, u8, level 0 first (== packed())."""
 
-    def __init__(self, flat_dev, resolution: int, visible=None):
+    def __init__(self, flat_dev, resolution: int, list_dev=None):
         self.flat_dev, self._res, self._levels = flat_dev, int(resolution), None
-        self.visible = visible     # number of set base bits when known
+        self.list_dev = list_dev   # compacted indices of the set base bits (include/lvx.h: vis_list)
 
     @classmethod
     def from_bits(cls, base) -> "CullingPyramid":
@@ -44,8 +44,9 @@ class CullingPyramid:
         flat[:res ** 3] = (b.to(dev) != 0).reshape(-1).to(torch.uint8)
         # reuse the device OR-mip kernels by presenting the bits as counts in packed words
         words = flat[:res ** 3].to(torch.int32) << 16
-        ops.occupied_pyramid(words, res, flat, ops.new_stats(dev))
-        return cls(flat, res)
+        vis_list = torch.empty(ops.list_words(res ** 3), dtype=torch.int32, device=dev)
+        ops.occupied_pyramid(words, res, flat, vis_list, ops.new_stats(dev))
+        return cls(flat, res, vis_list)
 
     @property
     def resolution(self) -> int:
@@ -78,6 +79,20 @@ class CullingPyramid:
         """CULP dump, byte-compatible with lv/culling.py:97-100."""
         parts = [b"CULP", struct.pack("<I", self._res)] + [l.tobytes() for l in self.levels]
         Path(path).write_bytes(b"".join(parts))
+
+
+def occupied_bits(pyramid) -> CullingPyramid:
+    """CullingPyramid.from_bits(counts > 0) straight from the packed words on the device
+    (lv/raytracer.py:665-668, lv/pipeline.py:115-116); cached on the pyramid."""
+    cached = getattr(pyramid, "_occupied_bits", None)
+    if cached is None:
+        torch = N.require_cuda()
+        res, base = pyramid.resolution, pyramid.base_dev
+        flat = torch.empty(int(ops.level_offsets(res)[-1]), dtype=torch.uint8, device=base.device)
+        vis_list = torch.empty(ops.list_words(res ** 3), dtype=torch.int32, device=base.device)
+        ops.occupied_pyramid(base, res, flat, vis_list, ops.new_stats(base.device))
+        cached = pyramid._occupied_bits = CullingPyramid(flat, res, vis_list)
+    return cached
 
 
 def or_mips(base) -> list:
@@ -129,5 +144,6 @@ def compute_visibility(eroded, g: GridDesc, cam: Camera, occupied=None) -> Culli
     solid = torch.empty(ops.cull_scratch_words(res), dtype=torch.int32, device=dev)
     vis = torch.empty(V, dtype=torch.uint8, device=dev)
     flat = torch.empty(int(ops.level_offsets(res)[-1]), dtype=torch.uint8, device=dev)
-    ops.cull(base, res, g.to_voxel(cam.position), solid, vis, flat, stats)
-    return CullingPyramid(flat, res)
+    vis_list = torch.empty(ops.list_words(V), dtype=torch.int32, device=dev)
+    ops.cull(base, res, g.to_voxel(cam.position), solid, vis, flat, vis_list, stats)
+    return CullingPyramid(flat, res, vis_list)

@@ -72,6 +72,7 @@ class FrameEngine:
         self.solid = t.empty(ops.cull_scratch_words(self.res), dtype=t.int32, device=d)
         self.vis_tmp = t.empty(V, dtype=t.uint8, device=d)
         self.cull_flat = t.empty(n_pyr, dtype=t.uint8, device=d)
+        self.vis_list = t.empty(ops.list_words(V), dtype=t.int32, device=d)
         self.offsets = t.empty(V + 1, dtype=t.int32, device=d)
         self.cursor = t.empty(V, dtype=t.int32, device=d)
         self.scan_scratch = t.empty(ops.scan_scratch_bytes(V), dtype=t.uint8, device=d)
@@ -149,9 +150,9 @@ class FrameEngine:
     def _stage_cull(self, cam):
         if self.strategy == "vcsv":
             ops.cull(self.base, self.res, self.grid.to_voxel(cam.position), self.solid, self.vis_tmp,
-                     self.cull_flat, self.stats)
+                     self.cull_flat, self.vis_list, self.stats)
         else:
-            ops.occupied_pyramid(self.base, self.res, self.cull_flat, self.stats)
+            ops.occupied_pyramid(self.base, self.res, self.cull_flat, self.vis_list, self.stats)
 
     def _stage_scan(self):
         cull_base = self.cull_flat[:self.V] if self.strategy == "vcsv" else None
@@ -160,11 +161,11 @@ class FrameEngine:
     def _stage_scatter(self):
         rt = ops.footprint_radius(self.lines.r, self.r_min)
         ops.scatter(self.lines, rt, self.res, self.method,
-                    self.cull_flat if self.strategy == "vcsv" else None,
+                    self.cull_flat if self.strategy == "vcsv" else None, self.vis_list,
                     self.offsets, self.cursor, self.frags, self.stats)
 
     def _stage_shade(self):
-        ops.shade(self.base, self.mips, self.res, self.cull_flat[:self.V], self.dirs, np.tan(AO_HALF_ANGLE),
+        ops.shade(self.base, self.mips, self.res, self.vis_list, self.dirs, np.tan(AO_HALF_ANGLE),
                   self.light, np.tan(SHADOW_HALF_ANGLE), self.ao, self.shadow, self.shade_scratch)
 
     def _stage_trace(self, cam, tile=None):

@@ -152,15 +152,19 @@ def cull_scratch_words(res: int) -> int:
     return int(lib().lvx_cull_scratch_words(res))
 
 
-def cull(base, res, cam_voxel, solid_bits, vis_tmp, cull_flat, stats):
+def list_words(n_voxels: int) -> int:
+    return int(lib().lvx_list_words(n_voxels))
+
+
+def cull(base, res, cam_voxel, solid_bits, vis_tmp, cull_flat, vis_list, stats):
     cv, cv_p = _dbl3(cam_voxel)
     check(lib().lvx_cull(_ptr(base), res, cv_p, _ptr(solid_bits), _ptr(vis_tmp), _ptr(cull_flat),
-                         _ptr(stats), _stream()), "lvx_cull")
+                         _ptr(vis_list), _ptr(stats), _stream()), "lvx_cull")
 
 
-def occupied_pyramid(base, res, cull_flat, stats):
-    check(lib().lvx_occupied_pyramid(_ptr(base), res, _ptr(cull_flat), _ptr(stats), _stream()),
-          "lvx_occupied_pyramid")
+def occupied_pyramid(base, res, cull_flat, vis_list, stats):
+    check(lib().lvx_occupied_pyramid(_ptr(base), res, _ptr(cull_flat), _ptr(vis_list), _ptr(stats),
+                                     _stream()), "lvx_occupied_pyramid")
 
 
 def scan_scratch_bytes(n_voxels: int) -> int:
@@ -172,9 +176,9 @@ def scan(base, cull_base, offsets, scratch, stats):
                          _ptr(stats), _stream()), "lvx_scan")
 
 
-def scatter(lines: DeviceLines, rt, res, method, cull_flat, offsets, cursor, frags, stats):
+def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, cursor, frags, stats):
     check(lib().lvx_scatter(_ptr(lines.verts), _ptr(lines.segs), lines.n_segments, float(rt), res,
-                            METHODS[method], _ptr(cull_flat), _ptr(offsets), _ptr(cursor), None,
+                            METHODS[method], _ptr(cull_flat), _ptr(vis_list), _ptr(offsets), _ptr(cursor),
                             _ptr(frags), frags.numel(), _ptr(stats), _stream()), "lvx_scatter")
 
 
@@ -182,10 +186,10 @@ def shade_scratch_bytes(n_voxels: int) -> int:
     return int(lib().lvx_shade_scratch_bytes(n_voxels))
 
 
-def shade(base, mips, res, visible, dirs, tan_ao, light, tan_shadow, ao, shadow, scratch):
+def shade(base, mips, res, vis_list, dirs, tan_ao, light, tan_shadow, ao, shadow, scratch):
     d = np.ascontiguousarray(dirs, dtype=np.float64)
     l, l_p = _dbl3(light)
-    check(lib().lvx_shade(_ptr(base), _ptr(mips), res, _ptr(visible), d.ctypes.data_as(C.c_void_p),
+    check(lib().lvx_shade(_ptr(base), _ptr(mips), res, _ptr(vis_list), d.ctypes.data_as(C.c_void_p),
                           int(d.shape[0]), float(tan_ao), l_p, float(tan_shadow), _ptr(ao), _ptr(shadow),
                           _ptr(scratch), _stream()), "lvx_shade")
 

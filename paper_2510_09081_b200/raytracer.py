@@ -112,12 +112,8 @@ class RenderScene:
         if self.culling is not None:
             return self.culling
         if self._march is None:
-            torch = N.require_cuda()
-            res = self.g.resolution
-            base = self.pyramid.base_dev
-            flat = torch.empty(int(ops.level_offsets(res)[-1]), dtype=torch.uint8, device=base.device)
-            ops.occupied_pyramid(base, res, flat, ops.new_stats(base.device))
-            self._march = CullingPyramid(flat, res)
+            from .culling import occupied_bits
+            self._march = occupied_bits(self.pyramid)
         return self._march
 
 

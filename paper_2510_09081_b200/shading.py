@@ -65,6 +65,9 @@ def compute_shading(pyramid, culling, g, light_dir) -> ShadingVolume:
     ao = torch.empty(V, dtype=torch.float32, device=dev)
     sh = torch.empty(V, dtype=torch.float32, device=dev)
     scratch = torch.empty(ops.shade_scratch_bytes(V), dtype=torch.uint8, device=dev)
-    ops.shade(pyramid.base_dev, pyramid.mips_dev, res, culling.base_dev, cone_directions(),
+    if culling.list_dev is None:
+        from .culling import CullingPyramid
+        culling = CullingPyramid.from_bits(culling.base_dev.reshape(res, res, res))
+    ops.shade(pyramid.base_dev, pyramid.mips_dev, res, culling.list_dev, cone_directions(),
               np.tan(AO_HALF_ANGLE), light, np.tan(SHADOW_HALF_ANGLE), ao, sh, scratch)
     return ShadingVolume(ao, sh, light, res)
