@@ -118,7 +118,7 @@ class ClockSampler:
 
 def algorithmic_bytes(stats, n_verts, V, pixels):
     """compulsory streams + one 4-byte read-modify-write per atomic."""
-    I, F, T, Vv = stats["voxels_visited"], stats["fragments"], stats["ray_capsule_tests"], stats["visible_voxels"]
+    I, F, T, Vv = stats["voxels_visited"], stats["fragments"], stats["ray_capsule_tests"], stats["shaded_voxels"]
     return {
         "upload": 12 * n_verts + 48 * n_verts,              # f32 in, f64 voxel-unit verts + f64 normals out
         "voxelize": 12 * n_verts + 4 * V + 8 * I,
@@ -233,7 +233,7 @@ def run_gpu(args):
         "stages_ms": {s: round(v, 4) for s, v in stage_ms.items()},
         "frame_stats": {k: last.stats[k] for k in ("voxels_visited", "fragments", "occupied_voxels", "visible_voxels",
                                                    "solid_voxels", "ray_capsule_tests", "culled_fraction", "long_lists",
-                                                   "wide_path")},
+                                                   "wide_path", "shaded_voxels", "shading")},
         "e2e": {"value": round(fps_e2e, 3), "unit": "frames/s", "ms_per_step": round(ms_e2e / args.steps, 4),
                 "h2d_bytes_per_step": int(host[0].numel() * 4),
                 "d2h_bytes_per_step": int(out_srgb.numel() + out_hit.numel() * 4 + 128)},

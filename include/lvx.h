@@ -151,12 +151,13 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
 
 /* ---- shading: lv/shading.py:72-155 _trilinear/_cone_trace/_shading_kernel, 170-185.
  * dirs_host: n_dirs*3 unit vectors (lv/shading.py:32-40); light_host: unit light direction.
- * ao/shadow: V f32, 1.0 where not visible.  n_dirs <= 15.  scratch: lvx_shade_scratch_bytes(V)
+ * ao/shadow: V f32; with fill_ones != 0 every voxel not in vis_list is set to 1.0 (the reference's
+ * volumes), with 0 only listed voxels are written (shading on demand, see lvx_trace_hits).  n_dirs <= 15.  scratch: lvx_shade_scratch_bytes(V)
  * (per-level non-empty masks). */
 int64_t lvx_shade_scratch_bytes(int64_t n_voxels);
 int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t *vis_list,
               const double *dirs_host, int n_dirs, double tan_ao, const double *light_host,
-              double tan_shadow, float *ao, float *shadow, void *scratch, void *stream);
+              double tan_shadow, float *ao, float *shadow, int fill_ones, void *scratch, void *stream);
 
 /* ---- render: lv/raytracer.py:459-515 _opaque_kernel, 518-645 _transparent_kernel, 94-97 _to_srgb.
  * rgb: h*w*3 f64 linear (may be NULL), srgb: h*w*3 u8 (may be NULL), hit_id: h*w i32. */
@@ -164,6 +165,22 @@ int lvx_render(const double *verts, const double *normals, const uint32_t *offse
                const uint8_t *bits_flat, int res, const float *ao, const float *shadow,
                const lvx_camera *cam_host, const lvx_render_params *params_host,
                double *rgb, uint8_t *srgb, int32_t *hit_id, uint64_t *stats, void *stream);
+
+/* ---- shading on demand (opaque mode).  Same image as lvx_shade(all visible) + lvx_render, but AO and
+ * shadow are cone-traced only for the voxels some pixel's hit actually interpolates:
+ *   lvx_trace_hits  first hit per pixel (hit_t f64 h*w, < 0 = miss; hit_id) + need_list = visible
+ *                   voxels among the 8 trilinear taps of every hit (lv/raytracer.py:368-390);
+ *                   need_bits: V/32 u32 scratch; need_list: lvx_list_words(V) u32
+ *   lvx_shade       with vis_list = need_list, fill_ones = 0
+ *   lvx_resolve     normal + colour per hit pixel (lv/raytracer.py:486-502), reading ao/shadow only
+ *                   where bits_flat marks the voxel visible (1.0 elsewhere, lv/shading.py:177-178) */
+int lvx_trace_hits(const double *verts, const double *normals, const uint32_t *offsets, const uint32_t *frags,
+                   const uint8_t *bits_flat, int res, const lvx_camera *cam_host,
+                   const lvx_render_params *params_host, double *hit_t, int32_t *hit_id, uint32_t *need_bits,
+                   uint32_t *need_list, uint64_t *stats, void *stream);
+int lvx_resolve(const double *verts, const double *normals, const uint8_t *bits_flat, int res, const float *ao,
+                const float *shadow, const lvx_camera *cam_host, const lvx_render_params *params_host,
+                const double *hit_t, const int32_t *hit_id, double *rgb, uint8_t *srgb, void *stream);
 
 #ifdef __cplusplus
 }

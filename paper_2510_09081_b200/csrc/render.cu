@@ -20,6 +20,11 @@ struct RenderArgs {
     uint8_t *srgb;
     int32_t *hit_id;
     uint64_t *stats;
+    // shading on demand (lvx_trace_hits / lvx_resolve)
+    double *hit_t;           // per pixel: t of the first hit, < 0 = miss
+    uint32_t *need_bits;     // V/32 words: voxels whose AO/shadow some hit pixel interpolates
+    uint32_t *need_list;     // compacted list of those voxels (list layout of lvx_device.cuh)
+    int guard_volumes;       // ao/sh hold values only where requested: read 1.0 where bits[] == 0
 };
 
 __device__ __forceinline__ bool clip_ok(const Capsule &c, double px, double py, double pz) {
@@ -202,7 +207,8 @@ __device__ __forceinline__ int empty_level(const RenderArgs &A, int x, int y, in
 }
 
 // lv/raytracer.py:368-390 (volumes are f32, widened exactly like the reference's astype(f64))
-__device__ __forceinline__ double tri3d(const float *__restrict__ vol, int res, double px, double py, double pz) {
+__device__ __forceinline__ double tri3d(const float *__restrict__ vol, const uint8_t *__restrict__ guard, int res,
+                                        double px, double py, double pz) {
     const double ux = px - 0.5, uy = py - 0.5, uz = pz - 0.5;
     const int ix = (int)floor(ux), iy = (int)floor(uy), iz = (int)floor(uz);
     const double fx = ux - ix, fy = uy - iy, fz = uz - iz;
@@ -219,7 +225,10 @@ __device__ __forceinline__ double tri3d(const float *__restrict__ vol, int res, 
             for (int dx = 0; dx < 2; dx++) {
                 const int x = min(max(ix + dx, 0), res - 1);
                 const double wx = dx ? fx : 1.0 - fx;
-                acc += wx * wy * wz * (double)vol[x + (int64_t)res * (y + (int64_t)res * z)];
+                const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
+                // non-visible voxels keep ao = shadow = 1 (lv/shading.py:177-178)
+                const double val = (guard && guard[idx] == 0) ? 1.0 : (double)vol[idx];
+                acc += wx * wy * wz * val;
             }
         }
     }
@@ -233,8 +242,9 @@ __device__ __forceinline__ void shade(const RenderArgs &A, const Capsule &c, dou
     const double sn = sqrt(sx * sx + sy * sy + sz * sz);
     if (sn == 0.0) { cr = cg = cb = 0.5; }
     else { cr = fabs(sx) / sn; cg = fabs(sy) / sn; cb = fabs(sz) / sn; }
-    const double ao = A.ao ? tri3d(A.ao, A.res, px, py, pz) : 1.0;
-    const double sh = A.sh ? tri3d(A.sh, A.res, px, py, pz) : 1.0;
+    const uint8_t *guard = A.guard_volumes ? A.bits : nullptr;
+    const double ao = A.ao ? tri3d(A.ao, guard, A.res, px, py, pz) : 1.0;
+    const double sh = A.sh ? tri3d(A.sh, guard, A.res, px, py, pz) : 1.0;
     double ndl = nx * A.p.light_to_source[0] + ny * A.p.light_to_source[1] + nz * A.p.light_to_source[2];
     if (ndl < 0.0) ndl = 0.0;
     const double k = 0.4 * ao + 0.6 * sh * ndl;
@@ -451,7 +461,11 @@ struct WarpShared {
     uint32_t hit_s[32], hit_i[32];
 };
 
-__global__ void __launch_bounds__(RC_WARPS * 32)
+#ifndef LVX_RC_MINB
+#define LVX_RC_MINB 6
+#endif
+template <bool DEFER>
+__global__ void __launch_bounds__(RC_WARPS * 32, LVX_RC_MINB)
 k_render_opaque_coop(const RenderArgs A) {
     __shared__ WarpShared sh_all[RC_WARPS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -623,29 +637,115 @@ k_render_opaque_coop(const RenderArgs A) {
         __syncwarp();
     }
 
-    if (live) {
-        double out_r = A.p.background[0], out_g = A.p.background[1], out_b = A.p.background[2];
-        int32_t out_id = -1;
-        if (best_t >= 0.0) {
-            const double hx = ox + dx * best_t, hy = oy + dy * best_t, hz = oz + dz * best_t;
-            const Capsule c = load_capsule(A.verts, A.normals, best_i, r, clip);
-            double nx, ny, nz;
-            capsule_normal(hx, hy, hz, c, nx, ny, nz);
-            shade(A, c, nx, ny, nz, hx, hy, hz, out_r, out_g, out_b);
-            out_id = (int32_t)best_i;
+    if (!DEFER) {
+        if (live) {
+            double out_r = A.p.background[0], out_g = A.p.background[1], out_b = A.p.background[2];
+            int32_t out_id = -1;
+            if (best_t >= 0.0) {
+                const double hx = ox + dx * best_t, hy = oy + dy * best_t, hz = oz + dz * best_t;
+                const Capsule c = load_capsule(A.verts, A.normals, best_i, r, clip);
+                double nx, ny, nz;
+                capsule_normal(hx, hy, hz, c, nx, ny, nz);
+                shade(A, c, nx, ny, nz, hx, hy, hz, out_r, out_g, out_b);
+                out_id = (int32_t)best_i;
+            }
+            const int64_t pix = (int64_t)py * w + px;
+            if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
+            if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
+            A.hit_id[pix] = out_id;
         }
-        const int64_t pix = (int64_t)py * w + px;
-        if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
-        if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
-        A.hit_id[pix] = out_id;
+    } else {
+        // Shading on demand: record the hit, and request AO/shadow for the (visible) voxels its
+        // trilinear lookup will read (lv/raytracer.py:368-390).  New requests are gathered per
+        // block in shared memory so the global list counter sees one atomic per block.
+        __shared__ uint32_t s_cnt, s_base;
+        __shared__ uint32_t s_items[RC_WARPS * 32 * 8];
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        if (live) {
+            const int64_t pix = (int64_t)py * w + px;
+            A.hit_t[pix] = best_t;
+            A.hit_id[pix] = best_t >= 0.0 ? (int32_t)best_i : -1;
+            if (best_t >= 0.0) {
+                const double hx = ox + dx * best_t, hy = oy + dy * best_t, hz = oz + dz * best_t;
+                const int ix = (int)floor(hx - 0.5), iy = (int)floor(hy - 0.5), iz = (int)floor(hz - 0.5);
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const int X = min(max(ix + (k & 1), 0), res - 1);
+                    const int Y = min(max(iy + ((k >> 1) & 1), 0), res - 1);
+                    const int Z = min(max(iz + (k >> 2), 0), res - 1);
+                    const uint32_t idx = (uint32_t)X + (uint32_t)res * ((uint32_t)Y + (uint32_t)res * (uint32_t)Z);
+                    if (A.bits[idx] != 0) {
+                        const uint32_t bit = 1u << (idx & 31);
+                        if ((atomicOr(&A.need_bits[idx >> 5], bit) & bit) == 0) s_items[atomicAdd(&s_cnt, 1u)] = idx;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t cnt = s_cnt;
+        if (threadIdx.x == 0 && cnt)
+            s_base = (uint32_t)atomicAdd(reinterpret_cast<unsigned long long *>(A.need_list), (unsigned long long)cnt);
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) A.need_list[LVX_LIST_HDR + s_base + i] = s_items[i];
     }
     if (lane == 0 && n_tests)
         atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)n_tests);
 }
 
+// Second half of shading on demand: one thread per pixel re-derives its ray (same expressions,
+// hence the same bits, as the trace kernel), and shades the recorded hit.
+__global__ void __launch_bounds__(128)
+k_resolve(const RenderArgs A) {
+    const int px = A.p.tile_x0 + blockIdx.x * 32 + (threadIdx.x & 31);
+    const int py = A.p.tile_y0 + blockIdx.y * 4 + (threadIdx.x >> 5);
+    if (px >= A.p.tile_x1 || py >= A.p.tile_y1) return;
+    const int w = A.cam.width, h = A.cam.height;
+    const int64_t pix = (int64_t)py * w + px;
+    double out_r = A.p.background[0], out_g = A.p.background[1], out_b = A.p.background[2];
+    const double best_t = A.hit_t[pix];
+    if (best_t >= 0.0) {
+        const double aspect = (double)w / (double)h;
+        const double u = (2.0 * (px + 0.5) / w - 1.0) * aspect * A.cam.tan_half_fov;
+        const double v = (1.0 - 2.0 * (py + 0.5) / h) * A.cam.tan_half_fov;
+        double dx = A.cam.fwd[0] + u * A.cam.right[0] + v * A.cam.up[0];
+        double dy = A.cam.fwd[1] + u * A.cam.right[1] + v * A.cam.up[1];
+        double dz = A.cam.fwd[2] + u * A.cam.right[2] + v * A.cam.up[2];
+        const double dn = sqrt(dx * dx + dy * dy + dz * dz);
+        dx = dx / dn; dy = dy / dn; dz = dz / dn;
+        const double hx = A.cam.pos[0] + dx * best_t, hy = A.cam.pos[1] + dy * best_t, hz = A.cam.pos[2] + dz * best_t;
+        const Capsule c = load_capsule(A.verts, A.normals, (int64_t)A.hit_id[pix], A.p.radius, A.p.use_clip != 0);
+        double nx, ny, nz;
+        capsule_normal(hx, hy, hz, c, nx, ny, nz);
+        shade(A, c, nx, ny, nz, hx, hy, hz, out_r, out_g, out_b);
+    }
+    if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
+    if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
+}
+
 }  // namespace lvx
 
 using namespace lvx;
+
+static int fill_args(RenderArgs &A, const double *verts, const double *normals, const uint32_t *offsets,
+                     const uint32_t *frags, const uint8_t *bits_flat, int res, const float *ao, const float *shadow,
+                     const lvx_camera *cam_host, const lvx_render_params *params_host, double *rgb, uint8_t *srgb,
+                     int32_t *hit_id, uint64_t *stats) {
+    if (!pow2(res) || !cam_host || !params_host || !hit_id) return LVX_E_ARG;
+    const lvx_render_params &p = *params_host;
+    if (p.mode < 0 || p.mode > 1 || p.k < 1 || p.k > 64 || !(p.alpha > 0.0 && p.alpha <= 1.0)) return LVX_E_ARG;
+    if (cam_host->width <= 0 || cam_host->height <= 0) return LVX_E_ARG;
+    if (p.tile_x0 < 0 || p.tile_y0 < 0 || p.tile_x1 > cam_host->width || p.tile_y1 > cam_host->height) return LVX_E_ARG;
+    if (p.use_clip && !normals) return LVX_E_ARG;
+    A.verts = verts; A.normals = normals; A.offsets = offsets; A.frags = frags; A.bits = bits_flat;
+    A.ao = ao; A.sh = shadow;
+    const LevelOffsets L = make_level_offsets(res);
+    for (int l = 0; l < 16; l++) A.bits_off[l] = l < L.n_levels ? (uint32_t)L.off[l] : 0;
+    A.res = res; A.n_levels = L.n_levels; A.cam = *cam_host; A.p = p;
+    A.rgb = rgb; A.srgb = srgb; A.hit_id = hit_id; A.stats = stats;
+    A.hit_t = nullptr; A.need_bits = nullptr; A.need_list = nullptr; A.guard_volumes = 0;
+    return LVX_OK;
+}
 
 extern "C" {
 
@@ -653,27 +753,59 @@ int lvx_render(const double *verts, const double *normals, const uint32_t *offse
                const uint8_t *bits_flat, int res, const float *ao, const float *shadow,
                const lvx_camera *cam_host, const lvx_render_params *params_host, double *rgb, uint8_t *srgb,
                int32_t *hit_id, uint64_t *stats, void *stream) {
-    if (!pow2(res) || !cam_host || !params_host || !hit_id) return LVX_E_ARG;
-    const lvx_render_params &p = *params_host;
-    if (p.mode < 0 || p.mode > 1 || p.k < 1 || p.k > 64 || !(p.alpha > 0.0 && p.alpha <= 1.0)) return LVX_E_ARG;
-    if (cam_host->width <= 0 || cam_host->height <= 0) return LVX_E_ARG;
-    if (p.tile_x0 < 0 || p.tile_y0 < 0 || p.tile_x1 > cam_host->width || p.tile_y1 > cam_host->height) return LVX_E_ARG;
-    if (p.use_clip && !normals) return LVX_E_ARG;
-    const int tw = p.tile_x1 - p.tile_x0, th = p.tile_y1 - p.tile_y0;
-    if (tw <= 0 || th <= 0) return LVX_OK;
     RenderArgs A;
-    A.verts = verts; A.normals = normals; A.offsets = offsets; A.frags = frags; A.bits = bits_flat;
-    A.ao = ao; A.sh = shadow;
-    const LevelOffsets L = make_level_offsets(res);
-    for (int l = 0; l < 16; l++) A.bits_off[l] = l < L.n_levels ? (uint32_t)L.off[l] : 0;
-    A.res = res; A.n_levels = L.n_levels; A.cam = *cam_host; A.p = p;
-    A.rgb = rgb; A.srgb = srgb; A.hit_id = hit_id; A.stats = stats;
-    const dim3 grid((tw + 7) / 8, (th + 15) / 16);
-    if (p.mode == 0) {
+    const int rc = fill_args(A, verts, normals, offsets, frags, bits_flat, res, ao, shadow, cam_host, params_host,
+                             rgb, srgb, hit_id, stats);
+    if (rc != LVX_OK) return rc;
+    const int tw = A.p.tile_x1 - A.p.tile_x0, th = A.p.tile_y1 - A.p.tile_y0;
+    if (tw <= 0 || th <= 0) return LVX_OK;
+    if (A.p.mode == 0) {
         const dim3 cgrid((tw + 8 * RC_WARPS - 1) / (8 * RC_WARPS), (th + 3) / 4);
-        k_render_opaque_coop<<<cgrid, RC_WARPS * 32, 0, (cudaStream_t)stream>>>(A);
+        k_render_opaque_coop<false><<<cgrid, RC_WARPS * 32, 0, (cudaStream_t)stream>>>(A);
+    } else {
+        const dim3 grid((tw + 7) / 8, (th + 15) / 16);
+        k_render<1><<<grid, 128, 0, (cudaStream_t)stream>>>(A);
     }
-    else k_render<1><<<grid, 128, 0, (cudaStream_t)stream>>>(A);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_trace_hits(const double *verts, const double *normals, const uint32_t *offsets, const uint32_t *frags,
+                   const uint8_t *bits_flat, int res, const lvx_camera *cam_host,
+                   const lvx_render_params *params_host, double *hit_t, int32_t *hit_id, uint32_t *need_bits,
+                   uint32_t *need_list, uint64_t *stats, void *stream) {
+    RenderArgs A;
+    const int rc = fill_args(A, verts, normals, offsets, frags, bits_flat, res, nullptr, nullptr, cam_host,
+                             params_host, nullptr, nullptr, hit_id, stats);
+    if (rc != LVX_OK) return rc;
+    if (A.p.mode != 0 || !hit_t || !need_bits || !need_list) return LVX_E_ARG;
+    const int tw = A.p.tile_x1 - A.p.tile_x0, th = A.p.tile_y1 - A.p.tile_y0;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t V = (int64_t)res * res * res;
+    LVX_CUDA(cudaMemsetAsync(need_bits, 0, (size_t)((V + 31) / 32) * 4, s));
+    LVX_CUDA(cudaMemsetAsync(need_list, 0, 8, s));
+    if (tw <= 0 || th <= 0) return LVX_OK;
+    A.hit_t = hit_t; A.need_bits = need_bits; A.need_list = need_list;
+    const dim3 cgrid((tw + 8 * RC_WARPS - 1) / (8 * RC_WARPS), (th + 3) / 4);
+    k_render_opaque_coop<true><<<cgrid, RC_WARPS * 32, 0, s>>>(A);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_resolve(const double *verts, const double *normals, const uint8_t *bits_flat, int res, const float *ao,
+                const float *shadow, const lvx_camera *cam_host, const lvx_render_params *params_host,
+                const double *hit_t, const int32_t *hit_id, double *rgb, uint8_t *srgb, void *stream) {
+    RenderArgs A;
+    const int rc = fill_args(A, verts, normals, nullptr, nullptr, bits_flat, res, ao, shadow, cam_host, params_host,
+                             rgb, srgb, const_cast<int32_t *>(hit_id), nullptr);
+    if (rc != LVX_OK) return rc;
+    if (!hit_t) return LVX_E_ARG;
+    const int tw = A.p.tile_x1 - A.p.tile_x0, th = A.p.tile_y1 - A.p.tile_y0;
+    if (tw <= 0 || th <= 0) return LVX_OK;
+    A.hit_t = const_cast<double *>(hit_t);
+    A.guard_volumes = 1;
+    const dim3 grid((tw + 31) / 32, (th + 3) / 4);
+    k_resolve<<<grid, 128, 0, (cudaStream_t)stream>>>(A);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -175,7 +175,7 @@ int64_t lvx_shade_scratch_bytes(int64_t n_voxels) {
 
 int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t *vis_list,
               const double *dirs_host, int n_dirs, double tan_ao, const double *light_host, double tan_shadow,
-              float *ao, float *shadow, void *scratch, void *stream) {
+              float *ao, float *shadow, int fill_ones, void *scratch, void *stream) {
     if (!pow2(res) || n_dirs < 1 || n_dirs > 15) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
@@ -199,7 +199,7 @@ int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t 
         k_nzmask<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(base, mips + P.mip_off[l], l, rl,
                                                                        masks + P.mask_off[l]);
     }
-    k_shade_fill<<<blocks_for(V / 4, 256), 256, 0, s>>>(V / 4, (float4 *)ao, (float4 *)shadow);
+    if (fill_ones) k_shade_fill<<<blocks_for(V / 4, 256), 256, 0, s>>>(V / 4, (float4 *)ao, (float4 *)shadow);
     // persistent grid-stride launch: 148 SMs x 16 CTAs of 128 threads
     unsigned nb = 148 * 16;
     const unsigned need = blocks_for(V, 128);

@@ -46,12 +46,21 @@ class FrameResult:
 class FrameEngine:
     def __init__(self, res: int, width: int, height: int, strategy="vcsv", mode="opaque", alpha=1.0, k=8,
                  method="capsule", r_min=0.5, light=(-0.5, -0.3, -0.8), clip=True, keep_rgb=False,
-                 early_termination=True, background=(0.1, 0.1, 0.12), device=None, frag_capacity=0):
+                 early_termination=True, background=(0.1, 0.1, 0.12), device=None, frag_capacity=0,
+                 shading="auto"):
         torch = N.require_cuda()
         if strategy not in ("vsv", "vcsv"):
             raise ValueError("strategy must be vsv or vcsv")
         if method not in ops.METHODS:
             raise ValueError(f"unknown voxelization method {method!r}")
+        if shading not in ("auto", "demand", "all"):
+            raise ValueError("shading must be auto, demand or all")
+        # "demand": AO/shadow are cone-traced only for voxels a hit pixel interpolates (opaque mode;
+        # identical image, `ao`/`shadow` then hold values only at those voxels).  "all": every
+        # visible voxel, like lv/shading.py:170-185.  "auto" = demand for opaque, all for transparent.
+        self.shading = ("demand" if mode == "opaque" else "all") if shading == "auto" else shading
+        if self.shading == "demand" and mode != "opaque":
+            raise ValueError("shading on demand needs opaque mode")
         self.torch = torch
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.res, self.w, self.h = int(res), int(width), int(height)
@@ -83,12 +92,16 @@ class FrameEngine:
         self.srgb = t.empty((self.h, self.w, 3), dtype=t.uint8, device=d)
         self.hit_id = t.empty((self.h, self.w), dtype=t.int32, device=d)
         self.frags = t.empty(max(int(frag_capacity), 1), dtype=t.int32, device=d)
+        if self.shading == "demand":
+            self.hit_t = t.empty((self.h, self.w), dtype=t.float64, device=d)
+            self.need_bits = t.empty(max(V // 32, 1), dtype=t.int32, device=d)
+            self.need_list = t.empty(ops.list_words(V), dtype=t.int32, device=d)
         self.wide = None
         self.use_wide = False
         self.lines = None
         self.grid = None
         self._verts32 = self._poly_off = None
-        self._ev = [t.cuda.Event(enable_timing=True) for _ in range(len(STAGES) + 1)]
+        self._ev = [t.cuda.Event(enable_timing=True) for _ in range(len(STAGES) + 3)]
         self.launches_per_frame = 0
 
     # ------------------------------------------------------------------ line set
@@ -165,13 +178,26 @@ class FrameEngine:
                     self.offsets, self.cursor, self.frags, self.stats)
 
     def _stage_shade(self):
-        ops.shade(self.base, self.mips, self.res, self.vis_list, self.dirs, np.tan(AO_HALF_ANGLE),
-                  self.light, np.tan(SHADOW_HALF_ANGLE), self.ao, self.shadow, self.shade_scratch)
+        demand = self.shading == "demand"
+        ops.shade(self.base, self.mips, self.res, self.need_list if demand else self.vis_list, self.dirs,
+                  np.tan(AO_HALF_ANGLE), self.light, np.tan(SHADOW_HALF_ANGLE), self.ao, self.shadow,
+                  self.shade_scratch, fill_ones=not demand)
 
     def _stage_trace(self, cam, tile=None):
         p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
         ops.render(self.lines, self.offsets, self.frags, self.cull_flat, self.res, self.ao, self.shadow,
                    ops.make_camera_struct(cam, self.grid), p, self.rgb, self.srgb, self.hit_id, self.stats)
+
+    def _stage_trace_hits(self, cam, tile=None):
+        p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
+        ops.trace_hits(self.lines, self.offsets, self.frags, self.cull_flat, self.res,
+                       ops.make_camera_struct(cam, self.grid), p, self.hit_t, self.hit_id, self.need_bits,
+                       self.need_list, self.stats)
+
+    def _stage_resolve(self, cam, tile=None):
+        p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
+        ops.resolve(self.lines, self.cull_flat, self.res, self.ao, self.shadow,
+                    ops.make_camera_struct(cam, self.grid), p, self.hit_t, self.hit_id, self.rgb, self.srgb)
 
     # ------------------------------------------------------------------ frame
     def _ensure_capacity(self, need: int):
@@ -203,8 +229,13 @@ class FrameEngine:
                 self._ensure_capacity(int(self.stats[N.ST_FRAG_TOTAL].item()))
                 first = False
             self._stage_scatter(); ev[6].record()
-            self._stage_shade(); ev[7].record()
-            self._stage_trace(cam, tile); ev[8].record()
+            if self.shading == "demand":
+                self._stage_trace_hits(cam, tile); ev[7].record()
+                self._stage_shade(); ev[8].record()
+                self._stage_resolve(cam, tile); ev[9].record()
+            else:
+                self._stage_shade(); ev[7].record()
+                self._stage_trace(cam, tile); ev[8].record()
             st = self.stats.cpu().numpy()          # the frame's only mandatory sync
             if st[N.ST_NEED_WIDE] and not self.use_wide:
                 self.use_wide = True               # a 16-bit count wrapped: exact 64-bit path from now on
@@ -225,6 +256,12 @@ class FrameEngine:
             raise ABufferError("fragment count mismatch between passes (nondeterministic traversal?)")
         out = FrameResult(self)
         out.stage_ms = {s: ev[i].elapsed_time(ev[i + 1]) for i, s in enumerate(STAGES)}
+        if self.shading == "demand":   # events 6..9 bracket trace_hits, shade, resolve
+            out.stage_ms["trace"] = ev[6].elapsed_time(ev[7]) + ev[8].elapsed_time(ev[9])
+            out.stage_ms["shade"] = ev[7].elapsed_time(ev[8])
+            shaded = int(self.need_list[:2].cpu().numpy().view(np.uint64)[0])
+        else:
+            shaded = int(st[N.ST_VISIBLE])
         occ = int(st[N.ST_OCCUPIED])
         out.stats = {
             "segments": self.lines.n_segments, "vertices": self.lines.n_vertices, "resolution": self.res,
@@ -234,5 +271,6 @@ class FrameEngine:
             "culled_fraction": (1.0 - int(st[N.ST_VISIBLE]) / occ) if (self.strategy == "vcsv" and occ) else 0.0,
             "ray_capsule_tests": int(st[N.ST_RAY_TESTS]), "long_lists": int(st[N.ST_LONG_LISTS]),
             "occ_saturated_voxels": int(st[N.ST_OCC_SAT]), "wide_path": bool(self.use_wide),
+            "shaded_voxels": shaded, "shading": self.shading,
         }
         return out

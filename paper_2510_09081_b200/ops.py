@@ -186,12 +186,12 @@ def shade_scratch_bytes(n_voxels: int) -> int:
     return int(lib().lvx_shade_scratch_bytes(n_voxels))
 
 
-def shade(base, mips, res, vis_list, dirs, tan_ao, light, tan_shadow, ao, shadow, scratch):
+def shade(base, mips, res, vis_list, dirs, tan_ao, light, tan_shadow, ao, shadow, scratch, fill_ones=True):
     d = np.ascontiguousarray(dirs, dtype=np.float64)
     l, l_p = _dbl3(light)
     check(lib().lvx_shade(_ptr(base), _ptr(mips), res, _ptr(vis_list), d.ctypes.data_as(C.c_void_p),
                           int(d.shape[0]), float(tan_ao), l_p, float(tan_shadow), _ptr(ao), _ptr(shadow),
-                          _ptr(scratch), _stream()), "lvx_shade")
+                          int(bool(fill_ones)), _ptr(scratch), _stream()), "lvx_shade")
 
 
 def make_camera_struct(cam, grid) -> N.lvx_camera:
@@ -210,3 +210,16 @@ def render(lines: DeviceLines, offsets, frags, bits_flat, res, ao, shadow, cam_s
     check(lib().lvx_render(_ptr(lines.verts), _ptr(lines.normals), _ptr(offsets), _ptr(frags), _ptr(bits_flat),
                            res, _ptr(ao), _ptr(shadow), C.byref(cam_struct), C.byref(params), _ptr(rgb),
                            _ptr(srgb), _ptr(hit_id), _ptr(stats), _stream()), "lvx_render")
+
+
+def trace_hits(lines: DeviceLines, offsets, frags, bits_flat, res, cam_struct, params, hit_t, hit_id, need_bits,
+               need_list, stats):
+    check(lib().lvx_trace_hits(_ptr(lines.verts), _ptr(lines.normals), _ptr(offsets), _ptr(frags), _ptr(bits_flat),
+                               res, C.byref(cam_struct), C.byref(params), _ptr(hit_t), _ptr(hit_id),
+                               _ptr(need_bits), _ptr(need_list), _ptr(stats), _stream()), "lvx_trace_hits")
+
+
+def resolve(lines: DeviceLines, bits_flat, res, ao, shadow, cam_struct, params, hit_t, hit_id, rgb, srgb):
+    check(lib().lvx_resolve(_ptr(lines.verts), _ptr(lines.normals), _ptr(bits_flat), res, _ptr(ao), _ptr(shadow),
+                            C.byref(cam_struct), C.byref(params), _ptr(hit_t), _ptr(hit_id), _ptr(rgb), _ptr(srgb),
+                            _stream()), "lvx_resolve")

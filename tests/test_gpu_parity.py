@@ -129,7 +129,7 @@ def test_random_scenes_vs_oracle(lvx, oracle, seed, res, r):
     cfg = lvx.PipelineConfig(res=res, width=96, height=80, strategy="vcsv", cam_azimuth=10.0 * seed)
     cam = lvx.make_camera(cfg, g)
     ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vcsv")
-    eng = lvx.FrameEngine(res, 96, 80, strategy="vcsv", keep_rgb=True)
+    eng = lvx.FrameEngine(res, 96, 80, strategy="vcsv", keep_rgb=True, shading="all")
     eng.set_topology(ls.polyline_offsets, ls.n_vertices)
     eng.load_vertices(ls.vertices)
     out = eng.run(cam, g, r_world)
@@ -145,6 +145,31 @@ def test_random_scenes_vs_oracle(lvx, oracle, seed, res, r):
     assert np.array_equal(eng.rgb.cpu().numpy(), ref.image.rgb)
     assert out.stats["ray_capsule_tests"] == ref.image.stats["ray_capsule_tests"]
     assert out.stats["voxels_visited"] == ref.pyramid.visited
+
+
+@pytest.mark.parametrize("seed,res,r,strategy", [(3, 32, 0.4, "vcsv"), (6, 64, 0.2, "vsv"), (9, 64, 0.9, "vcsv")])
+def test_shading_on_demand_same_image(lvx, oracle, seed, res, r, strategy):
+    """FrameEngine's default for opaque frames: AO/shadow only where a hit pixel reads them."""
+    ls = lvx.generate("random_streamlines", seed=seed, polylines=50, verts_per_line=40)
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=r)
+    cfg = lvx.PipelineConfig(res=res, width=112, height=72, strategy=strategy, cam_elevation=5.0 * seed)
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy=strategy)
+    eng = lvx.FrameEngine(res, 112, 72, strategy=strategy, keep_rgb=True)
+    assert eng.shading == "demand"
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    eng.load_vertices(ls.vertices)
+    out = eng.run(cam, g, r_world)
+    assert np.array_equal(eng.hit_id.cpu().numpy(), ref.image.hit_id)
+    assert np.array_equal(eng.rgb.cpu().numpy(), ref.image.rgb)
+    assert np.array_equal(eng.srgb.cpu().numpy(), ref.image.srgb)
+    assert out.stats["ray_capsule_tests"] == ref.image.stats["ray_capsule_tests"]
+    # the requested voxels carry the oracle's values; fewer voxels were shaded than are visible
+    n = out.stats["shaded_voxels"]
+    idx = eng.need_list.cpu().numpy().view(np.uint32)[16:16 + n].astype(np.int64)
+    assert len(np.unique(idx)) == n and 0 < n <= out.stats["visible_voxels"]
+    assert np.array_equal(eng.ao.cpu().numpy()[idx], ref.shading.ao.ravel()[idx])
+    assert np.array_equal(eng.shadow.cpu().numpy()[idx], ref.shading.shadow.ravel()[idx])
 
 
 def test_transparent_engine_vs_oracle(lvx, oracle):
