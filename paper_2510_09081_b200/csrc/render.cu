@@ -693,6 +693,261 @@ k_render_opaque_coop(const RenderArgs A) {
         atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)n_tests);
 }
 
+// ----------------------------------------------------------------------------- transparent, warp-cooperative
+// Same work sharing as the opaque kernel for lv/raytracer.py:518-645.  Per round every active ray
+// sits in one occupied voxel; the flattened (ray, fragment) pairs are rejected/intersected by all
+// lanes; in-voxel hits become (key = depth16 << 16 | slot, t, segment) records in a per-warp list,
+// which the owning lanes drain into their private k-slot buffers.  The k smallest keys above
+// `last_key` are a set, so the insertion order does not matter (keys are unique: the slot is in
+// the low bits) and the reference's result is reproduced exactly, including the re-scan of a
+// voxel when more than k hits were accepted (the ray then stays in the voxel for another round,
+// and its tests are counted again like the reference does).
+constexpr int HL_CAP = 128;
+
+struct WarpSharedT {
+    double dir[3][32];
+    double t_enter[32], inv_span[32];
+    int vox[3][32];
+    uint32_t fo[32];
+    uint32_t prefix[33];
+    uint32_t q_i[64];
+    uint32_t q_rs[64];
+    double hl_t[HL_CAP];
+    uint32_t hl_key[HL_CAP], hl_i[HL_CAP];
+    uint8_t hl_r[HL_CAP];
+};
+
+__global__ void __launch_bounds__(RC_WARPS * 32)
+k_render_transparent_coop(const RenderArgs A) {
+    __shared__ WarpSharedT sh_all[RC_WARPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpSharedT &S = sh_all[warp];
+    const int px = A.p.tile_x0 + blockIdx.x * (8 * RC_WARPS) + warp * 8 + (lane & 7);
+    const int py = A.p.tile_y0 + blockIdx.y * 4 + (lane >> 3);
+    const bool live = px < A.p.tile_x1 && py < A.p.tile_y1;
+    const int w = A.cam.width, h = A.cam.height, res = A.res;
+    const double ox = A.cam.pos[0], oy = A.cam.pos[1], oz = A.cam.pos[2];
+    const bool clip = A.p.use_clip != 0;
+    const double r = A.p.radius;
+    const int kslots = A.p.k;
+    const bool early = A.p.early_termination != 0;
+    const double alpha = A.p.alpha;
+    double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
+    bool active = false;
+    if (live) {
+        const double aspect = (double)w / (double)h;
+        const double u = (2.0 * (px + 0.5) / w - 1.0) * aspect * A.cam.tan_half_fov;
+        const double v = (1.0 - 2.0 * (py + 0.5) / h) * A.cam.tan_half_fov;
+        dx = A.cam.fwd[0] + u * A.cam.right[0] + v * A.cam.up[0];
+        dy = A.cam.fwd[1] + u * A.cam.right[1] + v * A.cam.up[1];
+        dz = A.cam.fwd[2] + u * A.cam.right[2] + v * A.cam.up[2];
+        const double dn = sqrt(dx * dx + dy * dy + dz * dz);
+        dx = dx / dn; dy = dy / dn; dz = dz / dn;
+        double t0 = 0.0;
+        t1 = 1e30;
+        const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            if (d[a] == 0.0) {
+                if (o[a] < 0.0 || o[a] > (double)res) { t0 = 1.0; t1 = -1.0; break; }
+            } else {
+                double ta = (0.0 - o[a]) / d[a], tb = ((double)res - o[a]) / d[a];
+                if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
+                if (ta > t0) t0 = ta;
+                if (tb < t1) t1 = tb;
+            }
+        }
+        active = t1 >= t0;
+        t = t0 > 0.0 ? t0 : 0.0;
+    }
+    S.dir[0][lane] = dx; S.dir[1][lane] = dy; S.dir[2][lane] = dz;
+    const RayInv inv = make_inv(dx, dy, dz);
+    int lvl_hint = 1;
+    double col_r = 0.0, col_g = 0.0, col_b = 0.0, acc_a = 0.0;
+    int64_t first_hit = -1;
+    uint32_t keybuf[64], ibuf[64];
+    double tbuf[64];
+    uint64_t n_tests = 0;
+    // per-voxel state of this lane's ray
+    bool repeat = false;
+    int64_t last_key = -1;
+    uint32_t n = 0;
+    double te = 0.0;
+    int x = 0, y = 0, z = 0;
+    __syncwarp();
+
+    for (;;) {
+        // ---- 1. next occupied voxel (or stay for a re-scan)
+        if (active && !repeat) {
+            for (;;) {
+                if ((early && acc_a >= 0.999) || !(t < t1)) { active = false; break; }
+                const double tm = t + 1e-6;
+                x = (int)floor(ox + dx * tm); y = (int)floor(oy + dy * tm); z = (int)floor(oz + dz * tm);
+                if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) { active = false; break; }
+                const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
+                if (A.bits[idx] != 0) {
+                    const uint32_t fo = A.offsets[idx];
+                    n = A.offsets[idx + 1] - fo;
+                    S.fo[lane] = fo;
+                    te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
+                    const double span = te - t;                  // t_enter = t (lv/raytracer.py:557-560)
+                    S.t_enter[lane] = t;
+                    S.inv_span[lane] = span > 0.0 ? 65535.0 / span : 0.0;
+                    last_key = -1;
+                    break;
+                }
+                const int l = lvl_hint = empty_level(A, x, y, z, lvl_hint);
+                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, l);
+                t = tl > t ? tl : t + 1e-6;
+            }
+        }
+        if (__ballot_sync(0xffffffffu, active) == 0) break;
+        S.vox[0][lane] = x; S.vox[1][lane] = y; S.vox[2][lane] = z;
+        // ---- 2. flatten (ray, fragment) pairs
+        uint32_t inc = active ? n : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        S.prefix[lane + 1] = inc;
+        if (lane == 0) S.prefix[0] = 0;
+        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane == 0) n_tests += T;
+        int kept = 0;
+        uint32_t accepted = 0;
+        uint32_t qn = 0, hl_n = 0;
+        __syncwarp();
+
+        // owners pull their records out of the hit list (insertion sort, lv/raytracer.py:589-607)
+        auto drain = [&]() {
+            for (uint32_t e = 0; e < hl_n; e++) {
+                if (S.hl_r[e] != (uint8_t)lane) continue;
+                const uint32_t key = S.hl_key[e];
+                if ((int64_t)key <= last_key) continue;
+                accepted++;
+                int j;
+                if (kept < kslots) { j = kept; kept++; }
+                else if (key < keybuf[kslots - 1]) j = kslots - 1;
+                else continue;
+                while (j > 0 && keybuf[j - 1] > key) {
+                    keybuf[j] = keybuf[j - 1]; tbuf[j] = tbuf[j - 1]; ibuf[j] = ibuf[j - 1];
+                    j--;
+                }
+                keybuf[j] = key; tbuf[j] = S.hl_t[e]; ibuf[j] = S.hl_i[e];
+            }
+            hl_n = 0;
+            __syncwarp();
+        };
+
+        for (uint32_t p0 = 0; p0 < T || qn > 0; p0 += 32) {
+            const uint32_t p = p0 + lane;
+            bool pass = false;
+            uint32_t rr = 0, ss = 0, ii = 0;
+            if (p < T) {
+                uint32_t lo = 0, hi = 32;
+#pragma unroll
+                for (int it = 0; it < 5; it++) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (S.prefix[mid] <= p) lo = mid; else hi = mid;
+                }
+                rr = lo;
+                ss = p - S.prefix[rr];
+                ii = A.frags[S.fo[rr] + ss];
+                const d3 va = ld3(A.verts + 3 * (int64_t)ii), vb = ld3(A.verts + 3 * (int64_t)ii + 3);
+                pass = !surely_misses(ox, oy, oz, S.dir[0][rr], S.dir[1][rr], S.dir[2][rr], va, vb, r);
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, pass);
+            if (pass) {
+                const uint32_t pos = qn + __popc(m & ((1u << lane) - 1u));
+                S.q_i[pos] = ii;
+                S.q_rs[pos] = (rr << 16) | ss;
+            }
+            qn += __popc(m);
+            __syncwarp();
+            const bool flush = p0 + 32 >= T;
+            if (qn >= 32 || (flush && qn > 0)) {
+                const uint32_t take = qn < 32 ? qn : 32;
+                bool hit = false;
+                double ht = 0.0;
+                uint32_t hr = 0, hs = 0, hi_ = 0, hkey = 0;
+                if (lane < take) {
+                    hi_ = S.q_i[lane];
+                    const uint32_t rs = S.q_rs[lane];
+                    hr = rs >> 16; hs = rs & 0xFFFFu;
+                    const double ddx = S.dir[0][hr], ddy = S.dir[1][hr], ddz = S.dir[2][hr];
+                    const Capsule c = load_capsule(A.verts, A.normals, (int64_t)hi_, r, clip);
+                    ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
+                    if (ht >= 0.0) {
+                        const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
+                        hit = hx == S.vox[0][hr] && hy == S.vox[1][hr] && hz == S.vox[2][hr];
+                        if (hit) {   // lv/raytracer.py:583-588
+                            int64_t q = (int64_t)((ht - S.t_enter[hr]) * S.inv_span[hr]);
+                            if (q < 0) q = 0; else if (q > 65535) q = 65535;
+                            hkey = ((uint32_t)q << 16) | hs;
+                        }
+                    }
+                }
+                __syncwarp();
+                uint32_t mv_i = 0, mv_rs = 0;
+                const bool mv = lane + 32 < qn;
+                if (mv) { mv_i = S.q_i[lane + 32]; mv_rs = S.q_rs[lane + 32]; }
+                __syncwarp();
+                if (mv) { S.q_i[lane] = mv_i; S.q_rs[lane] = mv_rs; }
+                qn -= take;
+                const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+                if (hl_n + __popc(hm) > HL_CAP) drain();
+                if (hit) {
+                    const uint32_t pos = hl_n + __popc(hm & ((1u << lane) - 1u));
+                    S.hl_t[pos] = ht; S.hl_key[pos] = hkey; S.hl_i[pos] = hi_; S.hl_r[pos] = (uint8_t)hr;
+                }
+                hl_n += __popc(hm);
+                __syncwarp();
+            }
+            if (flush && qn == 0) break;
+        }
+        drain();
+        // ---- blend the kept hits front to back (lv/raytracer.py:608-631)
+        if (active) {
+            for (int j = 0; j < kept; j++) {
+                if (early && acc_a >= 0.999) break;
+                const double tt = tbuf[j];
+                const int64_t i = ibuf[j];
+                const double hx = ox + dx * tt, hy = oy + dy * tt, hz = oz + dz * tt;
+                const Capsule c = load_capsule(A.verts, A.normals, i, r, clip);
+                double nx, ny, nz, cr, cg, cb;
+                capsule_normal(hx, hy, hz, c, nx, ny, nz);
+                shade(A, c, nx, ny, nz, hx, hy, hz, cr, cg, cb);
+                const double wgt = (1.0 - acc_a) * alpha;
+                col_r += wgt * cr; col_g += wgt * cg; col_b += wgt * cb;
+                acc_a += wgt;
+                if (first_hit < 0) first_hit = i;
+            }
+            // lv/raytracer.py:632-637
+            if (accepted <= (uint32_t)kslots || (early && acc_a >= 0.999)) {
+                repeat = false;
+                t = te > t ? te : t + 1e-6;
+            } else {
+                last_key = keybuf[kslots - 1];
+                repeat = true;
+            }
+        }
+        __syncwarp();
+    }
+
+    if (live) {
+        const double out_r = col_r + (1.0 - acc_a) * A.p.background[0];
+        const double out_g = col_g + (1.0 - acc_a) * A.p.background[1];
+        const double out_b = col_b + (1.0 - acc_a) * A.p.background[2];
+        const int64_t pix = (int64_t)py * w + px;
+        if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
+        if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
+        A.hit_id[pix] = (int32_t)first_hit;
+    }
+    if (lane == 0 && n_tests)
+        atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)n_tests);
+}
+
 // Second half of shading on demand: one thread per pixel re-derives its ray (same expressions,
 // hence the same bits, as the trace kernel), and shades the recorded hit.
 __global__ void __launch_bounds__(128)
@@ -763,8 +1018,8 @@ int lvx_render(const double *verts, const double *normals, const uint32_t *offse
         const dim3 cgrid((tw + 8 * RC_WARPS - 1) / (8 * RC_WARPS), (th + 3) / 4);
         k_render_opaque_coop<false><<<cgrid, RC_WARPS * 32, 0, (cudaStream_t)stream>>>(A);
     } else {
-        const dim3 grid((tw + 7) / 8, (th + 15) / 16);
-        k_render<1><<<grid, 128, 0, (cudaStream_t)stream>>>(A);
+        const dim3 cgrid((tw + 8 * RC_WARPS - 1) / (8 * RC_WARPS), (th + 3) / 4);
+        k_render_transparent_coop<<<cgrid, RC_WARPS * 32, 0, (cudaStream_t)stream>>>(A);
     }
     LVX_LAUNCH_CHECK();
     return LVX_OK;
