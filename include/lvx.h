@@ -83,11 +83,12 @@ int64_t lvx_pyramid_elems(int res);
 /* ---- line-set upload: lv/voxelizer.py:435-447 segment_arrays, lv/lineset.py:74-79
  * segment_vertex_ids, lv/lineset.py:213-242 compute_clip_normals.
  * verts_f32 (n_verts*3, world), poly_off (n_poly+1).  Outputs: verts (voxel-unit f64,
- * n_verts*3), normals (unit tangents f64, n_verts*3; may be NULL to skip), segs (start-vertex
+ * n_verts*3), verts_f (the same rounded to f32, n_verts*3; may be NULL; read only by the renderer's
+ * conservative pre-test), normals (unit tangents f64, n_verts*3; may be NULL to skip), segs (start-vertex
  * id of each of the n_verts-n_poly segments, ascending, int32). */
 int lvx_upload(const float *verts_f32, const int64_t *poly_off, int64_t n_verts, int64_t n_poly,
                const double *world_min_host, double voxel_size,
-               double *verts, double *normals, int32_t *segs, uint64_t *stats, void *stream);
+               double *verts, float *verts_f, double *normals, int32_t *segs, uint64_t *stats, void *stream);
 
 /* lv/lineset.py:81-82 LineSet.aabb(): out6 = {min xyz, max xyz} as f32 (device). */
 int lvx_aabb(const float *verts_f32, int64_t n_verts, float *out6, void *stream);
@@ -161,7 +162,7 @@ int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t 
 
 /* ---- render: lv/raytracer.py:459-515 _opaque_kernel, 518-645 _transparent_kernel, 94-97 _to_srgb.
  * rgb: h*w*3 f64 linear (may be NULL), srgb: h*w*3 u8 (may be NULL), hit_id: h*w i32. */
-int lvx_render(const double *verts, const double *normals, const uint32_t *offsets, const uint32_t *frags,
+int lvx_render(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
                const uint8_t *bits_flat, int res, const float *ao, const float *shadow,
                const lvx_camera *cam_host, const lvx_render_params *params_host,
                double *rgb, uint8_t *srgb, int32_t *hit_id, uint64_t *stats, void *stream);
@@ -174,7 +175,7 @@ int lvx_render(const double *verts, const double *normals, const uint32_t *offse
  *   lvx_shade       with vis_list = need_list, fill_ones = 0
  *   lvx_resolve     normal + colour per hit pixel (lv/raytracer.py:486-502), reading ao/shadow only
  *                   where bits_flat marks the voxel visible (1.0 elsewhere, lv/shading.py:177-178) */
-int lvx_trace_hits(const double *verts, const double *normals, const uint32_t *offsets, const uint32_t *frags,
+int lvx_trace_hits(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
                    const uint8_t *bits_flat, int res, const lvx_camera *cam_host,
                    const lvx_render_params *params_host, double *hit_t, int32_t *hit_id, uint32_t *need_bits,
                    uint32_t *need_list, uint64_t *stats, void *stream);

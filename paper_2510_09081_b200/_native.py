@@ -41,7 +41,7 @@ SIGNATURES = {
     "lvx_stats_reset": (_I, [_P, _P]),
     "lvx_num_levels": (_I, [_I]),
     "lvx_pyramid_elems": (_L, [_I]),
-    "lvx_upload": (_I, [_P, _P, _L, _L, _P, _D, _P, _P, _P, _P, _P]),
+    "lvx_upload": (_I, [_P, _P, _L, _L, _P, _D, _P, _P, _P, _P, _P, _P]),
     "lvx_aabb": (_I, [_P, _L, _P, _P]),
     "lvx_clear": (_I, [_P, _L, _P]),
     "lvx_voxelize": (_I, [_P, _P, _P, _L, _L, _I, _D, _D, _D, _I, _I, _P, _P, _P, _P]),
@@ -59,9 +59,9 @@ SIGNATURES = {
     "lvx_scatter": (_I, [_P, _P, _L, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P]),
     "lvx_shade_scratch_bytes": (_L, [_L]),
     "lvx_shade": (_I, [_P, _P, _I, _P, _P, _I, _D, _P, _D, _P, _P, _I, _P, _P]),
-    "lvx_trace_hits": (_I, [_P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "lvx_trace_hits": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lvx_resolve": (_I, [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "lvx_render": (_I, [_P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "lvx_render": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

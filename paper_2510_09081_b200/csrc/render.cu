@@ -9,6 +9,7 @@ namespace lvx {
 
 struct RenderArgs {
     const double *verts, *normals;
+    const float *verts_f;      // voxel-unit vertices rounded to f32 (conservative pre-test only)
     const uint32_t *offsets, *frags;
     const uint8_t *bits;
     const float *ao, *sh;
@@ -50,6 +51,30 @@ __device__ __forceinline__ bool surely_misses(double ox, double oy, double oz, d
     const double h = (ox - a.x) * nx + (oy - a.y) * ny + (oz - a.z) * nz;
     const double R = r + 1e-4;
     return h * h > R * R * nn;
+}
+
+// Single-precision version used by the cooperative kernels.  It bounds the distance between the
+// ray LINE through P (a point of the ray inside the current voxel, so all differences are a few
+// voxels long) and the SEGMENT [a, b]: every surface the f64 routine can return lies within
+// r + 3.2e-5 of the segment, the f32 evaluation (inputs rounded to f32 at magnitudes <= 1024,
+// i.e. <= 6.1e-5 absolute) is accurate to a few 1e-4, so "distance > r + 2e-3" proves a miss.
+// ~40 full-rate FMA-able operations instead of ~60 half-rate f64 ones, and it also rejects rays that
+// pass the infinite cylinder beyond the segment's ends.
+__device__ __forceinline__ bool surely_misses_f32(float Px, float Py, float Pz, float Dx, float Dy, float Dz,
+                                                  const float *__restrict__ vf, int64_t i, float R2) {
+    const float ax = vf[3 * i], ay = vf[3 * i + 1], az = vf[3 * i + 2];
+    const float bx = vf[3 * i + 3], by = vf[3 * i + 4], bz = vf[3 * i + 5];
+    const float wx = ax - Px, wy = ay - Py, wz = az - Pz;
+    const float ex = bx - ax, ey = by - ay, ez = bz - az;
+    // (explicit fmaf: the translation unit is compiled with -fmad=false for the f64 code)
+    const float dw = fmaf(Dx, wx, fmaf(Dy, wy, Dz * wz)), de = fmaf(Dx, ex, fmaf(Dy, ey, Dz * ez));
+    const float wpx = fmaf(-Dx, dw, wx), wpy = fmaf(-Dy, dw, wy), wpz = fmaf(-Dz, dw, wz);   // w, e perpendicular to D
+    const float epx = fmaf(-Dx, de, ex), epy = fmaf(-Dy, de, ey), epz = fmaf(-Dz, de, ez);
+    const float ee = fmaf(epx, epx, fmaf(epy, epy, epz * epz));
+    float sgm = 0.f;
+    if (ee > 1e-12f) sgm = fminf(fmaxf(__fdividef(-fmaf(wpx, epx, fmaf(wpy, epy, wpz * epz)), ee), 0.f), 1.f);
+    const float qx = fmaf(sgm, epx, wpx), qy = fmaf(sgm, epy, wpy), qz = fmaf(sgm, epz, wpz);
+    return fmaf(qx, qx, fmaf(qy, qy, qz * qz)) > R2;
 }
 
 __device__ __forceinline__ Capsule load_capsule_lazy(const double *__restrict__ normals, int64_t i, const d3 &a,
@@ -452,6 +477,7 @@ constexpr int RC_WARPS = 4;
 
 struct WarpShared {
     double dir[3][32];
+    float dirf[3][32], pf[3][32];   // f32 direction and a ray point inside the current voxel
     int vox[3][32];
     uint32_t fo[32];
     uint32_t prefix[33];
@@ -509,6 +535,8 @@ k_render_opaque_coop(const RenderArgs A) {
         t = t0 > 0.0 ? t0 : 0.0;
     }
     S.dir[0][lane] = dx; S.dir[1][lane] = dy; S.dir[2][lane] = dz;
+    S.dirf[0][lane] = (float)dx; S.dirf[1][lane] = (float)dy; S.dirf[2][lane] = (float)dz;
+    const float R2f = ((float)r + 2e-3f) * ((float)r + 2e-3f);
     const RayInv inv = make_inv(dx, dy, dz);
     int lvl_hint = 1;
     double best_t = -1.0;      // final hit of this lane's ray
@@ -542,6 +570,10 @@ k_render_opaque_coop(const RenderArgs A) {
         }
         if (__ballot_sync(0xffffffffu, active) == 0) break;
         S.vox[0][lane] = x; S.vox[1][lane] = y; S.vox[2][lane] = z;
+        {   // a point of the ray inside the voxel (its centre-most parameter), for the f32 pre-test
+            const double tc = 0.5 * (t + te);
+            S.pf[0][lane] = (float)(ox + dx * tc); S.pf[1][lane] = (float)(oy + dy * tc); S.pf[2][lane] = (float)(oz + dz * tc);
+        }
         // ---- 2. flatten (ray, fragment) pairs
         uint32_t inc = active ? n : 0;
 #pragma unroll
@@ -555,7 +587,7 @@ k_render_opaque_coop(const RenderArgs A) {
         if (lane == 0) n_tests += T;
         double cur_t = -1.0;           // best hit of this lane's ray in this voxel
         uint32_t cur_s = 0xffffffffu, cur_i = 0;
-        uint32_t qn = 0;
+        uint32_t qn = 0, own = 0;
         __syncwarp();
         for (uint32_t p0 = 0; p0 < T || qn > 0; p0 += 32) {
             const uint32_t p = p0 + lane;
@@ -563,17 +595,12 @@ k_render_opaque_coop(const RenderArgs A) {
             uint32_t rr = 0, ss = 0, ii = 0;
             if (p < T) {
                 // owner ray: largest rr with prefix[rr] <= p
-                uint32_t lo = 0, hi = 32;
-#pragma unroll
-                for (int it = 0; it < 5; it++) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (S.prefix[mid] <= p) lo = mid; else hi = mid;
-                }
-                rr = lo;
+                while (S.prefix[own + 1] <= p) own++;       // owner ray: prefix[own] <= p < prefix[own+1]
+                rr = own;
                 ss = p - S.prefix[rr];
                 ii = A.frags[S.fo[rr] + ss];
-                const d3 va = ld3(A.verts + 3 * (int64_t)ii), vb = ld3(A.verts + 3 * (int64_t)ii + 3);
-                pass = !surely_misses(ox, oy, oz, S.dir[0][rr], S.dir[1][rr], S.dir[2][rr], va, vb, r);
+                pass = !surely_misses_f32(S.pf[0][rr], S.pf[1][rr], S.pf[2][rr], S.dirf[0][rr], S.dirf[1][rr],
+                                          S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
             }
             // ---- 3. compact survivors into the queue
             const uint32_t m = __ballot_sync(0xffffffffu, pass);
@@ -706,6 +733,7 @@ constexpr int HL_CAP = 128;
 
 struct WarpSharedT {
     double dir[3][32];
+    float dirf[3][32], pf[3][32];
     double t_enter[32], inv_span[32];
     int vox[3][32];
     uint32_t fo[32];
@@ -761,6 +789,8 @@ k_render_transparent_coop(const RenderArgs A) {
         t = t0 > 0.0 ? t0 : 0.0;
     }
     S.dir[0][lane] = dx; S.dir[1][lane] = dy; S.dir[2][lane] = dz;
+    S.dirf[0][lane] = (float)dx; S.dirf[1][lane] = (float)dy; S.dirf[2][lane] = (float)dz;
+    const float R2f = ((float)r + 2e-3f) * ((float)r + 2e-3f);
     const RayInv inv = make_inv(dx, dy, dz);
     int lvl_hint = 1;
     double col_r = 0.0, col_g = 0.0, col_b = 0.0, acc_a = 0.0;
@@ -803,6 +833,10 @@ k_render_transparent_coop(const RenderArgs A) {
         }
         if (__ballot_sync(0xffffffffu, active) == 0) break;
         S.vox[0][lane] = x; S.vox[1][lane] = y; S.vox[2][lane] = z;
+        {   // a point of the ray inside the voxel (its centre-most parameter), for the f32 pre-test
+            const double tc = 0.5 * (t + te);
+            S.pf[0][lane] = (float)(ox + dx * tc); S.pf[1][lane] = (float)(oy + dy * tc); S.pf[2][lane] = (float)(oz + dz * tc);
+        }
         // ---- 2. flatten (ray, fragment) pairs
         uint32_t inc = active ? n : 0;
 #pragma unroll
@@ -816,7 +850,7 @@ k_render_transparent_coop(const RenderArgs A) {
         if (lane == 0) n_tests += T;
         int kept = 0;
         uint32_t accepted = 0;
-        uint32_t qn = 0, hl_n = 0;
+        uint32_t qn = 0, hl_n = 0, own = 0;
         __syncwarp();
 
         // owners pull their records out of the hit list (insertion sort, lv/raytracer.py:589-607)
@@ -845,17 +879,12 @@ k_render_transparent_coop(const RenderArgs A) {
             bool pass = false;
             uint32_t rr = 0, ss = 0, ii = 0;
             if (p < T) {
-                uint32_t lo = 0, hi = 32;
-#pragma unroll
-                for (int it = 0; it < 5; it++) {
-                    const uint32_t mid = (lo + hi) >> 1;
-                    if (S.prefix[mid] <= p) lo = mid; else hi = mid;
-                }
-                rr = lo;
+                while (S.prefix[own + 1] <= p) own++;       // owner ray: prefix[own] <= p < prefix[own+1]
+                rr = own;
                 ss = p - S.prefix[rr];
                 ii = A.frags[S.fo[rr] + ss];
-                const d3 va = ld3(A.verts + 3 * (int64_t)ii), vb = ld3(A.verts + 3 * (int64_t)ii + 3);
-                pass = !surely_misses(ox, oy, oz, S.dir[0][rr], S.dir[1][rr], S.dir[2][rr], va, vb, r);
+                pass = !surely_misses_f32(S.pf[0][rr], S.pf[1][rr], S.pf[2][rr], S.dirf[0][rr], S.dirf[1][rr],
+                                          S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
             }
             const uint32_t m = __ballot_sync(0xffffffffu, pass);
             if (pass) {
@@ -982,7 +1011,7 @@ k_resolve(const RenderArgs A) {
 
 using namespace lvx;
 
-static int fill_args(RenderArgs &A, const double *verts, const double *normals, const uint32_t *offsets,
+static int fill_args(RenderArgs &A, const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets,
                      const uint32_t *frags, const uint8_t *bits_flat, int res, const float *ao, const float *shadow,
                      const lvx_camera *cam_host, const lvx_render_params *params_host, double *rgb, uint8_t *srgb,
                      int32_t *hit_id, uint64_t *stats) {
@@ -992,7 +1021,7 @@ static int fill_args(RenderArgs &A, const double *verts, const double *normals, 
     if (cam_host->width <= 0 || cam_host->height <= 0) return LVX_E_ARG;
     if (p.tile_x0 < 0 || p.tile_y0 < 0 || p.tile_x1 > cam_host->width || p.tile_y1 > cam_host->height) return LVX_E_ARG;
     if (p.use_clip && !normals) return LVX_E_ARG;
-    A.verts = verts; A.normals = normals; A.offsets = offsets; A.frags = frags; A.bits = bits_flat;
+    A.verts = verts; A.verts_f = verts_f; A.normals = normals; A.offsets = offsets; A.frags = frags; A.bits = bits_flat;
     A.ao = ao; A.sh = shadow;
     const LevelOffsets L = make_level_offsets(res);
     for (int l = 0; l < 16; l++) A.bits_off[l] = l < L.n_levels ? (uint32_t)L.off[l] : 0;
@@ -1004,14 +1033,15 @@ static int fill_args(RenderArgs &A, const double *verts, const double *normals, 
 
 extern "C" {
 
-int lvx_render(const double *verts, const double *normals, const uint32_t *offsets, const uint32_t *frags,
+int lvx_render(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
                const uint8_t *bits_flat, int res, const float *ao, const float *shadow,
                const lvx_camera *cam_host, const lvx_render_params *params_host, double *rgb, uint8_t *srgb,
                int32_t *hit_id, uint64_t *stats, void *stream) {
     RenderArgs A;
-    const int rc = fill_args(A, verts, normals, offsets, frags, bits_flat, res, ao, shadow, cam_host, params_host,
+    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, bits_flat, res, ao, shadow, cam_host, params_host,
                              rgb, srgb, hit_id, stats);
     if (rc != LVX_OK) return rc;
+    if (!verts_f) return LVX_E_ARG;
     const int tw = A.p.tile_x1 - A.p.tile_x0, th = A.p.tile_y1 - A.p.tile_y0;
     if (tw <= 0 || th <= 0) return LVX_OK;
     if (A.p.mode == 0) {
@@ -1025,15 +1055,15 @@ int lvx_render(const double *verts, const double *normals, const uint32_t *offse
     return LVX_OK;
 }
 
-int lvx_trace_hits(const double *verts, const double *normals, const uint32_t *offsets, const uint32_t *frags,
+int lvx_trace_hits(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
                    const uint8_t *bits_flat, int res, const lvx_camera *cam_host,
                    const lvx_render_params *params_host, double *hit_t, int32_t *hit_id, uint32_t *need_bits,
                    uint32_t *need_list, uint64_t *stats, void *stream) {
     RenderArgs A;
-    const int rc = fill_args(A, verts, normals, offsets, frags, bits_flat, res, nullptr, nullptr, cam_host,
+    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, bits_flat, res, nullptr, nullptr, cam_host,
                              params_host, nullptr, nullptr, hit_id, stats);
     if (rc != LVX_OK) return rc;
-    if (A.p.mode != 0 || !hit_t || !need_bits || !need_list) return LVX_E_ARG;
+    if (A.p.mode != 0 || !verts_f || !hit_t || !need_bits || !need_list) return LVX_E_ARG;
     const int tw = A.p.tile_x1 - A.p.tile_x0, th = A.p.tile_y1 - A.p.tile_y0;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
@@ -1051,7 +1081,7 @@ int lvx_resolve(const double *verts, const double *normals, const uint8_t *bits_
                 const float *shadow, const lvx_camera *cam_host, const lvx_render_params *params_host,
                 const double *hit_t, const int32_t *hit_id, double *rgb, uint8_t *srgb, void *stream) {
     RenderArgs A;
-    const int rc = fill_args(A, verts, normals, nullptr, nullptr, bits_flat, res, ao, shadow, cam_host, params_host,
+    const int rc = fill_args(A, verts, nullptr, normals, nullptr, nullptr, bits_flat, res, ao, shadow, cam_host, params_host,
                              rgb, srgb, const_cast<int32_t *>(hit_id), nullptr);
     if (rc != LVX_OK) return rc;
     if (!hit_t) return LVX_E_ARG;

@@ -30,15 +30,15 @@ __device__ __forceinline__ double len3(const d3 &d) { return sqrt(d.x * d.x + d.
 __global__ void __launch_bounds__(256)
 k_upload(const float *__restrict__ v32, const int64_t *__restrict__ off, int64_t n_verts, int64_t n_poly,
          double wx, double wy, double wz, double vs, int64_t uniform_len,
-         double *__restrict__ verts, double *__restrict__ normals, int32_t *__restrict__ segs,
-         uint64_t *__restrict__ stats) {
+         double *__restrict__ verts, float *__restrict__ verts_f, double *__restrict__ normals,
+         int32_t *__restrict__ segs, uint64_t *__restrict__ stats) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_verts) return;
     const d3 w = wv(v32, i);
     // lv/voxelizer.py:438
-    verts[3 * i] = (w.x - wx) / vs;
-    verts[3 * i + 1] = (w.y - wy) / vs;
-    verts[3 * i + 2] = (w.z - wz) / vs;
+    const double vx = (w.x - wx) / vs, vy = (w.y - wy) / vs, vz = (w.z - wz) / vs;
+    verts[3 * i] = vx; verts[3 * i + 1] = vy; verts[3 * i + 2] = vz;
+    if (verts_f) { verts_f[3 * i] = (float)vx; verts_f[3 * i + 1] = (float)vy; verts_f[3 * i + 2] = (float)vz; }
     const int64_t p = uniform_len > 0 ? i / uniform_len : find_polyline(off, n_poly, i);
     const int64_t s = off[p], e = off[p + 1];
     // lv/lineset.py:74-79: vertex i starts segment number i - p unless it ends its polyline
@@ -149,15 +149,15 @@ int lvx_clear(void *ptr, int64_t bytes, void *stream) {
 }
 
 int lvx_upload(const float *verts_f32, const int64_t *poly_off, int64_t n_verts, int64_t n_poly,
-               const double *world_min_host, double voxel_size, double *verts, double *normals,
-               int32_t *segs, uint64_t *stats, void *stream) {
+               const double *world_min_host, double voxel_size, double *verts, float *verts_f,
+               double *normals, int32_t *segs, uint64_t *stats, void *stream) {
     if (n_verts < 2 || n_poly < 1 || !(voxel_size > 0) || n_verts > 0x7fffffffLL) return LVX_E_ARG;
     // uniform-length hint: valid only if n_verts divides evenly; the kernel still reads off[p], so
     // a wrong hint cannot happen silently -- the host wrapper passes it only when verified.
     int64_t uniform = 0;
     k_upload<<<blocks_for(n_verts, 256), 256, 0, (cudaStream_t)stream>>>(
         verts_f32, poly_off, n_verts, n_poly, world_min_host[0], world_min_host[1], world_min_host[2],
-        voxel_size, uniform, verts, normals, segs, stats);
+        voxel_size, uniform, verts, verts_f, normals, segs, stats);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -111,6 +111,7 @@ class FrameEngine:
         self._poly_off = t.from_numpy(np.ascontiguousarray(polyline_offsets, dtype=np.int64)).to(self.dev)
         self._verts32 = t.empty((int(n_vertices), 3), dtype=t.float32, device=self.dev)
         self._verts64 = t.empty((int(n_vertices), 3), dtype=t.float64, device=self.dev)
+        self._vertsf = t.empty((int(n_vertices), 3), dtype=t.float32, device=self.dev)
         self._normals = t.empty((int(n_vertices), 3), dtype=t.float64, device=self.dev) if self.clip else None
         self._segs = t.empty(int(n_vertices) - (len(polyline_offsets) - 1), dtype=t.int32, device=self.dev)
 
@@ -136,9 +137,11 @@ class FrameEngine:
         N.check(N.lib().lvx_upload(ops._ptr(self._verts32), ops._ptr(self._poly_off),
                                    int(self._verts32.shape[0]), int(self._poly_off.shape[0]) - 1,
                                    wm.ctypes.data_as(C.c_void_p), float(grid.voxel_size),
-                                   ops._ptr(self._verts64), ops._ptr(self._normals), ops._ptr(self._segs),
+                                   ops._ptr(self._verts64), ops._ptr(self._vertsf), ops._ptr(self._normals),
+                                   ops._ptr(self._segs),
                                    ops._ptr(self.stats), ops._stream()), "lvx_upload")
-        self.lines = ops.DeviceLines(self._verts32, self._poly_off, self._verts64, self._normals, self._segs,
+        self.lines = ops.DeviceLines(self._verts32, self._poly_off, self._verts64, self._vertsf, self._normals,
+                                     self._segs,
                                      int(self._verts32.shape[0]), int(self._poly_off.shape[0]) - 1,
                                      float(r_world) / float(grid.voxel_size), grid, float(r_world))
         self.grid = grid

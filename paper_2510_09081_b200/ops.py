@@ -57,6 +57,7 @@ class DeviceLines:
     verts32: "object"     # (Nv,3) f32 world
     poly_off: "object"    # (P+1,) i64
     verts: "object"       # (Nv,3) f64 voxel units
+    verts_f: "object"     # (Nv,3) the same rounded to f32 (renderer pre-test)
     normals: "object"     # (Nv,3) f64 unit tangents, or None
     segs: "object"        # (N,) i32 ascending start-vertex ids
     n_vertices: int
@@ -81,16 +82,17 @@ def upload(verts32, poly_off, grid, r_world, stats, with_normals=True, normals=N
     nv, npoly = int(verts32.shape[0]), int(poly_off.shape[0]) - 1
     dev = verts32.device
     verts = torch.empty((nv, 3), dtype=torch.float64, device=dev)
+    verts_f = torch.empty((nv, 3), dtype=torch.float32, device=dev)
     segs = torch.empty(nv - npoly, dtype=torch.int32, device=dev)
     out_n = None
     if with_normals and normals is None:
         out_n = torch.empty((nv, 3), dtype=torch.float64, device=dev)
     wm, wm_p = _dbl3(grid.world_min)
     check(lib().lvx_upload(_ptr(verts32), _ptr(poly_off), nv, npoly, wm_p, float(grid.voxel_size),
-                           _ptr(verts), _ptr(out_n), _ptr(segs), _ptr(stats), _stream()), "lvx_upload")
+                           _ptr(verts), _ptr(verts_f), _ptr(out_n), _ptr(segs), _ptr(stats), _stream()), "lvx_upload")
     if normals is not None:
         out_n = normals
-    return DeviceLines(verts32, poly_off, verts, out_n if with_normals else None, segs, nv, npoly,
+    return DeviceLines(verts32, poly_off, verts, verts_f, out_n if with_normals else None, segs, nv, npoly,
                        float(r_world) / float(grid.voxel_size), grid, float(r_world))
 
 
@@ -207,14 +209,14 @@ def make_camera_struct(cam, grid) -> N.lvx_camera:
 
 def render(lines: DeviceLines, offsets, frags, bits_flat, res, ao, shadow, cam_struct, params, rgb, srgb,
            hit_id, stats):
-    check(lib().lvx_render(_ptr(lines.verts), _ptr(lines.normals), _ptr(offsets), _ptr(frags), _ptr(bits_flat),
+    check(lib().lvx_render(_ptr(lines.verts), _ptr(lines.verts_f), _ptr(lines.normals), _ptr(offsets), _ptr(frags), _ptr(bits_flat),
                            res, _ptr(ao), _ptr(shadow), C.byref(cam_struct), C.byref(params), _ptr(rgb),
                            _ptr(srgb), _ptr(hit_id), _ptr(stats), _stream()), "lvx_render")
 
 
 def trace_hits(lines: DeviceLines, offsets, frags, bits_flat, res, cam_struct, params, hit_t, hit_id, need_bits,
                need_list, stats):
-    check(lib().lvx_trace_hits(_ptr(lines.verts), _ptr(lines.normals), _ptr(offsets), _ptr(frags), _ptr(bits_flat),
+    check(lib().lvx_trace_hits(_ptr(lines.verts), _ptr(lines.verts_f), _ptr(lines.normals), _ptr(offsets), _ptr(frags), _ptr(bits_flat),
                                res, C.byref(cam_struct), C.byref(params), _ptr(hit_t), _ptr(hit_id),
                                _ptr(need_bits), _ptr(need_list), _ptr(stats), _stream()), "lvx_trace_hits")
 
