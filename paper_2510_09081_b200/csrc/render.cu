@@ -685,10 +685,10 @@ k_render_opaque_coop(const RenderArgs A) {
         // Shading on demand: record the hit, and request AO/shadow for the (visible) voxels its
         // trilinear lookup will read (lv/raytracer.py:368-390).  New requests are gathered per
         // block in shared memory so the global list counter sees one atomic per block.
-        __shared__ uint32_t s_cnt, s_base;
-        __shared__ uint32_t s_items[RC_WARPS * 32 * 8];
-        if (threadIdx.x == 0) s_cnt = 0;
-        __syncthreads();
+        // (warp-level only: a block-wide barrier here would park finished warps until the slowest
+        // warp of the block leaves the trace loop)
+        uint32_t items[8];
+        int n_items = 0;
         if (live) {
             const int64_t pix = (int64_t)py * w + px;
             A.hit_t[pix] = best_t;
@@ -702,19 +702,35 @@ k_render_opaque_coop(const RenderArgs A) {
                     const int Y = min(max(iy + ((k >> 1) & 1), 0), res - 1);
                     const int Z = min(max(iz + (k >> 2), 0), res - 1);
                     const uint32_t idx = (uint32_t)X + (uint32_t)res * ((uint32_t)Y + (uint32_t)res * (uint32_t)Z);
+                    bool fresh = false;
                     if (A.bits[idx] != 0) {
                         const uint32_t bit = 1u << (idx & 31);
-                        if ((atomicOr(&A.need_bits[idx >> 5], bit) & bit) == 0) s_items[atomicAdd(&s_cnt, 1u)] = idx;
+                        fresh = (atomicOr(&A.need_bits[idx >> 5], bit) & bit) == 0;
                     }
+                    items[k] = idx;
+                    if (fresh) n_items |= 1 << k;
                 }
             }
         }
-        __syncthreads();
-        const uint32_t cnt = s_cnt;
-        if (threadIdx.x == 0 && cnt)
-            s_base = (uint32_t)atomicAdd(reinterpret_cast<unsigned long long *>(A.need_list), (unsigned long long)cnt);
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) A.need_list[LVX_LIST_HDR + s_base + i] = s_items[i];
+        // one global atomic per warp: exclusive scan of the per-lane counts
+        const uint32_t mine = __popc((uint32_t)n_items);
+        uint32_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total) {
+            unsigned long long b = 0;
+            if (lane == 0)
+                b = atomicAdd(reinterpret_cast<unsigned long long *>(A.need_list), (unsigned long long)total);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            uint32_t pos = (uint32_t)b + incl - mine;
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                if (n_items & (1 << k)) A.need_list[LVX_LIST_HDR + pos++] = items[k];
+        }
     }
     if (lane == 0 && n_tests)
         atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)n_tests);

@@ -15,8 +15,11 @@
 
 namespace lvx {
 
+#ifndef LVX_VOX_MINB
+#define LVX_VOX_MINB 6
+#endif
 template <bool WIDE>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, LVX_VOX_MINB)
 k_voxelize(const double *__restrict__ verts, const double *__restrict__ normals,
            const int32_t *__restrict__ segs, int64_t seg_begin, int64_t seg_end, int use_clip,
            double r, double rt, double r_min, int res, int method,
