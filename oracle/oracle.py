@@ -130,14 +130,17 @@ def _split_levels(flat, res):
 
 # ----------------------------------------------------------------------------- stages
 
-def voxelize(ls, cn, g, method="capsule", r_min=0.5, workers=None, r_world=None):
-    """voxelizer.py:466-498 -> namespace(base, occ_levels, occ_flat, grid, r_min, saturated, visited)"""
+def voxelize(ls, cn, g, method="capsule", r_min=0.5, workers=None, r_world=None, seg_range=None):
+    """voxelizer.py:466-498 -> namespace(base, occ_levels, occ_flat, grid, r_min, saturated, visited).
+    `seg_range=(lo, hi)` voxelizes only segments segs[lo:hi] (one chunk of voxelizer.py:461-463)."""
     if method not in METHODS:
         raise ValueError(f"unknown voxelization method {method!r}")
     if not r_min > 0:
         raise ValueError("r_min must be positive")
     res = g.resolution
     verts, segs, normals, use_clip, r = segment_arrays(ls, cn, g, r_world)
+    if seg_range is not None:
+        segs = np.ascontiguousarray(segs[seg_range[0]:seg_range[1]])
     base = np.zeros((res, res, res), dtype=np.uint32)
     visited = C.c_int64(0)
     sat = C.c_int64(0)

@@ -29,6 +29,7 @@ class FrameResult:
         self._e = engine
         self.stats = {}
         self.stage_ms = {}
+        self.trace_kernel_ms = None
 
     @property
     def srgb_dev(self):
@@ -103,6 +104,22 @@ class FrameEngine:
         self._verts32 = self._poly_off = None
         self._ev = [t.cuda.Event(enable_timing=True) for _ in range(len(STAGES) + 3)]
         self.launches_per_frame = 0
+
+    def kernel_launches_per_frame(self) -> int:
+        """Number of lvx kernels one `run` enqueues (csrc/*.cu), for bench.py's `gpu_launches`."""
+        levels = int(self.res).bit_length()
+        n = 1 + 1                                   # stats_reset, upload
+        n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
+        n += levels - 1                             # mips
+        n += (4 if self.strategy == "vcsv" else 1) + (levels - 1)   # solid, visibility, march, dilate | occupied; or-mips
+        n += 1                                      # scan
+        n += 3                                      # cursor copy, scatter, order
+        n += levels + 1                             # non-empty masks, shade
+        if self.shading == "demand":
+            n += 2                                  # trace_hits, resolve
+        else:
+            n += 1 + 1                              # shade fill, render
+        return n
 
     # ------------------------------------------------------------------ line set
     def set_topology(self, polyline_offsets: np.ndarray, n_vertices: int):
@@ -259,9 +276,11 @@ class FrameEngine:
             raise ABufferError("fragment count mismatch between passes (nondeterministic traversal?)")
         out = FrameResult(self)
         out.stage_ms = {s: ev[i].elapsed_time(ev[i + 1]) for i, s in enumerate(STAGES)}
+        out.trace_kernel_ms = out.stage_ms["trace"]
         if self.shading == "demand":   # events 6..9 bracket trace_hits, shade, resolve
             out.stage_ms["trace"] = ev[6].elapsed_time(ev[7]) + ev[8].elapsed_time(ev[9])
             out.stage_ms["shade"] = ev[7].elapsed_time(ev[8])
+            out.trace_kernel_ms = ev[6].elapsed_time(ev[7])
             shaded = int(self.need_list[:2].cpu().numpy().view(np.uint64)[0])
         else:
             shaded = int(st[N.ST_VISIBLE])

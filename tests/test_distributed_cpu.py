@@ -1,0 +1,91 @@
+"""world_size-2 gloo tests (CPU) of the multi-GPU host logic: segment sharding, the exact
+all-reduce merge of packed occupancy grids, screen tiles and frame assignment."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2510_09081_b200 import distributed as D
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, scene_name, out_dir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from helpers import Scene
+        from oracle import oracle as orc
+        orc.set_threads(2)
+        sc = Scene(scene_name)
+        cn = orc.compute_clip_normals(sc.ls)
+        b = D.shard_bounds(sc.ls.n_segments, world)
+        part = orc.voxelize(sc.ls, cn, sc.g, r_min=sc.r_min, r_world=sc.r_world,
+                            seg_range=(int(b[rank]), int(b[rank + 1])))
+        local = torch.from_numpy(part.base.view(np.int32).reshape(-1).copy())
+        merged, visited = D.merge_partial_grids(local)
+        full = orc.voxelize(sc.ls, cn, sc.g, r_min=sc.r_min, r_world=sc.r_world)
+        ok = np.array_equal(merged.numpy().view(np.uint32), full.base.reshape(-1)) and visited == full.visited
+        # the partial grids really differ from the merged one (the test would be vacuous otherwise)
+        differs = not np.array_equal(part.base, full.base)
+        np.save(os.path.join(out_dir, f"ok{rank}.npy"), np.array([ok, differs]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scene", ["helix64_vcsv", "diag_vcsv"])   # diag: 16-bit occupancy saturates
+def test_sharded_voxelize_merge_gloo(scene, tmp_path, oracle):
+    world = 2
+    port = _free_port()
+    mp.spawn(_worker, args=(world, port, scene, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        ok, differs = np.load(tmp_path / f"ok{r}.npy")
+        assert ok and differs
+
+
+def test_widen_pack_roundtrip_and_saturation():
+    base = np.array([0, (3 << 16) | 100, (0xFFFF << 16) | 0xFFFF, (40000 << 16) | 50000], dtype=np.uint32)
+    t = torch.from_numpy(base.view(np.int32).copy())
+    wide = D.widen_packed(t)
+    assert wide.tolist() == [0, (3 << 32) | 100, (0xFFFF << 32) | 0xFFFF, (40000 << 32) | 50000]
+    packed, visited = D.pack_wide(wide)
+    assert np.array_equal(packed.numpy().view(np.uint32), base) and visited == 3 + 0xFFFF + 40000
+    # two ranks holding the last word: both fields must saturate separately, no carry between them
+    packed2, visited2 = D.pack_wide(wide + wide)
+    want = np.array([0, (6 << 16) | 200, (0xFFFF << 16) | 0xFFFF, (0xFFFF << 16) | 0xFFFF], dtype=np.uint32)
+    assert np.array_equal(packed2.numpy().view(np.uint32), want) and visited2 == 2 * visited
+
+
+@pytest.mark.parametrize("n,world", [(0, 4), (1, 4), (10, 3), (1000003, 8), (7, 8)])
+def test_shard_bounds_cover(n, world):
+    b = D.shard_bounds(n, world)
+    assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
+    assert len(b) - 1 == max(1, min(world, max(1, n)))
+
+
+@pytest.mark.parametrize("w,h,world", [(1920, 1080, 1), (1920, 1080, 8), (64, 37, 4), (5, 3, 8)])
+def test_tiles_partition_the_image(w, h, world):
+    seen = np.zeros((h, w), dtype=np.int32)
+    for x0, y0, x1, y1 in D.tile_rects(w, h, world):
+        assert 0 <= x0 <= x1 <= w and 0 <= y0 <= y1 <= h
+        seen[y0:y1, x0:x1] += 1
+    assert (seen == 1).all()
+
+
+def test_frames_for_rank_partition():
+    frames = sorted(f for r in range(8) for f in D.frames_for_rank(100, r, 8))
+    assert frames == list(range(100))

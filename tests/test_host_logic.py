@@ -1,0 +1,93 @@
+"""Host-side logic (no GPU): generators, grid fit and camera reproduce the reference bit for bit
+(checked against the golden fixtures made from the live reference), configuration rules, .lns I/O."""
+import numpy as np
+import pytest
+
+import paper_2510_09081_b200 as lvx
+from helpers import SCENES, Scene, h
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_generators_grid_and_camera_match_reference(name):
+    sc = Scene(name)
+    cfg = lvx.PipelineConfig(**sc.meta["cfg"])
+    ls = lvx.pipeline.load_input(cfg)
+    assert h(ls.vertices) == sc.hash["vertices_f32"]
+    assert np.array_equal(ls.polyline_offsets, sc.arr["polyline_offsets"])
+    g, r_world = lvx.fit_grid(ls, cfg.res, radius_voxels=cfg.r if cfg.r > 0 else None)
+    assert [float(x).hex() for x in g.world_min] == sc.meta["grid"]["world_min"]
+    assert float(g.voxel_size).hex() == sc.meta["grid"]["voxel_size"]
+    assert float(r_world).hex() == sc.meta["r_world"]
+    cam = lvx.make_camera(cfg, g)
+    c = sc.meta["camera"]
+    assert [float(x).hex() for x in cam.position] == c["position"]
+    assert [float(x).hex() for x in cam.forward] == c["forward"]
+    assert [float(x).hex() for x in cam.up] == c["up"]
+    assert [float(x).hex() for x in cfg.light_vector()] == sc.meta["light"]
+
+
+def test_config_rules():
+    C = lvx.PipelineConfig
+    C().validate()
+    for bad in (dict(res=100), dict(method="x"), dict(strategy="y"), dict(mode="z"), dict(alpha=0.0),
+                dict(alpha=1.5), dict(k=0), dict(k=65), dict(r=-1.0), dict(r_min=0.0), dict(workers=-1),
+                dict(width=0), dict(cam_fov=180.0), dict(light="0,0,0"), dict(light="a,b"),
+                dict(strategy="vcsv", mode="transparent")):
+        with pytest.raises(lvx.ConfigError):
+            C(**bad).validate()
+
+
+def test_config_sources(tmp_path):
+    f = tmp_path / "c.cfg"
+    f.write_text("# comment\nres = 64\nmode=transparent\ndump = yes\n")
+    cfg = lvx.PipelineConfig.from_sources(str(f), {"res": 32, "alpha": None})
+    assert cfg.res == 32 and cfg.mode == "transparent" and cfg.dump is True
+    f.write_text("nonsense\n")
+    with pytest.raises(lvx.ConfigError):
+        lvx.PipelineConfig.from_sources(str(f))
+    with pytest.raises(lvx.ConfigError):
+        lvx.PipelineConfig.from_sources(None, {"nope": 1})
+
+
+def test_lineset_validation_and_segments():
+    v = np.zeros((5, 3), np.float32)
+    v[:, 0] = np.arange(5)
+    ls = lvx.LineSet(v, [0, 2, 5], 0.1)
+    assert ls.n_segments == 3 and ls.segment_vertex_ids().tolist() == [0, 2, 3]
+    for off in ([0, 1, 5], [1, 5], [0, 4]):
+        with pytest.raises(lvx.LineSetError):
+            lvx.LineSet(v, off, 0.1)
+    with pytest.raises(lvx.LineSetError):
+        lvx.LineSet(v, [0, 5], 0.0)
+
+
+@pytest.mark.parametrize("fmt", ["lns-binary", "lns-text"])
+def test_lns_roundtrip(tmp_path, fmt):
+    ls = lvx.generate("random_streamlines", seed=5, polylines=4, verts_per_line=6)
+    p = tmp_path / "a.lns"
+    lvx.save_lineset(ls, p, fmt)
+    back = lvx.load_lineset(p)
+    assert np.array_equal(back.vertices, ls.vertices) and np.array_equal(back.polyline_offsets, ls.polyline_offsets)
+    assert back.radius == pytest.approx(ls.radius)
+    p.write_bytes(b"LNS1\x00")
+    with pytest.raises(lvx.ParseError):
+        lvx.load_lineset(p)
+
+
+def test_decimate_keeps_ends():
+    ls = lvx.generate("helix", verts=11)
+    d = lvx.decimate(ls, 4)
+    assert d.n_vertices == 4 and np.array_equal(d.vertices[-1], ls.vertices[-1])
+
+
+def test_bundles_generator_shape():
+    ls = lvx.generate("bundles", seed=0, n_bundles=2, fibers=5, verts=11)
+    assert ls.n_polylines == 10 and ls.n_segments == 100
+
+
+def test_grid_desc_rules():
+    with pytest.raises(ValueError):
+        lvx.GridDesc(48, np.zeros(3), 1.0)
+    g = lvx.GridDesc(64, np.array([1.0, 2.0, 3.0]), 0.5)
+    assert g.n_levels == 7 and g.flat_index(1, 2, 3) == 1 + 64 * (2 + 64 * 3)
+    assert np.allclose(g.to_world(g.to_voxel([2.0, 3.0, 4.0])), [2.0, 3.0, 4.0])
