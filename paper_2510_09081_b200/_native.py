@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblvx_b200.so")
+# LVX_LIB selects an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("LVX_LIB") or os.path.join(_HERE, "liblvx_b200.so")
 
 # stats block indices (include/lvx.h)
 ST_VISITED, ST_SATURATED, ST_NEED_WIDE, ST_SOLID, ST_FRAG_TOTAL, ST_MISMATCH, ST_RAY_TESTS, \
@@ -56,12 +57,14 @@ SIGNATURES = {
     "lvx_list_words": (_L, [_L]),
     "lvx_scan_scratch_bytes": (_L, [_L]),
     "lvx_scan": (_I, [_P, _P, _L, _P, _P, _P, _P]),
-    "lvx_scatter": (_I, [_P, _P, _L, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P]),
+    "lvx_loose_words": (_L, [_L]),
+    "lvx_scatter": (_I, [_P, _P, _L, _D, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
+    "lvx_march_levels": (_I, [_P, _I, _P, _P]),
     "lvx_shade_scratch_bytes": (_L, [_L]),
     "lvx_shade": (_I, [_P, _P, _I, _P, _P, _I, _D, _P, _D, _P, _P, _I, _P, _P]),
-    "lvx_trace_hits": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "lvx_trace_hits": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lvx_resolve": (_I, [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "lvx_render": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "lvx_render": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

@@ -10,7 +10,22 @@
 // (SURVEY.md §7 H2).  The reference's extra counting traversal (_chunk_count_kernel) exists only
 // to rebuild deterministic cursors and to assert determinism; here the assertion is the
 // cursor==end check in the ordering pass (LVX_ST_MISMATCH -> ABufferError on the host).
+//
+// Loose bits.  A list holds every segment whose TRAVERSAL footprint (radius rt = max(r,r_min)+0.5)
+// covers the voxel, ~5x more than the capsules (radius r) that really reach into it.  A ray hit is
+// only accepted when the hit point lies inside the voxel being visited (lv/raytracer.py:446-452),
+// and every surface point _ray_capsule can return lies within r + 3.2e-5 of the segment, so a
+// fragment whose segment is provably farther than r_tight = r + 1e-3 from the voxel's cube can never
+// yield an accepted hit there.  The scatter pass has the segment in registers and proves this per
+// incidence with a separating-direction lower bound (f32, ~70 flops); the flag rides through the
+// ordering pass in bit 0 of the packed word and ends up in a 1-bit-per-fragment mask the ray
+// tracer consults before it touches the segment's vertices.  `frags` itself stays the reference's
+// array, bit for bit.
 #include "lvx_device.cuh"
+
+#ifndef LVX_BATCH
+#define LVX_BATCH 4   // cells of a traversal row whose atomics are issued back to back
+#endif
 
 namespace lvx {
 
@@ -122,20 +137,71 @@ k_scan(const uint32_t *__restrict__ base, const uint8_t *__restrict__ cull, int6
 // lv/abuffer.py:226-255 _write_kernel.  The hierarchical segment rejection (_segment_visible,
 // 145-181) is an acceleration only -- culled voxels are skipped per cell (252-253) -- so the
 // output does not depend on it.
+// Lower bound on the distance between segment [a, b] and the unit cube centred at the origin
+// (a, b given relative to the cube centre).  Three rounds of alternating projections give a
+// near-optimal separating direction n; for ANY n, dist >= (min(n.a, n.b) - max_cube n.y) / |n|.
+// Returns true when that bound exceeds R, i.e. the capsule of radius R certainly misses the cube.
+__device__ __forceinline__ bool segment_misses_cube(float ax, float ay, float az, float bx, float by, float bz, float R) {
+    const float dx = bx - ax, dy = by - ay, dz = bz - az;
+    const float dd = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float inv = dd > 0.f ? __fdividef(1.f, dd) : 0.f;
+    float qx = 0.f, qy = 0.f, qz = 0.f, px = ax, py = ay, pz = az;
+#pragma unroll
+    for (int it = 0; it < 3; it++) {
+        float t = fmaf(qx - ax, dx, fmaf(qy - ay, dy, (qz - az) * dz)) * inv;
+        t = fminf(fmaxf(t, 0.f), 1.f);
+        px = fmaf(t, dx, ax); py = fmaf(t, dy, ay); pz = fmaf(t, dz, az);
+        qx = fminf(fmaxf(px, -0.5f), 0.5f); qy = fminf(fmaxf(py, -0.5f), 0.5f); qz = fminf(fmaxf(pz, -0.5f), 0.5f);
+    }
+    const float nx = px - qx, ny = py - qy, nz = pz - qz;
+    const float nn = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+    if (!(nn > 0.f)) return false;                      // the segment touches the cube
+    const float na = fmaf(nx, ax, fmaf(ny, ay, nz * az)), nb = fmaf(nx, bx, fmaf(ny, by, nz * bz));
+    const float gap = fminf(na, nb) - 0.5f * (fabsf(nx) + fabsf(ny) + fabsf(nz));
+    return gap > 0.f && gap * gap > R * R * nn;
+}
+
+// lv/abuffer.py:226-255 _write_kernel.  The hierarchical segment rejection (_segment_visible,
+// 145-181) is an acceleration only -- culled voxels are skipped per cell (252-253) -- so the
+// output does not depend on it.  Words are written as (segment << 1) | loose; the ordering pass
+// strips the flag again.
 __global__ void __launch_bounds__(128)
 k_scatter(const double *__restrict__ verts, const int32_t *__restrict__ segs, int64_t n_seg, double rt,
-          int res, int method, const uint8_t *__restrict__ cull0, uint32_t *__restrict__ cursor,
+          float r_tight, int res, int method, const uint8_t *__restrict__ cull0, uint32_t *__restrict__ cursor,
           uint32_t *__restrict__ frags, int64_t cap) {
     const int64_t si = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (si >= n_seg) return;
     const int64_t i = segs[si];
     const d3 a = ld3(verts + 3 * i), b = ld3(verts + 3 * i + 3);
     const int64_t res64 = res;
-    for_each_cell(method, a, b, rt, res, [&](int x, int y, int z) {
-        const int64_t idx = x + res64 * (y + res64 * z);
-        if (cull0 && cull0[idx] == 0) return;
-        const uint32_t pos = atomicAdd(&cursor[idx], 1u);
-        if ((int64_t)pos < cap) frags[pos] = (uint32_t)i;
+    // Rows of the traversal are handled four cells at a time: the four cursor atomics are issued
+    // back to back (their latencies overlap) before the first dependent fragment store.
+    for_each_row(method, a, b, rt, res, [&](int x, int y, int z, int axis, int len) {
+        const int64_t stride = axis == 0 ? 1 : (axis == 1 ? res64 : res64 * res64);
+        const int64_t idx0 = x + res64 * (y + res64 * z);
+        const double sx = axis == 0 ? 1.0 : 0.0, sy = axis == 1 ? 1.0 : 0.0, sz = axis == 2 ? 1.0 : 0.0;
+        for (int u0 = 0; u0 < len; u0 += LVX_BATCH) {
+            uint32_t word[LVX_BATCH], pos[LVX_BATCH];
+            bool on[LVX_BATCH];
+#pragma unroll
+            for (int k = 0; k < LVX_BATCH; k++) {
+                const int u = u0 + k;
+                on[k] = u < len && !(cull0 && cull0[idx0 + u * stride] == 0);
+                word[k] = 0;
+                if (on[k]) {
+                    const double cx = x + 0.5 + u * sx, cy = y + 0.5 + u * sy, cz = z + 0.5 + u * sz;
+                    const bool loose = r_tight >= 0.f &&
+                                       segment_misses_cube((float)(a.x - cx), (float)(a.y - cy), (float)(a.z - cz),
+                                                           (float)(b.x - cx), (float)(b.y - cy), (float)(b.z - cz), r_tight);
+                    word[k] = ((uint32_t)i << 1) | (loose ? 1u : 0u);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < LVX_BATCH; k++) pos[k] = on[k] ? atomicAdd(&cursor[idx0 + (u0 + k) * stride], 1u) : 0u;
+#pragma unroll
+            for (int k = 0; k < LVX_BATCH; k++)
+                if (on[k] && (int64_t)pos[k] < cap) frags[pos[k]] = word[k];
+        }
     });
 }
 
@@ -182,37 +248,91 @@ __device__ void warp_bitonic(uint32_t *f, uint32_t n, int lane) {
 constexpr int ORDER_WARPS = 8;
 constexpr int ORDER_CAP = 512;   // fragments staged per warp for long lists (2 KiB)
 
-// bitonic sort of one value per lane (ascending by lane), network truncated to LG stages:
-// sorts the first 2^LG lanes when the rest hold +inf
+// Bitonic sort inside aligned groups of W = 2^LG lanes (li = lane index inside the group); every
+// group ends up ascending.  Lanes past a list's end hold 0xffffffff.
 template <int LG>
-__device__ __forceinline__ uint32_t warp_sort(uint32_t v, int lane) {
+__device__ __forceinline__ uint32_t group_sort(uint32_t v, int li) {
 #pragma unroll
     for (int lk = 1; lk <= LG; lk++) {
 #pragma unroll
         for (int lj = lk - 1; lj >= 0; lj--) {
             const uint32_t o = __shfl_xor_sync(0xffffffffu, v, 1 << lj);
             // keep the smaller value on the lower lane of an ascending block
-            const bool keep_min = (((lane >> lk) ^ (lane >> lj)) & 1) == 0;
+            const bool keep_min = (((li >> lk) ^ (li >> lj)) & 1) == 0;
             v = keep_min ? min(v, o) : max(v, o);
         }
     }
     return v;
 }
 
-__device__ __forceinline__ void sort_short(uint32_t *f, uint32_t nn, uint32_t val, int lane) {
-    const uint32_t next = __shfl_down_sync(0xffffffffu, val, 1);
-    if (__ballot_sync(0xffffffffu, lane + 1 < nn && val > next) == 0) return;   // already ascending
-    if (nn <= 4) val = warp_sort<2>(val, lane);
-    else if (nn <= 8) val = warp_sort<3>(val, lane);
-    else if (nn <= 16) val = warp_sort<4>(val, lane);
-    else val = warp_sort<5>(val, lane);
-    if (lane < nn) f[lane] = val;
+// Short lists, 32 / W of them side by side: lane group g sorts the g-th list of size class W
+// (W/2 < n <= W, or n <= 2 for W = 2) named by the set bits of `cls`; b, n are the per-lane list
+// bounds of the warp's 32 current list entries.  Each group loads its list with one (partial)
+// 128-byte line, sorts it in registers, stores the stripped segment ids and publishes the loose
+// bits of its fragments.
+template <int LG>
+__device__ __forceinline__ void sort_class(uint32_t cls, uint32_t b, uint32_t n, uint32_t *__restrict__ frags,
+                                           uint32_t *__restrict__ loose_bits, int lane) {
+    constexpr int W = 1 << LG, G = 32 / W;
+    const int g = lane >> LG, li = lane & (W - 1);
+    while (cls) {
+        int src = -1;
+#pragma unroll
+        for (int k = 0; k < G; k++) {
+            if (cls) {
+                const int sbit = __ffs(cls) - 1;
+                cls &= cls - 1;
+                if (k == g) src = sbit;
+            }
+        }
+        const uint32_t bb = __shfl_sync(0xffffffffu, b, src < 0 ? 0 : src);
+        const uint32_t nsrc = __shfl_sync(0xffffffffu, n, src < 0 ? 0 : src);   // (all lanes take part)
+        const uint32_t nn = src < 0 ? 0u : nsrc;
+        uint32_t val = 0xffffffffu;
+        if ((uint32_t)li < nn) val = frags[bb + li];
+        val = group_sort<LG>(val, li);
+        const bool mine = (uint32_t)li < nn;
+        if (mine) frags[bb + li] = val >> 1;
+        const uint32_t bal = __ballot_sync(0xffffffffu, mine && (val & 1u));
+        if (loose_bits && li == 0 && nn) {
+            const uint32_t gm = W == 32 ? bal : ((bal >> (g * W)) & ((1u << (W & 31)) - 1u));
+            if (gm) {
+                const uint32_t sh = bb & 31u, w = bb >> 5;
+                atomicOr(&loose_bits[w], gm << sh);
+                if (sh && (gm >> (32u - sh))) atomicOr(&loose_bits[w + 1], gm >> (32u - sh));
+            }
+        }
+    }
+}
+
+// bit k of `mask` = fragment (b + k) is loose; two lanes publish the (at most two) mask words
+__device__ __forceinline__ void emit_loose(uint32_t *__restrict__ loose_bits, uint32_t b, uint32_t mask, int lane) {
+    if (!loose_bits || !mask) return;
+    const uint32_t sh = b & 31u, w = b >> 5;
+    if (lane == 0) {
+        const uint32_t lo = mask << sh;
+        if (lo) atomicOr(&loose_bits[w], lo);
+    } else if (lane == 1 && sh) {
+        const uint32_t hi = mask >> (32u - sh);
+        if (hi) atomicOr(&loose_bits[w + 1], hi);
+    }
+}
+
+// long lists: strip the flag from the sorted packed words in `src` into f[0..nn) and publish the mask
+__device__ __forceinline__ void strip_long(const uint32_t *src, uint32_t *f, uint32_t b, uint32_t nn, int lane,
+                                           uint32_t *__restrict__ loose_bits) {
+    for (uint32_t i0 = 0; i0 < nn; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const uint32_t v = i < nn ? src[i] : 0u;
+        if (i < nn) f[i] = v >> 1;
+        emit_loose(loose_bits, b + i0, __ballot_sync(0xffffffffu, i < nn && (v & 1u)), lane);
+    }
 }
 
 __global__ void __launch_bounds__(ORDER_WARPS * 32)
 k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ cursor,
         const uint32_t *__restrict__ vis_list, uint32_t *__restrict__ frags, int64_t cap,
-        uint64_t *__restrict__ stats) {
+        uint32_t *__restrict__ loose_bits, uint64_t *__restrict__ stats) {
     __shared__ uint32_t stage[ORDER_WARPS][ORDER_CAP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n_lists = (int64_t)*reinterpret_cast<const unsigned long long *>(vis_list);
@@ -230,36 +350,30 @@ k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ curso
             if (cursor[v] != e) stats[LVX_ST_MISMATCH] = 1;   // lv/abuffer.py:310-311
             if ((int64_t)e > cap) n = 0;                      // never touch memory past the buffer
         }
-        uint32_t work = __ballot_sync(0xffffffffu, n > 1);
         n_long += __popc(__ballot_sync(0xffffffffu, n > 32));
+        // short lists by size class, several lists per warp step
+        sort_class<1>(__ballot_sync(0xffffffffu, n >= 1 && n <= 2), b, n, frags, loose_bits, lane);
+        sort_class<2>(__ballot_sync(0xffffffffu, n > 2 && n <= 4), b, n, frags, loose_bits, lane);
+        sort_class<3>(__ballot_sync(0xffffffffu, n > 4 && n <= 8), b, n, frags, loose_bits, lane);
+        sort_class<4>(__ballot_sync(0xffffffffu, n > 8 && n <= 16), b, n, frags, loose_bits, lane);
+        sort_class<5>(__ballot_sync(0xffffffffu, n > 16 && n <= 32), b, n, frags, loose_bits, lane);
+        // long lists one at a time: staged through shared memory, or in place beyond the stage
+        uint32_t work = __ballot_sync(0xffffffffu, n > 32);
         while (work) {
-            // two lists per iteration: both loads are issued before either sort
             const int s0 = __ffs(work) - 1;
             work &= work - 1;
-            const int s1 = work ? __ffs(work) - 1 : -1;
-            if (s1 >= 0) work &= work - 1;
-            const uint32_t b0 = __shfl_sync(0xffffffffu, b, s0), n0 = __shfl_sync(0xffffffffu, n, s0);
-            const uint32_t b1 = __shfl_sync(0xffffffffu, b, s1 < 0 ? 0 : s1);
-            const uint32_t n1 = s1 < 0 ? 0 : __shfl_sync(0xffffffffu, n, s1 < 0 ? 0 : s1);
-            uint32_t v0 = 0xffffffffu, v1 = 0xffffffffu;
-            if (n0 <= 32 && lane < n0) v0 = frags[b0 + lane];
-            if (n1 <= 32 && lane < n1) v1 = frags[b1 + lane];
-#pragma unroll
-            for (int k = 0; k < 2; k++) {
-                const uint32_t bb = k ? b1 : b0, nn = k ? n1 : n0;
-                if (nn < 2) continue;
-                uint32_t *f = frags + bb;
-                if (nn <= 32) sort_short(f, nn, k ? v1 : v0, lane);
-                else if (nn <= ORDER_CAP) {
-                    uint32_t *buf = stage[warp];
-                    for (uint32_t i = lane; i < nn; i += 32) buf[i] = f[i];
-                    __syncwarp();
-                    warp_bitonic(buf, nn, lane);
-                    for (uint32_t i = lane; i < nn; i += 32) f[i] = buf[i];
-                    __syncwarp();
-                } else {
-                    warp_bitonic(f, nn, lane);
-                }
+            const uint32_t bb = __shfl_sync(0xffffffffu, b, s0), nn = __shfl_sync(0xffffffffu, n, s0);
+            uint32_t *f = frags + bb;
+            if (nn <= ORDER_CAP) {
+                uint32_t *buf = stage[warp];
+                for (uint32_t i = lane; i < nn; i += 32) buf[i] = f[i];
+                __syncwarp();
+                warp_bitonic(buf, nn, lane);
+                strip_long(buf, f, bb, nn, lane, loose_bits);
+                __syncwarp();
+            } else {
+                warp_bitonic(f, nn, lane);
+                strip_long(f, f, bb, nn, lane, loose_bits);
             }
         }
     }
@@ -297,22 +411,26 @@ int lvx_scan(const uint32_t *base, const uint8_t *cull_base, int64_t n_voxels, u
     return LVX_OK;
 }
 
-int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double rt, int res, int method,
+int64_t lvx_loose_words(int64_t frag_capacity) { return (frag_capacity + 31) / 32 + 1; }
+
+int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double rt, double r_tight, int res, int method,
                 const uint8_t *cull_flat, const uint32_t *vis_list, const uint32_t *offsets, uint32_t *cursor,
-                uint32_t *frags, int64_t frag_capacity, uint64_t *stats, void *stream) {
+                uint32_t *frags, int64_t frag_capacity, uint32_t *loose_bits, uint64_t *stats, void *stream) {
     if (!vis_list) return LVX_E_ARG;
     if (!pow2(res) || method < 0 || method > 2) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
     k_copy_u32<<<blocks_for((V + 3) / 4, 256), 256, 0, s>>>(offsets, cursor, V);
+    if (loose_bits) LVX_CUDA(cudaMemsetAsync(loose_bits, 0, (size_t)lvx_loose_words(frag_capacity) * 4, s));
+    else r_tight = -1.0;
     if (n_seg > 0)
-        k_scatter<<<blocks_for(n_seg, 128), 128, 0, s>>>(verts, segs, n_seg, rt, res, method, cull_flat, cursor,
-                                                        frags, frag_capacity);
+        k_scatter<<<blocks_for(n_seg, 128), 128, 0, s>>>(verts, segs, n_seg, rt, (float)r_tight, res, method, cull_flat,
+                                                        cursor, frags, frag_capacity);
     {
         unsigned nb = 148 * 8;   // persistent: 148 SMs x 8 CTAs of 8 warps
         const unsigned need = blocks_for((V + 31) / 32, ORDER_WARPS);
         if (nb > need) nb = need;
-        k_order<<<nb, ORDER_WARPS * 32, 0, s>>>(offsets, cursor, vis_list, frags, frag_capacity, stats);
+        k_order<<<nb, ORDER_WARPS * 32, 0, s>>>(offsets, cursor, vis_list, frags, frag_capacity, loose_bits, stats);
     }
     LVX_LAUNCH_CHECK();
     return LVX_OK;

@@ -4,7 +4,7 @@
 set -e
 cd "$(dirname "$0")"
 NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
-OUT=../liblvx_b200.so
+OUT=${LVX_OUT:-../liblvx_b200.so}
 $NVCC -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=c++17 \
       -Xcompiler -fPIC -shared ${LVX_NVCC_EXTRA} \
       upload.cu voxelize.cu cull.cu abuffer.cu shade.cu render.cu -o $OUT

@@ -259,6 +259,46 @@ k_ormip(const uint8_t *__restrict__ src, int rsrc, uint8_t *__restrict__ out) {
     out[i] = m ? 1 : 0;
 }
 
+// March table for the ray tracer: one byte per level-0 voxel = 255 if the voxel's bit is set, else
+// the value lv/raytracer.py:316-326 _empty_level would return there (largest l such that the
+// ancestors at levels 1..l are all clear).  One load per DDA step instead of a walk up the pyramid.
+// One thread per 4 x-adjacent voxels (they share every ancestor from level 2 up).
+struct MarchOffsets { uint32_t off[16]; };
+__global__ void __launch_bounds__(256)
+k_march_levels(const uint8_t *__restrict__ flat, const MarchOffsets O, int res, int n_levels, int64_t n4,
+               uint8_t *__restrict__ skip) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n4) return;
+    const int r4 = res >> 2;
+    const int x0 = (int)(g % r4) << 2, y = (int)((g / r4) % res), z = (int)(g / ((int64_t)r4 * res));
+    const uchar4 b = *reinterpret_cast<const uchar4 *>(flat + (x0 + (int64_t)res * (y + (int64_t)res * z)));
+    uchar4 out = make_uchar4(255, 255, 255, 255);
+    if (!(b.x && b.y && b.z && b.w)) {
+        int up = 0;          // result for a voxel whose level-1 parent is clear
+        uint8_t p1a = 1, p1b = 1;
+        if (n_levels > 1) {
+            const uint32_t r1 = (uint32_t)res >> 1;
+            const uint32_t i1 = O.off[1] + ((uint32_t)x0 >> 1) + r1 * (((uint32_t)y >> 1) + r1 * ((uint32_t)z >> 1));
+            p1a = flat[i1]; p1b = flat[i1 + 1];
+            if (!(p1a && p1b)) {
+                up = 1;
+                while (up < n_levels - 1) {
+                    const int nl = up + 1;
+                    const uint32_t rl = (uint32_t)res >> nl;
+                    if (flat[O.off[nl] + ((uint32_t)x0 >> nl) + rl * (((uint32_t)y >> nl) + rl * ((uint32_t)z >> nl))] != 0) break;
+                    up = nl;
+                }
+            }
+        }
+        const uint8_t la = p1a ? 0 : (uint8_t)up, lb = p1b ? 0 : (uint8_t)up;
+        if (!b.x) out.x = la;
+        if (!b.y) out.y = la;
+        if (!b.z) out.z = lb;
+        if (!b.w) out.w = lb;
+    }
+    *reinterpret_cast<uchar4 *>(skip + 4 * g) = out;
+}
+
 static int or_mips(uint8_t *flat, int res, cudaStream_t s) {
     const LevelOffsets L = make_level_offsets(res);
     for (int l = 1; l < L.n_levels; l++) {
@@ -314,6 +354,17 @@ int lvx_occupied_pyramid(const uint32_t *base, int res, uint8_t *cull_flat, uint
     k_occupied<<<blocks_for(V, 256), 256, 0, s>>>(base, V, cull_flat, vis_list, stats);
     LVX_LAUNCH_CHECK();
     return or_mips(cull_flat, res, s);
+}
+
+int lvx_march_levels(const uint8_t *bits_flat, int res, uint8_t *march, void *stream) {
+    if (!pow2(res) || res < 4 || !bits_flat || !march) return LVX_E_ARG;
+    const LevelOffsets L = make_level_offsets(res);
+    MarchOffsets O;
+    for (int l = 0; l < 16; l++) O.off[l] = l < L.n_levels ? (uint32_t)L.off[l] : 0;
+    const int64_t n4 = L.off[1] / 4;
+    k_march_levels<<<blocks_for(n4, 256), 256, 0, (cudaStream_t)stream>>>(bits_flat, O, res, L.n_levels, n4, march);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
 }
 
 int64_t lvx_list_words(int64_t n_voxels) { return n_voxels + LVX_LIST_HDR; }

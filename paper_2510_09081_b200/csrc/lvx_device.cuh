@@ -50,24 +50,28 @@ __device__ __forceinline__ void rank3(double ax, double ay, double az, int &a0, 
 // list per segment, lv/voxelizer.py:180-206).  Out-of-grid cells are skipped by clamping the
 // loop bounds, which is what the callers' `continue` does (lv/voxelizer.py:321-322).
 
+// Row form: f(x, y, z, axis, len) receives the cells (x, y, z) + u * e_axis, u in [0, len), of one
+// innermost loop of the traversal, so that callers can issue the memory operations of a whole row
+// (typically 3-4 cells) back to back instead of one dependent atomic at a time.
+
 template <class F>
-__device__ __forceinline__ void cells_aabb(const d3 &v0, const d3 &v1, double r, int res, F &&f) {
+__device__ __forceinline__ void rows_aabb(const d3 &v0, const d3 &v1, double r, int res, F &&f) {
     // lv/voxelizer.py:116-140
     int x0 = (int)floor(fmin(v0.x, v1.x) - r), x1 = (int)floor(fmax(v0.x, v1.x) + r);
     int y0 = (int)floor(fmin(v0.y, v1.y) - r), y1 = (int)floor(fmax(v0.y, v1.y) + r);
     int z0 = (int)floor(fmin(v0.z, v1.z) - r), z1 = (int)floor(fmax(v0.z, v1.z) + r);
     x0 = max(x0, 0); y0 = max(y0, 0); z0 = max(z0, 0);
     x1 = min(x1, res - 1); y1 = min(y1, res - 1); z1 = min(z1, res - 1);
+    if (x1 < x0) return;
     for (int z = z0; z <= z1; z++)
-        for (int y = y0; y <= y1; y++)
-            for (int x = x0; x <= x1; x++) f(x, y, z);
+        for (int y = y0; y <= y1; y++) f(x0, y, z, 0, x1 - x0 + 1);
 }
 
 template <class F>
-__device__ __forceinline__ void cells_capsule(const d3 &a, const d3 &b, double r, int res, F &&f) {
+__device__ __forceinline__ void rows_capsule(const d3 &a, const d3 &b, double r, int res, F &&f) {
     // lv/voxelizer.py:143-206 (Algorithm 1 of the paper)
     d3 d{b.x - a.x, b.y - a.y, b.z - a.z};
-    if (d.x == 0.0 && d.y == 0.0 && d.z == 0.0) { cells_aabb(a, b, r, res, f); return; }
+    if (d.x == 0.0 && d.y == 0.0 && d.z == 0.0) { rows_aabb(a, b, r, res, f); return; }
     int a0, a1, a2;
     rank3(fabs(d.x), fabs(d.y), fabs(d.z), a0, a1, a2);
     double d0 = sel(d, a0), d1 = sel(d, a1), d2 = sel(d, a2);
@@ -102,16 +106,28 @@ __device__ __forceinline__ void cells_capsule(const d3 &a, const d3 &b, double r
             int j_max = min((int)floor(fmax(p0_1, p1_1) + r1), hi_j);
             int k_min = max((int)floor(fmin(p0_2, p1_2) - r2), lo_k);
             int k_max = min((int)floor(fmax(p0_2, p1_2) + r2), hi_k);
-            for (int j = j_min; j <= j_max; j++)
-                for (int k = k_min; k <= k_max; k++) {
-                    int x = a0 == 0 ? ci : (a1 == 0 ? j : k);
-                    int y = a0 == 1 ? ci : (a1 == 1 ? j : k);
-                    int z = a0 == 2 ? ci : (a1 == 2 ? j : k);
-                    f(x, y, z);
+            if (k_max >= k_min)
+                for (int j = j_min; j <= j_max; j++) {
+                    const int x = a0 == 0 ? ci : (a1 == 0 ? j : k_min);
+                    const int y = a0 == 1 ? ci : (a1 == 1 ? j : k_min);
+                    const int z = a0 == 2 ? ci : (a1 == 2 ? j : k_min);
+                    f(x, y, z, a2, k_max - k_min + 1);
                 }
         }
         t0 = t1; p0_1 = p1_1; p0_2 = p1_2;
     }
+}
+
+template <class F>
+__device__ __forceinline__ void cells_aabb(const d3 &v0, const d3 &v1, double r, int res, F &&f) {
+    rows_aabb(v0, v1, r, res, [&](int x, int y, int z, int, int len) { for (int u = 0; u < len; u++) f(x + u, y, z); });
+}
+
+template <class F>
+__device__ __forceinline__ void cells_capsule(const d3 &a, const d3 &b, double r, int res, F &&f) {
+    rows_capsule(a, b, r, res, [&](int x, int y, int z, int axis, int len) {
+        for (int u = 0; u < len; u++) f(x + (axis == 0 ? u : 0), y + (axis == 1 ? u : 0), z + (axis == 2 ? u : 0));
+    });
 }
 
 template <class F>
@@ -147,6 +163,14 @@ __device__ __forceinline__ void for_each_cell(int method, const d3 &a, const d3 
     if (method == 1) cells_capsule(a, b, rt, res, f);
     else if (method == 0) cells_dda(a, b, res, f);
     else cells_aabb(a, b, rt, res, f);
+}
+
+// f(x, y, z, axis, len); the dda method yields rows of one cell
+template <class F>
+__device__ __forceinline__ void for_each_row(int method, const d3 &a, const d3 &b, double rt, int res, F &&f) {
+    if (method == 1) rows_capsule(a, b, rt, res, f);
+    else if (method == 0) cells_dda(a, b, res, [&](int x, int y, int z) { f(x, y, z, 0, 1); });
+    else rows_aabb(a, b, rt, res, f);
 }
 
 // ----------------------------------------------------------------------------- capsule

@@ -11,10 +11,10 @@ struct RenderArgs {
     const double *verts, *normals;
     const float *verts_f;      // voxel-unit vertices rounded to f32 (conservative pre-test only)
     const uint32_t *offsets, *frags;
-    const uint8_t *bits;
+    const uint32_t *loose;     // 1 bit per fragment: this capsule cannot reach into this voxel (may be NULL)
+    const uint8_t *march;      // per voxel: 255 = occupied/visible, else the empty level (lvx_march_levels)
     const float *ao, *sh;
-    uint32_t bits_off[16];
-    int res, n_levels;
+    int res;
     lvx_camera cam;
     lvx_render_params p;
     double *rgb;
@@ -25,7 +25,7 @@ struct RenderArgs {
     double *hit_t;           // per pixel: t of the first hit, < 0 = miss
     uint32_t *need_bits;     // V/32 words: voxels whose AO/shadow some hit pixel interpolates
     uint32_t *need_list;     // compacted list of those voxels (list layout of lvx_device.cuh)
-    int guard_volumes;       // ao/sh hold values only where requested: read 1.0 where bits[] == 0
+    int guard_volumes;       // ao/sh hold values only where requested: read 1.0 where march[] != 255
 };
 
 __device__ __forceinline__ bool clip_ok(const Capsule &c, double px, double py, double pz) {
@@ -35,25 +35,7 @@ __device__ __forceinline__ bool clip_ok(const Capsule &c, double px, double py, 
     return true;
 }
 
-// Conservative miss test: every surface _ray_capsule can return a point on (cylinder body, end
-// spheres, clip disks incl. their 1e-9 slacks) lies within r + ~1e-9/r of the segment's axis
-// LINE, so a ray whose line-to-line distance from the axis exceeds r + 1e-4 cannot hit and the
-// full f64 routine would return -1.  ~25 flops, no division or square root; it removes most of
-// the tests (lists hold every segment within the 1-voxel traversal footprint, the capsule
-// itself is much thinner).  Near-parallel and degenerate cases are never rejected here.
-__device__ __forceinline__ bool surely_misses(double ox, double oy, double oz, double dx, double dy, double dz,
-                                              const d3 &a, const d3 &b, double r) {
-    const double bax = b.x - a.x, bay = b.y - a.y, baz = b.z - a.z;
-    const double baba = bax * bax + bay * bay + baz * baz;
-    const double nx = dy * baz - dz * bay, ny = dz * bax - dx * baz, nz = dx * bay - dy * bax;
-    const double nn = nx * nx + ny * ny + nz * nz;
-    if (!(baba > 1e-12) || !(nn > 1e-6 * baba)) return false;
-    const double h = (ox - a.x) * nx + (oy - a.y) * ny + (oz - a.z) * nz;
-    const double R = r + 1e-4;
-    return h * h > R * R * nn;
-}
-
-// Single-precision version used by the cooperative kernels.  It bounds the distance between the
+// Conservative miss test (single precision).  It bounds the distance between the
 // ray LINE through P (a point of the ray inside the current voxel, so all differences are a few
 // voxels long) and the SEGMENT [a, b]: every surface the f64 routine can return lies within
 // r + 3.2e-5 of the segment, the f32 evaluation (inputs rounded to f32 at magnitudes <= 1024,
@@ -77,16 +59,10 @@ __device__ __forceinline__ bool surely_misses_f32(float Px, float Py, float Pz, 
     return fmaf(qx, qx, fmaf(qy, qy, qz * qz)) > R2;
 }
 
-__device__ __forceinline__ Capsule load_capsule_lazy(const double *__restrict__ normals, int64_t i, const d3 &a,
-                                                     const d3 &b, double r, bool clip) {
-    Capsule c;
-    c.a = a; c.b = b; c.r = r; c.clip = clip;
-    if (clip) { c.n0 = ld3(normals + 3 * i); c.n1 = ld3(normals + 3 * i + 3); }
-    else { c.n0 = d3{0, 0, 0}; c.n1 = d3{0, 0, 0}; }
-    return c;
-}
-
-// lv/raytracer.py:113-222: smallest t >= 0 on the clipped capsule surface, or -1
+// lv/raytracer.py:113-222: smallest t >= 0 on the clipped capsule surface, or -1.
+// The candidate loops are deliberately NOT unrolled: the routine is executed by few lanes at a time and
+// the cooperative kernels were stalling on instruction fetch (ncu: 26 % no_instruction stalls at
+// ~7000 SASS instructions per kernel); rolled loops execute the same operations in the same order.
 __device__ double ray_capsule(double ox, double oy, double oz, double dx, double dy, double dz, const Capsule &c) {
     const double ax = c.a.x, ay = c.a.y, az = c.a.z, bx = c.b.x, by = c.b.y, bz = c.b.z, r = c.r;
     const double bax = bx - ax, bay = by - ay, baz = bz - az;
@@ -106,7 +82,7 @@ __device__ double ray_capsule(double ox, double oy, double oz, double dx, double
             const double disc = b_ * b_ - a_ * c_;
             if (disc >= 0.0) {
                 const double sq = sqrt(disc);
-#pragma unroll
+#pragma unroll 1
                 for (int k = 0; k < 2; k++) {
                     const double t = (-b_ + (k ? sq : -sq)) / a_;
                     if (t >= 0.0) {
@@ -120,7 +96,7 @@ __device__ double ray_capsule(double ox, double oy, double oz, double dx, double
             }
         }
     }
-#pragma unroll
+#pragma unroll 1
     for (int cap = 0; cap < 2; cap++) {
         const double cx = cap ? bx : ax, cy = cap ? by : ay, cz = cap ? bz : az;
         const double ocx = ox - cx, ocy = oy - cy, ocz = oz - cz;
@@ -129,7 +105,7 @@ __device__ double ray_capsule(double ox, double oy, double oz, double dx, double
         const double disc = bq * bq - cq;
         if (disc < 0.0) continue;
         const double sq = sqrt(disc);
-#pragma unroll
+#pragma unroll 1
         for (int k = 0; k < 2; k++) {
             const double t = -bq + (k ? sq : -sq);
             if (t < 0.0) continue;
@@ -141,7 +117,7 @@ __device__ double ray_capsule(double ox, double oy, double oz, double dx, double
         }
     }
     if (c.clip) {
-#pragma unroll
+#pragma unroll 1
         for (int pl = 0; pl < 2; pl++) {
             const double nx = pl ? c.n1.x : c.n0.x, ny = pl ? c.n1.y : c.n0.y, nz = pl ? c.n1.z : c.n0.z;
             const double qx = pl ? bx : ax, qy = pl ? by : ay, qz = pl ? bz : az;
@@ -203,32 +179,19 @@ __device__ __forceinline__ double voxel_exit(double ox, double oy, double oz, do
     const double ax = dx != 0.0 ? nx * inv.ix : big;
     const double ay = dy != 0.0 ? ny * inv.iy : big;
     const double az = dz != 0.0 ? nz * inv.iz : big;
+    // the axis with the smallest estimate: ONE exact division (converged across the warp) ...
     const double m = fmin(ax, fmin(ay, az));
+    const double num = m == ax ? nx : (m == ay ? ny : nz);
+    const double den = m == ax ? dx : (m == ay ? dy : dz);
+    double t = den != 0.0 ? num / den : big;
+    // ... and the exact quotient of any other axis whose estimate is within 1e-13 of it (rare)
     const double lim = m + fabs(m) * 1e-13 + 1e-290;
-    double t = big;
-    if (ax <= lim) t = fmin(t, nx / dx);
-    if (ay <= lim) t = fmin(t, ny / dy);
-    if (az <= lim) t = fmin(t, nz / dz);
-    return t;
-}
-
-// lv/raytracer.py:316-326: largest level whose node containing (x,y,z) is clear.  A parent is the OR
-// of its children, so "clear" is monotone in the level and the answer can be found from any
-// starting level (`hint`, normally the previous step's answer) instead of always climbing from 1.
-__device__ __forceinline__ bool node_clear(const RenderArgs &A, int l, int x, int y, int z) {
-    const uint32_t rl = (uint32_t)A.res >> l;
-    return A.bits[A.bits_off[l] + ((uint32_t)x >> l) + rl * (((uint32_t)y >> l) + rl * ((uint32_t)z >> l))] == 0;
-}
-__device__ __forceinline__ int empty_level(const RenderArgs &A, int x, int y, int z, int hint) {
-    const int top = A.n_levels - 1;
-    int l = hint < 1 ? 1 : (hint > top ? top : hint);
-    if (top < 1) return 0;
-    if (node_clear(A, l, x, y, z)) {
-        while (l < top && node_clear(A, l + 1, x, y, z)) l++;
-        return l;
+    if ((int)(ax <= lim) + (int)(ay <= lim) + (int)(az <= lim) > 1) {
+        if (ax <= lim) t = fmin(t, nx / dx);
+        if (ay <= lim) t = fmin(t, ny / dy);
+        if (az <= lim) t = fmin(t, nz / dz);
     }
-    do { l--; } while (l >= 1 && !node_clear(A, l, x, y, z));
-    return l;
+    return t;
 }
 
 // lv/raytracer.py:368-390 (volumes are f32, widened exactly like the reference's astype(f64))
@@ -252,7 +215,7 @@ __device__ __forceinline__ double tri3d(const float *__restrict__ vol, const uin
                 const double wx = dx ? fx : 1.0 - fx;
                 const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
                 // non-visible voxels keep ao = shadow = 1 (lv/shading.py:177-178)
-                const double val = (guard && guard[idx] == 0) ? 1.0 : (double)vol[idx];
+                const double val = (guard && guard[idx] != 255) ? 1.0 : (double)vol[idx];
                 acc += wx * wy * wz * val;
             }
         }
@@ -267,7 +230,7 @@ __device__ __forceinline__ void shade(const RenderArgs &A, const Capsule &c, dou
     const double sn = sqrt(sx * sx + sy * sy + sz * sz);
     if (sn == 0.0) { cr = cg = cb = 0.5; }
     else { cr = fabs(sx) / sn; cg = fabs(sy) / sn; cb = fabs(sz) / sn; }
-    const uint8_t *guard = A.guard_volumes ? A.bits : nullptr;
+    const uint8_t *guard = A.guard_volumes ? A.march : nullptr;
     const double ao = A.ao ? tri3d(A.ao, guard, A.res, px, py, pz) : 1.0;
     const double sh = A.sh ? tri3d(A.sh, guard, A.res, px, py, pz) : 1.0;
     double ndl = nx * A.p.light_to_source[0] + ny * A.p.light_to_source[1] + nz * A.p.light_to_source[2];
@@ -282,207 +245,140 @@ __device__ __forceinline__ uint8_t to_srgb8(double v) {   // lv/raytracer.py:94-
     return (uint8_t)(int)rint(s * 255.0);
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(128)
-k_render(const RenderArgs A) {
-    const int px = A.p.tile_x0 + blockIdx.x * 8 + (threadIdx.x & 7);
-    const int py = A.p.tile_y0 + blockIdx.y * 16 + (threadIdx.x >> 3);
-    const bool live = px < A.p.tile_x1 && py < A.p.tile_y1;
-    uint32_t n_tests = 0;
-    if (live) {
-        const int w = A.cam.width, h = A.cam.height, res = A.res;
-        // lv/raytracer.py:414-423
-        const double aspect = (double)w / (double)h;
-        const double u = (2.0 * (px + 0.5) / w - 1.0) * aspect * A.cam.tan_half_fov;
-        const double v = (1.0 - 2.0 * (py + 0.5) / h) * A.cam.tan_half_fov;
-        double dx = A.cam.fwd[0] + u * A.cam.right[0] + v * A.cam.up[0];
-        double dy = A.cam.fwd[1] + u * A.cam.right[1] + v * A.cam.up[1];
-        double dz = A.cam.fwd[2] + u * A.cam.right[2] + v * A.cam.up[2];
-        const double dn = sqrt(dx * dx + dy * dy + dz * dz);
-        dx = dx / dn; dy = dy / dn; dz = dz / dn;
-        const double ox = A.cam.pos[0], oy = A.cam.pos[1], oz = A.cam.pos[2];
-        // lv/raytracer.py:272-291
-        double t0 = 0.0, t1 = 1e30;
-        {
-            const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
-#pragma unroll
-            for (int a = 0; a < 3; a++) {
-                if (d[a] == 0.0) {
-                    if (o[a] < 0.0 || o[a] > (double)res) { t0 = 1.0; t1 = -1.0; break; }
-                } else {
-                    double ta = (0.0 - o[a]) / d[a], tb = ((double)res - o[a]) / d[a];
-                    if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
-                    if (ta > t0) t0 = ta;
-                    if (tb < t1) t1 = tb;
-                }
-            }
-        }
-        const bool clip = A.p.use_clip != 0;
-        const double r = A.p.radius;
-        const RayInv inv = make_inv(dx, dy, dz);
-        int lvl_hint = 1;
-        double out_r, out_g, out_b;
-        int32_t out_id;
-        if (MODE == 0) {
-            out_r = A.p.background[0]; out_g = A.p.background[1]; out_b = A.p.background[2];
-            out_id = -1;
-            if (t1 >= t0) {
-                double t = t0 > 0.0 ? t0 : 0.0;
-                while (t < t1) {
-                    const double tm = t + 1e-6;
-                    const int x = (int)floor(ox + dx * tm), y = (int)floor(oy + dy * tm), z = (int)floor(oz + dz * tm);
-                    if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) break;
-                    const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
-                    double te;
-                    if (A.bits[idx] != 0) {
-                        // lv/raytracer.py:430-456
-                        double best = -1.0;
-                        int64_t best_i = -1;
-                        const uint32_t fo = A.offsets[idx], fe = A.offsets[idx + 1];
-                        for (uint32_t s = fo; s < fe; s++) {
-                            const int64_t i = A.frags[s];
-                            n_tests++;
-                            const d3 va = ld3(A.verts + 3 * i), vb = ld3(A.verts + 3 * i + 3);
-                            if (surely_misses(ox, oy, oz, dx, dy, dz, va, vb, r)) continue;
-                            const Capsule c = load_capsule_lazy(A.normals, i, va, vb, r, clip);
-                            const double tt = ray_capsule(ox, oy, oz, dx, dy, dz, c);
-                            if (tt < 0.0) continue;
-                            const int hx = (int)floor(ox + dx * tt), hy = (int)floor(oy + dy * tt), hz = (int)floor(oz + dz * tt);
-                            if (hx != x || hy != y || hz != z) continue;   // belongs to another voxel's list
-                            if (best < 0.0 || tt < best) { best = tt; best_i = i; }
-                        }
-                        if (best >= 0.0) {
-                            const double hx = ox + dx * best, hy = oy + dy * best, hz = oz + dz * best;
-                            const Capsule c = load_capsule(A.verts, A.normals, best_i, r, clip);
-                            double nx, ny, nz;
-                            capsule_normal(hx, hy, hz, c, nx, ny, nz);
-                            shade(A, c, nx, ny, nz, hx, hy, hz, out_r, out_g, out_b);
-                            out_id = (int32_t)best_i;
-                            break;
-                        }
-                        te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
-                    } else {
-                        const int l = lvl_hint = empty_level(A, x, y, z, lvl_hint);
-                        te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, l);
-                    }
-                    t = te > t ? te : t + 1e-6;
-                }
-            }
-        } else {
-            double col_r = 0.0, col_g = 0.0, col_b = 0.0, acc_a = 0.0;
-            int64_t first_hit = -1;
-            int64_t keybuf[64];
-            double tbuf[64];
-            int32_t ibuf[64];
-            const int kslots = A.p.k;
-            const bool early = A.p.early_termination != 0;
-            const double alpha = A.p.alpha;
-            if (t1 >= t0) {
-                double t = t0 > 0.0 ? t0 : 0.0;
-                while (t < t1) {
-                    if (early && acc_a >= 0.999) break;
-                    const double tm = t + 1e-6;
-                    const int x = (int)floor(ox + dx * tm), y = (int)floor(oy + dy * tm), z = (int)floor(oz + dz * tm);
-                    if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) break;
-                    const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
-                    if (A.bits[idx] == 0) {
-                        const int l = lvl_hint = empty_level(A, x, y, z, lvl_hint);
-                        const double te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, l);
-                        t = te > t ? te : t + 1e-6;
-                        continue;
-                    }
-                    const double te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
-                    const double t_enter = t, span = te - t_enter;
-                    const double inv_span = span > 0.0 ? 65535.0 / span : 0.0;
-                    const uint32_t fo = A.offsets[idx], fn = A.offsets[idx + 1] - fo;
-                    int64_t last_key = -1;
-                    for (;;) {
-                        int kept = 0;
-                        uint32_t accepted = 0;
-                        for (uint32_t s = 0; s < fn; s++) {
-                            const int64_t i = A.frags[fo + s];
-                            n_tests++;
-                            const d3 va = ld3(A.verts + 3 * i), vb = ld3(A.verts + 3 * i + 3);
-                            if (surely_misses(ox, oy, oz, dx, dy, dz, va, vb, r)) continue;
-                            const Capsule c = load_capsule_lazy(A.normals, i, va, vb, r, clip);
-                            const double tt = ray_capsule(ox, oy, oz, dx, dy, dz, c);
-                            if (tt < 0.0) continue;
-                            const int hx = (int)floor(ox + dx * tt), hy = (int)floor(oy + dy * tt), hz = (int)floor(oz + dz * tt);
-                            if (hx != x || hy != y || hz != z) continue;
-                            int64_t q = (int64_t)((tt - t_enter) * inv_span);   // int(): truncation
-                            if (q < 0) q = 0; else if (q > 65535) q = 65535;
-                            const int64_t key = (q << 16) | (int64_t)s;
-                            if (key <= last_key) continue;
-                            accepted++;
-                            int j;
-                            if (kept < kslots) { j = kept; kept++; }
-                            else if (key < keybuf[kslots - 1]) j = kslots - 1;
-                            else continue;
-                            while (j > 0 && keybuf[j - 1] > key) {
-                                keybuf[j] = keybuf[j - 1]; tbuf[j] = tbuf[j - 1]; ibuf[j] = ibuf[j - 1];
-                                j--;
-                            }
-                            keybuf[j] = key; tbuf[j] = tt; ibuf[j] = (int32_t)i;
-                        }
-                        for (int j = 0; j < kept; j++) {
-                            if (early && acc_a >= 0.999) break;
-                            const double tt = tbuf[j];
-                            const int64_t i = ibuf[j];
-                            const double hx = ox + dx * tt, hy = oy + dy * tt, hz = oz + dz * tt;
-                            const Capsule c = load_capsule(A.verts, A.normals, i, r, clip);
-                            double nx, ny, nz, cr, cg, cb;
-                            capsule_normal(hx, hy, hz, c, nx, ny, nz);
-                            shade(A, c, nx, ny, nz, hx, hy, hz, cr, cg, cb);
-                            const double wgt = (1.0 - acc_a) * alpha;
-                            col_r += wgt * cr; col_g += wgt * cg; col_b += wgt * cb;
-                            acc_a += wgt;
-                            if (first_hit < 0) first_hit = i;
-                        }
-                        if (accepted <= (uint32_t)kslots) break;
-                        if (early && acc_a >= 0.999) break;
-                        last_key = keybuf[kslots - 1];
-                    }
-                    t = te > t ? te : t + 1e-6;
-                }
-            }
-            out_r = col_r + (1.0 - acc_a) * A.p.background[0];
-            out_g = col_g + (1.0 - acc_a) * A.p.background[1];
-            out_b = col_b + (1.0 - acc_a) * A.p.background[2];
-            out_id = (int32_t)first_hit;
-        }
-        const int64_t pix = (int64_t)py * w + px;
-        if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
-        if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
-        A.hit_id[pix] = out_id;
-    }
-    uint64_t tests = warp_sum_u64(n_tests);
-    if ((threadIdx.x & 31) == 0 && tests)
-        atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)tests);
-}
-
-// ----------------------------------------------------------------------------- opaque, warp-cooperative
-// The per-pixel loop above spends most of its instructions in the heavy f64 intersection with 2-3
-// of 32 lanes active (ncu: profiles/r01c).  This kernel keeps the reference's per-ray semantics
-// (lv/raytracer.py:459-515) but shares the work of a warp's 8x4 pixel tile:
-//   1. every unfinished ray marches (hierarchical skip) to its next occupied voxel;
-//   2. the (ray, fragment) pairs of all 32 rays are flattened with a warp prefix sum and dealt
-//      round-robin to the lanes -> the cheap conservative reject runs fully converged, fragment
-//      ids are read coalesced;
-//   3. pairs that survive the reject are compacted into a shared-memory queue; whenever 32 are
-//      queued the full clipped ray-capsule routine runs on all 32 lanes at once;
-//   4. hits are folded on the owning lane by (t, slot) -- "min t, first slot wins ties" (453) --
-//      and rays without a hit step to the voxel exit.
-// Shading runs once, after the loop, for all hit rays together.
+// ----------------------------------------------------------------------------- warp-cooperative tracing
+// A per-pixel loop spends most of its instructions in the heavy f64 intersection with 2-3 of 32
+// lanes active (ncu: profiles/r01c).  The kernels below keep the reference's per-ray semantics
+// (lv/raytracer.py:459-515, 518-645) but share the work of a warp's 8x4 pixel tile.  Per round:
+//   1. every unfinished ray marches to its next occupied voxel: one byte of the march table per
+//      DDA step says "occupied" or how large the surrounding empty node is (hierarchical skip);
+//   2./3. stage A: each lane reads the loose-bit words of its voxel's list (abuffer.cu: a set bit
+//      means the capsule cannot reach into this voxel) and the lanes push their remaining (tight)
+//      fragments, one per lane per step, into queue A (ballot + popc compaction);
+//   4. stage B: 32 queued pairs at a time read the fragment's segment (f32 copy) and run the cheap
+//      conservative miss test fully converged; survivors are compacted into queue B;
+//   5. stage C: 32 queued pairs at a time run the full clipped f64 ray-capsule routine; accepted
+//      hits are folded on the owning lane (opaque: min t, first slot wins ties -- 453; transparent:
+//      per-warp hit list -> per-lane k-slot buffers).
+// Pairs are taken from the back of the queues; the order of processing never matters because
+// hits are folded with an order-independent rule.
 constexpr int RC_WARPS = 4;
+#define LVX_FULL 0xffffffffu
 
-struct WarpShared {
+struct PairQueues {
     double dir[3][32];
     float dirf[3][32], pf[3][32];   // f32 direction and a ray point inside the current voxel
     int vox[3][32];
-    uint32_t fo[32];
-    uint32_t prefix[33];
-    uint32_t q_i[64];
-    uint32_t q_rs[64];
+    uint32_t qa_rs[64], qa_g[64];   // queue A: (ray << 16 | slot), global fragment index
+    uint32_t qb_rs[64], qb_i[64];   // queue B: (ray << 16 | slot), segment index
+};
+
+// Runs stages A-C for one round.  `n` = this lane's list length (0 if the ray is idle), `fo` its
+// first fragment; `stage_c(valid, rs, seg)` is called with 32 (or fewer, at the end) queue-B entries.
+// Returns the number of (ray, fragment) pairs of the round (= the reference's test count).
+template <class F>
+__device__ __forceinline__ uint32_t run_pairs(const RenderArgs &A, PairQueues &S, uint32_t n, uint32_t fo, int lane,
+                                              float R2f, F &&stage_c) {
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t qa = 0, qb = 0;
+
+    auto drain_b = [&]() {
+        const uint32_t take = qb < 32 ? qb : 32, base = qb - take;
+        const bool valid = (uint32_t)lane < take;
+        const uint32_t rs = valid ? S.qb_rs[base + lane] : 0, ii = valid ? S.qb_i[base + lane] : 0;
+        qb = base;
+        __syncwarp();
+        stage_c(valid, rs, ii);
+    };
+    // ---- stage B: conservative f32 miss test on (up to) 32 queued pairs, survivors -> queue B
+    auto drain_a = [&]() {
+        const uint32_t take = qa < 32 ? qa : 32, base = qa - take;
+        bool pass = false;
+        uint32_t rs1 = 0, ii = 0;
+        if ((uint32_t)lane < take) {
+            rs1 = S.qa_rs[base + lane];
+            ii = A.frags[S.qa_g[base + lane]];
+            const uint32_t rr = rs1 >> 16;
+            pass = !surely_misses_f32(S.pf[0][rr], S.pf[1][rr], S.pf[2][rr], S.dirf[0][rr], S.dirf[1][rr],
+                                      S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
+        }
+        qa = base;
+        const uint32_t mb = __ballot_sync(LVX_FULL, pass);
+        if (pass) {
+            const uint32_t pos = qb + __popc(mb & lt_mask);
+            S.qb_rs[pos] = rs1; S.qb_i[pos] = ii;
+        }
+        qb += __popc(mb);
+        __syncwarp();
+        while (qb >= 32) drain_b();          // ---- stage C
+    };
+
+    // ---- stage A: every lane walks the loose-bit words of its own list; in each step all lanes
+    // that still have a tight fragment in their current word push one pair (their lowest bit).
+    // Loose fragments are never enumerated at all.
+    const uint32_t last = fo + n - 1;                       // valid when n > 0
+    const uint32_t w0 = fo >> 5, nw = n ? (last >> 5) - w0 + 1 : 0;
+    const uint32_t maxw = __reduce_max_sync(LVX_FULL, nw);
+    for (uint32_t wi = 0; wi < maxw; wi++) {
+        uint32_t mask = 0;
+        const uint32_t w = w0 + wi;
+        if (wi < nw) {
+            const uint32_t lw = A.loose ? A.loose[w] : 0u;
+            const uint32_t lo = wi == 0 ? (fo & 31u) : 0u;
+            const uint32_t hi = (w == (last >> 5)) ? (last & 31u) : 31u;     // inclusive
+            mask = ~lw & (0xffffffffu >> (31u - hi)) & (0xffffffffu << lo);
+        }
+        for (;;) {
+            const uint32_t ma = __ballot_sync(LVX_FULL, mask != 0);
+            if (ma == 0) break;
+            if (mask) {
+                const uint32_t g = (w << 5) + (uint32_t)(__ffs(mask) - 1);
+                mask &= mask - 1;
+                const uint32_t pos = qa + __popc(ma & lt_mask);
+                S.qa_rs[pos] = ((uint32_t)lane << 16) | (g - fo); S.qa_g[pos] = g;
+            }
+            qa += __popc(ma);
+            __syncwarp();
+            if (qa >= 32) drain_a();
+        }
+    }
+    while (qa > 0) drain_a();
+    while (qb > 0) drain_b();
+    return __reduce_add_sync(LVX_FULL, n);
+}
+
+// lv/raytracer.py:414-423 + 272-291: the pixel's ray and its parameter range inside the grid
+__device__ __forceinline__ bool setup_ray(const RenderArgs &A, int px, int py, double &dx, double &dy, double &dz,
+                                          double &t, double &t1) {
+    const int w = A.cam.width, h = A.cam.height, res = A.res;
+    const double aspect = (double)w / (double)h;
+    const double u = (2.0 * (px + 0.5) / w - 1.0) * aspect * A.cam.tan_half_fov;
+    const double v = (1.0 - 2.0 * (py + 0.5) / h) * A.cam.tan_half_fov;
+    dx = A.cam.fwd[0] + u * A.cam.right[0] + v * A.cam.up[0];
+    dy = A.cam.fwd[1] + u * A.cam.right[1] + v * A.cam.up[1];
+    dz = A.cam.fwd[2] + u * A.cam.right[2] + v * A.cam.up[2];
+    const double dn = sqrt(dx * dx + dy * dy + dz * dz);
+    dx = dx / dn; dy = dy / dn; dz = dz / dn;
+    double t0 = 0.0;
+    t1 = 1e30;
+    const double o[3] = {A.cam.pos[0], A.cam.pos[1], A.cam.pos[2]}, d[3] = {dx, dy, dz};
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        if (d[a] == 0.0) {
+            if (o[a] < 0.0 || o[a] > (double)res) { t0 = 1.0; t1 = -1.0; break; }
+        } else {
+            double ta = (0.0 - o[a]) / d[a], tb = ((double)res - o[a]) / d[a];
+            if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
+            if (ta > t0) t0 = ta;
+            if (tb < t1) t1 = tb;
+        }
+    }
+    t = t0 > 0.0 ? t0 : 0.0;
+    return t1 >= t0;
+}
+
+// ----------------------------------------------------------------------------- opaque
+struct WarpShared {
+    PairQueues q;
     double hit_t[32];
     uint32_t hit_s[32], hit_i[32];
 };
@@ -500,45 +396,17 @@ k_render_opaque_coop(const RenderArgs A) {
     const int px = A.p.tile_x0 + blockIdx.x * (8 * RC_WARPS) + warp * 8 + (lane & 7);
     const int py = A.p.tile_y0 + blockIdx.y * 4 + (lane >> 3);
     const bool live = px < A.p.tile_x1 && py < A.p.tile_y1;
-    const int w = A.cam.width, h = A.cam.height, res = A.res;
+    const int w = A.cam.width, res = A.res;
     const double ox = A.cam.pos[0], oy = A.cam.pos[1], oz = A.cam.pos[2];
     const bool clip = A.p.use_clip != 0;
     const double r = A.p.radius;
     double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
     bool active = false;
-    if (live) {
-        // lv/raytracer.py:414-423
-        const double aspect = (double)w / (double)h;
-        const double u = (2.0 * (px + 0.5) / w - 1.0) * aspect * A.cam.tan_half_fov;
-        const double v = (1.0 - 2.0 * (py + 0.5) / h) * A.cam.tan_half_fov;
-        dx = A.cam.fwd[0] + u * A.cam.right[0] + v * A.cam.up[0];
-        dy = A.cam.fwd[1] + u * A.cam.right[1] + v * A.cam.up[1];
-        dz = A.cam.fwd[2] + u * A.cam.right[2] + v * A.cam.up[2];
-        const double dn = sqrt(dx * dx + dy * dy + dz * dz);
-        dx = dx / dn; dy = dy / dn; dz = dz / dn;
-        // lv/raytracer.py:272-291
-        double t0 = 0.0;
-        t1 = 1e30;
-        const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
-#pragma unroll
-        for (int a = 0; a < 3; a++) {
-            if (d[a] == 0.0) {
-                if (o[a] < 0.0 || o[a] > (double)res) { t0 = 1.0; t1 = -1.0; break; }
-            } else {
-                double ta = (0.0 - o[a]) / d[a], tb = ((double)res - o[a]) / d[a];
-                if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
-                if (ta > t0) t0 = ta;
-                if (tb < t1) t1 = tb;
-            }
-        }
-        active = t1 >= t0;
-        t = t0 > 0.0 ? t0 : 0.0;
-    }
-    S.dir[0][lane] = dx; S.dir[1][lane] = dy; S.dir[2][lane] = dz;
-    S.dirf[0][lane] = (float)dx; S.dirf[1][lane] = (float)dy; S.dirf[2][lane] = (float)dz;
+    if (live) active = setup_ray(A, px, py, dx, dy, dz, t, t1);
+    S.q.dir[0][lane] = dx; S.q.dir[1][lane] = dy; S.q.dir[2][lane] = dz;
+    S.q.dirf[0][lane] = (float)dx; S.q.dirf[1][lane] = (float)dy; S.q.dirf[2][lane] = (float)dz;
     const float R2f = ((float)r + 2e-3f) * ((float)r + 2e-3f);
     const RayInv inv = make_inv(dx, dy, dz);
-    int lvl_hint = 1;
     double best_t = -1.0;      // final hit of this lane's ray
     int64_t best_i = -1;
     uint64_t n_tests = 0;
@@ -546,7 +414,7 @@ k_render_opaque_coop(const RenderArgs A) {
 
     for (;;) {
         // ---- 1. march to the next occupied voxel (lv/raytracer.py:475-482, 506-509)
-        uint32_t n = 0;
+        uint32_t n = 0, fo = 0;
         double te = 0.0;
         int x = 0, y = 0, z = 0;
         if (active) {
@@ -556,107 +424,58 @@ k_render_opaque_coop(const RenderArgs A) {
                 x = (int)floor(ox + dx * tm); y = (int)floor(oy + dy * tm); z = (int)floor(oz + dz * tm);
                 if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) { active = false; break; }
                 const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
-                if (A.bits[idx] != 0) {
-                    const uint32_t fo = A.offsets[idx];
+                const int lv = A.march[idx];
+                if (lv == 255) {
+                    fo = A.offsets[idx];
                     n = A.offsets[idx + 1] - fo;
-                    S.fo[lane] = fo;
                     te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
                     break;
                 }
-                const int l = lvl_hint = empty_level(A, x, y, z, lvl_hint);
-                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, l);
+                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, lv);
                 t = tl > t ? tl : t + 1e-6;
             }
         }
-        if (__ballot_sync(0xffffffffu, active) == 0) break;
-        S.vox[0][lane] = x; S.vox[1][lane] = y; S.vox[2][lane] = z;
+        if (__ballot_sync(LVX_FULL, active) == 0) break;
+        S.q.vox[0][lane] = x; S.q.vox[1][lane] = y; S.q.vox[2][lane] = z;
         {   // a point of the ray inside the voxel (its centre-most parameter), for the f32 pre-test
             const double tc = 0.5 * (t + te);
-            S.pf[0][lane] = (float)(ox + dx * tc); S.pf[1][lane] = (float)(oy + dy * tc); S.pf[2][lane] = (float)(oz + dz * tc);
+            S.q.pf[0][lane] = (float)(ox + dx * tc); S.q.pf[1][lane] = (float)(oy + dy * tc); S.q.pf[2][lane] = (float)(oz + dz * tc);
         }
-        // ---- 2. flatten (ray, fragment) pairs
-        uint32_t inc = active ? n : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += v;
-        }
-        S.prefix[lane + 1] = inc;
-        if (lane == 0) S.prefix[0] = 0;
-        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
-        if (lane == 0) n_tests += T;
         double cur_t = -1.0;           // best hit of this lane's ray in this voxel
         uint32_t cur_s = 0xffffffffu, cur_i = 0;
-        uint32_t qn = 0, own = 0;
-        __syncwarp();
-        for (uint32_t p0 = 0; p0 < T || qn > 0; p0 += 32) {
-            const uint32_t p = p0 + lane;
-            bool pass = false;
-            uint32_t rr = 0, ss = 0, ii = 0;
-            if (p < T) {
-                // owner ray: largest rr with prefix[rr] <= p
-                while (S.prefix[own + 1] <= p) own++;       // owner ray: prefix[own] <= p < prefix[own+1]
-                rr = own;
-                ss = p - S.prefix[rr];
-                ii = A.frags[S.fo[rr] + ss];
-                pass = !surely_misses_f32(S.pf[0][rr], S.pf[1][rr], S.pf[2][rr], S.dirf[0][rr], S.dirf[1][rr],
-                                          S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
+        const uint32_t T = run_pairs(A, S.q, active ? n : 0u, fo, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii) {
+            bool hit = false;
+            double ht = 0.0;
+            const uint32_t hr = rs >> 16, hs = rs & 0xFFFFu;
+            if (valid) {
+                const double ddx = S.q.dir[0][hr], ddy = S.q.dir[1][hr], ddz = S.q.dir[2][hr];
+                const Capsule c = load_capsule(A.verts, A.normals, (int64_t)ii, r, clip);
+                ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
+                if (ht >= 0.0) {   // lv/raytracer.py:446-452: the hit must lie in the ray's current voxel
+                    const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
+                    hit = hx == S.q.vox[0][hr] && hy == S.q.vox[1][hr] && hz == S.q.vox[2][hr];
+                }
             }
-            // ---- 3. compact survivors into the queue
-            const uint32_t m = __ballot_sync(0xffffffffu, pass);
-            if (pass) {
-                const uint32_t pos = qn + __popc(m & ((1u << lane) - 1u));
-                S.q_i[pos] = ii;
-                S.q_rs[pos] = (rr << 16) | ss;
-            }
-            qn += __popc(m);
+            // fold hits on the owning lanes: min t, then lowest slot (lv/raytracer.py:453)
+            uint32_t hm = __ballot_sync(LVX_FULL, hit);
+            if (hm == 0) return;
+            if (hit) { S.hit_t[lane] = ht; S.hit_s[lane] = hs; S.hit_i[lane] = ii; }
             __syncwarp();
-            const bool flush = p0 + 32 >= T;          // last batch of pairs: drain what is left
-            if (qn >= 32 || (flush && qn > 0)) {
-                const uint32_t take = qn < 32 ? qn : 32;
-                bool hit = false;
-                double ht = 0.0;
-                uint32_t hr = 0, hs = 0, hi_ = 0;
-                if (lane < take) {
-                    hi_ = S.q_i[lane];
-                    const uint32_t rs = S.q_rs[lane];
-                    hr = rs >> 16; hs = rs & 0xFFFFu;
-                    const double ddx = S.dir[0][hr], ddy = S.dir[1][hr], ddz = S.dir[2][hr];
-                    const Capsule c = load_capsule(A.verts, A.normals, (int64_t)hi_, r, clip);
-                    ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
-                    if (ht >= 0.0) {   // lv/raytracer.py:446-452: the hit must lie in the ray's current voxel
-                        const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
-                        hit = hx == S.vox[0][hr] && hy == S.vox[1][hr] && hz == S.vox[2][hr];
+            while (hm) {
+                const int src = __ffs(hm) - 1;
+                hm &= hm - 1;
+                const uint32_t owner = __shfl_sync(LVX_FULL, hr, src);
+                if ((uint32_t)lane == owner) {
+                    const double tt = S.hit_t[src];
+                    const uint32_t s2 = S.hit_s[src];
+                    if (cur_t < 0.0 || tt < cur_t || (tt == cur_t && s2 < cur_s)) {
+                        cur_t = tt; cur_s = s2; cur_i = S.hit_i[src];
                     }
                 }
-                __syncwarp();
-                // move the queue tail down
-                uint32_t mv_i = 0, mv_rs = 0;
-                const bool mv = lane + 32 < qn;
-                if (mv) { mv_i = S.q_i[lane + 32]; mv_rs = S.q_rs[lane + 32]; }
-                __syncwarp();
-                if (mv) { S.q_i[lane] = mv_i; S.q_rs[lane] = mv_rs; }
-                qn -= take;
-                // ---- 4. fold hits on the owning lanes: min t, then lowest slot (lv/raytracer.py:453)
-                uint32_t hm = __ballot_sync(0xffffffffu, hit);
-                if (hit) { S.hit_t[lane] = ht; S.hit_s[lane] = hs; S.hit_i[lane] = hi_; }
-                __syncwarp();
-                while (hm) {
-                    const int src = __ffs(hm) - 1;
-                    hm &= hm - 1;
-                    const uint32_t owner = __shfl_sync(0xffffffffu, hr, src);
-                    if ((uint32_t)lane == owner) {
-                        const double tt = S.hit_t[src];
-                        const uint32_t s2 = S.hit_s[src];
-                        if (cur_t < 0.0 || tt < cur_t || (tt == cur_t && s2 < cur_s)) {
-                            cur_t = tt; cur_s = s2; cur_i = S.hit_i[src];
-                        }
-                    }
-                }
-                __syncwarp();
             }
-            if (flush && qn == 0) break;
-        }
+            __syncwarp();
+        });
+        if (lane == 0) n_tests += T;
         if (active) {
             if (cur_t >= 0.0) { best_t = cur_t; best_i = cur_i; active = false; }
             else t = te > t ? te : t + 1e-6;
@@ -683,8 +502,7 @@ k_render_opaque_coop(const RenderArgs A) {
         }
     } else {
         // Shading on demand: record the hit, and request AO/shadow for the (visible) voxels its
-        // trilinear lookup will read (lv/raytracer.py:368-390).  New requests are gathered per
-        // block in shared memory so the global list counter sees one atomic per block.
+        // trilinear lookup will read (lv/raytracer.py:368-390).
         // (warp-level only: a block-wide barrier here would park finished warps until the slowest
         // warp of the block leaves the trace loop)
         uint32_t items[8];
@@ -703,7 +521,7 @@ k_render_opaque_coop(const RenderArgs A) {
                     const int Z = min(max(iz + (k >> 2), 0), res - 1);
                     const uint32_t idx = (uint32_t)X + (uint32_t)res * ((uint32_t)Y + (uint32_t)res * (uint32_t)Z);
                     bool fresh = false;
-                    if (A.bits[idx] != 0) {
+                    if (A.march[idx] == 255) {
                         const uint32_t bit = 1u << (idx & 31);
                         fresh = (atomicOr(&A.need_bits[idx >> 5], bit) & bit) == 0;
                     }
@@ -717,15 +535,15 @@ k_render_opaque_coop(const RenderArgs A) {
         uint32_t incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            const uint32_t v = __shfl_up_sync(LVX_FULL, incl, o);
             if (lane >= o) incl += v;
         }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t total = __shfl_sync(LVX_FULL, incl, 31);
         if (total) {
             unsigned long long b = 0;
             if (lane == 0)
                 b = atomicAdd(reinterpret_cast<unsigned long long *>(A.need_list), (unsigned long long)total);
-            b = __shfl_sync(0xffffffffu, b, 0);
+            b = __shfl_sync(LVX_FULL, b, 0);
             uint32_t pos = (uint32_t)b + incl - mine;
 #pragma unroll
             for (int k = 0; k < 8; k++)
@@ -736,32 +554,38 @@ k_render_opaque_coop(const RenderArgs A) {
         atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)n_tests);
 }
 
-// ----------------------------------------------------------------------------- transparent, warp-cooperative
-// Same work sharing as the opaque kernel for lv/raytracer.py:518-645.  Per round every active ray
-// sits in one occupied voxel; the flattened (ray, fragment) pairs are rejected/intersected by all
-// lanes; in-voxel hits become (key = depth16 << 16 | slot, t, segment) records in a per-warp list,
+// ----------------------------------------------------------------------------- transparent
+// Same work sharing for lv/raytracer.py:518-645.  Per round every active ray sits in one occupied
+// voxel.  In-voxel hits become (key = depth16 << 16 | slot, t, segment) records in a per-warp list,
 // which the owning lanes drain into their private k-slot buffers.  The k smallest keys above
 // `last_key` are a set, so the insertion order does not matter (keys are unique: the slot is in
 // the low bits) and the reference's result is reproduced exactly, including the re-scan of a
 // voxel when more than k hits were accepted (the ray then stays in the voxel for another round,
 // and its tests are counted again like the reference does).
-constexpr int HL_CAP = 128;
+//
+// Deferred shading.  Control flow only needs the accumulated alpha, which depends on the NUMBER
+// of blended hits (A += (1-A)*alpha), not on their colour.  So the blend step just fixes each
+// hit's weight w = (1-A)*alpha and appends (ray, w, t, segment) to a per-warp FIFO; whenever 32
+// entries are queued their normals, AO/shadow lookups and colours are evaluated on all 32 lanes
+// at once and the owning lanes add w*colour in FIFO order -- per ray that is the reference's
+// order of additions, so the f64 sums keep their bits.
+constexpr int HL_CAP = 96;
 
 struct WarpSharedT {
-    double dir[3][32];
-    float dirf[3][32], pf[3][32];
+    PairQueues q;
     double t_enter[32], inv_span[32];
-    int vox[3][32];
-    uint32_t fo[32];
-    uint32_t prefix[33];
-    uint32_t q_i[64];
-    uint32_t q_rs[64];
     double hl_t[HL_CAP];
     uint32_t hl_key[HL_CAP], hl_i[HL_CAP];
     uint8_t hl_r[HL_CAP];
+    double d_w[64], d_t[64];        // deferred shading FIFO
+    uint32_t d_i[64], d_ray[64];
+    double d_c[3][32];              // w * colour of the batch being folded
 };
 
-__global__ void __launch_bounds__(RC_WARPS * 32)
+#ifndef LVX_RT_MINB
+#define LVX_RT_MINB 4
+#endif
+__global__ void __launch_bounds__(RC_WARPS * 32, LVX_RT_MINB)
 k_render_transparent_coop(const RenderArgs A) {
     __shared__ WarpSharedT sh_all[RC_WARPS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -769,58 +593,63 @@ k_render_transparent_coop(const RenderArgs A) {
     const int px = A.p.tile_x0 + blockIdx.x * (8 * RC_WARPS) + warp * 8 + (lane & 7);
     const int py = A.p.tile_y0 + blockIdx.y * 4 + (lane >> 3);
     const bool live = px < A.p.tile_x1 && py < A.p.tile_y1;
-    const int w = A.cam.width, h = A.cam.height, res = A.res;
+    const int w = A.cam.width, res = A.res;
     const double ox = A.cam.pos[0], oy = A.cam.pos[1], oz = A.cam.pos[2];
     const bool clip = A.p.use_clip != 0;
     const double r = A.p.radius;
     const int kslots = A.p.k;
     const bool early = A.p.early_termination != 0;
     const double alpha = A.p.alpha;
+    const uint32_t lt_mask = (1u << lane) - 1u;
     double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
     bool active = false;
-    if (live) {
-        const double aspect = (double)w / (double)h;
-        const double u = (2.0 * (px + 0.5) / w - 1.0) * aspect * A.cam.tan_half_fov;
-        const double v = (1.0 - 2.0 * (py + 0.5) / h) * A.cam.tan_half_fov;
-        dx = A.cam.fwd[0] + u * A.cam.right[0] + v * A.cam.up[0];
-        dy = A.cam.fwd[1] + u * A.cam.right[1] + v * A.cam.up[1];
-        dz = A.cam.fwd[2] + u * A.cam.right[2] + v * A.cam.up[2];
-        const double dn = sqrt(dx * dx + dy * dy + dz * dz);
-        dx = dx / dn; dy = dy / dn; dz = dz / dn;
-        double t0 = 0.0;
-        t1 = 1e30;
-        const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
-#pragma unroll
-        for (int a = 0; a < 3; a++) {
-            if (d[a] == 0.0) {
-                if (o[a] < 0.0 || o[a] > (double)res) { t0 = 1.0; t1 = -1.0; break; }
-            } else {
-                double ta = (0.0 - o[a]) / d[a], tb = ((double)res - o[a]) / d[a];
-                if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
-                if (ta > t0) t0 = ta;
-                if (tb < t1) t1 = tb;
-            }
-        }
-        active = t1 >= t0;
-        t = t0 > 0.0 ? t0 : 0.0;
-    }
-    S.dir[0][lane] = dx; S.dir[1][lane] = dy; S.dir[2][lane] = dz;
-    S.dirf[0][lane] = (float)dx; S.dirf[1][lane] = (float)dy; S.dirf[2][lane] = (float)dz;
+    if (live) active = setup_ray(A, px, py, dx, dy, dz, t, t1);
+    S.q.dir[0][lane] = dx; S.q.dir[1][lane] = dy; S.q.dir[2][lane] = dz;
+    S.q.dirf[0][lane] = (float)dx; S.q.dirf[1][lane] = (float)dy; S.q.dirf[2][lane] = (float)dz;
     const float R2f = ((float)r + 2e-3f) * ((float)r + 2e-3f);
     const RayInv inv = make_inv(dx, dy, dz);
-    int lvl_hint = 1;
     double col_r = 0.0, col_g = 0.0, col_b = 0.0, acc_a = 0.0;
     int64_t first_hit = -1;
     uint32_t keybuf[64], ibuf[64];
     double tbuf[64];
     uint64_t n_tests = 0;
+    uint32_t qd = 0;           // entries in the deferred shading FIFO
     // per-voxel state of this lane's ray
     bool repeat = false;
     int64_t last_key = -1;
-    uint32_t n = 0;
+    uint32_t n = 0, fo = 0;
     double te = 0.0;
     int x = 0, y = 0, z = 0;
     __syncwarp();
+
+    // shades the first min(qd, 32) FIFO entries and folds w*colour into the owners' sums
+    auto shade_batch = [&]() {
+        const uint32_t take = qd < 32 ? qd : 32;
+        if ((uint32_t)lane < take) {
+            const uint32_t rr = S.d_ray[lane];
+            const int64_t i = S.d_i[lane];
+            const double tt = S.d_t[lane], wgt = S.d_w[lane];
+            const double ddx = S.q.dir[0][rr], ddy = S.q.dir[1][rr], ddz = S.q.dir[2][rr];
+            const double hx = ox + ddx * tt, hy = oy + ddy * tt, hz = oz + ddz * tt;   // lv/raytracer.py:612-620
+            const Capsule c = load_capsule(A.verts, A.normals, i, r, clip);
+            double nx, ny, nz, cr, cg, cb;
+            capsule_normal(hx, hy, hz, c, nx, ny, nz);
+            shade(A, c, nx, ny, nz, hx, hy, hz, cr, cg, cb);
+            S.d_c[0][lane] = wgt * cr; S.d_c[1][lane] = wgt * cg; S.d_c[2][lane] = wgt * cb;
+        }
+        __syncwarp();
+        for (uint32_t e = 0; e < take; e++)
+            if (S.d_ray[e] == (uint32_t)lane) { col_r += S.d_c[0][e]; col_g += S.d_c[1][e]; col_b += S.d_c[2][e]; }
+        // move the tail (at most 31 entries) to the front
+        const bool mv = (uint32_t)lane + 32 < qd;
+        double mw = 0.0, mt = 0.0;
+        uint32_t mi = 0, mr = 0;
+        if (mv) { mw = S.d_w[lane + 32]; mt = S.d_t[lane + 32]; mi = S.d_i[lane + 32]; mr = S.d_ray[lane + 32]; }
+        __syncwarp();
+        if (mv) { S.d_w[lane] = mw; S.d_t[lane] = mt; S.d_i[lane] = mi; S.d_ray[lane] = mr; }
+        qd -= take;
+        __syncwarp();
+    };
 
     for (;;) {
         // ---- 1. next occupied voxel (or stay for a re-scan)
@@ -831,10 +660,10 @@ k_render_transparent_coop(const RenderArgs A) {
                 x = (int)floor(ox + dx * tm); y = (int)floor(oy + dy * tm); z = (int)floor(oz + dz * tm);
                 if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) { active = false; break; }
                 const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
-                if (A.bits[idx] != 0) {
-                    const uint32_t fo = A.offsets[idx];
+                const int lv = A.march[idx];
+                if (lv == 255) {
+                    fo = A.offsets[idx];
                     n = A.offsets[idx + 1] - fo;
-                    S.fo[lane] = fo;
                     te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
                     const double span = te - t;                  // t_enter = t (lv/raytracer.py:557-560)
                     S.t_enter[lane] = t;
@@ -842,32 +671,18 @@ k_render_transparent_coop(const RenderArgs A) {
                     last_key = -1;
                     break;
                 }
-                const int l = lvl_hint = empty_level(A, x, y, z, lvl_hint);
-                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, l);
+                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, lv);
                 t = tl > t ? tl : t + 1e-6;
             }
         }
-        if (__ballot_sync(0xffffffffu, active) == 0) break;
-        S.vox[0][lane] = x; S.vox[1][lane] = y; S.vox[2][lane] = z;
-        {   // a point of the ray inside the voxel (its centre-most parameter), for the f32 pre-test
+        if (__ballot_sync(LVX_FULL, active) == 0) break;
+        S.q.vox[0][lane] = x; S.q.vox[1][lane] = y; S.q.vox[2][lane] = z;
+        {
             const double tc = 0.5 * (t + te);
-            S.pf[0][lane] = (float)(ox + dx * tc); S.pf[1][lane] = (float)(oy + dy * tc); S.pf[2][lane] = (float)(oz + dz * tc);
+            S.q.pf[0][lane] = (float)(ox + dx * tc); S.q.pf[1][lane] = (float)(oy + dy * tc); S.q.pf[2][lane] = (float)(oz + dz * tc);
         }
-        // ---- 2. flatten (ray, fragment) pairs
-        uint32_t inc = active ? n : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += v;
-        }
-        S.prefix[lane + 1] = inc;
-        if (lane == 0) S.prefix[0] = 0;
-        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
-        if (lane == 0) n_tests += T;
         int kept = 0;
-        uint32_t accepted = 0;
-        uint32_t qn = 0, hl_n = 0, own = 0;
-        __syncwarp();
+        uint32_t accepted = 0, hl_n = 0;
 
         // owners pull their records out of the hit list (insertion sort, lv/raytracer.py:589-607)
         auto drain = [&]() {
@@ -890,84 +705,63 @@ k_render_transparent_coop(const RenderArgs A) {
             __syncwarp();
         };
 
-        for (uint32_t p0 = 0; p0 < T || qn > 0; p0 += 32) {
-            const uint32_t p = p0 + lane;
-            bool pass = false;
-            uint32_t rr = 0, ss = 0, ii = 0;
-            if (p < T) {
-                while (S.prefix[own + 1] <= p) own++;       // owner ray: prefix[own] <= p < prefix[own+1]
-                rr = own;
-                ss = p - S.prefix[rr];
-                ii = A.frags[S.fo[rr] + ss];
-                pass = !surely_misses_f32(S.pf[0][rr], S.pf[1][rr], S.pf[2][rr], S.dirf[0][rr], S.dirf[1][rr],
-                                          S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
-            }
-            const uint32_t m = __ballot_sync(0xffffffffu, pass);
-            if (pass) {
-                const uint32_t pos = qn + __popc(m & ((1u << lane) - 1u));
-                S.q_i[pos] = ii;
-                S.q_rs[pos] = (rr << 16) | ss;
-            }
-            qn += __popc(m);
-            __syncwarp();
-            const bool flush = p0 + 32 >= T;
-            if (qn >= 32 || (flush && qn > 0)) {
-                const uint32_t take = qn < 32 ? qn : 32;
-                bool hit = false;
-                double ht = 0.0;
-                uint32_t hr = 0, hs = 0, hi_ = 0, hkey = 0;
-                if (lane < take) {
-                    hi_ = S.q_i[lane];
-                    const uint32_t rs = S.q_rs[lane];
-                    hr = rs >> 16; hs = rs & 0xFFFFu;
-                    const double ddx = S.dir[0][hr], ddy = S.dir[1][hr], ddz = S.dir[2][hr];
-                    const Capsule c = load_capsule(A.verts, A.normals, (int64_t)hi_, r, clip);
-                    ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
-                    if (ht >= 0.0) {
-                        const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
-                        hit = hx == S.vox[0][hr] && hy == S.vox[1][hr] && hz == S.vox[2][hr];
-                        if (hit) {   // lv/raytracer.py:583-588
-                            int64_t q = (int64_t)((ht - S.t_enter[hr]) * S.inv_span[hr]);
-                            if (q < 0) q = 0; else if (q > 65535) q = 65535;
-                            hkey = ((uint32_t)q << 16) | hs;
-                        }
+        __syncwarp();
+        const uint32_t T = run_pairs(A, S.q, active ? n : 0u, fo, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii) {
+            bool hit = false;
+            uint32_t hkey = 0;
+            double ht = 0.0;
+            const uint32_t hr = rs >> 16, hs = rs & 0xFFFFu;
+            if (valid) {
+                const double ddx = S.q.dir[0][hr], ddy = S.q.dir[1][hr], ddz = S.q.dir[2][hr];
+                const Capsule c = load_capsule(A.verts, A.normals, (int64_t)ii, r, clip);
+                ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
+                if (ht >= 0.0) {
+                    const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
+                    hit = hx == S.q.vox[0][hr] && hy == S.q.vox[1][hr] && hz == S.q.vox[2][hr];
+                    if (hit) {   // lv/raytracer.py:583-588
+                        int64_t q = (int64_t)((ht - S.t_enter[hr]) * S.inv_span[hr]);
+                        if (q < 0) q = 0; else if (q > 65535) q = 65535;
+                        hkey = ((uint32_t)q << 16) | hs;
                     }
                 }
-                __syncwarp();
-                uint32_t mv_i = 0, mv_rs = 0;
-                const bool mv = lane + 32 < qn;
-                if (mv) { mv_i = S.q_i[lane + 32]; mv_rs = S.q_rs[lane + 32]; }
-                __syncwarp();
-                if (mv) { S.q_i[lane] = mv_i; S.q_rs[lane] = mv_rs; }
-                qn -= take;
-                const uint32_t hm = __ballot_sync(0xffffffffu, hit);
-                if (hl_n + __popc(hm) > HL_CAP) drain();
-                if (hit) {
-                    const uint32_t pos = hl_n + __popc(hm & ((1u << lane) - 1u));
-                    S.hl_t[pos] = ht; S.hl_key[pos] = hkey; S.hl_i[pos] = hi_; S.hl_r[pos] = (uint8_t)hr;
-                }
-                hl_n += __popc(hm);
-                __syncwarp();
             }
-            if (flush && qn == 0) break;
-        }
+            const uint32_t hm = __ballot_sync(LVX_FULL, hit);
+            if (hm == 0) return;
+            if (hl_n + __popc(hm) > HL_CAP) drain();
+            if (hit) {
+                const uint32_t pos = hl_n + __popc(hm & lt_mask);
+                S.hl_t[pos] = ht; S.hl_key[pos] = hkey; S.hl_i[pos] = ii; S.hl_r[pos] = (uint8_t)hr;
+            }
+            hl_n += __popc(hm);
+            __syncwarp();
+        });
+        if (lane == 0) n_tests += T;
         drain();
-        // ---- blend the kept hits front to back (lv/raytracer.py:608-631)
-        if (active) {
-            for (int j = 0; j < kept; j++) {
-                if (early && acc_a >= 0.999) break;
-                const double tt = tbuf[j];
-                const int64_t i = ibuf[j];
-                const double hx = ox + dx * tt, hy = oy + dy * tt, hz = oz + dz * tt;
-                const Capsule c = load_capsule(A.verts, A.normals, i, r, clip);
-                double nx, ny, nz, cr, cg, cb;
-                capsule_normal(hx, hy, hz, c, nx, ny, nz);
-                shade(A, c, nx, ny, nz, hx, hy, hz, cr, cg, cb);
-                const double wgt = (1.0 - acc_a) * alpha;
-                col_r += wgt * cr; col_g += wgt * cg; col_b += wgt * cb;
-                acc_a += wgt;
-                if (first_hit < 0) first_hit = i;
+        // ---- blend the kept hits front to back (lv/raytracer.py:608-631): fix the weights now,
+        // queue the colours
+        {
+            const int kmax = __reduce_max_sync(LVX_FULL, active ? kept : 0);
+            bool stopped = !active;
+            for (int j = 0; j < kmax; j++) {
+                if (!stopped && (j >= kept || (early && acc_a >= 0.999))) stopped = true;
+                double wgt = 0.0;
+                if (!stopped) {
+                    wgt = (1.0 - acc_a) * alpha;
+                    acc_a += wgt;
+                    if (first_hit < 0) first_hit = ibuf[j];
+                }
+                const uint32_t pm = __ballot_sync(LVX_FULL, !stopped);
+                if (pm == 0) break;
+                if (!stopped) {
+                    const uint32_t pos = qd + __popc(pm & lt_mask);
+                    S.d_w[pos] = wgt; S.d_t[pos] = tbuf[j]; S.d_i[pos] = ibuf[j]; S.d_ray[pos] = (uint32_t)lane;
+                }
+                qd += __popc(pm);
+                __syncwarp();
+                if (qd >= 32) shade_batch();
             }
+        }
+        if (active) {
             // lv/raytracer.py:632-637
             if (accepted <= (uint32_t)kslots || (early && acc_a >= 0.999)) {
                 repeat = false;
@@ -979,6 +773,7 @@ k_render_transparent_coop(const RenderArgs A) {
         }
         __syncwarp();
     }
+    while (qd > 0) shade_batch();
 
     if (live) {
         const double out_r = col_r + (1.0 - acc_a) * A.p.background[0];
@@ -1028,20 +823,18 @@ k_resolve(const RenderArgs A) {
 using namespace lvx;
 
 static int fill_args(RenderArgs &A, const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets,
-                     const uint32_t *frags, const uint8_t *bits_flat, int res, const float *ao, const float *shadow,
+                     const uint32_t *frags, const uint32_t *loose_bits, const uint8_t *march, int res, const float *ao, const float *shadow,
                      const lvx_camera *cam_host, const lvx_render_params *params_host, double *rgb, uint8_t *srgb,
                      int32_t *hit_id, uint64_t *stats) {
-    if (!pow2(res) || !cam_host || !params_host || !hit_id) return LVX_E_ARG;
+    if (!pow2(res) || res > 1024 || !cam_host || !params_host || !hit_id || !march) return LVX_E_ARG;
     const lvx_render_params &p = *params_host;
     if (p.mode < 0 || p.mode > 1 || p.k < 1 || p.k > 64 || !(p.alpha > 0.0 && p.alpha <= 1.0)) return LVX_E_ARG;
     if (cam_host->width <= 0 || cam_host->height <= 0) return LVX_E_ARG;
     if (p.tile_x0 < 0 || p.tile_y0 < 0 || p.tile_x1 > cam_host->width || p.tile_y1 > cam_host->height) return LVX_E_ARG;
     if (p.use_clip && !normals) return LVX_E_ARG;
-    A.verts = verts; A.verts_f = verts_f; A.normals = normals; A.offsets = offsets; A.frags = frags; A.bits = bits_flat;
+    A.verts = verts; A.verts_f = verts_f; A.normals = normals; A.offsets = offsets; A.frags = frags; A.loose = loose_bits; A.march = march;
     A.ao = ao; A.sh = shadow;
-    const LevelOffsets L = make_level_offsets(res);
-    for (int l = 0; l < 16; l++) A.bits_off[l] = l < L.n_levels ? (uint32_t)L.off[l] : 0;
-    A.res = res; A.n_levels = L.n_levels; A.cam = *cam_host; A.p = p;
+    A.res = res; A.cam = *cam_host; A.p = p;
     A.rgb = rgb; A.srgb = srgb; A.hit_id = hit_id; A.stats = stats;
     A.hit_t = nullptr; A.need_bits = nullptr; A.need_list = nullptr; A.guard_volumes = 0;
     return LVX_OK;
@@ -1050,11 +843,11 @@ static int fill_args(RenderArgs &A, const double *verts, const float *verts_f, c
 extern "C" {
 
 int lvx_render(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
-               const uint8_t *bits_flat, int res, const float *ao, const float *shadow,
+               const uint32_t *loose_bits, const uint8_t *march, int res, const float *ao, const float *shadow,
                const lvx_camera *cam_host, const lvx_render_params *params_host, double *rgb, uint8_t *srgb,
                int32_t *hit_id, uint64_t *stats, void *stream) {
     RenderArgs A;
-    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, bits_flat, res, ao, shadow, cam_host, params_host,
+    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, loose_bits, march, res, ao, shadow, cam_host, params_host,
                              rgb, srgb, hit_id, stats);
     if (rc != LVX_OK) return rc;
     if (!verts_f) return LVX_E_ARG;
@@ -1072,11 +865,11 @@ int lvx_render(const double *verts, const float *verts_f, const double *normals,
 }
 
 int lvx_trace_hits(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
-                   const uint8_t *bits_flat, int res, const lvx_camera *cam_host,
+                   const uint32_t *loose_bits, const uint8_t *march, int res, const lvx_camera *cam_host,
                    const lvx_render_params *params_host, double *hit_t, int32_t *hit_id, uint32_t *need_bits,
                    uint32_t *need_list, uint64_t *stats, void *stream) {
     RenderArgs A;
-    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, bits_flat, res, nullptr, nullptr, cam_host,
+    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, loose_bits, march, res, nullptr, nullptr, cam_host,
                              params_host, nullptr, nullptr, hit_id, stats);
     if (rc != LVX_OK) return rc;
     if (A.p.mode != 0 || !verts_f || !hit_t || !need_bits || !need_list) return LVX_E_ARG;
@@ -1093,11 +886,11 @@ int lvx_trace_hits(const double *verts, const float *verts_f, const double *norm
     return LVX_OK;
 }
 
-int lvx_resolve(const double *verts, const double *normals, const uint8_t *bits_flat, int res, const float *ao,
+int lvx_resolve(const double *verts, const double *normals, const uint8_t *march, int res, const float *ao,
                 const float *shadow, const lvx_camera *cam_host, const lvx_render_params *params_host,
                 const double *hit_t, const int32_t *hit_id, double *rgb, uint8_t *srgb, void *stream) {
     RenderArgs A;
-    const int rc = fill_args(A, verts, nullptr, normals, nullptr, nullptr, bits_flat, res, ao, shadow, cam_host, params_host,
+    const int rc = fill_args(A, verts, nullptr, normals, nullptr, nullptr, nullptr, march, res, ao, shadow, cam_host, params_host,
                              rgb, srgb, const_cast<int32_t *>(hit_id), nullptr);
     if (rc != LVX_OK) return rc;
     if (!hit_t) return LVX_E_ARG;

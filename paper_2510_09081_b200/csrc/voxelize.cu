@@ -13,6 +13,10 @@
 // 256^3 grid (64 MiB) is L2-resident on B200 while the atomics run.
 #include "lvx_device.cuh"
 
+#ifndef LVX_BATCH
+#define LVX_BATCH 4   // cells of a traversal row whose atomics are issued back to back
+#endif
+
 namespace lvx {
 
 #ifndef LVX_VOX_MINB
@@ -34,19 +38,39 @@ k_voxelize(const double *__restrict__ verts, const double *__restrict__ normals,
         const double ratio = r / rc;
         const double corr = ratio * ratio;
         const int64_t res64 = res;
-        for_each_cell(method, c.a, c.b, rt, res, [&](int x, int y, int z) {
-            const uint32_t q = occupancy_q(x + 0.5, y + 0.5, z + 0.5, c, rc, corr);
-            const int64_t idx = x + res64 * (y + res64 * z);
-            visited++;
-            if (WIDE) {
-                atomicAdd(&wide[idx], (1ull << 32) | (unsigned long long)q);
-            } else {
-                const uint32_t inc = 0x10000u + q;
-                const uint32_t old = atomicAdd(&base[idx], inc);
-                if (old + inc < old) stats[LVX_ST_NEED_WIDE] = 1;   // count field wrapped
-                if ((old & 0xFFFFu) + q > 0xFFFFu) {
-                    atomicSub(&base[idx], 0x10000u);                  // undo the carry into count
-                    atomicOr(&occ_sat[idx >> 5], 1u << (idx & 31));
+        // rows of the traversal, four cells at a time: four occupancies, then the four atomics
+        // back to back, then the (rare) carry repairs that depend on their results
+        for_each_row(method, c.a, c.b, rt, res, [&](int x, int y, int z, int axis, int len) {
+            const int64_t stride = axis == 0 ? 1 : (axis == 1 ? res64 : res64 * res64);
+            const int64_t idx0 = x + res64 * (y + res64 * z);
+            const double sx = axis == 0 ? 1.0 : 0.0, sy = axis == 1 ? 1.0 : 0.0, sz = axis == 2 ? 1.0 : 0.0;
+            visited += (uint64_t)len;
+            for (int u0 = 0; u0 < len; u0 += LVX_BATCH) {
+                uint32_t q[LVX_BATCH], old[LVX_BATCH];
+#pragma unroll
+                for (int k = 0; k < LVX_BATCH; k++) {
+                    const int u = u0 + k;
+                    q[k] = u < len ? occupancy_q(x + 0.5 + u * sx, y + 0.5 + u * sy, z + 0.5 + u * sz, c, rc, corr) : 0u;
+                }
+                if (WIDE) {
+#pragma unroll
+                    for (int k = 0; k < LVX_BATCH; k++)
+                        if (u0 + k < len) atomicAdd(&wide[idx0 + (u0 + k) * stride], (1ull << 32) | (unsigned long long)q[k]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < LVX_BATCH; k++)
+                        old[k] = u0 + k < len ? atomicAdd(&base[idx0 + (u0 + k) * stride], 0x10000u + q[k]) : 0u;
+#pragma unroll
+                    for (int k = 0; k < LVX_BATCH; k++) {
+                        if (u0 + k >= len) continue;
+                        const uint32_t inc = 0x10000u + q[k];
+                        const int64_t idx = idx0 + (u0 + k) * stride;
+                        if (old[k] + inc < old[k]) stats[LVX_ST_NEED_WIDE] = 1;   // count field wrapped
+                        if ((old[k] & 0xFFFFu) + q[k] > 0xFFFFu) {
+                            atomicSub(&base[idx], 0x10000u);                  // undo the carry into count
+                            atomicOr(&occ_sat[idx >> 5], 1u << (idx & 31));
+                        }
+                    }
                 }
             }
         });

@@ -93,6 +93,8 @@ class FrameEngine:
         self.srgb = t.empty((self.h, self.w, 3), dtype=t.uint8, device=d)
         self.hit_id = t.empty((self.h, self.w), dtype=t.int32, device=d)
         self.frags = t.empty(max(int(frag_capacity), 1), dtype=t.int32, device=d)
+        self.loose = t.empty(ops.loose_words(self.frags.numel()), dtype=t.int32, device=d)
+        self.march = t.empty(V, dtype=t.uint8, device=d)
         if self.shading == "demand":
             self.hit_t = t.empty((self.h, self.w), dtype=t.float64, device=d)
             self.need_bits = t.empty(max(V // 32, 1), dtype=t.int32, device=d)
@@ -113,7 +115,7 @@ class FrameEngine:
         n += levels - 1                             # mips
         n += (4 if self.strategy == "vcsv" else 1) + (levels - 1)   # solid, visibility, march, dilate | occupied; or-mips
         n += 1                                      # scan
-        n += 3                                      # cursor copy, scatter, order
+        n += 3 + 1                                  # cursor copy, scatter, order; march table
         n += levels + 1                             # non-empty masks, shade
         if self.shading == "demand":
             n += 2                                  # trace_hits, resolve
@@ -186,6 +188,7 @@ class FrameEngine:
                      self.cull_flat, self.vis_list, self.stats)
         else:
             ops.occupied_pyramid(self.base, self.res, self.cull_flat, self.vis_list, self.stats)
+        ops.march_levels(self.cull_flat, self.res, self.march)
 
     def _stage_scan(self):
         cull_base = self.cull_flat[:self.V] if self.strategy == "vcsv" else None
@@ -195,7 +198,7 @@ class FrameEngine:
         rt = ops.footprint_radius(self.lines.r, self.r_min)
         ops.scatter(self.lines, rt, self.res, self.method,
                     self.cull_flat if self.strategy == "vcsv" else None, self.vis_list,
-                    self.offsets, self.cursor, self.frags, self.stats)
+                    self.offsets, self.cursor, self.frags, self.stats, loose=self.loose)
 
     def _stage_shade(self):
         demand = self.shading == "demand"
@@ -205,18 +208,18 @@ class FrameEngine:
 
     def _stage_trace(self, cam, tile=None):
         p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
-        ops.render(self.lines, self.offsets, self.frags, self.cull_flat, self.res, self.ao, self.shadow,
+        ops.render(self.lines, self.offsets, self.frags, self.loose, self.march, self.res, self.ao, self.shadow,
                    ops.make_camera_struct(cam, self.grid), p, self.rgb, self.srgb, self.hit_id, self.stats)
 
     def _stage_trace_hits(self, cam, tile=None):
         p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
-        ops.trace_hits(self.lines, self.offsets, self.frags, self.cull_flat, self.res,
+        ops.trace_hits(self.lines, self.offsets, self.frags, self.loose, self.march, self.res,
                        ops.make_camera_struct(cam, self.grid), p, self.hit_t, self.hit_id, self.need_bits,
                        self.need_list, self.stats)
 
     def _stage_resolve(self, cam, tile=None):
         p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
-        ops.resolve(self.lines, self.cull_flat, self.res, self.ao, self.shadow,
+        ops.resolve(self.lines, self.march, self.res, self.ao, self.shadow,
                     ops.make_camera_struct(cam, self.grid), p, self.hit_t, self.hit_id, self.rgb, self.srgb)
 
     # ------------------------------------------------------------------ frame
@@ -226,6 +229,7 @@ class FrameEngine:
             if cap >= 2 ** 32:
                 cap = need
             self.frags = self.torch.empty(cap, dtype=self.torch.int32, device=self.dev)
+            self.loose = self.torch.empty(ops.loose_words(cap), dtype=self.torch.int32, device=self.dev)
 
     def run(self, cam, grid: GridDesc, r_world: float, tile=None, seg_range=None, after_voxelize=None):
         """One frame on the already loaded vertices.  `after_voxelize(engine)` is the hook where the

@@ -178,10 +178,26 @@ def scan(base, cull_base, offsets, scratch, stats):
                          _ptr(stats), _stream()), "lvx_scan")
 
 
-def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, cursor, frags, stats):
-    check(lib().lvx_scatter(_ptr(lines.verts), _ptr(lines.segs), lines.n_segments, float(rt), res,
+TIGHT_MARGIN = 1e-3   # voxels; see csrc/abuffer.cu "Loose bits"
+
+
+def loose_words(frag_capacity: int) -> int:
+    return int(lib().lvx_loose_words(int(frag_capacity)))
+
+
+def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, cursor, frags, stats, loose=None):
+    """`loose` (optional int32 tensor of loose_words(frags.numel())): receives the per-fragment
+    "capsule of radius lines.r cannot reach into this voxel" bits for the ray tracer."""
+    if loose is not None and loose.numel() < loose_words(frags.numel()):
+        raise ValueError("loose-bit buffer too small for the fragment buffer")
+    check(lib().lvx_scatter(_ptr(lines.verts), _ptr(lines.segs), lines.n_segments, float(rt),
+                            float(lines.r) + TIGHT_MARGIN, res,
                             METHODS[method], _ptr(cull_flat), _ptr(vis_list), _ptr(offsets), _ptr(cursor),
-                            _ptr(frags), frags.numel(), _ptr(stats), _stream()), "lvx_scatter")
+                            _ptr(frags), frags.numel(), _ptr(loose), _ptr(stats), _stream()), "lvx_scatter")
+
+
+def march_levels(bits_flat, res, march):
+    check(lib().lvx_march_levels(_ptr(bits_flat), res, _ptr(march), _stream()), "lvx_march_levels")
 
 
 def shade_scratch_bytes(n_voxels: int) -> int:
@@ -207,21 +223,21 @@ def make_camera_struct(cam, grid) -> N.lvx_camera:
     return c
 
 
-def render(lines: DeviceLines, offsets, frags, bits_flat, res, ao, shadow, cam_struct, params, rgb, srgb,
+def render(lines: DeviceLines, offsets, frags, loose, march, res, ao, shadow, cam_struct, params, rgb, srgb,
            hit_id, stats):
-    check(lib().lvx_render(_ptr(lines.verts), _ptr(lines.verts_f), _ptr(lines.normals), _ptr(offsets), _ptr(frags), _ptr(bits_flat),
-                           res, _ptr(ao), _ptr(shadow), C.byref(cam_struct), C.byref(params), _ptr(rgb),
+    check(lib().lvx_render(_ptr(lines.verts), _ptr(lines.verts_f), _ptr(lines.normals), _ptr(offsets), _ptr(frags),
+                           _ptr(loose), _ptr(march), res, _ptr(ao), _ptr(shadow), C.byref(cam_struct), C.byref(params), _ptr(rgb),
                            _ptr(srgb), _ptr(hit_id), _ptr(stats), _stream()), "lvx_render")
 
 
-def trace_hits(lines: DeviceLines, offsets, frags, bits_flat, res, cam_struct, params, hit_t, hit_id, need_bits,
+def trace_hits(lines: DeviceLines, offsets, frags, loose, march, res, cam_struct, params, hit_t, hit_id, need_bits,
                need_list, stats):
-    check(lib().lvx_trace_hits(_ptr(lines.verts), _ptr(lines.verts_f), _ptr(lines.normals), _ptr(offsets), _ptr(frags), _ptr(bits_flat),
-                               res, C.byref(cam_struct), C.byref(params), _ptr(hit_t), _ptr(hit_id),
+    check(lib().lvx_trace_hits(_ptr(lines.verts), _ptr(lines.verts_f), _ptr(lines.normals), _ptr(offsets), _ptr(frags),
+                               _ptr(loose), _ptr(march), res, C.byref(cam_struct), C.byref(params), _ptr(hit_t), _ptr(hit_id),
                                _ptr(need_bits), _ptr(need_list), _ptr(stats), _stream()), "lvx_trace_hits")
 
 
-def resolve(lines: DeviceLines, bits_flat, res, ao, shadow, cam_struct, params, hit_t, hit_id, rgb, srgb):
-    check(lib().lvx_resolve(_ptr(lines.verts), _ptr(lines.normals), _ptr(bits_flat), res, _ptr(ao), _ptr(shadow),
+def resolve(lines: DeviceLines, march, res, ao, shadow, cam_struct, params, hit_t, hit_id, rgb, srgb):
+    check(lib().lvx_resolve(_ptr(lines.verts), _ptr(lines.normals), _ptr(march), res, _ptr(ao), _ptr(shadow),
                             C.byref(cam_struct), C.byref(params), _ptr(hit_t), _ptr(hit_id), _ptr(rgb), _ptr(srgb),
                             _stream()), "lvx_resolve")

@@ -151,7 +151,12 @@ def render(scene: RenderScene, cam: Camera, settings: RenderSettings, tile=None,
     srgb = torch.zeros((h, w, 3), dtype=torch.uint8, device=dev)
     hit = torch.zeros((h, w), dtype=torch.int32, device=dev)
     stats = ops.new_stats(dev)
-    ops.render(lines, scene.abuf.table.offsets_dev, scene.abuf.fragments_dev, bits.flat_dev, res, ao, sh,
+    march = torch.empty(res ** 3, dtype=torch.uint8, device=dev)
+    ops.march_levels(bits.flat_dev, res, march)
+    abuf = scene.abuf
+    # the loose bits are valid for capsules no thicker than the radius they were built with
+    loose = abuf.loose_dev if getattr(abuf, "loose_dev", None) is not None and lines.r <= abuf.tight_radius else None
+    ops.render(lines, abuf.table.offsets_dev, abuf.fragments_dev, loose, march, res, ao, sh,
                ops.make_camera_struct(cam, g), make_params(settings, lines, light, tile, w, h),
                rgb, srgb, hit, stats)
     return Image(rgb, srgb, hit, stats={"ray_capsule_tests": int(stats[N.ST_RAY_TESTS].item())})
