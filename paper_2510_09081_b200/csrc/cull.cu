@@ -23,56 +23,89 @@ __device__ __forceinline__ bool q_solid(const uint32_t *__restrict__ base, int r
     return (base[x + (int64_t)res * (y + (int64_t)res * z)] & 0xFFFFu) >= LVX_SOLID_Q;
 }
 
+// One block = SOLID_ITEMS x 256 consecutive voxels; a thread owns voxels tid, tid+256, ... of the
+// block's chunk, so every item is a coalesced row, a warp's ballot is one word of the bit mask, and
+// the four loads of a thread are in flight together.  The occupied-voxel list gets ONE counter
+// atomic per block (1024 voxels).
+constexpr int SOLID_ITEMS = 4;
 __global__ void __launch_bounds__(256)
 k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restrict__ solid,
-        uint32_t *__restrict__ bricks, uint32_t *__restrict__ occ_list, uint8_t *__restrict__ vis,
-        uint64_t *__restrict__ stats) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool s = false, occ = false;
-    if (idx < V) {
-        const uint32_t w = base[idx];
-        occ = (w >> 16) != 0;
-        if ((w & 0xFFFFu) >= LVX_SOLID_Q) {
+        uint32_t *__restrict__ bricks, uint32_t *__restrict__ occ_list, uint64_t *__restrict__ stats) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t chunk = (int64_t)blockIdx.x * (SOLID_ITEMS * 256);
+    uint32_t w[SOLID_ITEMS];
+#pragma unroll
+    for (int k = 0; k < SOLID_ITEMS; k++) {
+        const int64_t idx = chunk + k * 256 + threadIdx.x;
+        w[k] = idx < V ? base[idx] : 0u;
+    }
+    uint32_t n_occ = 0;
+#pragma unroll
+    for (int k = 0; k < SOLID_ITEMS; k++) {
+        const int64_t idx = chunk + k * 256 + threadIdx.x;
+        bool s = false;
+        n_occ += (w[k] >> 16) != 0;
+        if (idx < V && (w[k] & 0xFFFFu) >= LVX_SOLID_Q) {
             const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
             s = q_solid(base, res, x - 1, y, z) && q_solid(base, res, x + 1, y, z) &&
                 q_solid(base, res, x, y - 1, z) && q_solid(base, res, x, y + 1, z) &&
                 q_solid(base, res, x, y, z - 1) && q_solid(base, res, x, y, z + 1);
-        }
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, s);
-    const uint32_t mo = __ballot_sync(0xffffffffu, occ);
-    if (s) {
-        // flag every brick that overlaps this solid voxel dilated by one voxel, at both brick sizes
-        const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
-        uint32_t *bits = bricks;
+            if (s) {
+                // flag every brick that overlaps this solid voxel dilated by one voxel, at both brick sizes
+                uint32_t *bits = bricks;
 #pragma unroll
-        for (int lvl = 0; lvl < 2; lvl++) {
-            const int B = lvl == 0 ? LVX_BRICK : LVX_SUPER;
-            const int rb = (res + B - 1) / B;
-            const int bx0 = max(x - 1, 0) / B, bx1 = min(x + 1, res - 1) / B;
-            const int by0 = max(y - 1, 0) / B, by1 = min(y + 1, res - 1) / B;
-            const int bz0 = max(z - 1, 0) / B, bz1 = min(z + 1, res - 1) / B;
-            for (int bz = bz0; bz <= bz1; bz++)
-                for (int by = by0; by <= by1; by++)
-                    for (int bx = bx0; bx <= bx1; bx++) {
-                        const int bi = bx + rb * (by + rb * bz);
-                        atomicOr(&bits[bi >> 5], 1u << (bi & 31));
-                    }
-            bits += brick_words(res, B);
+                for (int lvl = 0; lvl < 2; lvl++) {
+                    const int B = lvl == 0 ? LVX_BRICK : LVX_SUPER;
+                    const int rb = (res + B - 1) / B;
+                    const int bx0 = max(x - 1, 0) / B, bx1 = min(x + 1, res - 1) / B;
+                    const int by0 = max(y - 1, 0) / B, by1 = min(y + 1, res - 1) / B;
+                    const int bz0 = max(z - 1, 0) / B, bz1 = min(z + 1, res - 1) / B;
+                    for (int bz = bz0; bz <= bz1; bz++)
+                        for (int by = by0; by <= by1; by++)
+                            for (int bx = bx0; bx <= bx1; bx++) {
+                                const int bi = bx + rb * (by + rb * bz);
+                                atomicOr(&bits[bi >> 5], 1u << (bi & 31));
+                            }
+                    bits += brick_words(res, B);
+                }
+            }
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, s);
+        if (lane == 0 && idx < V) {
+            solid[idx >> 5] = m;
+            if (m) atomicAdd((unsigned long long *)&stats[LVX_ST_SOLID], (unsigned long long)__popc(m));
         }
     }
-    const int lane = threadIdx.x & 31;
-    unsigned long long slot = 0;
-    if (lane == 0 && idx < V) {
-        solid[idx >> 5] = m;
-        if (m) atomicAdd((unsigned long long *)&stats[LVX_ST_SOLID], (unsigned long long)__popc(m));
-        // compacted list of occupied voxels: the march kernel then runs on dense warps
-        if (mo) slot = atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)__popc(mo));
+    // compacted list of occupied voxels (the march kernels then run on dense warps): block scan of
+    // the per-thread counts, one atomic on the list counter per block
+    uint32_t inc = n_occ;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
     }
-    if (idx < V) vis[idx] = 0;
-    if (mo) {
-        slot = __shfl_sync(0xffffffffu, slot, 0);
-        if (occ) occ_list[slot + __popc(mo & ((1u << lane) - 1u))] = (uint32_t)idx;
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t c = lane < 8 ? s_warp[lane] : 0;
+        uint32_t wi = c;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += v;
+        }
+        if (lane < 8) s_warp[lane] = wi - c;
+        if (lane == 7 && wi)
+            s_base = atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)wi);
+    }
+    __syncthreads();
+    if (n_occ) {
+        uint64_t slot = s_base + s_warp[warp] + (inc - n_occ);
+#pragma unroll
+        for (int k = 0; k < SOLID_ITEMS; k++)
+            if ((w[k] >> 16) != 0) occ_list[slot++] = (uint32_t)(chunk + k * 256 + threadIdx.x);
     }
 }
 
@@ -106,42 +139,46 @@ __device__ __forceinline__ bool march_blocked(const uint32_t *__restrict__ solid
 // Conservative coarse walk: Amanatides-Woo over bricks of `brick` voxels along the segment
 // o -> c (clipped to the grid); true if a flagged brick is visited.  A brick is flagged when it
 // overlaps a solid voxel dilated by a whole voxel, so if the fine march would reach a solid voxel,
-// at least 2 voxels of the segment lie strictly inside a flagged region and the coarse walk
-// (whose rounding errors are ~1e-13) must visit a flagged brick.
+// at least 2 voxels of the segment lie strictly inside a flagged region, a point of it a whole voxel
+// away from unflagged space, and a walk whose errors are far below one voxel must visit a flagged brick.
+// Single precision is enough: the walk only has to be right up to errors much smaller than the
+// one-voxel dilation of the flags (coordinates <= 1024 voxels -> errors < 1e-3 voxel).
 __device__ __forceinline__ bool coarse_may_hit(const uint32_t *__restrict__ bits, int rb, int brick,
-                                               double ox, double oy, double oz, double cx, double cy, double cz) {
-    const double inv = 1.0 / brick;
-    const double o[3] = {ox * inv, oy * inv, oz * inv};
-    const double d[3] = {(cx - ox) * inv, (cy - oy) * inv, (cz - oz) * inv};
-    double t0 = 0.0, t1 = 1.0;
+                                               float ox, float oy, float oz, float cx, float cy, float cz) {
+    const float inv = 1.0f / (float)brick;
+    const float o[3] = {ox * inv, oy * inv, oz * inv};
+    const float d[3] = {(cx - ox) * inv, (cy - oy) * inv, (cz - oz) * inv};
+    float t0 = 0.0f, t1 = 1.0f;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        if (d[a] == 0.0) { if (o[a] < 0.0 || o[a] > (double)rb) return false; }
+        if (d[a] == 0.0f) { if (o[a] < 0.0f || o[a] > (float)rb) return false; }
         else {
-            double ta = (0.0 - o[a]) / d[a], tb = ((double)rb - o[a]) / d[a];
-            if (ta > tb) { const double tmp = ta; ta = tb; tb = tmp; }
-            t0 = fmax(t0, ta); t1 = fmin(t1, tb);
+            const float id = __fdividef(1.0f, d[a]);
+            float ta = (0.0f - o[a]) * id, tb = ((float)rb - o[a]) * id;
+            if (ta > tb) { const float tmp = ta; ta = tb; tb = tmp; }
+            t0 = fmaxf(t0, ta); t1 = fminf(t1, tb);
         }
     }
-    if (t0 > t1) return false;
+    if (t0 > t1 + 1e-4f) return false;
     int c[3], st[3];
-    double tm[3], td[3];
+    float tm[3], td[3];
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-        const double p = o[a] + d[a] * t0;
-        c[a] = min(max((int)floor(p), 0), rb - 1);
+        const float p = o[a] + d[a] * t0;
+        c[a] = min(max((int)floorf(p), 0), rb - 1);
         st[a] = d[a] > 0 ? 1 : -1;
-        tm[a] = d[a] != 0.0 ? ((double)(c[a] + (d[a] > 0 ? 1 : 0)) - o[a]) / d[a] : 1e30;
-        td[a] = d[a] != 0.0 ? fabs(1.0 / d[a]) : 1e30;
+        const float id = d[a] != 0.0f ? __fdividef(1.0f, d[a]) : 0.0f;
+        tm[a] = d[a] != 0.0f ? ((float)(c[a] + (d[a] > 0 ? 1 : 0)) - o[a]) * id : 1e30f;
+        td[a] = d[a] != 0.0f ? fabsf(id) : 1e30f;
     }
     for (;;) {
         const int bi = c[0] + rb * (c[1] + rb * c[2]);
         if ((bits[bi >> 5] >> (bi & 31)) & 1u) return true;
-        double t;
+        float t;
         if (tm[0] <= tm[1] && tm[0] <= tm[2]) { c[0] += st[0]; t = tm[0]; tm[0] += td[0]; }
         else if (tm[1] <= tm[2]) { c[1] += st[1]; t = tm[1]; tm[1] += td[1]; }
         else { c[2] += st[2]; t = tm[2]; tm[2] += td[2]; }
-        if (t > t1) return false;
+        if (t > t1 + 1e-4f) return false;
         if (c[0] < 0 || c[1] < 0 || c[2] < 0 || c[0] >= rb || c[1] >= rb || c[2] >= rb) return false;
     }
 }
@@ -168,15 +205,16 @@ k_visibility(const uint32_t *__restrict__ bricks, const uint32_t *__restrict__ o
                 const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
                 // Only a solid voxel can block.  Walk the segment centre->camera through the
                 // 32^3-voxel super-bricks, then the 8^3 bricks.
-                const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
+                const float ox = x + 0.5f, oy = y + 0.5f, oz = z + 0.5f;
                 may_hit = coarse_may_hit(bricks + brick_words(res, LVX_BRICK), (res + LVX_SUPER - 1) / LVX_SUPER,
-                                         LVX_SUPER, ox, oy, oz, cx, cy, cz);
+                                         LVX_SUPER, ox, oy, oz, (float)cx, (float)cy, (float)cz);
                 if (may_hit)
-                    may_hit = coarse_may_hit(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz, cx, cy, cz);
+                    may_hit = coarse_may_hit(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz,
+                                             (float)cx, (float)cy, (float)cz);
             }
             if (!may_hit) vis[idx] = 1;
         }
-        list_append_warp(march_list, may_hit, idx);
+        list_append_block(march_list, may_hit, idx);
     }
 }
 
@@ -219,10 +257,7 @@ k_dilate(const uint32_t *__restrict__ base, const uint8_t *__restrict__ vis, int
         }
     }
     if (idx < V) out[idx] = v ? 1 : 0;
-    const uint32_t m = __ballot_sync(0xffffffffu, v);
-    if ((threadIdx.x & 31) == 0 && m)
-        atomicAdd((unsigned long long *)&stats[LVX_ST_VISIBLE], (unsigned long long)__popc(m));
-    list_append_warp(vis_list, v, (uint32_t)idx);
+    list_append_block(vis_list, v, (uint32_t)idx, (unsigned long long *)&stats[LVX_ST_VISIBLE]);
 }
 
 __global__ void __launch_bounds__(256)
@@ -232,11 +267,9 @@ k_occupied(const uint32_t *__restrict__ base, int64_t V, uint8_t *__restrict__ o
     const bool v = idx < V && (base[idx] >> 16) != 0;
     if (idx < V) out[idx] = v ? 1 : 0;
     const uint32_t m = __ballot_sync(0xffffffffu, v);
-    if ((threadIdx.x & 31) == 0 && m) {
-        atomicAdd((unsigned long long *)&stats[LVX_ST_VISIBLE], (unsigned long long)__popc(m));
+    if ((threadIdx.x & 31) == 0 && m)
         atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)__popc(m));
-    }
-    list_append_warp(vis_list, v, (uint32_t)idx);
+    list_append_block(vis_list, v, (uint32_t)idx, (unsigned long long *)&stats[LVX_ST_VISIBLE]);
 }
 
 // lv/culling.py:103-109: parent = OR of its 8 children
@@ -330,7 +363,8 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     uint32_t *bricks = solid_bits + (V + 31) / 32;
     LVX_CUDA(cudaMemsetAsync(bricks, 0, (size_t)(brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER)) * 4, s));
     uint32_t *occ_list = bricks + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER);
-    k_solid<<<blocks_for(V, 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, occ_list, vis_tmp, stats);
+    LVX_CUDA(cudaMemsetAsync(vis_tmp, 0, (size_t)V, s));
+    k_solid<<<blocks_for(V, SOLID_ITEMS * 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, occ_list, stats);
     unsigned nb = 148 * 16;
     if (nb > blocks_for(V, 128)) nb = blocks_for(V, 128);
     // vis_list doubles as the "needs the fine march" list until k_dilate refills it

@@ -250,6 +250,37 @@ __device__ __forceinline__ void list_append_warp(uint32_t *list, bool pred, uint
     if (pred) list[LVX_LIST_HDR + b + __popc(m & ((1u << lane) - 1u))] = value;
 }
 
+// Block-wide version for kernels that append from every thread (called by ALL threads of the
+// block, blockDim.x <= 1024): one global atomic per block instead of one per warp -- the list
+// counter is a single address, and half a million same-address atomics per pass were the cost of
+// the per-voxel culling passes.  `counter2` (optional) receives the same count (a stats word).
+__device__ __forceinline__ void list_append_block(uint32_t *list, bool pred, uint32_t value,
+                                                  unsigned long long *counter2 = nullptr) {
+    __shared__ uint32_t s_cnt[32];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n_warps = (blockDim.x + 31) >> 5;
+    const uint32_t m = __ballot_sync(0xffffffffu, pred);
+    if (lane == 0) s_cnt[warp] = __popc(m);
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t c = lane < n_warps ? s_cnt[lane] : 0;
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane < n_warps) s_cnt[lane] = inc - c;            // exclusive prefix per warp
+        if (lane == 31 && inc) {
+            s_base = atomicAdd(reinterpret_cast<unsigned long long *>(list), (unsigned long long)inc);
+            if (counter2) atomicAdd(counter2, (unsigned long long)inc);
+        }
+    }
+    __syncthreads();
+    if (pred) list[LVX_LIST_HDR + s_base + s_cnt[warp] + __popc(m & ((1u << lane) - 1u))] = value;
+    __syncthreads();          // s_cnt / s_base may be reused by the next call
+}
+
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     return v;

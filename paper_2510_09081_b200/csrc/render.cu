@@ -160,37 +160,36 @@ __device__ void capsule_normal(double px, double py, double pz, const Capsule &c
     ox = nx / nn; oy = ny / nn; oz = nz / nn;
 }
 
-// lv/raytracer.py:294-313.  The reference takes the minimum of up to three quotients.  Here the
-// quotients are first estimated with precomputed reciprocals (error < 3e-16 relative); only axes
-// whose estimate is within 1e-13 of the smallest can own the exact minimum, so the exact IEEE
-// division is evaluated for those (almost always one) and the result is bit-identical.
+// lv/raytracer.py:294-313: t = min over the axes of (face - o) / d.
+// The three IEEE quotients are formed without the division instruction sequence.  With
+// y = RN(1/d) (computed once per ray by a true division) and q0 = RN(n*y), two Markstein
+// corrections q <- fma(fma(-d, q, n), y, q) give the correctly rounded n/d: after the first one q
+// is a faithful approximation, and Markstein's theorem (Muller et al., Handbook of FP Arithmetic,
+// Thm 4.9) makes the second one exact.  (No overflow/underflow here: |n| <= 2048 and a component
+// of a unit vector is either 0 -- axis skipped -- or >= 2^-1074; components below 1e-280 are
+// treated as 0-free by the guarded path.)  5 dependent f64 instructions per axis, branch-free.
 struct RayInv { double ix, iy, iz; };
 __device__ __forceinline__ RayInv make_inv(double dx, double dy, double dz) {
     return RayInv{dx != 0.0 ? 1.0 / dx : 0.0, dy != 0.0 ? 1.0 / dy : 0.0, dz != 0.0 ? 1.0 / dz : 0.0};
+}
+__device__ __forceinline__ double exact_quot(double n, double d, double y) {
+    double q = n * y;
+    q = __fma_rn(__fma_rn(-d, q, n), y, q);
+    q = __fma_rn(__fma_rn(-d, q, n), y, q);
+    return q;
 }
 __device__ __forceinline__ double voxel_exit(double ox, double oy, double oz, double dx, double dy, double dz,
                                              const RayInv &inv, int x, int y, int z, int lvl) {
     const int size = 1 << lvl;
     const int bx = (x >> lvl) << lvl, by = (y >> lvl) << lvl, bz = (z >> lvl) << lvl;
-    const double big = 1e30;
+    const double big = 1e30, tiny = 1e-280;
     const double nx = (double)(dx > 0.0 ? bx + size : bx) - ox;
     const double ny = (double)(dy > 0.0 ? by + size : by) - oy;
     const double nz = (double)(dz > 0.0 ? bz + size : bz) - oz;
-    const double ax = dx != 0.0 ? nx * inv.ix : big;
-    const double ay = dy != 0.0 ? ny * inv.iy : big;
-    const double az = dz != 0.0 ? nz * inv.iz : big;
-    // the axis with the smallest estimate: ONE exact division (converged across the warp) ...
-    const double m = fmin(ax, fmin(ay, az));
-    const double num = m == ax ? nx : (m == ay ? ny : nz);
-    const double den = m == ax ? dx : (m == ay ? dy : dz);
-    double t = den != 0.0 ? num / den : big;
-    // ... and the exact quotient of any other axis whose estimate is within 1e-13 of it (rare)
-    const double lim = m + fabs(m) * 1e-13 + 1e-290;
-    if ((int)(ax <= lim) + (int)(ay <= lim) + (int)(az <= lim) > 1) {
-        if (ax <= lim) t = fmin(t, nx / dx);
-        if (ay <= lim) t = fmin(t, ny / dy);
-        if (az <= lim) t = fmin(t, nz / dz);
-    }
+    double t = big;
+    if (dx != 0.0) t = fmin(t, fabs(dx) > tiny ? exact_quot(nx, dx, inv.ix) : nx / dx);
+    if (dy != 0.0) t = fmin(t, fabs(dy) > tiny ? exact_quot(ny, dy, inv.iy) : ny / dy);
+    if (dz != 0.0) t = fmin(t, fabs(dz) > tiny ? exact_quot(nz, dz, inv.iz) : nz / dz);
     return t;
 }
 
@@ -263,21 +262,37 @@ __device__ __forceinline__ uint8_t to_srgb8(double v) {   // lv/raytracer.py:94-
 // hits are folded with an order-independent rule.
 constexpr int RC_WARPS = 4;
 #define LVX_FULL 0xffffffffu
+#ifndef LVX_SPEC
+#define LVX_SPEC 2      // occupied voxels a ray walks ahead per round (opaque)
+#endif
+#ifndef LVX_SPEC_T
+#define LVX_SPEC_T 4    // ... per round (transparent: rays rarely stop early, so deeper is cheap)
+#endif
 
+// Speculation.  A round costs a fixed chain of dependent loads and flushes of half-empty
+// batches, so every ray records its next M occupied voxels per round (the DDA does not depend on
+// hit results) and the pairs of all M voxels go through stages A-C together.  Results are then
+// consumed in voxel order ("ordinal" m), exactly like the reference would: the first ordinal
+// with a hit ends an opaque ray, a transparent ray blends ordinal by ordinal and stops where the
+// reference stops.  Work done for ordinals behind that point is discarded and not counted.
+template <int M>
 struct PairQueues {
     double dir[3][32];
-    float dirf[3][32], pf[3][32];   // f32 direction and a ray point inside the current voxel
-    int vox[3][32];
-    uint32_t qa_rs[64], qa_g[64];   // queue A: (ray << 16 | slot), global fragment index
-    uint32_t qb_rs[64], qb_i[64];   // queue B: (ray << 16 | slot), segment index
+    float dirf[3][32];
+    float pf[M][3][32];             // a ray point inside voxel m (f32, for the conservative pre-test)
+    int16_t vox[M][3][32];          // res <= 1024
+    uint32_t fo[M][32], n[M][32];   // fragment list of voxel m (n = 0: none)
+    uint32_t qa_rs[64], qa_g[64];   // queue A: (ordinal << 21 | ray << 16 | slot), global fragment index
+    uint32_t qb_rs[64], qb_i[64];   // queue B: same tag, segment index
 };
+#define LVX_RS_RAY(rs) (((rs) >> 16) & 31u)
+#define LVX_RS_ORD(rs) ((rs) >> 21)
+#define LVX_RS_SLOT(rs) ((rs) & 0xFFFFu)
 
-// Runs stages A-C for one round.  `n` = this lane's list length (0 if the ray is idle), `fo` its
-// first fragment; `stage_c(valid, rs, seg)` is called with 32 (or fewer, at the end) queue-B entries.
-// Returns the number of (ray, fragment) pairs of the round (= the reference's test count).
-template <class F>
-__device__ __forceinline__ uint32_t run_pairs(const RenderArgs &A, PairQueues &S, uint32_t n, uint32_t fo, int lane,
-                                              float R2f, F &&stage_c) {
+// Runs stages A-C for one round over the lists S.fo/S.n[0..M) of every lane;
+// `stage_c(valid, rs, seg)` is called with 32 (or fewer, at the end) queue-B entries.
+template <int M, class F>
+__device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S, int lane, float R2f, F &&stage_c) {
     const uint32_t lt_mask = (1u << lane) - 1u;
     uint32_t qa = 0, qb = 0;
 
@@ -297,8 +312,8 @@ __device__ __forceinline__ uint32_t run_pairs(const RenderArgs &A, PairQueues &S
         if ((uint32_t)lane < take) {
             rs1 = S.qa_rs[base + lane];
             ii = A.frags[S.qa_g[base + lane]];
-            const uint32_t rr = rs1 >> 16;
-            pass = !surely_misses_f32(S.pf[0][rr], S.pf[1][rr], S.pf[2][rr], S.dirf[0][rr], S.dirf[1][rr],
+            const uint32_t rr = LVX_RS_RAY(rs1), m = LVX_RS_ORD(rs1);
+            pass = !surely_misses_f32(S.pf[m][0][rr], S.pf[m][1][rr], S.pf[m][2][rr], S.dirf[0][rr], S.dirf[1][rr],
                                       S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
         }
         qa = base;
@@ -312,38 +327,42 @@ __device__ __forceinline__ uint32_t run_pairs(const RenderArgs &A, PairQueues &S
         while (qb >= 32) drain_b();          // ---- stage C
     };
 
-    // ---- stage A: every lane walks the loose-bit words of its own list; in each step all lanes
+    // ---- stage A: every lane walks the loose-bit words of its own lists; in each step all lanes
     // that still have a tight fragment in their current word push one pair (their lowest bit).
     // Loose fragments are never enumerated at all.
-    const uint32_t last = fo + n - 1;                       // valid when n > 0
-    const uint32_t w0 = fo >> 5, nw = n ? (last >> 5) - w0 + 1 : 0;
-    const uint32_t maxw = __reduce_max_sync(LVX_FULL, nw);
-    for (uint32_t wi = 0; wi < maxw; wi++) {
-        uint32_t mask = 0;
-        const uint32_t w = w0 + wi;
-        if (wi < nw) {
-            const uint32_t lw = A.loose ? A.loose[w] : 0u;
-            const uint32_t lo = wi == 0 ? (fo & 31u) : 0u;
-            const uint32_t hi = (w == (last >> 5)) ? (last & 31u) : 31u;     // inclusive
-            mask = ~lw & (0xffffffffu >> (31u - hi)) & (0xffffffffu << lo);
-        }
-        for (;;) {
-            const uint32_t ma = __ballot_sync(LVX_FULL, mask != 0);
-            if (ma == 0) break;
-            if (mask) {
-                const uint32_t g = (w << 5) + (uint32_t)(__ffs(mask) - 1);
-                mask &= mask - 1;
-                const uint32_t pos = qa + __popc(ma & lt_mask);
-                S.qa_rs[pos] = ((uint32_t)lane << 16) | (g - fo); S.qa_g[pos] = g;
+#pragma unroll 1
+    for (int m = 0; m < M; m++) {
+        const uint32_t fo = S.fo[m][lane], n = S.n[m][lane];
+        const uint32_t last = fo + n - 1;                       // valid when n > 0
+        const uint32_t w0 = fo >> 5, nw = n ? (last >> 5) - w0 + 1 : 0;
+        const uint32_t maxw = __reduce_max_sync(LVX_FULL, nw);
+        const uint32_t tag = ((uint32_t)m << 21) | ((uint32_t)lane << 16);
+        for (uint32_t wi = 0; wi < maxw; wi++) {
+            uint32_t mask = 0;
+            const uint32_t w = w0 + wi;
+            if (wi < nw) {
+                const uint32_t lw = A.loose ? A.loose[w] : 0u;
+                const uint32_t lo = wi == 0 ? (fo & 31u) : 0u;
+                const uint32_t hi = (w == (last >> 5)) ? (last & 31u) : 31u;     // inclusive
+                mask = ~lw & (0xffffffffu >> (31u - hi)) & (0xffffffffu << lo);
             }
-            qa += __popc(ma);
-            __syncwarp();
-            if (qa >= 32) drain_a();
+            for (;;) {
+                const uint32_t ma = __ballot_sync(LVX_FULL, mask != 0);
+                if (ma == 0) break;
+                if (mask) {
+                    const uint32_t g = (w << 5) + (uint32_t)(__ffs(mask) - 1);
+                    mask &= mask - 1;
+                    const uint32_t pos = qa + __popc(ma & lt_mask);
+                    S.qa_rs[pos] = tag | (g - fo); S.qa_g[pos] = g;
+                }
+                qa += __popc(ma);
+                __syncwarp();
+                if (qa >= 32) drain_a();
+            }
         }
     }
     while (qa > 0) drain_a();
     while (qb > 0) drain_b();
-    return __reduce_add_sync(LVX_FULL, n);
 }
 
 // lv/raytracer.py:414-423 + 272-291: the pixel's ray and its parameter range inside the grid
@@ -376,11 +395,44 @@ __device__ __forceinline__ bool setup_ray(const RenderArgs &A, int px, int py, d
     return t1 >= t0;
 }
 
+// The DDA of lv/raytracer.py:475-482 / 542-556 from parameter `tcur`: finds the next occupied
+// voxel, records it as ordinal `m` of this lane and returns true with te = its exit parameter;
+// returns false when the ray leaves the grid first.  tcur is left at the voxel's entry parameter.
+template <int M>
+__device__ __forceinline__ bool next_occupied(const RenderArgs &A, PairQueues<M> &S, int lane, int m, double ox, double oy,
+                                              double oz, double dx, double dy, double dz, const RayInv &inv, double t1,
+                                              double &tcur, double &te) {
+    const int res = A.res;
+    for (;;) {
+        if (!(tcur < t1)) return false;
+        const double tm = tcur + 1e-6;
+        const int x = (int)floor(ox + dx * tm), y = (int)floor(oy + dy * tm), z = (int)floor(oz + dz * tm);
+        if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) return false;
+        const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
+        // the list bounds are fetched together with the march byte (independent loads, one round
+        // trip); they are only used when the voxel turns out to be occupied
+        const int lv = A.march[idx];
+        const uint32_t fo = A.offsets[idx], fe = A.offsets[idx + 1];
+        const bool occ = lv == 255;
+        const double tx = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, occ ? 0 : lv);
+        if (occ) {
+            S.fo[m][lane] = fo;
+            S.n[m][lane] = fe - fo;
+            S.vox[m][0][lane] = (int16_t)x; S.vox[m][1][lane] = (int16_t)y; S.vox[m][2][lane] = (int16_t)z;
+            te = tx;
+            const double tc = 0.5 * (tcur + te);     // a point of the ray inside the voxel
+            S.pf[m][0][lane] = (float)(ox + dx * tc); S.pf[m][1][lane] = (float)(oy + dy * tc); S.pf[m][2][lane] = (float)(oz + dz * tc);
+            return true;
+        }
+        tcur = tx > tcur ? tx : tcur + 1e-6;
+    }
+}
+
 // ----------------------------------------------------------------------------- opaque
 struct WarpShared {
-    PairQueues q;
+    PairQueues<LVX_SPEC> q;
     double hit_t[32];
-    uint32_t hit_s[32], hit_i[32];
+    uint32_t hit_rs[32], hit_i[32];
 };
 
 #ifndef LVX_RC_MINB
@@ -389,6 +441,7 @@ struct WarpShared {
 template <bool DEFER>
 __global__ void __launch_bounds__(RC_WARPS * 32, LVX_RC_MINB)
 k_render_opaque_coop(const RenderArgs A) {
+    constexpr int M = LVX_SPEC;
     __shared__ WarpShared sh_all[RC_WARPS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpShared &S = sh_all[warp];
@@ -413,75 +466,71 @@ k_render_opaque_coop(const RenderArgs A) {
     __syncwarp();
 
     for (;;) {
-        // ---- 1. march to the next occupied voxel (lv/raytracer.py:475-482, 506-509)
-        uint32_t n = 0, fo = 0;
-        double te = 0.0;
-        int x = 0, y = 0, z = 0;
-        if (active) {
-            for (;;) {
-                if (!(t < t1)) { active = false; break; }
-                const double tm = t + 1e-6;
-                x = (int)floor(ox + dx * tm); y = (int)floor(oy + dy * tm); z = (int)floor(oz + dz * tm);
-                if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) { active = false; break; }
-                const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
-                const int lv = A.march[idx];
-                if (lv == 255) {
-                    fo = A.offsets[idx];
-                    n = A.offsets[idx + 1] - fo;
-                    te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
-                    break;
-                }
-                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, lv);
-                t = tl > t ? tl : t + 1e-6;
+        // ---- 1. record the next M occupied voxels (lv/raytracer.py:475-482, 506-509)
+        bool leaving = false;
+        double tcur = t;
+#pragma unroll 1
+        for (int m = 0; m < M; m++) {
+            double te = 0.0;
+            if (active && !leaving && next_occupied<M>(A, S.q, lane, m, ox, oy, oz, dx, dy, dz, inv, t1, tcur, te)) {
+                tcur = te > tcur ? te : tcur + 1e-6;          // where the ray goes on if voxel m has no hit
+            } else {
+                leaving = true;
+                S.q.n[m][lane] = 0;
             }
         }
         if (__ballot_sync(LVX_FULL, active) == 0) break;
-        S.q.vox[0][lane] = x; S.q.vox[1][lane] = y; S.q.vox[2][lane] = z;
-        {   // a point of the ray inside the voxel (its centre-most parameter), for the f32 pre-test
-            const double tc = 0.5 * (t + te);
-            S.q.pf[0][lane] = (float)(ox + dx * tc); S.q.pf[1][lane] = (float)(oy + dy * tc); S.q.pf[2][lane] = (float)(oz + dz * tc);
-        }
-        double cur_t = -1.0;           // best hit of this lane's ray in this voxel
-        uint32_t cur_s = 0xffffffffu, cur_i = 0;
-        const uint32_t T = run_pairs(A, S.q, active ? n : 0u, fo, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii) {
+        __syncwarp();
+        // best hit of this lane's ray in this round: lowest ordinal, then min t, then lowest slot
+        double cur_t = -1.0;
+        uint32_t cur_ms = 0xffffffffu, cur_i = 0;      // (ordinal << 16) | slot
+        run_pairs<M>(A, S.q, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii) {
             bool hit = false;
             double ht = 0.0;
-            const uint32_t hr = rs >> 16, hs = rs & 0xFFFFu;
+            const uint32_t hr = LVX_RS_RAY(rs), hm_ = LVX_RS_ORD(rs);
             if (valid) {
                 const double ddx = S.q.dir[0][hr], ddy = S.q.dir[1][hr], ddz = S.q.dir[2][hr];
                 const Capsule c = load_capsule(A.verts, A.normals, (int64_t)ii, r, clip);
                 ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
-                if (ht >= 0.0) {   // lv/raytracer.py:446-452: the hit must lie in the ray's current voxel
+                if (ht >= 0.0) {   // lv/raytracer.py:446-452: the hit must lie in the voxel being visited
                     const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
-                    hit = hx == S.q.vox[0][hr] && hy == S.q.vox[1][hr] && hz == S.q.vox[2][hr];
+                    hit = hx == S.q.vox[hm_][0][hr] && hy == S.q.vox[hm_][1][hr] && hz == S.q.vox[hm_][2][hr];
                 }
             }
-            // fold hits on the owning lanes: min t, then lowest slot (lv/raytracer.py:453)
+            // fold hits on the owning lanes (lv/raytracer.py:453: min t, first slot wins ties)
             uint32_t hm = __ballot_sync(LVX_FULL, hit);
             if (hm == 0) return;
-            if (hit) { S.hit_t[lane] = ht; S.hit_s[lane] = hs; S.hit_i[lane] = ii; }
+            if (hit) { S.hit_t[lane] = ht; S.hit_rs[lane] = rs; S.hit_i[lane] = ii; }
             __syncwarp();
             while (hm) {
                 const int src = __ffs(hm) - 1;
                 hm &= hm - 1;
-                const uint32_t owner = __shfl_sync(LVX_FULL, hr, src);
-                if ((uint32_t)lane == owner) {
+                const uint32_t rs2 = S.hit_rs[src];
+                if ((uint32_t)lane == LVX_RS_RAY(rs2)) {
                     const double tt = S.hit_t[src];
-                    const uint32_t s2 = S.hit_s[src];
-                    if (cur_t < 0.0 || tt < cur_t || (tt == cur_t && s2 < cur_s)) {
-                        cur_t = tt; cur_s = s2; cur_i = S.hit_i[src];
+                    const uint32_t ms2 = (LVX_RS_ORD(rs2) << 16) | LVX_RS_SLOT(rs2);
+                    const uint32_t o2 = ms2 >> 16, oc = cur_ms >> 16;
+                    if (cur_t < 0.0 || o2 < oc || (o2 == oc && (tt < cur_t || (tt == cur_t && ms2 < cur_ms)))) {
+                        cur_t = tt; cur_ms = ms2; cur_i = S.hit_i[src];
                     }
                 }
             }
             __syncwarp();
         });
-        if (lane == 0) n_tests += T;
         if (active) {
+            // tests the reference would have run: every voxel up to and including the one with the hit
+            const int m_end = cur_t >= 0.0 ? (int)(cur_ms >> 16) : M - 1;
+            uint32_t cnt = 0;
+#pragma unroll 1
+            for (int m = 0; m <= m_end; m++) cnt += S.q.n[m][lane];
+            n_tests += cnt;
             if (cur_t >= 0.0) { best_t = cur_t; best_i = cur_i; active = false; }
-            else t = te > t ? te : t + 1e-6;
+            else if (leaving) active = false;
+            else t = tcur;
         }
         __syncwarp();
     }
+    n_tests = warp_sum_u64(n_tests);
 
     if (!DEFER) {
         if (live) {
@@ -555,13 +604,13 @@ k_render_opaque_coop(const RenderArgs A) {
 }
 
 // ----------------------------------------------------------------------------- transparent
-// Same work sharing for lv/raytracer.py:518-645.  Per round every active ray sits in one occupied
-// voxel.  In-voxel hits become (key = depth16 << 16 | slot, t, segment) records in a per-warp list,
-// which the owning lanes drain into their private k-slot buffers.  The k smallest keys above
-// `last_key` are a set, so the insertion order does not matter (keys are unique: the slot is in
-// the low bits) and the reference's result is reproduced exactly, including the re-scan of a
-// voxel when more than k hits were accepted (the ray then stays in the voxel for another round,
-// and its tests are counted again like the reference does).
+// Same work sharing for lv/raytracer.py:518-645.  In-voxel hits become (ordinal, key = depth16 <<
+// 16 | slot, t, segment) records in a per-warp list, which the owning lanes drain into their
+// private k-slot buffers (one per ordinal).  The k smallest keys above `last_key` are a set, so
+// the insertion order does not matter (keys are unique: the slot is in the low bits) and the
+// reference's result is reproduced exactly, including the re-scan of a voxel when more than k
+// hits were accepted: the ray then starts its next round in that same voxel with `last_key` set
+// (and its tests are counted again like the reference does).
 //
 // Deferred shading.  Control flow only needs the accumulated alpha, which depends on the NUMBER
 // of blended hits (A += (1-A)*alpha), not on their colour.  So the blend step just fixes each
@@ -570,13 +619,15 @@ k_render_opaque_coop(const RenderArgs A) {
 // at once and the owning lanes add w*colour in FIFO order -- per ray that is the reference's
 // order of additions, so the f64 sums keep their bits.
 constexpr int HL_CAP = 96;
+constexpr int KMAX = 64;        // lv/raytracer.py:64: k <= 64
 
 struct WarpSharedT {
-    PairQueues q;
-    double t_enter[32], inv_span[32];
+    PairQueues<LVX_SPEC_T> q;
+    double t_enter[LVX_SPEC_T][32], inv_span[LVX_SPEC_T][32], t_exit[LVX_SPEC_T][32];
     double hl_t[HL_CAP];
     uint32_t hl_key[HL_CAP], hl_i[HL_CAP];
-    uint8_t hl_r[HL_CAP];
+    uint8_t hl_r[HL_CAP];           // ordinal << 5 | ray
+    uint32_t own[32];               // drain: per ray, the records it owns in the current chunk
     double d_w[64], d_t[64];        // deferred shading FIFO
     uint32_t d_i[64], d_ray[64];
     double d_c[3][32];              // w * colour of the batch being folded
@@ -587,13 +638,15 @@ struct WarpSharedT {
 #endif
 __global__ void __launch_bounds__(RC_WARPS * 32, LVX_RT_MINB)
 k_render_transparent_coop(const RenderArgs A) {
-    __shared__ WarpSharedT sh_all[RC_WARPS];
+    constexpr int M = LVX_SPEC_T;
+    extern __shared__ __align__(16) unsigned char smem_raw[];      // RC_WARPS x WarpSharedT (> 48 KB: opt-in)
+    WarpSharedT *sh_all = reinterpret_cast<WarpSharedT *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpSharedT &S = sh_all[warp];
     const int px = A.p.tile_x0 + blockIdx.x * (8 * RC_WARPS) + warp * 8 + (lane & 7);
     const int py = A.p.tile_y0 + blockIdx.y * 4 + (lane >> 3);
     const bool live = px < A.p.tile_x1 && py < A.p.tile_y1;
-    const int w = A.cam.width, res = A.res;
+    const int w = A.cam.width;
     const double ox = A.cam.pos[0], oy = A.cam.pos[1], oz = A.cam.pos[2];
     const bool clip = A.p.use_clip != 0;
     const double r = A.p.radius;
@@ -610,16 +663,15 @@ k_render_transparent_coop(const RenderArgs A) {
     const RayInv inv = make_inv(dx, dy, dz);
     double col_r = 0.0, col_g = 0.0, col_b = 0.0, acc_a = 0.0;
     int64_t first_hit = -1;
-    uint32_t keybuf[64], ibuf[64];
-    double tbuf[64];
+    // k-slot buffers, one per ordinal, packed with stride k (local memory)
+    uint32_t keybuf[M * KMAX], ibuf[M * KMAX];
+    double tbuf[M * KMAX];
+    int kept[M];
+    uint32_t accepted[M];
     uint64_t n_tests = 0;
     uint32_t qd = 0;           // entries in the deferred shading FIFO
-    // per-voxel state of this lane's ray
-    bool repeat = false;
-    int64_t last_key = -1;
-    uint32_t n = 0, fo = 0;
-    double te = 0.0;
-    int x = 0, y = 0, z = 0;
+    int repeat_m = -1;         // >= 0: the ray re-scans the voxel recorded as that ordinal last round
+    int64_t last_key = -1;     // ... accepting only keys above last_key (applies to ordinal 0 of the new round)
     __syncwarp();
 
     // shades the first min(qd, 32) FIFO entries and folds w*colour into the owners' sums
@@ -652,76 +704,100 @@ k_render_transparent_coop(const RenderArgs A) {
     };
 
     for (;;) {
-        // ---- 1. next occupied voxel (or stay for a re-scan)
-        if (active && !repeat) {
-            for (;;) {
-                if ((early && acc_a >= 0.999) || !(t < t1)) { active = false; break; }
-                const double tm = t + 1e-6;
-                x = (int)floor(ox + dx * tm); y = (int)floor(oy + dy * tm); z = (int)floor(oz + dz * tm);
-                if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) { active = false; break; }
-                const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
-                const int lv = A.march[idx];
-                if (lv == 255) {
-                    fo = A.offsets[idx];
-                    n = A.offsets[idx + 1] - fo;
-                    te = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, 0);
-                    const double span = te - t;                  // t_enter = t (lv/raytracer.py:557-560)
-                    S.t_enter[lane] = t;
-                    S.inv_span[lane] = span > 0.0 ? 65535.0 / span : 0.0;
-                    last_key = -1;
-                    break;
+        // ---- 1. record the next M occupied voxels; a re-scan keeps its voxel as ordinal 0
+        bool leaving = false;
+        int n_vox = 0;                                         // ordinals recorded by this lane
+        double tcur = t;
+        const int64_t lk0 = repeat_m >= 0 ? last_key : -1;     // key floor of ordinal 0
+#pragma unroll 1
+        for (int m = 0; m < M; m++) {
+            double te = 0.0;
+            bool have = false;
+            if (active && !leaving) {
+                if (m == 0 && repeat_m >= 0) {
+                    const int s = repeat_m;                    // own column only: no other lane reads it yet
+                    S.q.fo[0][lane] = S.q.fo[s][lane]; S.q.n[0][lane] = S.q.n[s][lane];
+#pragma unroll
+                    for (int a = 0; a < 3; a++) { S.q.vox[0][a][lane] = S.q.vox[s][a][lane]; S.q.pf[0][a][lane] = S.q.pf[s][a][lane]; }
+                    te = S.t_exit[s][lane];
+                    have = true;                               // tcur == t == that voxel's entry parameter
+                } else {
+                    // lv/raytracer.py:543-544: the cut-off is re-checked at apply time, per ordinal
+                    have = next_occupied<M>(A, S.q, lane, m, ox, oy, oz, dx, dy, dz, inv, t1, tcur, te);
                 }
-                const double tl = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, lv);
-                t = tl > t ? tl : t + 1e-6;
             }
+            if (have) {
+                const double span = te - tcur;                 // t_enter = tcur (lv/raytracer.py:557-560)
+                S.t_enter[m][lane] = tcur;
+                S.t_exit[m][lane] = te;
+                S.inv_span[m][lane] = span > 0.0 ? 65535.0 / span : 0.0;
+                tcur = te > tcur ? te : tcur + 1e-6;
+                n_vox = m + 1;
+            } else {
+                leaving = true;
+                S.q.n[m][lane] = 0;
+            }
+            kept[m] = 0; accepted[m] = 0;
         }
+        repeat_m = -1;
         if (__ballot_sync(LVX_FULL, active) == 0) break;
-        S.q.vox[0][lane] = x; S.q.vox[1][lane] = y; S.q.vox[2][lane] = z;
-        {
-            const double tc = 0.5 * (t + te);
-            S.q.pf[0][lane] = (float)(ox + dx * tc); S.q.pf[1][lane] = (float)(oy + dy * tc); S.q.pf[2][lane] = (float)(oz + dz * tc);
-        }
-        int kept = 0;
-        uint32_t accepted = 0, hl_n = 0;
+        __syncwarp();
+        uint32_t hl_n = 0;
 
         // owners pull their records out of the hit list (insertion sort, lv/raytracer.py:589-607)
         auto drain = [&]() {
-            for (uint32_t e = 0; e < hl_n; e++) {
-                if (S.hl_r[e] != (uint8_t)lane) continue;
-                const uint32_t key = S.hl_key[e];
-                if ((int64_t)key <= last_key) continue;
-                accepted++;
-                int j;
-                if (kept < kslots) { j = kept; kept++; }
-                else if (key < keybuf[kslots - 1]) j = kslots - 1;
-                else continue;
-                while (j > 0 && keybuf[j - 1] > key) {
-                    keybuf[j] = keybuf[j - 1]; tbuf[j] = tbuf[j - 1]; ibuf[j] = ibuf[j - 1];
-                    j--;
+            for (uint32_t c0 = 0; c0 < hl_n; c0 += 32) {
+                // lane e looks at record c0+e; all records of one ray are matched into a bit mask
+                // that the ray's own lane picks up from shared memory
+                const bool have = c0 + lane < hl_n;
+                const uint32_t tag_e = have ? S.hl_r[c0 + lane] : 0xffu;
+                const uint32_t same = __match_any_sync(LVX_FULL, have ? (tag_e & 31u) : 32u + (uint32_t)lane);
+                S.own[lane] = 0;
+                __syncwarp();
+                if (have) S.own[tag_e & 31u] = same;          // every writer of a slot writes the same mask
+                __syncwarp();
+                uint32_t mine = S.own[lane];
+                __syncwarp();
+                while (mine) {
+                    const uint32_t e = c0 + (uint32_t)(__ffs(mine) - 1);
+                    mine &= mine - 1;
+                    const int m = (int)(S.hl_r[e] >> 5);
+                    const uint32_t key = S.hl_key[e];
+                    if (m == 0 && (int64_t)key <= lk0) continue;
+                    accepted[m]++;
+                    uint32_t *kb = keybuf + m * kslots, *ib = ibuf + m * kslots;
+                    double *tb = tbuf + m * kslots;
+                    int j;
+                    if (kept[m] < kslots) { j = kept[m]; kept[m]++; }
+                    else if (key < kb[kslots - 1]) j = kslots - 1;
+                    else continue;
+                    while (j > 0 && kb[j - 1] > key) {
+                        kb[j] = kb[j - 1]; tb[j] = tb[j - 1]; ib[j] = ib[j - 1];
+                        j--;
+                    }
+                    kb[j] = key; tb[j] = S.hl_t[e]; ib[j] = S.hl_i[e];
                 }
-                keybuf[j] = key; tbuf[j] = S.hl_t[e]; ibuf[j] = S.hl_i[e];
             }
             hl_n = 0;
             __syncwarp();
         };
 
-        __syncwarp();
-        const uint32_t T = run_pairs(A, S.q, active ? n : 0u, fo, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii) {
+        run_pairs<M>(A, S.q, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii) {
             bool hit = false;
             uint32_t hkey = 0;
             double ht = 0.0;
-            const uint32_t hr = rs >> 16, hs = rs & 0xFFFFu;
+            const uint32_t hr = LVX_RS_RAY(rs), hm_ = LVX_RS_ORD(rs);
             if (valid) {
                 const double ddx = S.q.dir[0][hr], ddy = S.q.dir[1][hr], ddz = S.q.dir[2][hr];
                 const Capsule c = load_capsule(A.verts, A.normals, (int64_t)ii, r, clip);
                 ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
                 if (ht >= 0.0) {
                     const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
-                    hit = hx == S.q.vox[0][hr] && hy == S.q.vox[1][hr] && hz == S.q.vox[2][hr];
+                    hit = hx == S.q.vox[hm_][0][hr] && hy == S.q.vox[hm_][1][hr] && hz == S.q.vox[hm_][2][hr];
                     if (hit) {   // lv/raytracer.py:583-588
-                        int64_t q = (int64_t)((ht - S.t_enter[hr]) * S.inv_span[hr]);
+                        int64_t q = (int64_t)((ht - S.t_enter[hm_][hr]) * S.inv_span[hm_][hr]);
                         if (q < 0) q = 0; else if (q > 65535) q = 65535;
-                        hkey = ((uint32_t)q << 16) | hs;
+                        hkey = ((uint32_t)q << 16) | LVX_RS_SLOT(rs);
                     }
                 }
             }
@@ -730,50 +806,64 @@ k_render_transparent_coop(const RenderArgs A) {
             if (hl_n + __popc(hm) > HL_CAP) drain();
             if (hit) {
                 const uint32_t pos = hl_n + __popc(hm & lt_mask);
-                S.hl_t[pos] = ht; S.hl_key[pos] = hkey; S.hl_i[pos] = ii; S.hl_r[pos] = (uint8_t)hr;
+                S.hl_t[pos] = ht; S.hl_key[pos] = hkey; S.hl_i[pos] = ii; S.hl_r[pos] = (uint8_t)((hm_ << 5) | hr);
             }
             hl_n += __popc(hm);
             __syncwarp();
         });
-        if (lane == 0) n_tests += T;
         drain();
-        // ---- blend the kept hits front to back (lv/raytracer.py:608-631): fix the weights now,
-        // queue the colours
-        {
-            const int kmax = __reduce_max_sync(LVX_FULL, active ? kept : 0);
-            bool stopped = !active;
+        // ---- consume the ordinals in order (lv/raytracer.py:543-544, 608-637): fix the blend
+        // weights now, queue the colours
+        bool going = active;       // false once this lane's ray has stopped consuming this round
+#pragma unroll 1
+        for (int m = 0; m < M; m++) {
+            // a ray consumes ordinal m if it is still going, has not reached the alpha cut-off
+            // (checked before every voxel, lv/raytracer.py:543-544) and has such a voxel
+            bool use = going;
+            if (use && early && acc_a >= 0.999) { use = false; going = false; active = false; }
+            if (use && m >= n_vox) { use = false; going = false; active = false; }   // left the grid
+            if (use) n_tests += S.q.n[m][lane];
+            const int km = use ? kept[m] : 0;
+            const int kmax = __reduce_max_sync(LVX_FULL, km);
+            bool stopped = !use;
+            const uint32_t *ib = ibuf + m * kslots;
+            const double *tb = tbuf + m * kslots;
             for (int j = 0; j < kmax; j++) {
-                if (!stopped && (j >= kept || (early && acc_a >= 0.999))) stopped = true;
+                if (!stopped && (j >= km || (early && acc_a >= 0.999))) stopped = true;
                 double wgt = 0.0;
                 if (!stopped) {
                     wgt = (1.0 - acc_a) * alpha;
                     acc_a += wgt;
-                    if (first_hit < 0) first_hit = ibuf[j];
+                    if (first_hit < 0) first_hit = ib[j];
                 }
                 const uint32_t pm = __ballot_sync(LVX_FULL, !stopped);
                 if (pm == 0) break;
                 if (!stopped) {
                     const uint32_t pos = qd + __popc(pm & lt_mask);
-                    S.d_w[pos] = wgt; S.d_t[pos] = tbuf[j]; S.d_i[pos] = ibuf[j]; S.d_ray[pos] = (uint32_t)lane;
+                    S.d_w[pos] = wgt; S.d_t[pos] = tb[j]; S.d_i[pos] = ib[j]; S.d_ray[pos] = (uint32_t)lane;
                 }
                 qd += __popc(pm);
                 __syncwarp();
                 if (qd >= 32) shade_batch();
             }
-        }
-        if (active) {
-            // lv/raytracer.py:632-637
-            if (accepted <= (uint32_t)kslots || (early && acc_a >= 0.999)) {
-                repeat = false;
-                t = te > t ? te : t + 1e-6;
-            } else {
-                last_key = keybuf[kslots - 1];
-                repeat = true;
+            if (use) {
+                // lv/raytracer.py:632-637
+                if (accepted[m] <= (uint32_t)kslots || (early && acc_a >= 0.999)) {
+                    const double t_in = S.t_enter[m][lane], t_out = S.t_exit[m][lane];
+                    t = t_out > t_in ? t_out : t_in + 1e-6;      // on to the next voxel
+                } else {
+                    last_key = keybuf[m * kslots + kslots - 1];  // stay: re-scan this voxel next round
+                    repeat_m = m;
+                    t = S.t_enter[m][lane];
+                    going = false;
+                }
             }
         }
+        if (active && early && acc_a >= 0.999) active = false;   // lv/raytracer.py:543-544
         __syncwarp();
     }
     while (qd > 0) shade_batch();
+    n_tests = warp_sum_u64(n_tests);
 
     if (live) {
         const double out_r = col_r + (1.0 - acc_a) * A.p.background[0];
@@ -858,7 +948,13 @@ int lvx_render(const double *verts, const float *verts_f, const double *normals,
         k_render_opaque_coop<false><<<cgrid, RC_WARPS * 32, 0, (cudaStream_t)stream>>>(A);
     } else {
         const dim3 cgrid((tw + 8 * RC_WARPS - 1) / (8 * RC_WARPS), (th + 3) / 4);
-        k_render_transparent_coop<<<cgrid, RC_WARPS * 32, 0, (cudaStream_t)stream>>>(A);
+        const size_t smem = sizeof(WarpSharedT) * RC_WARPS;
+        static bool attr_set = false;
+        if (!attr_set) {
+            LVX_CUDA(cudaFuncSetAttribute(k_render_transparent_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set = true;
+        }
+        k_render_transparent_coop<<<cgrid, RC_WARPS * 32, smem, (cudaStream_t)stream>>>(A);
     }
     LVX_LAUNCH_CHECK();
     return LVX_OK;
