@@ -50,6 +50,7 @@ enum {
     LVX_ST_VISIBLE = 9,      /* visible voxels = culling.base.sum() */
     LVX_ST_OCCUPIED = 10,    /* voxels with count > 0 */
     LVX_ST_OCC_SAT = 11,     /* voxels whose 16-bit occupancy sum saturated */
+    LVX_ST_TILE_CURSOR = 12, /* scratch: pixel-tile queue of the persistent trace kernels (reset by every launch) */
     LVX_STATS_WORDS = 16
 };
 

@@ -193,13 +193,27 @@ __device__ __forceinline__ double voxel_exit(double ox, double oy, double oz, do
     return t;
 }
 
-// lv/raytracer.py:368-390 (volumes are f32, widened exactly like the reference's astype(f64))
-__device__ __forceinline__ double tri3d(const float *__restrict__ vol, const uint8_t *__restrict__ guard, int res,
-                                        double px, double py, double pz) {
+// lv/raytracer.py:368-390 (volumes are f32, widened exactly like the reference's astype(f64)).
+// The AO and the shadow volume are sampled at the same point, so the corner indices and weights
+// are formed once; each sum keeps the reference's order of additions.
+struct ShadeCtx {
+    const double *verts, *normals;
+    const float *ao, *sh;
+    const uint8_t *guard;      // non-NULL: volumes hold values only where guard[idx] == 255, 1.0 elsewhere
+    int res, clip;
+    double r, l0, l1, l2;      // capsule radius, direction to the light
+};
+__device__ __forceinline__ ShadeCtx make_shade_ctx(const RenderArgs &A) {
+    return ShadeCtx{A.verts, A.normals, A.ao, A.sh, A.guard_volumes ? A.march : nullptr, A.res, A.p.use_clip != 0,
+                    A.p.radius, A.p.light_to_source[0], A.p.light_to_source[1], A.p.light_to_source[2]};
+}
+
+__device__ __forceinline__ void tri3d2(const ShadeCtx &cx, double px, double py, double pz, double &ao, double &sh) {
+    const int res = cx.res;
     const double ux = px - 0.5, uy = py - 0.5, uz = pz - 0.5;
     const int ix = (int)floor(ux), iy = (int)floor(uy), iz = (int)floor(uz);
     const double fx = ux - ix, fy = uy - iy, fz = uz - iz;
-    double acc = 0.0;
+    double acc_a = 0.0, acc_s = 0.0;
 #pragma unroll
     for (int dz = 0; dz < 2; dz++) {
         const int z = min(max(iz + dz, 0), res - 1);
@@ -214,28 +228,46 @@ __device__ __forceinline__ double tri3d(const float *__restrict__ vol, const uin
                 const double wx = dx ? fx : 1.0 - fx;
                 const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
                 // non-visible voxels keep ao = shadow = 1 (lv/shading.py:177-178)
-                const double val = (guard && guard[idx] != 255) ? 1.0 : (double)vol[idx];
-                acc += wx * wy * wz * val;
+                const bool unit = cx.guard && cx.guard[idx] != 255;
+                const double w = wx * wy * wz;
+                if (cx.ao) acc_a += w * (unit ? 1.0 : (double)cx.ao[idx]);
+                if (cx.sh) acc_s += w * (unit ? 1.0 : (double)cx.sh[idx]);
             }
         }
     }
-    return acc;
+    ao = cx.ao ? acc_a : 1.0;
+    sh = cx.sh ? acc_s : 1.0;
 }
 
 // lv/raytracer.py:393-411
-__device__ __forceinline__ void shade(const RenderArgs &A, const Capsule &c, double nx, double ny, double nz,
+__device__ __forceinline__ void shade(const ShadeCtx &cx, const Capsule &c, double nx, double ny, double nz,
                                       double px, double py, double pz, double &cr, double &cg, double &cb) {
     const double sx = c.b.x - c.a.x, sy = c.b.y - c.a.y, sz = c.b.z - c.a.z;
     const double sn = sqrt(sx * sx + sy * sy + sz * sz);
     if (sn == 0.0) { cr = cg = cb = 0.5; }
     else { cr = fabs(sx) / sn; cg = fabs(sy) / sn; cb = fabs(sz) / sn; }
-    const uint8_t *guard = A.guard_volumes ? A.march : nullptr;
-    const double ao = A.ao ? tri3d(A.ao, guard, A.res, px, py, pz) : 1.0;
-    const double sh = A.sh ? tri3d(A.sh, guard, A.res, px, py, pz) : 1.0;
-    double ndl = nx * A.p.light_to_source[0] + ny * A.p.light_to_source[1] + nz * A.p.light_to_source[2];
+    double ao, sh;
+    tri3d2(cx, px, py, pz, ao, sh);
+    double ndl = nx * cx.l0 + ny * cx.l1 + nz * cx.l2;
     if (ndl < 0.0) ndl = 0.0;
     const double k = 0.4 * ao + 0.6 * sh * ndl;
     cr = cr * k; cg = cg * k; cb = cb * k;
+}
+
+// normal + colour of the hit of segment i at (hx, hy, hz) (lv/raytracer.py:502-505, 612-620)
+struct rgb3 { double r, g, b; };
+__device__ __forceinline__ rgb3 shade_hit_inl(const ShadeCtx &cx, int64_t i, double hx, double hy, double hz) {
+    const Capsule c = load_capsule(cx.verts, cx.normals, i, cx.r, cx.clip != 0);
+    double nx, ny, nz;
+    rgb3 o;
+    capsule_normal(hx, hy, hz, c, nx, ny, nz);
+    shade(cx, c, nx, ny, nz, hx, hy, hz, o.r, o.g, o.b);
+    return o;
+}
+// One out-of-line copy for the transparent kernel, which shades from two places: the kernel's code
+// size, not its arithmetic, is what limits it (ncu: instruction-fetch stalls lead the stall list).
+__device__ __noinline__ rgb3 shade_hit(const ShadeCtx *cx, int64_t i, double hx, double hy, double hz) {
+    return shade_hit_inl(*cx, i, hx, hy, hz);
 }
 
 __device__ __forceinline__ uint8_t to_srgb8(double v) {   // lv/raytracer.py:94-97
@@ -262,6 +294,13 @@ __device__ __forceinline__ uint8_t to_srgb8(double v) {   // lv/raytracer.py:94-
 // hits are folded with an order-independent rule.
 constexpr int RC_WARPS = 4;
 #define LVX_FULL 0xffffffffu
+// -DLVX_COUNT: debug build that counts the work of each stage in the spare stats words
+// (12: occupied voxels recorded, 13: tight pairs queued, 14: pairs surviving the f32 test, 15: accepted hits)
+#ifdef LVX_COUNT
+#define LVX_CNT(slot, n) do { if (lane == 0 && (n)) atomicAdd((unsigned long long *)&A.stats[slot], (unsigned long long)(n)); } while (0)
+#else
+#define LVX_CNT(slot, n) do { } while (0)
+#endif
 #ifndef LVX_SPEC
 #define LVX_SPEC 2      // occupied voxels a ray walks ahead per round (opaque)
 #endif
@@ -290,79 +329,99 @@ struct PairQueues {
 #define LVX_RS_SLOT(rs) ((rs) & 0xFFFFu)
 
 // Runs stages A-C for one round over the lists S.fo/S.n[0..M) of every lane;
-// `stage_c(valid, rs, seg)` is called with 32 (or fewer, at the end) queue-B entries.
+// `stage_c(valid, rs, seg, last)` is called with 32 (or fewer, at the end) queue-B entries; the
+// final call has last = true (and possibly no valid entry at all).
+// Written as one loop with a single call site per stage: the stages are large (stage C inlines the
+// f64 intersection routine), and every extra inlined copy costs instruction-cache capacity.
 template <int M, class F>
 __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S, int lane, float R2f, F &&stage_c) {
     const uint32_t lt_mask = (1u << lane) - 1u;
     uint32_t qa = 0, qb = 0;
-
-    auto drain_b = [&]() {
-        const uint32_t take = qb < 32 ? qb : 32, base = qb - take;
-        const bool valid = (uint32_t)lane < take;
-        const uint32_t rs = valid ? S.qb_rs[base + lane] : 0, ii = valid ? S.qb_i[base + lane] : 0;
-        qb = base;
-        __syncwarp();
-        stage_c(valid, rs, ii);
-    };
-    // ---- stage B: conservative f32 miss test on (up to) 32 queued pairs, survivors -> queue B
-    auto drain_a = [&]() {
-        const uint32_t take = qa < 32 ? qa : 32, base = qa - take;
-        bool pass = false;
-        uint32_t rs1 = 0, ii = 0;
-        if ((uint32_t)lane < take) {
-            rs1 = S.qa_rs[base + lane];
-            ii = A.frags[S.qa_g[base + lane]];
-            const uint32_t rr = LVX_RS_RAY(rs1), m = LVX_RS_ORD(rs1);
-            pass = !surely_misses_f32(S.pf[m][0][rr], S.pf[m][1][rr], S.pf[m][2][rr], S.dirf[0][rr], S.dirf[1][rr],
-                                      S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
+    // stage-A cursor: ordinal m, word wi of this lane's list, tight bits left in that word
+    int m = -1;
+    uint32_t wi = 0, maxw = 0, mask = 0, fo = 0, w0 = 0, nw = 0, last = 0, tag = 0;
+    bool a_done = false;
+    for (;;) {
+        // ---- stage C: full batches, or whatever is left once the producers are done
+        const bool tail = a_done && qa == 0;
+        if (qb >= 32 || tail) {
+            const uint32_t take = qb < 32 ? qb : 32, base = qb - take;
+            const bool valid = (uint32_t)lane < take;
+            const uint32_t rs = valid ? S.qb_rs[base + lane] : 0, ii = valid ? S.qb_i[base + lane] : 0;
+            qb = base;
+            __syncwarp();
+            const bool fin = tail && qb == 0;
+            stage_c(valid, rs, ii, fin);
+            if (fin) break;
+            continue;
         }
-        qa = base;
-        const uint32_t mb = __ballot_sync(LVX_FULL, pass);
-        if (pass) {
-            const uint32_t pos = qb + __popc(mb & lt_mask);
-            S.qb_rs[pos] = rs1; S.qb_i[pos] = ii;
+        // ---- stage B: conservative f32 miss test on (up to) 32 queued pairs, survivors -> queue B
+        if (qa >= 32 || (a_done && qa > 0)) {
+            const uint32_t take = qa < 32 ? qa : 32, base = qa - take;
+            bool pass = false;
+            uint32_t rs1 = 0, ii = 0;
+            if ((uint32_t)lane < take) {
+                rs1 = S.qa_rs[base + lane];
+                ii = A.frags[S.qa_g[base + lane]];
+                const uint32_t rr = LVX_RS_RAY(rs1), mm = LVX_RS_ORD(rs1);
+                pass = !surely_misses_f32(S.pf[mm][0][rr], S.pf[mm][1][rr], S.pf[mm][2][rr], S.dirf[0][rr], S.dirf[1][rr],
+                                          S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
+            }
+            qa = base;
+            const uint32_t mb = __ballot_sync(LVX_FULL, pass);
+            if (pass) {
+                const uint32_t pos = qb + __popc(mb & lt_mask);
+                S.qb_rs[pos] = rs1; S.qb_i[pos] = ii;
+            }
+            qb += __popc(mb);
+#if LVX_COUNT != 2
+            LVX_CNT(14, __popc(mb));
+#endif
+            __syncwarp();
+            continue;
         }
-        qb += __popc(mb);
-        __syncwarp();
-        while (qb >= 32) drain_b();          // ---- stage C
-    };
-
-    // ---- stage A: every lane walks the loose-bit words of its own lists; in each step all lanes
-    // that still have a tight fragment in their current word push one pair (their lowest bit).
-    // Loose fragments are never enumerated at all.
-#pragma unroll 1
-    for (int m = 0; m < M; m++) {
-        const uint32_t fo = S.fo[m][lane], n = S.n[m][lane];
-        const uint32_t last = fo + n - 1;                       // valid when n > 0
-        const uint32_t w0 = fo >> 5, nw = n ? (last >> 5) - w0 + 1 : 0;
-        const uint32_t maxw = __reduce_max_sync(LVX_FULL, nw);
-        const uint32_t tag = ((uint32_t)m << 21) | ((uint32_t)lane << 16);
-        for (uint32_t wi = 0; wi < maxw; wi++) {
-            uint32_t mask = 0;
-            const uint32_t w = w0 + wi;
+        // ---- stage A: every lane walks the loose-bit words of its own lists; in each step all lanes
+        // that still have a tight fragment in their current word push one pair (their lowest bit).
+        // Loose fragments are never enumerated at all.
+        const uint32_t ma = __ballot_sync(LVX_FULL, mask != 0);
+        if (ma == 0) {
+            // next word of this ordinal, or the next ordinal
+            if (m >= 0 && wi + 1 < maxw) {
+                wi++;
+            } else {
+                m++;
+                if (m >= M) { a_done = true; continue; }
+                fo = S.fo[m][lane];
+                const uint32_t n = S.n[m][lane];
+                last = fo + n - 1;                                  // valid when n > 0
+                w0 = fo >> 5;
+                nw = n ? (last >> 5) - w0 + 1 : 0;
+                maxw = __reduce_max_sync(LVX_FULL, nw);
+                tag = ((uint32_t)m << 21) | ((uint32_t)lane << 16);
+                wi = 0;
+                if (maxw == 0) continue;
+            }
             if (wi < nw) {
+                const uint32_t w = w0 + wi;
                 const uint32_t lw = A.loose ? A.loose[w] : 0u;
                 const uint32_t lo = wi == 0 ? (fo & 31u) : 0u;
                 const uint32_t hi = (w == (last >> 5)) ? (last & 31u) : 31u;     // inclusive
                 mask = ~lw & (0xffffffffu >> (31u - hi)) & (0xffffffffu << lo);
             }
-            for (;;) {
-                const uint32_t ma = __ballot_sync(LVX_FULL, mask != 0);
-                if (ma == 0) break;
-                if (mask) {
-                    const uint32_t g = (w << 5) + (uint32_t)(__ffs(mask) - 1);
-                    mask &= mask - 1;
-                    const uint32_t pos = qa + __popc(ma & lt_mask);
-                    S.qa_rs[pos] = tag | (g - fo); S.qa_g[pos] = g;
-                }
-                qa += __popc(ma);
-                __syncwarp();
-                if (qa >= 32) drain_a();
-            }
+            continue;
         }
+        if (mask) {
+            const uint32_t g = ((w0 + wi) << 5) + (uint32_t)(__ffs(mask) - 1);
+            mask &= mask - 1;
+            const uint32_t pos = qa + __popc(ma & lt_mask);
+            S.qa_rs[pos] = tag | (g - fo); S.qa_g[pos] = g;
+        }
+        qa += __popc(ma);
+#if LVX_COUNT != 2
+        LVX_CNT(13, __popc(ma));
+#endif
+        __syncwarp();
     }
-    while (qa > 0) drain_a();
-    while (qb > 0) drain_b();
 }
 
 // lv/raytracer.py:414-423 + 272-291: the pixel's ray and its parameter range inside the grid
@@ -395,37 +454,88 @@ __device__ __forceinline__ bool setup_ray(const RenderArgs &A, int px, int py, d
     return t1 >= t0;
 }
 
-// The DDA of lv/raytracer.py:475-482 / 542-556 from parameter `tcur`: finds the next occupied
-// voxel, records it as ordinal `m` of this lane and returns true with te = its exit parameter;
-// returns false when the ray leaves the grid first.  tcur is left at the voxel's entry parameter.
+// One DDA step of lv/raytracer.py:475-482 / 542-556 from parameter `tcur`.  Returns 0 when the
+// ray has left the grid, 1 after skipping an empty node, 2 after recording an occupied voxel as
+// ordinal `m` of this lane (tent = its entry parameter, te = its exit parameter).  In both of the
+// latter cases tcur has advanced to where the ray goes on (lv/raytracer.py:506-509).
 template <int M>
-__device__ __forceinline__ bool next_occupied(const RenderArgs &A, PairQueues<M> &S, int lane, int m, double ox, double oy,
-                                              double oz, double dx, double dy, double dz, const RayInv &inv, double t1,
-                                              double &tcur, double &te) {
+__device__ __forceinline__ int dda_step(const RenderArgs &A, PairQueues<M> &S, int lane, int m, double ox, double oy,
+                                        double oz, double dx, double dy, double dz, const RayInv &inv, double t1,
+                                        double &tcur, double &tent, double &te) {
     const int res = A.res;
-    for (;;) {
-        if (!(tcur < t1)) return false;
-        const double tm = tcur + 1e-6;
-        const int x = (int)floor(ox + dx * tm), y = (int)floor(oy + dy * tm), z = (int)floor(oz + dz * tm);
-        if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) return false;
-        const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
-        // the list bounds are fetched together with the march byte (independent loads, one round
-        // trip); they are only used when the voxel turns out to be occupied
-        const int lv = A.march[idx];
-        const uint32_t fo = A.offsets[idx], fe = A.offsets[idx + 1];
-        const bool occ = lv == 255;
-        const double tx = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, occ ? 0 : lv);
-        if (occ) {
-            S.fo[m][lane] = fo;
-            S.n[m][lane] = fe - fo;
-            S.vox[m][0][lane] = (int16_t)x; S.vox[m][1][lane] = (int16_t)y; S.vox[m][2][lane] = (int16_t)z;
-            te = tx;
-            const double tc = 0.5 * (tcur + te);     // a point of the ray inside the voxel
-            S.pf[m][0][lane] = (float)(ox + dx * tc); S.pf[m][1][lane] = (float)(oy + dy * tc); S.pf[m][2][lane] = (float)(oz + dz * tc);
-            return true;
-        }
-        tcur = tx > tcur ? tx : tcur + 1e-6;
+    if (!(tcur < t1)) return 0;
+    const double tm = tcur + 1e-6;
+    const int x = (int)floor(ox + dx * tm), y = (int)floor(oy + dy * tm), z = (int)floor(oz + dz * tm);
+    if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) return 0;
+    const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
+    // the list bounds are fetched together with the march byte (independent loads, one round
+    // trip); they are only used when the voxel turns out to be occupied
+    const int lv = A.march[idx];
+    const uint32_t fo = A.offsets[idx], fe = A.offsets[idx + 1];
+    const bool occ = lv == 255;
+    const double tx = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, occ ? 0 : lv);
+    if (occ) {
+        S.fo[m][lane] = fo;
+        S.n[m][lane] = fe - fo;
+        S.vox[m][0][lane] = (int16_t)x; S.vox[m][1][lane] = (int16_t)y; S.vox[m][2][lane] = (int16_t)z;
+        tent = tcur;
+        te = tx;
+        const double tc = 0.5 * (tcur + tx);     // a point of the ray inside the voxel
+        S.pf[m][0][lane] = (float)(ox + dx * tc); S.pf[m][1][lane] = (float)(oy + dy * tc); S.pf[m][2][lane] = (float)(oz + dz * tc);
     }
+    tcur = tx > tcur ? tx : tcur + 1e-6;
+    return occ ? 2 : 1;
+}
+
+// ----------------------------------------------------------------------------- ray supply
+// The trace kernels are persistent: a warp draws 8x4 pixel tiles from a global counter and hands
+// their pixels to lanes whose ray has finished, so that a warp does not march on with a handful of
+// live rays (ncu before: 10-15 of 32 threads active in the DDA and intersection code).  A fresh
+// warp takes a whole tile, lane k = pixel k of the tile; later refills fill idle lanes with the
+// next pixels of the warp's current tile.
+#ifndef LVX_REFILL
+#define LVX_REFILL 32     // idle lanes that trigger a refill (measured on C2/C3: 4, 8 and 16 are slower than
+                          // waiting for the whole tile -- mixing rays of different tiles in a warp costs
+                          // more in lost voxel/segment reuse than the idle lanes do)
+#endif
+struct TileQueue {
+    uint32_t pend_tile, pend_mask;   // warp-uniform: tile being handed out, its pixels not yet assigned
+    uint32_t n_tiles, tiles_x;
+    bool more;                       // the global counter has not run out yet
+};
+__device__ __forceinline__ TileQueue make_tile_queue(const RenderArgs &A) {
+    const uint32_t tx = (uint32_t)(A.p.tile_x1 - A.p.tile_x0 + 7) / 8, ty = (uint32_t)(A.p.tile_y1 - A.p.tile_y0 + 3) / 4;
+    return TileQueue{0u, 0u, tx * ty, tx, true};
+}
+// Called by the whole warp.  Lanes with has == false may receive a pixel: returns true and sets px, py.
+__device__ __forceinline__ bool assign_pixels(const RenderArgs &A, TileQueue &Q, bool has, int lane, int &px, int &py) {
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    bool got = false;
+    for (;;) {
+        const uint32_t idle = __ballot_sync(LVX_FULL, !has && !got);
+        if (idle == 0) break;
+        if (Q.pend_mask == 0) {
+            if (!Q.more) break;
+            unsigned long long tile = 0;
+            if (lane == 0) tile = atomicAdd((unsigned long long *)&A.stats[LVX_ST_TILE_CURSOR], 1ull);
+            tile = __shfl_sync(LVX_FULL, tile, 0);
+            if (tile >= (unsigned long long)Q.n_tiles) { Q.more = false; break; }
+            Q.pend_tile = (uint32_t)tile;
+            Q.pend_mask = 0xffffffffu;
+        }
+        const uint32_t n_take = min(__popc(idle), __popc(Q.pend_mask));
+        const uint32_t rank = __popc(idle & lt_mask);
+        uint32_t mybit = 0;
+        if (!has && !got && rank < n_take) {
+            const uint32_t bit = __fns(Q.pend_mask, 0, (int)rank + 1);
+            px = A.p.tile_x0 + (int)(Q.pend_tile % Q.tiles_x) * 8 + (int)(bit & 7u);
+            py = A.p.tile_y0 + (int)(Q.pend_tile / Q.tiles_x) * 4 + (int)(bit >> 3);
+            got = true;
+            mybit = 1u << bit;
+        }
+        Q.pend_mask &= ~__reduce_or_sync(LVX_FULL, mybit);
+    }
+    return got;
 }
 
 // ----------------------------------------------------------------------------- opaque
@@ -445,46 +555,125 @@ k_render_opaque_coop(const RenderArgs A) {
     __shared__ WarpShared sh_all[RC_WARPS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpShared &S = sh_all[warp];
-    // block = 4 warps side by side: 32 x 4 pixels, each warp an 8x4 tile
-    const int px = A.p.tile_x0 + blockIdx.x * (8 * RC_WARPS) + warp * 8 + (lane & 7);
-    const int py = A.p.tile_y0 + blockIdx.y * 4 + (lane >> 3);
-    const bool live = px < A.p.tile_x1 && py < A.p.tile_y1;
     const int w = A.cam.width, res = A.res;
     const double ox = A.cam.pos[0], oy = A.cam.pos[1], oz = A.cam.pos[2];
     const bool clip = A.p.use_clip != 0;
     const double r = A.p.radius;
-    double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
-    bool active = false;
-    if (live) active = setup_ray(A, px, py, dx, dy, dz, t, t1);
-    S.q.dir[0][lane] = dx; S.q.dir[1][lane] = dy; S.q.dir[2][lane] = dz;
-    S.q.dirf[0][lane] = (float)dx; S.q.dirf[1][lane] = (float)dy; S.q.dirf[2][lane] = (float)dz;
     const float R2f = ((float)r + 2e-3f) * ((float)r + 2e-3f);
-    const RayInv inv = make_inv(dx, dy, dz);
+    TileQueue Q = make_tile_queue(A);
+    bool has = false, active = false;     // this lane holds a pixel / its ray is still marching
+    int px = 0, py = 0;
+    double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
+    RayInv inv{0.0, 0.0, 0.0};
     double best_t = -1.0;      // final hit of this lane's ray
     int64_t best_i = -1;
     uint64_t n_tests = 0;
-    __syncwarp();
 
     for (;;) {
-        // ---- 1. record the next M occupied voxels (lv/raytracer.py:475-482, 506-509)
-        bool leaving = false;
-        double tcur = t;
-#pragma unroll 1
-        for (int m = 0; m < M; m++) {
-            double te = 0.0;
-            if (active && !leaving && next_occupied<M>(A, S.q, lane, m, ox, oy, oz, dx, dy, dz, inv, t1, tcur, te)) {
-                tcur = te > tcur ? te : tcur + 1e-6;          // where the ray goes on if voxel m has no hit
-            } else {
-                leaving = true;
-                S.q.n[m][lane] = 0;
+        uint32_t am = __ballot_sync(LVX_FULL, active);
+        if (__popc(am) <= 32 - LVX_REFILL) {
+            // ---- 0. retire finished rays, hand new pixels to the idle lanes
+            const bool done = has && !active;
+            if (__ballot_sync(LVX_FULL, done)) {
+                if (!DEFER) {
+                    if (done) {
+                        double out_r = A.p.background[0], out_g = A.p.background[1], out_b = A.p.background[2];
+                        int32_t out_id = -1;
+                        if (best_t >= 0.0) {
+                            const rgb3 c = shade_hit_inl(make_shade_ctx(A), best_i, ox + dx * best_t, oy + dy * best_t, oz + dz * best_t);
+                            out_r = c.r; out_g = c.g; out_b = c.b;
+                            out_id = (int32_t)best_i;
+                        }
+                        const int64_t pix = (int64_t)py * w + px;
+                        if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
+                        if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
+                        A.hit_id[pix] = out_id;
+                    }
+                } else {
+                    // Shading on demand: record the hit, and request AO/shadow for the (visible) voxels
+                    // its trilinear lookup will read (lv/raytracer.py:368-390).
+                    uint32_t items[8];
+                    int n_items = 0;
+                    if (done) {
+                        const int64_t pix = (int64_t)py * w + px;
+                        A.hit_t[pix] = best_t;
+                        A.hit_id[pix] = best_t >= 0.0 ? (int32_t)best_i : -1;
+                        if (best_t >= 0.0) {
+                            const double hx = ox + dx * best_t, hy = oy + dy * best_t, hz = oz + dz * best_t;
+                            const int ix = (int)floor(hx - 0.5), iy = (int)floor(hy - 0.5), iz = (int)floor(hz - 0.5);
+#pragma unroll
+                            for (int k = 0; k < 8; k++) {
+                                const int X = min(max(ix + (k & 1), 0), res - 1);
+                                const int Y = min(max(iy + ((k >> 1) & 1), 0), res - 1);
+                                const int Z = min(max(iz + (k >> 2), 0), res - 1);
+                                const uint32_t idx = (uint32_t)X + (uint32_t)res * ((uint32_t)Y + (uint32_t)res * (uint32_t)Z);
+                                bool fresh = false;
+                                if (A.march[idx] == 255) {
+                                    const uint32_t bit = 1u << (idx & 31);
+                                    fresh = (atomicOr(&A.need_bits[idx >> 5], bit) & bit) == 0;
+                                }
+                                items[k] = idx;
+                                if (fresh) n_items |= 1 << k;
+                            }
+                        }
+                    }
+                    // one global atomic per warp: exclusive scan of the per-lane counts
+                    const uint32_t mine = __popc((uint32_t)n_items);
+                    uint32_t incl = mine;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t v = __shfl_up_sync(LVX_FULL, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const uint32_t total = __shfl_sync(LVX_FULL, incl, 31);
+                    if (total) {
+                        unsigned long long b = 0;
+                        if (lane == 0)
+                            b = atomicAdd(reinterpret_cast<unsigned long long *>(A.need_list), (unsigned long long)total);
+                        b = __shfl_sync(LVX_FULL, b, 0);
+                        uint32_t pos = (uint32_t)b + incl - mine;
+#pragma unroll
+                        for (int k = 0; k < 8; k++)
+                            if (n_items & (1 << k)) A.need_list[LVX_LIST_HDR + pos++] = items[k];
+                    }
+                }
+                if (done) has = false;
+            }
+            if (assign_pixels(A, Q, has, lane, px, py)) {
+                has = px < A.p.tile_x1 && py < A.p.tile_y1;     // pixels of a partial tile beyond the rect
+                best_t = -1.0; best_i = -1;
+                active = has && setup_ray(A, px, py, dx, dy, dz, t, t1);
+                S.q.dir[0][lane] = dx; S.q.dir[1][lane] = dy; S.q.dir[2][lane] = dz;
+                S.q.dirf[0][lane] = (float)dx; S.q.dirf[1][lane] = (float)dy; S.q.dirf[2][lane] = (float)dz;
+                inv = make_inv(dx, dy, dz);
+            }
+            __syncwarp();
+            am = __ballot_sync(LVX_FULL, active);
+            if (am == 0) {
+                if (!Q.more && Q.pend_mask == 0 && __ballot_sync(LVX_FULL, has) == 0) break;
+                continue;
             }
         }
-        if (__ballot_sync(LVX_FULL, active) == 0) break;
+        // ---- 1. record the next M occupied voxels (lv/raytracer.py:475-482, 506-509); every lane
+        // steps its own DDA until it has M of them or leaves the grid
+        bool leaving = false, go = active;
+        int n_vox = 0;
+        double tcur = t;
+        while (__any_sync(LVX_FULL, go)) {
+            if (go) {
+                double tent, te;
+                const int st = dda_step<M>(A, S.q, lane, n_vox, ox, oy, oz, dx, dy, dz, inv, t1, tcur, tent, te);
+                if (st == 0) { leaving = true; go = false; }
+                else if (st == 2 && ++n_vox == M) go = false;
+            }
+        }
+#pragma unroll 1
+        for (int m = n_vox; m < M; m++) S.q.n[m][lane] = 0;
         __syncwarp();
         // best hit of this lane's ray in this round: lowest ordinal, then min t, then lowest slot
         double cur_t = -1.0;
         uint32_t cur_ms = 0xffffffffu, cur_i = 0;      // (ordinal << 16) | slot
-        run_pairs<M>(A, S.q, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii) {
+        run_pairs<M>(A, S.q, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool) {
             bool hit = false;
             double ht = 0.0;
             const uint32_t hr = LVX_RS_RAY(rs), hm_ = LVX_RS_ORD(rs);
@@ -531,74 +720,6 @@ k_render_opaque_coop(const RenderArgs A) {
         __syncwarp();
     }
     n_tests = warp_sum_u64(n_tests);
-
-    if (!DEFER) {
-        if (live) {
-            double out_r = A.p.background[0], out_g = A.p.background[1], out_b = A.p.background[2];
-            int32_t out_id = -1;
-            if (best_t >= 0.0) {
-                const double hx = ox + dx * best_t, hy = oy + dy * best_t, hz = oz + dz * best_t;
-                const Capsule c = load_capsule(A.verts, A.normals, best_i, r, clip);
-                double nx, ny, nz;
-                capsule_normal(hx, hy, hz, c, nx, ny, nz);
-                shade(A, c, nx, ny, nz, hx, hy, hz, out_r, out_g, out_b);
-                out_id = (int32_t)best_i;
-            }
-            const int64_t pix = (int64_t)py * w + px;
-            if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
-            if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
-            A.hit_id[pix] = out_id;
-        }
-    } else {
-        // Shading on demand: record the hit, and request AO/shadow for the (visible) voxels its
-        // trilinear lookup will read (lv/raytracer.py:368-390).
-        // (warp-level only: a block-wide barrier here would park finished warps until the slowest
-        // warp of the block leaves the trace loop)
-        uint32_t items[8];
-        int n_items = 0;
-        if (live) {
-            const int64_t pix = (int64_t)py * w + px;
-            A.hit_t[pix] = best_t;
-            A.hit_id[pix] = best_t >= 0.0 ? (int32_t)best_i : -1;
-            if (best_t >= 0.0) {
-                const double hx = ox + dx * best_t, hy = oy + dy * best_t, hz = oz + dz * best_t;
-                const int ix = (int)floor(hx - 0.5), iy = (int)floor(hy - 0.5), iz = (int)floor(hz - 0.5);
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    const int X = min(max(ix + (k & 1), 0), res - 1);
-                    const int Y = min(max(iy + ((k >> 1) & 1), 0), res - 1);
-                    const int Z = min(max(iz + (k >> 2), 0), res - 1);
-                    const uint32_t idx = (uint32_t)X + (uint32_t)res * ((uint32_t)Y + (uint32_t)res * (uint32_t)Z);
-                    bool fresh = false;
-                    if (A.march[idx] == 255) {
-                        const uint32_t bit = 1u << (idx & 31);
-                        fresh = (atomicOr(&A.need_bits[idx >> 5], bit) & bit) == 0;
-                    }
-                    items[k] = idx;
-                    if (fresh) n_items |= 1 << k;
-                }
-            }
-        }
-        // one global atomic per warp: exclusive scan of the per-lane counts
-        const uint32_t mine = __popc((uint32_t)n_items);
-        uint32_t incl = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(LVX_FULL, incl, o);
-            if (lane >= o) incl += v;
-        }
-        const uint32_t total = __shfl_sync(LVX_FULL, incl, 31);
-        if (total) {
-            unsigned long long b = 0;
-            if (lane == 0)
-                b = atomicAdd(reinterpret_cast<unsigned long long *>(A.need_list), (unsigned long long)total);
-            b = __shfl_sync(LVX_FULL, b, 0);
-            uint32_t pos = (uint32_t)b + incl - mine;
-#pragma unroll
-            for (int k = 0; k < 8; k++)
-                if (n_items & (1 << k)) A.need_list[LVX_LIST_HDR + pos++] = items[k];
-        }
-    }
     if (lane == 0 && n_tests)
         atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)n_tests);
 }
@@ -639,13 +760,13 @@ struct WarpSharedT {
 __global__ void __launch_bounds__(RC_WARPS * 32, LVX_RT_MINB)
 k_render_transparent_coop(const RenderArgs A) {
     constexpr int M = LVX_SPEC_T;
-    extern __shared__ __align__(16) unsigned char smem_raw[];      // RC_WARPS x WarpSharedT (> 48 KB: opt-in)
+    extern __shared__ __align__(16) unsigned char smem_raw[];      // RC_WARPS x WarpSharedT + ShadeCtx (> 48 KB: opt-in)
     WarpSharedT *sh_all = reinterpret_cast<WarpSharedT *>(smem_raw);
+    ShadeCtx *ctx = reinterpret_cast<ShadeCtx *>(smem_raw + sizeof(WarpSharedT) * RC_WARPS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     WarpSharedT &S = sh_all[warp];
-    const int px = A.p.tile_x0 + blockIdx.x * (8 * RC_WARPS) + warp * 8 + (lane & 7);
-    const int py = A.p.tile_y0 + blockIdx.y * 4 + (lane >> 3);
-    const bool live = px < A.p.tile_x1 && py < A.p.tile_y1;
+    if (threadIdx.x == 0) *ctx = make_shade_ctx(A);
+    __syncthreads();
     const int w = A.cam.width;
     const double ox = A.cam.pos[0], oy = A.cam.pos[1], oz = A.cam.pos[2];
     const bool clip = A.p.use_clip != 0;
@@ -654,13 +775,12 @@ k_render_transparent_coop(const RenderArgs A) {
     const bool early = A.p.early_termination != 0;
     const double alpha = A.p.alpha;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
-    bool active = false;
-    if (live) active = setup_ray(A, px, py, dx, dy, dz, t, t1);
-    S.q.dir[0][lane] = dx; S.q.dir[1][lane] = dy; S.q.dir[2][lane] = dz;
-    S.q.dirf[0][lane] = (float)dx; S.q.dirf[1][lane] = (float)dy; S.q.dirf[2][lane] = (float)dz;
     const float R2f = ((float)r + 2e-3f) * ((float)r + 2e-3f);
-    const RayInv inv = make_inv(dx, dy, dz);
+    TileQueue Q = make_tile_queue(A);
+    bool has = false, active = false;
+    int px = 0, py = 0;
+    double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
+    RayInv inv{0.0, 0.0, 0.0};
     double col_r = 0.0, col_g = 0.0, col_b = 0.0, acc_a = 0.0;
     int64_t first_hit = -1;
     // k-slot buffers, one per ordinal, packed with stride k (local memory)
@@ -672,24 +792,20 @@ k_render_transparent_coop(const RenderArgs A) {
     uint32_t qd = 0;           // entries in the deferred shading FIFO
     int repeat_m = -1;         // >= 0: the ray re-scans the voxel recorded as that ordinal last round
     int64_t last_key = -1;     // ... accepting only keys above last_key (applies to ordinal 0 of the new round)
-    __syncwarp();
 
     // shades the first min(qd, 32) FIFO entries and folds w*colour into the owners' sums
     auto shade_batch = [&]() {
         const uint32_t take = qd < 32 ? qd : 32;
         if ((uint32_t)lane < take) {
             const uint32_t rr = S.d_ray[lane];
-            const int64_t i = S.d_i[lane];
             const double tt = S.d_t[lane], wgt = S.d_w[lane];
             const double ddx = S.q.dir[0][rr], ddy = S.q.dir[1][rr], ddz = S.q.dir[2][rr];
-            const double hx = ox + ddx * tt, hy = oy + ddy * tt, hz = oz + ddz * tt;   // lv/raytracer.py:612-620
-            const Capsule c = load_capsule(A.verts, A.normals, i, r, clip);
-            double nx, ny, nz, cr, cg, cb;
-            capsule_normal(hx, hy, hz, c, nx, ny, nz);
-            shade(A, c, nx, ny, nz, hx, hy, hz, cr, cg, cb);
-            S.d_c[0][lane] = wgt * cr; S.d_c[1][lane] = wgt * cg; S.d_c[2][lane] = wgt * cb;
+            // lv/raytracer.py:612-620
+            const rgb3 c = shade_hit(ctx, (int64_t)S.d_i[lane], ox + ddx * tt, oy + ddy * tt, oz + ddz * tt);
+            S.d_c[0][lane] = wgt * c.r; S.d_c[1][lane] = wgt * c.g; S.d_c[2][lane] = wgt * c.b;
         }
         __syncwarp();
+#pragma unroll 1
         for (uint32_t e = 0; e < take; e++)
             if (S.d_ray[e] == (uint32_t)lane) { col_r += S.d_c[0][e]; col_g += S.d_c[1][e]; col_b += S.d_c[2][e]; }
         // move the tail (at most 31 entries) to the front
@@ -704,43 +820,83 @@ k_render_transparent_coop(const RenderArgs A) {
     };
 
     for (;;) {
+        uint32_t am = __ballot_sync(LVX_FULL, active);
+        if (__popc(am) <= 32 - LVX_REFILL) {
+            // ---- 0. retire finished rays (their queued colours first), hand new pixels to idle lanes
+            const bool done = has && !active;
+            if (__ballot_sync(LVX_FULL, done)) {
+                while (qd > 0) shade_batch();
+                if (done) {
+                    const double out_r = col_r + (1.0 - acc_a) * A.p.background[0];
+                    const double out_g = col_g + (1.0 - acc_a) * A.p.background[1];
+                    const double out_b = col_b + (1.0 - acc_a) * A.p.background[2];
+                    const int64_t pix = (int64_t)py * w + px;
+                    if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
+                    if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
+                    A.hit_id[pix] = (int32_t)first_hit;
+                    has = false;
+                }
+            }
+            if (assign_pixels(A, Q, has, lane, px, py)) {
+                has = px < A.p.tile_x1 && py < A.p.tile_y1;
+                col_r = col_g = col_b = acc_a = 0.0;
+                first_hit = -1; repeat_m = -1; last_key = -1;
+                active = has && setup_ray(A, px, py, dx, dy, dz, t, t1);
+                S.q.dir[0][lane] = dx; S.q.dir[1][lane] = dy; S.q.dir[2][lane] = dz;
+                S.q.dirf[0][lane] = (float)dx; S.q.dirf[1][lane] = (float)dy; S.q.dirf[2][lane] = (float)dz;
+                inv = make_inv(dx, dy, dz);
+            }
+            __syncwarp();
+            am = __ballot_sync(LVX_FULL, active);
+            if (am == 0) {
+                if (!Q.more && Q.pend_mask == 0 && __ballot_sync(LVX_FULL, has) == 0) break;
+                continue;
+            }
+        }
         // ---- 1. record the next M occupied voxels; a re-scan keeps its voxel as ordinal 0
-        bool leaving = false;
+        bool go = active;
         int n_vox = 0;                                         // ordinals recorded by this lane
         double tcur = t;
         const int64_t lk0 = repeat_m >= 0 ? last_key : -1;     // key floor of ordinal 0
-#pragma unroll 1
-        for (int m = 0; m < M; m++) {
-            double te = 0.0;
-            bool have = false;
-            if (active && !leaving) {
-                if (m == 0 && repeat_m >= 0) {
-                    const int s = repeat_m;                    // own column only: no other lane reads it yet
-                    S.q.fo[0][lane] = S.q.fo[s][lane]; S.q.n[0][lane] = S.q.n[s][lane];
+        if (active && repeat_m >= 0) {
+            const int s = repeat_m;                            // own column only: no other lane reads it yet
+            S.q.fo[0][lane] = S.q.fo[s][lane]; S.q.n[0][lane] = S.q.n[s][lane];
 #pragma unroll
-                    for (int a = 0; a < 3; a++) { S.q.vox[0][a][lane] = S.q.vox[s][a][lane]; S.q.pf[0][a][lane] = S.q.pf[s][a][lane]; }
-                    te = S.t_exit[s][lane];
-                    have = true;                               // tcur == t == that voxel's entry parameter
-                } else {
-                    // lv/raytracer.py:543-544: the cut-off is re-checked at apply time, per ordinal
-                    have = next_occupied<M>(A, S.q, lane, m, ox, oy, oz, dx, dy, dz, inv, t1, tcur, te);
-                }
-            }
-            if (have) {
-                const double span = te - tcur;                 // t_enter = tcur (lv/raytracer.py:557-560)
-                S.t_enter[m][lane] = tcur;
-                S.t_exit[m][lane] = te;
-                S.inv_span[m][lane] = span > 0.0 ? 65535.0 / span : 0.0;
-                tcur = te > tcur ? te : tcur + 1e-6;
-                n_vox = m + 1;
-            } else {
-                leaving = true;
-                S.q.n[m][lane] = 0;
-            }
-            kept[m] = 0; accepted[m] = 0;
+            for (int a = 0; a < 3; a++) { S.q.vox[0][a][lane] = S.q.vox[s][a][lane]; S.q.pf[0][a][lane] = S.q.pf[s][a][lane]; }
+            const double te = S.t_exit[s][lane];               // tcur == t == that voxel's entry parameter
+            const double span = te - tcur;
+            S.t_enter[0][lane] = tcur; S.t_exit[0][lane] = te;
+            S.inv_span[0][lane] = span > 0.0 ? 65535.0 / span : 0.0;
+            tcur = te > tcur ? te : tcur + 1e-6;
+            n_vox = 1;
+            if (M == 1) go = false;
         }
         repeat_m = -1;
-        if (__ballot_sync(LVX_FULL, active) == 0) break;
+#if defined(LVX_COUNT) && LVX_COUNT == 2
+        { const uint32_t al = __popc(am); LVX_CNT(13, 1); LVX_CNT(14, al); }
+#endif
+        while (__any_sync(LVX_FULL, go)) {
+#if defined(LVX_COUNT) && LVX_COUNT == 2
+            { const uint32_t gl = __popc(__ballot_sync(LVX_FULL, go)); LVX_CNT(15, 1); LVX_CNT(11, gl); }
+#endif
+            if (go) {
+                // lv/raytracer.py:543-544: the alpha cut-off is re-checked at apply time, per ordinal
+                double tent, te;
+                const int st = dda_step<M>(A, S.q, lane, n_vox, ox, oy, oz, dx, dy, dz, inv, t1, tcur, tent, te);
+                if (st == 0) go = false;
+                else if (st == 2) {
+                    const double span = te - tent;             // t_enter = the previous exit (lv/raytracer.py:557-560)
+                    S.t_enter[n_vox][lane] = tent; S.t_exit[n_vox][lane] = te;
+                    S.inv_span[n_vox][lane] = span > 0.0 ? 65535.0 / span : 0.0;
+                    if (++n_vox == M) go = false;
+                }
+            }
+        }
+#pragma unroll 1
+        for (int m = 0; m < M; m++) {
+            if (m >= n_vox) S.q.n[m][lane] = 0;
+            kept[m] = 0; accepted[m] = 0;
+        }
         __syncwarp();
         uint32_t hl_n = 0;
 
@@ -782,7 +938,7 @@ k_render_transparent_coop(const RenderArgs A) {
             __syncwarp();
         };
 
-        run_pairs<M>(A, S.q, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii) {
+        run_pairs<M>(A, S.q, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool fin) {
             bool hit = false;
             uint32_t hkey = 0;
             double ht = 0.0;
@@ -802,16 +958,17 @@ k_render_transparent_coop(const RenderArgs A) {
                 }
             }
             const uint32_t hm = __ballot_sync(LVX_FULL, hit);
-            if (hm == 0) return;
-            if (hl_n + __popc(hm) > HL_CAP) drain();
-            if (hit) {
+            if (hit) {      // the list has room for 32 more records at this point
                 const uint32_t pos = hl_n + __popc(hm & lt_mask);
                 S.hl_t[pos] = ht; S.hl_key[pos] = hkey; S.hl_i[pos] = ii; S.hl_r[pos] = (uint8_t)((hm_ << 5) | hr);
             }
             hl_n += __popc(hm);
+#if LVX_COUNT != 2
+            LVX_CNT(15, __popc(hm));
+#endif
             __syncwarp();
+            if (hl_n + 32 > HL_CAP || fin) drain();
         });
-        drain();
         // ---- consume the ordinals in order (lv/raytracer.py:543-544, 608-637): fix the blend
         // weights now, queue the colours
         bool going = active;       // false once this lane's ray has stopped consuming this round
@@ -862,18 +1019,7 @@ k_render_transparent_coop(const RenderArgs A) {
         if (active && early && acc_a >= 0.999) active = false;   // lv/raytracer.py:543-544
         __syncwarp();
     }
-    while (qd > 0) shade_batch();
     n_tests = warp_sum_u64(n_tests);
-
-    if (live) {
-        const double out_r = col_r + (1.0 - acc_a) * A.p.background[0];
-        const double out_g = col_g + (1.0 - acc_a) * A.p.background[1];
-        const double out_b = col_b + (1.0 - acc_a) * A.p.background[2];
-        const int64_t pix = (int64_t)py * w + px;
-        if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
-        if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
-        A.hit_id[pix] = (int32_t)first_hit;
-    }
     if (lane == 0 && n_tests)
         atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)n_tests);
 }
@@ -899,10 +1045,8 @@ k_resolve(const RenderArgs A) {
         const double dn = sqrt(dx * dx + dy * dy + dz * dz);
         dx = dx / dn; dy = dy / dn; dz = dz / dn;
         const double hx = A.cam.pos[0] + dx * best_t, hy = A.cam.pos[1] + dy * best_t, hz = A.cam.pos[2] + dz * best_t;
-        const Capsule c = load_capsule(A.verts, A.normals, (int64_t)A.hit_id[pix], A.p.radius, A.p.use_clip != 0);
-        double nx, ny, nz;
-        capsule_normal(hx, hy, hz, c, nx, ny, nz);
-        shade(A, c, nx, ny, nz, hx, hy, hz, out_r, out_g, out_b);
+        const rgb3 c = shade_hit_inl(make_shade_ctx(A), (int64_t)A.hit_id[pix], hx, hy, hz);
+        out_r = c.r; out_g = c.g; out_b = c.b;
     }
     if (A.rgb) { A.rgb[3 * pix] = out_r; A.rgb[3 * pix + 1] = out_g; A.rgb[3 * pix + 2] = out_b; }
     if (A.srgb) { A.srgb[3 * pix] = to_srgb8(out_r); A.srgb[3 * pix + 1] = to_srgb8(out_g); A.srgb[3 * pix + 2] = to_srgb8(out_b); }
@@ -911,6 +1055,19 @@ k_resolve(const RenderArgs A) {
 }  // namespace lvx
 
 using namespace lvx;
+
+// persistent launch: one warp per 8x4 pixel tile at most, otherwise every SM filled to its occupancy
+static unsigned persistent_grid(int tw, int th, int blocks_per_sm) {
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n_sm <= 0)
+            n_sm = 148;
+    }
+    const int64_t tiles = (int64_t)((tw + 7) / 8) * ((th + 3) / 4);
+    const int64_t need = (tiles + RC_WARPS - 1) / RC_WARPS, fill = (int64_t)n_sm * (blocks_per_sm > 0 ? blocks_per_sm : 1);
+    return (unsigned)(need < fill ? need : fill);
+}
 
 static int fill_args(RenderArgs &A, const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets,
                      const uint32_t *frags, const uint32_t *loose_bits, const uint8_t *march, int res, const float *ao, const float *shadow,
@@ -943,18 +1100,21 @@ int lvx_render(const double *verts, const float *verts_f, const double *normals,
     if (!verts_f) return LVX_E_ARG;
     const int tw = A.p.tile_x1 - A.p.tile_x0, th = A.p.tile_y1 - A.p.tile_y0;
     if (tw <= 0 || th <= 0) return LVX_OK;
+    if (!stats) return LVX_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    LVX_CUDA(cudaMemsetAsync(stats + LVX_ST_TILE_CURSOR, 0, 8, s));
     if (A.p.mode == 0) {
-        const dim3 cgrid((tw + 8 * RC_WARPS - 1) / (8 * RC_WARPS), (th + 3) / 4);
-        k_render_opaque_coop<false><<<cgrid, RC_WARPS * 32, 0, (cudaStream_t)stream>>>(A);
+        static int per_sm = 0;
+        if (!per_sm) LVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_opaque_coop<false>, RC_WARPS * 32, 0));
+        k_render_opaque_coop<false><<<persistent_grid(tw, th, per_sm), RC_WARPS * 32, 0, s>>>(A);
     } else {
-        const dim3 cgrid((tw + 8 * RC_WARPS - 1) / (8 * RC_WARPS), (th + 3) / 4);
-        const size_t smem = sizeof(WarpSharedT) * RC_WARPS;
-        static bool attr_set = false;
-        if (!attr_set) {
+        const size_t smem = sizeof(WarpSharedT) * RC_WARPS + sizeof(ShadeCtx);
+        static int per_sm = 0;
+        if (!per_sm) {
             LVX_CUDA(cudaFuncSetAttribute(k_render_transparent_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr_set = true;
+            LVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_transparent_coop, RC_WARPS * 32, smem));
         }
-        k_render_transparent_coop<<<cgrid, RC_WARPS * 32, smem, (cudaStream_t)stream>>>(A);
+        k_render_transparent_coop<<<persistent_grid(tw, th, per_sm), RC_WARPS * 32, smem, s>>>(A);
     }
     LVX_LAUNCH_CHECK();
     return LVX_OK;
@@ -972,12 +1132,15 @@ int lvx_trace_hits(const double *verts, const float *verts_f, const double *norm
     const int tw = A.p.tile_x1 - A.p.tile_x0, th = A.p.tile_y1 - A.p.tile_y0;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
+    if (!stats) return LVX_E_ARG;
     LVX_CUDA(cudaMemsetAsync(need_bits, 0, (size_t)((V + 31) / 32) * 4, s));
     LVX_CUDA(cudaMemsetAsync(need_list, 0, 8, s));
     if (tw <= 0 || th <= 0) return LVX_OK;
+    LVX_CUDA(cudaMemsetAsync(stats + LVX_ST_TILE_CURSOR, 0, 8, s));
     A.hit_t = hit_t; A.need_bits = need_bits; A.need_list = need_list;
-    const dim3 cgrid((tw + 8 * RC_WARPS - 1) / (8 * RC_WARPS), (th + 3) / 4);
-    k_render_opaque_coop<true><<<cgrid, RC_WARPS * 32, 0, s>>>(A);
+    static int per_sm = 0;
+    if (!per_sm) LVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_opaque_coop<true>, RC_WARPS * 32, 0));
+    k_render_opaque_coop<true><<<persistent_grid(tw, th, per_sm), RC_WARPS * 32, 0, s>>>(A);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }
