@@ -35,27 +35,39 @@ __device__ __forceinline__ bool clip_ok(const Capsule &c, double px, double py, 
     return true;
 }
 
-// Conservative miss test (single precision).  It bounds the distance between the
-// ray LINE through P (a point of the ray inside the current voxel, so all differences are a few
-// voxels long) and the SEGMENT [a, b]: every surface the f64 routine can return lies within
-// r + 3.2e-5 of the segment, the f32 evaluation (inputs rounded to f32 at magnitudes <= 1024,
-// i.e. <= 6.1e-5 absolute) is accurate to a few 1e-4, so "distance > r + 2e-3" proves a miss.
-// ~40 full-rate FMA-able operations instead of ~60 half-rate f64 ones, and it also rejects rays that
-// pass the infinite cylinder beyond the segment's ends.
-__device__ __forceinline__ bool surely_misses_f32(float Px, float Py, float Pz, float Dx, float Dy, float Dz,
+// Conservative miss test (single precision).  An accepted hit is a point of the ray that lies
+// inside the voxel being visited (lv/raytracer.py:446-452) and within r + 3.2e-5 of the segment
+// [a, b] (every surface the f64 routine can return is that close to the capsule's axis).  The ray's
+// stretch inside the voxel is contained in {C + s*D, |s| <= h}: C = the ray point half-way between
+// the voxel's entry and exit parameters, h = half their difference + 1e-3 (the march parameters
+// differ from the geometric entry/exit by at most the reference's 1e-6 nudges).  So if the
+// distance between that stretch and the segment exceeds r + 2e-3 the pair cannot produce an
+// accepted hit.  The closest-points computation is the standard clamped two-segment solve; all
+// differences are a few voxels long and the f32 inputs are rounded at magnitudes <= 1024
+// (<= 6.1e-5 absolute), which the 2e-3 margin covers several times.  ~55 full-rate operations
+// against ~500 half-rate f64 ones for the exact routine, and unlike a ray-LINE test it also rejects
+// capsules the ray only reaches before or after this voxel.
+__device__ __forceinline__ bool surely_misses_f32(float Cx, float Cy, float Cz, float h, float Dx, float Dy, float Dz,
                                                   const float *__restrict__ vf, int64_t i, float R2) {
     const float ax = vf[3 * i], ay = vf[3 * i + 1], az = vf[3 * i + 2];
     const float bx = vf[3 * i + 3], by = vf[3 * i + 4], bz = vf[3 * i + 5];
-    const float wx = ax - Px, wy = ay - Py, wz = az - Pz;
+    const float wx = ax - Cx, wy = ay - Cy, wz = az - Cz;
     const float ex = bx - ax, ey = by - ay, ez = bz - az;
     // (explicit fmaf: the translation unit is compiled with -fmad=false for the f64 code)
     const float dw = fmaf(Dx, wx, fmaf(Dy, wy, Dz * wz)), de = fmaf(Dx, ex, fmaf(Dy, ey, Dz * ez));
-    const float wpx = fmaf(-Dx, dw, wx), wpy = fmaf(-Dy, dw, wy), wpz = fmaf(-Dz, dw, wz);   // w, e perpendicular to D
-    const float epx = fmaf(-Dx, de, ex), epy = fmaf(-Dy, de, ey), epz = fmaf(-Dz, de, ez);
-    const float ee = fmaf(epx, epx, fmaf(epy, epy, epz * epz));
-    float sgm = 0.f;
-    if (ee > 1e-12f) sgm = fminf(fmaxf(__fdividef(-fmaf(wpx, epx, fmaf(wpy, epy, wpz * epz)), ee), 0.f), 1.f);
-    const float qx = fmaf(sgm, epx, wpx), qy = fmaf(sgm, epy, wpy), qz = fmaf(sgm, epz, wpz);
+    const float ee = fmaf(ex, ex, fmaf(ey, ey, ez * ez)), ew = fmaf(ex, wx, fmaf(ey, wy, ez * wz));
+    const float den = fmaf(-de, de, ee);                    // |D| = 1
+    float sr = 0.f;                                         // parameter on the ray stretch
+    if (den > 1e-12f) sr = fminf(fmaxf(__fdividef(fmaf(dw, ee, -de * ew), den), -h), h);
+    float u = 0.f;                                          // parameter on the segment
+    if (ee > 1e-12f) {
+        u = __fdividef(fmaf(de, sr, -ew), ee);
+        if (u < 0.f) { u = 0.f; sr = fminf(fmaxf(dw, -h), h); }
+        else if (u > 1.f) { u = 1.f; sr = fminf(fmaxf(dw + de, -h), h); }
+    } else {
+        sr = fminf(fmaxf(dw, -h), h);
+    }
+    const float qx = fmaf(u, ex, fmaf(-sr, Dx, wx)), qy = fmaf(u, ey, fmaf(-sr, Dy, wy)), qz = fmaf(u, ez, fmaf(-sr, Dz, wz));
     return fmaf(qx, qx, fmaf(qy, qy, qz * qz)) > R2;
 }
 
@@ -294,6 +306,11 @@ __device__ __forceinline__ uint8_t to_srgb8(double v) {   // lv/raytracer.py:94-
 // hits are folded with an order-independent rule.
 constexpr int RC_WARPS = 4;
 #define LVX_FULL 0xffffffffu
+// Values derived from threadIdx that live for the whole kernel (lane, the warp's shared-memory
+// offset, the lower-lanes mask).  Under register pressure ptxas rematerialises them at every use
+// -- S2R + shifts were ~10 % of the executed instructions (ncu source view); an empty volatile asm
+// makes the value opaque, so it stays in its register.
+#define LVX_PIN(x) asm volatile("" : "+r"(x))
 // -DLVX_COUNT: debug build that counts the work of each stage in the spare stats words
 // (12: occupied voxels recorded, 13: tight pairs queued, 14: pairs surviving the f32 test, 15: accepted hits)
 #ifdef LVX_COUNT
@@ -318,7 +335,8 @@ template <int M>
 struct PairQueues {
     double dir[3][32];
     float dirf[3][32];
-    float pf[M][3][32];             // a ray point inside voxel m (f32, for the conservative pre-test)
+    float pf[M][3][32];             // the ray's mid point inside voxel m (f32, for the conservative pre-test)
+    float hf[M][32];                // ... and half the parameter length of its stretch there (+ margin)
     int16_t vox[M][3][32];          // res <= 1024
     uint32_t fo[M][32], n[M][32];   // fragment list of voxel m (n = 0: none)
     uint32_t qa_rs[64], qa_g[64];   // queue A: (ordinal << 21 | ray << 16 | slot), global fragment index
@@ -334,8 +352,8 @@ struct PairQueues {
 // Written as one loop with a single call site per stage: the stages are large (stage C inlines the
 // f64 intersection routine), and every extra inlined copy costs instruction-cache capacity.
 template <int M, class F>
-__device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S, int lane, float R2f, F &&stage_c) {
-    const uint32_t lt_mask = (1u << lane) - 1u;
+__device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S, int lane, uint32_t lt_mask, float R2f,
+                                          F &&stage_c) {
     uint32_t qa = 0, qb = 0;
     // stage-A cursor: ordinal m, word wi of this lane's list, tight bits left in that word
     int m = -1;
@@ -364,8 +382,8 @@ __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S,
                 rs1 = S.qa_rs[base + lane];
                 ii = A.frags[S.qa_g[base + lane]];
                 const uint32_t rr = LVX_RS_RAY(rs1), mm = LVX_RS_ORD(rs1);
-                pass = !surely_misses_f32(S.pf[mm][0][rr], S.pf[mm][1][rr], S.pf[mm][2][rr], S.dirf[0][rr], S.dirf[1][rr],
-                                          S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
+                pass = !surely_misses_f32(S.pf[mm][0][rr], S.pf[mm][1][rr], S.pf[mm][2][rr], S.hf[mm][rr], S.dirf[0][rr],
+                                          S.dirf[1][rr], S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
             }
             qa = base;
             const uint32_t mb = __ballot_sync(LVX_FULL, pass);
@@ -383,7 +401,7 @@ __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S,
         // ---- stage A: every lane walks the loose-bit words of its own lists; in each step all lanes
         // that still have a tight fragment in their current word push one pair (their lowest bit).
         // Loose fragments are never enumerated at all.
-        const uint32_t ma = __ballot_sync(LVX_FULL, mask != 0);
+        uint32_t ma = __ballot_sync(LVX_FULL, mask != 0);
         if (ma == 0) {
             // next word of this ordinal, or the next ordinal
             if (m >= 0 && wi + 1 < maxw) {
@@ -410,17 +428,20 @@ __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S,
             }
             continue;
         }
-        if (mask) {
-            const uint32_t g = ((w0 + wi) << 5) + (uint32_t)(__ffs(mask) - 1);
-            mask &= mask - 1;
-            const uint32_t pos = qa + __popc(ma & lt_mask);
-            S.qa_rs[pos] = tag | (g - fo); S.qa_g[pos] = g;
-        }
-        qa += __popc(ma);
+        do {    // (tight loop: this is the most frequent step of the whole kernel)
+            if (mask) {
+                const uint32_t g = ((w0 + wi) << 5) + (uint32_t)(__ffs(mask) - 1);
+                mask &= mask - 1;
+                const uint32_t pos = qa + __popc(ma & lt_mask);
+                S.qa_rs[pos] = tag | (g - fo); S.qa_g[pos] = g;
+            }
+            qa += __popc(ma);
 #if LVX_COUNT != 2
-        LVX_CNT(13, __popc(ma));
+            LVX_CNT(13, __popc(ma));
 #endif
-        __syncwarp();
+            __syncwarp();
+            ma = __ballot_sync(LVX_FULL, mask != 0);
+        } while (ma != 0 && qa < 32);
     }
 }
 
@@ -482,6 +503,7 @@ __device__ __forceinline__ int dda_step(const RenderArgs &A, PairQueues<M> &S, i
         te = tx;
         const double tc = 0.5 * (tcur + tx);     // a point of the ray inside the voxel
         S.pf[m][0][lane] = (float)(ox + dx * tc); S.pf[m][1][lane] = (float)(oy + dy * tc); S.pf[m][2][lane] = (float)(oz + dz * tc);
+        S.hf[m][lane] = (float)(0.5 * (tx - tcur)) + 1e-3f;
     }
     tcur = tx > tcur ? tx : tcur + 1e-6;
     return occ ? 2 : 1;
@@ -552,9 +574,13 @@ template <bool DEFER>
 __global__ void __launch_bounds__(RC_WARPS * 32, LVX_RC_MINB)
 k_render_opaque_coop(const RenderArgs A) {
     constexpr int M = LVX_SPEC;
-    __shared__ WarpShared sh_all[RC_WARPS];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    WarpShared &S = sh_all[warp];
+    __shared__ __align__(16) unsigned char smem_raw[sizeof(WarpShared) * RC_WARPS];
+    uint32_t lane_u = threadIdx.x & 31u, soff = (threadIdx.x >> 5) * (uint32_t)sizeof(WarpShared);
+    LVX_PIN(lane_u); LVX_PIN(soff);
+    const int lane = (int)lane_u;
+    WarpShared &S = *reinterpret_cast<WarpShared *>(smem_raw + soff);
+    uint32_t lt_mask = (1u << lane_u) - 1u;
+    LVX_PIN(lt_mask);
     const int w = A.cam.width, res = A.res;
     const double ox = A.cam.pos[0], oy = A.cam.pos[1], oz = A.cam.pos[2];
     const bool clip = A.p.use_clip != 0;
@@ -673,7 +699,7 @@ k_render_opaque_coop(const RenderArgs A) {
         // best hit of this lane's ray in this round: lowest ordinal, then min t, then lowest slot
         double cur_t = -1.0;
         uint32_t cur_ms = 0xffffffffu, cur_i = 0;      // (ordinal << 16) | slot
-        run_pairs<M>(A, S.q, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool) {
+        run_pairs<M>(A, S.q, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool) {
             bool hit = false;
             double ht = 0.0;
             const uint32_t hr = LVX_RS_RAY(rs), hm_ = LVX_RS_ORD(rs);
@@ -761,10 +787,11 @@ __global__ void __launch_bounds__(RC_WARPS * 32, LVX_RT_MINB)
 k_render_transparent_coop(const RenderArgs A) {
     constexpr int M = LVX_SPEC_T;
     extern __shared__ __align__(16) unsigned char smem_raw[];      // RC_WARPS x WarpSharedT + ShadeCtx (> 48 KB: opt-in)
-    WarpSharedT *sh_all = reinterpret_cast<WarpSharedT *>(smem_raw);
     ShadeCtx *ctx = reinterpret_cast<ShadeCtx *>(smem_raw + sizeof(WarpSharedT) * RC_WARPS);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    WarpSharedT &S = sh_all[warp];
+    uint32_t lane_u = threadIdx.x & 31u, soff = (threadIdx.x >> 5) * (uint32_t)sizeof(WarpSharedT);
+    LVX_PIN(lane_u); LVX_PIN(soff);
+    const int lane = (int)lane_u;
+    WarpSharedT &S = *reinterpret_cast<WarpSharedT *>(smem_raw + soff);
     if (threadIdx.x == 0) *ctx = make_shade_ctx(A);
     __syncthreads();
     const int w = A.cam.width;
@@ -774,7 +801,8 @@ k_render_transparent_coop(const RenderArgs A) {
     const int kslots = A.p.k;
     const bool early = A.p.early_termination != 0;
     const double alpha = A.p.alpha;
-    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t lt_mask = (1u << lane_u) - 1u;
+    LVX_PIN(lt_mask);
     const float R2f = ((float)r + 2e-3f) * ((float)r + 2e-3f);
     TileQueue Q = make_tile_queue(A);
     bool has = false, active = false;
@@ -863,6 +891,7 @@ k_render_transparent_coop(const RenderArgs A) {
             S.q.fo[0][lane] = S.q.fo[s][lane]; S.q.n[0][lane] = S.q.n[s][lane];
 #pragma unroll
             for (int a = 0; a < 3; a++) { S.q.vox[0][a][lane] = S.q.vox[s][a][lane]; S.q.pf[0][a][lane] = S.q.pf[s][a][lane]; }
+            S.q.hf[0][lane] = S.q.hf[s][lane];
             const double te = S.t_exit[s][lane];               // tcur == t == that voxel's entry parameter
             const double span = te - tcur;
             S.t_enter[0][lane] = tcur; S.t_exit[0][lane] = te;
@@ -938,7 +967,7 @@ k_render_transparent_coop(const RenderArgs A) {
             __syncwarp();
         };
 
-        run_pairs<M>(A, S.q, lane, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool fin) {
+        run_pairs<M>(A, S.q, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool fin) {
             bool hit = false;
             uint32_t hkey = 0;
             double ht = 0.0;
