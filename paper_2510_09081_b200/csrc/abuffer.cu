@@ -165,34 +165,46 @@ __device__ __forceinline__ bool segment_misses_cube(float ax, float ay, float az
 // 145-181) is an acceleration only -- culled voxels are skipped per cell (252-253) -- so the
 // output does not depend on it.  Words are written as (segment << 1) | loose; the ordering pass
 // strips the flag again.
+// Culled voxels are not looked up: k_init_cursor parks their cursor at LVX_CURSOR_CULLED, far
+// above any fragment capacity, so the position their atomic returns fails the capacity test and
+// nothing is stored -- one dependent memory round trip per cell (the atomic) instead of two.
+#define LVX_CURSOR_CULLED 0xF0000000u
 __global__ void __launch_bounds__(128)
 k_scatter(const double *__restrict__ verts, const int32_t *__restrict__ segs, int64_t n_seg, double rt,
-          float r_tight, int res, int method, const uint8_t *__restrict__ cull0, uint32_t *__restrict__ cursor,
+          float r_tight, int res, int method, uint32_t *__restrict__ cursor,
           uint32_t *__restrict__ frags, int64_t cap) {
     const int64_t si = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (si >= n_seg) return;
     const int64_t i = segs[si];
     const d3 a = ld3(verts + 3 * i), b = ld3(verts + 3 * i + 3);
     const int64_t res64 = res;
+    // f32 view of the segment for the loose test.  Cells whose centre is farther than
+    // r_tight + sqrt(3)/2 from the segment are loose without the separating-direction search.
+    const SegF sf = make_segf(a, b);
+    const float bfx = sf.ax + sf.ex, bfy = sf.ay + sf.ey, bfz = sf.az + sf.ez;
+    const float far2 = (r_tight + 0.8661f) * (r_tight + 0.8661f) * 1.001f + 1e-4f;
     // Rows of the traversal are handled four cells at a time: the four cursor atomics are issued
     // back to back (their latencies overlap) before the first dependent fragment store.
     for_each_row(method, a, b, rt, res, [&](int x, int y, int z, int axis, int len) {
         const int64_t stride = axis == 0 ? 1 : (axis == 1 ? res64 : res64 * res64);
         const int64_t idx0 = x + res64 * (y + res64 * z);
-        const double sx = axis == 0 ? 1.0 : 0.0, sy = axis == 1 ? 1.0 : 0.0, sz = axis == 2 ? 1.0 : 0.0;
+        const float sx = axis == 0 ? 1.f : 0.f, sy = axis == 1 ? 1.f : 0.f, sz = axis == 2 ? 1.f : 0.f;
+        const float fx = (float)(x - sf.ox) + 0.5f, fy = (float)(y - sf.oy) + 0.5f, fz = (float)(z - sf.oz) + 0.5f;
         for (int u0 = 0; u0 < len; u0 += LVX_BATCH) {
             uint32_t word[LVX_BATCH], pos[LVX_BATCH];
             bool on[LVX_BATCH];
 #pragma unroll
             for (int k = 0; k < LVX_BATCH; k++) {
                 const int u = u0 + k;
-                on[k] = u < len && !(cull0 && cull0[idx0 + u * stride] == 0);
+                on[k] = u < len;
                 word[k] = 0;
                 if (on[k]) {
-                    const double cx = x + 0.5 + u * sx, cy = y + 0.5 + u * sy, cz = z + 0.5 + u * sz;
-                    const bool loose = r_tight >= 0.f &&
-                                       segment_misses_cube((float)(a.x - cx), (float)(a.y - cy), (float)(a.z - cz),
-                                                           (float)(b.x - cx), (float)(b.y - cy), (float)(b.z - cz), r_tight);
+                    const float cx = fx + (float)u * sx, cy = fy + (float)u * sy, cz = fz + (float)u * sz;
+                    bool loose = false;
+                    if (r_tight >= 0.f) {
+                        loose = segf_dist2(sf, cx, cy, cz) > far2 ||
+                                segment_misses_cube(sf.ax - cx, sf.ay - cy, sf.az - cz, bfx - cx, bfy - cy, bfz - cz, r_tight);
+                    }
                     word[k] = ((uint32_t)i << 1) | (loose ? 1u : 0u);
                 }
             }
@@ -381,11 +393,20 @@ k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ curso
         atomicAdd((unsigned long long *)&stats[LVX_ST_LONG_LISTS], (unsigned long long)n_long);
 }
 
+// cursor[v] = offsets[v] for visible voxels, LVX_CURSOR_CULLED for culled ones (cull0 == NULL: all visible)
 __global__ void __launch_bounds__(256)
-k_copy_u32(const uint32_t *__restrict__ src, uint32_t *__restrict__ dst, int64_t n) {
-    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    if (i + 3 < n) *reinterpret_cast<uint4 *>(dst + i) = *reinterpret_cast<const uint4 *>(src + i);
-    else for (int64_t k = i; k < n; k++) dst[k] = src[k];
+k_init_cursor(const uint32_t *__restrict__ offsets, const uint8_t *__restrict__ cull0, uint32_t *__restrict__ cursor, int64_t n) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;   // n is a multiple of 8 (lvx_scan)
+    if (i >= n) return;
+    uint4 o = *reinterpret_cast<const uint4 *>(offsets + i);
+    if (cull0) {
+        const uchar4 c = *reinterpret_cast<const uchar4 *>(cull0 + i);
+        if (!c.x) o.x = LVX_CURSOR_CULLED;
+        if (!c.y) o.y = LVX_CURSOR_CULLED;
+        if (!c.z) o.z = LVX_CURSOR_CULLED;
+        if (!c.w) o.w = LVX_CURSOR_CULLED;
+    }
+    *reinterpret_cast<uint4 *>(cursor + i) = o;
 }
 
 }  // namespace lvx
@@ -420,11 +441,13 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
     if (!pow2(res) || method < 0 || method > 2) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
-    k_copy_u32<<<blocks_for((V + 3) / 4, 256), 256, 0, s>>>(offsets, cursor, V);
+    if (V & 3) return LVX_E_ARG;
+    if (frag_capacity >= (int64_t)LVX_CURSOR_CULLED) return LVX_E_ARG;
+    k_init_cursor<<<blocks_for(V / 4, 256), 256, 0, s>>>(offsets, cull_flat, cursor, V);
     if (loose_bits) LVX_CUDA(cudaMemsetAsync(loose_bits, 0, (size_t)lvx_loose_words(frag_capacity) * 4, s));
     else r_tight = -1.0;
     if (n_seg > 0)
-        k_scatter<<<blocks_for(n_seg, 128), 128, 0, s>>>(verts, segs, n_seg, rt, (float)r_tight, res, method, cull_flat,
+        k_scatter<<<blocks_for(n_seg, 128), 128, 0, s>>>(verts, segs, n_seg, rt, (float)r_tight, res, method,
                                                         cursor, frags, frag_capacity);
     {
         unsigned nb = 148 * 8;   // persistent: 148 SMs x 8 CTAs of 8 warps

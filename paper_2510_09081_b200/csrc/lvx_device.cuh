@@ -201,6 +201,31 @@ __device__ __forceinline__ double capsule_sdf(double px, double py, double pz, c
     return sdf;
 }
 
+// Single-precision view of one segment in a frame whose origin is an integer voxel near its start,
+// for CONSERVATIVE pre-tests only: cell centres are exact in it (small integers + 0.5) and the end
+// points are rounded at magnitudes of a few voxels (~1e-6 absolute), far below the margins the
+// callers use.  Exact results never depend on it.
+struct SegF {
+    int ox, oy, oz;
+    float ax, ay, az, ex, ey, ez, inv_ee;
+};
+__device__ __forceinline__ SegF make_segf(const d3 &a, const d3 &b) {
+    SegF s;
+    s.ox = (int)floor(a.x); s.oy = (int)floor(a.y); s.oz = (int)floor(a.z);
+    s.ax = (float)(a.x - s.ox); s.ay = (float)(a.y - s.oy); s.az = (float)(a.z - s.oz);
+    s.ex = (float)(b.x - a.x); s.ey = (float)(b.y - a.y); s.ez = (float)(b.z - a.z);
+    const float ee = fmaf(s.ex, s.ex, fmaf(s.ey, s.ey, s.ez * s.ez));
+    s.inv_ee = ee > 0.f ? __fdividef(1.f, ee) : 0.f;
+    return s;
+}
+// squared distance from the point (px, py, pz) (same frame) to the segment, accurate to ~1e-5 relative
+__device__ __forceinline__ float segf_dist2(const SegF &s, float px, float py, float pz) {
+    const float wx = px - s.ax, wy = py - s.ay, wz = pz - s.az;
+    const float h = fminf(fmaxf(fmaf(wx, s.ex, fmaf(wy, s.ey, wz * s.ez)) * s.inv_ee, 0.f), 1.f);
+    const float qx = fmaf(-h, s.ex, wx), qy = fmaf(-h, s.ey, wy), qz = fmaf(-h, s.ez, wz);
+    return fmaf(qx, qx, fmaf(qy, qy, qz * qz));
+}
+
 // lv/voxelizer.py:286-298 _occupancy followed by q = int(round(occ * 4096)) (328)
 __device__ __forceinline__ uint32_t occupancy_q(double px, double py, double pz, const Capsule &c,
                                                 double rc, double corr) {

@@ -765,7 +765,10 @@ k_render_opaque_coop(const RenderArgs A) {
 // entries are queued their normals, AO/shadow lookups and colours are evaluated on all 32 lanes
 // at once and the owning lanes add w*colour in FIFO order -- per ray that is the reference's
 // order of additions, so the f64 sums keep their bits.
-constexpr int HL_CAP = 96;
+#ifndef LVX_HL_CAP
+#define LVX_HL_CAP 96
+#endif
+constexpr int HL_CAP = LVX_HL_CAP;   // >= 64: a batch of 32 hits must fit on top of 32 undrained ones
 constexpr int KMAX = 64;        // lv/raytracer.py:64: k <= 64
 
 struct WarpSharedT {

@@ -20,7 +20,7 @@
 namespace lvx {
 
 #ifndef LVX_VOX_MINB
-#define LVX_VOX_MINB 6
+#define LVX_VOX_MINB 4
 #endif
 template <bool WIDE>
 __global__ void __launch_bounds__(128, LVX_VOX_MINB)
@@ -38,19 +38,29 @@ k_voxelize(const double *__restrict__ verts, const double *__restrict__ normals,
         const double ratio = r / rc;
         const double corr = ratio * ratio;
         const int64_t res64 = res;
+        // About two thirds of the cells of the conservative traversal (radius rt = rc + 0.5 boxes)
+        // have their centre farther than rc + 0.5 from the segment: there sdf >= 0.5, the clip terms
+        // can only raise it, occ clamps to 0 and q = 0 exactly (lv/voxelizer.py:286-298, 328).  A
+        // full-rate f32 distance with a 1e-3 relative + 1e-4 absolute margin proves that case, and
+        // only the remaining cells pay for the f64 distance, square root and division.
+        const SegF sf = make_segf(c.a, c.b);
+        const float far2 = (float)((rc + 0.5) * (rc + 0.5)) * 1.001f + 1e-4f;
         // rows of the traversal, four cells at a time: four occupancies, then the four atomics
         // back to back, then the (rare) carry repairs that depend on their results
         for_each_row(method, c.a, c.b, rt, res, [&](int x, int y, int z, int axis, int len) {
             const int64_t stride = axis == 0 ? 1 : (axis == 1 ? res64 : res64 * res64);
             const int64_t idx0 = x + res64 * (y + res64 * z);
             const double sx = axis == 0 ? 1.0 : 0.0, sy = axis == 1 ? 1.0 : 0.0, sz = axis == 2 ? 1.0 : 0.0;
+            const float fx = (float)(x - sf.ox) + 0.5f, fy = (float)(y - sf.oy) + 0.5f, fz = (float)(z - sf.oz) + 0.5f;
             visited += (uint64_t)len;
             for (int u0 = 0; u0 < len; u0 += LVX_BATCH) {
                 uint32_t q[LVX_BATCH], old[LVX_BATCH];
 #pragma unroll
                 for (int k = 0; k < LVX_BATCH; k++) {
                     const int u = u0 + k;
-                    q[k] = u < len ? occupancy_q(x + 0.5 + u * sx, y + 0.5 + u * sy, z + 0.5 + u * sz, c, rc, corr) : 0u;
+                    q[k] = 0u;
+                    if (u < len && !(segf_dist2(sf, fx + (float)u * (float)sx, fy + (float)u * (float)sy, fz + (float)u * (float)sz) > far2))
+                        q[k] = occupancy_q(x + 0.5 + u * sx, y + 0.5 + u * sy, z + 0.5 + u * sz, c, rc, corr);
                 }
                 if (WIDE) {
 #pragma unroll
