@@ -220,6 +220,10 @@ __device__ __forceinline__ ShadeCtx make_shade_ctx(const RenderArgs &A) {
                     A.p.radius, A.p.light_to_source[0], A.p.light_to_source[1], A.p.light_to_source[2]};
 }
 
+#if defined(LVX_COUNT) && LVX_COUNT == 3
+__device__ uint32_t g_dbg_bits[1 << 22];      // debug: voxels whose AO/shadow some blended hit reads (res <= 512)
+__device__ unsigned long long g_dbg_unique;
+#endif
 __device__ __forceinline__ void tri3d2(const ShadeCtx &cx, double px, double py, double pz, double &ao, double &sh) {
     const int res = cx.res;
     const double ux = px - 0.5, uy = py - 0.5, uz = pz - 0.5;
@@ -241,6 +245,10 @@ __device__ __forceinline__ void tri3d2(const ShadeCtx &cx, double px, double py,
                 const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
                 // non-visible voxels keep ao = shadow = 1 (lv/shading.py:177-178)
                 const bool unit = cx.guard && cx.guard[idx] != 255;
+#if defined(LVX_COUNT) && LVX_COUNT == 3
+                { const uint32_t bit = 1u << (idx & 31);
+                  if (!(atomicOr(&g_dbg_bits[idx >> 5], bit) & bit)) atomicAdd(&g_dbg_unique, 1ull); }
+#endif
                 const double w = wx * wy * wz;
                 if (cx.ao) acc_a += w * (unit ? 1.0 : (double)cx.ao[idx]);
                 if (cx.sh) acc_s += w * (unit ? 1.0 : (double)cx.sh[idx]);
@@ -346,14 +354,14 @@ struct PairQueues {
 #define LVX_RS_ORD(rs) ((rs) >> 21)
 #define LVX_RS_SLOT(rs) ((rs) & 0xFFFFu)
 
-// Runs stages A-C for one round over the lists S.fo/S.n[0..M) of every lane;
+// Runs stages A-C for one round over the lists S.fo/S.n[0..n_ord) of every lane (n_ord <= M);
 // `stage_c(valid, rs, seg, last)` is called with 32 (or fewer, at the end) queue-B entries; the
 // final call has last = true (and possibly no valid entry at all).
 // Written as one loop with a single call site per stage: the stages are large (stage C inlines the
 // f64 intersection routine), and every extra inlined copy costs instruction-cache capacity.
 template <int M, class F>
-__device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S, int lane, uint32_t lt_mask, float R2f,
-                                          F &&stage_c) {
+__device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S, int n_ord, int lane, uint32_t lt_mask,
+                                          float R2f, F &&stage_c) {
     uint32_t qa = 0, qb = 0;
     // stage-A cursor: ordinal m, word wi of this lane's list, tight bits left in that word
     int m = -1;
@@ -408,7 +416,7 @@ __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S,
                 wi++;
             } else {
                 m++;
-                if (m >= M) { a_done = true; continue; }
+                if (m >= n_ord) { a_done = true; continue; }
                 fo = S.fo[m][lane];
                 const uint32_t n = S.n[m][lane];
                 last = fo + n - 1;                                  // valid when n > 0
@@ -561,8 +569,14 @@ __device__ __forceinline__ bool assign_pixels(const RenderArgs &A, TileQueue &Q,
 }
 
 // ----------------------------------------------------------------------------- opaque
+#ifndef LVX_SPEC_MAX
+#define LVX_SPEC_MAX LVX_SPEC   // look-ahead when only a few rays of the tile are still marching.  Measured on C2:
+                                // 4 -> trace 2.80 ms, 8 -> 4.3 ms against 2.76 ms for a fixed depth of 2 (the
+                                // extra ordinals are mostly wasted behind the first hit, and the larger
+                                // queues cost a resident CTA), so the depth stays fixed.
+#endif
 struct WarpShared {
-    PairQueues<LVX_SPEC> q;
+    PairQueues<LVX_SPEC_MAX> q;
     double hit_t[32];
     uint32_t hit_rs[32], hit_i[32];
 };
@@ -573,7 +587,7 @@ struct WarpShared {
 template <bool DEFER>
 __global__ void __launch_bounds__(RC_WARPS * 32, LVX_RC_MINB)
 k_render_opaque_coop(const RenderArgs A) {
-    constexpr int M = LVX_SPEC;
+    constexpr int M = LVX_SPEC_MAX;
     __shared__ __align__(16) unsigned char smem_raw[sizeof(WarpShared) * RC_WARPS];
     uint32_t lane_u = threadIdx.x & 31u, soff = (threadIdx.x >> 5) * (uint32_t)sizeof(WarpShared);
     LVX_PIN(lane_u); LVX_PIN(soff);
@@ -680,26 +694,35 @@ k_render_opaque_coop(const RenderArgs A) {
                 continue;
             }
         }
-        // ---- 1. record the next M occupied voxels (lv/raytracer.py:475-482, 506-509); every lane
-        // steps its own DDA until it has M of them or leaves the grid
+        // ---- 1. record the next Mr occupied voxels (lv/raytracer.py:475-482, 506-509); every lane
+        // steps its own DDA until it has Mr of them or leaves the grid.  A round has fixed costs
+        // (a partly filled f64 batch above all), so the fewer rays are left, the deeper they look ahead.
+        const int n_act = __popc(am);
+        const int Mr = n_act > 16 ? LVX_SPEC : (n_act > 8 ? min(2 * LVX_SPEC, M) : M);
         bool leaving = false, go = active;
         int n_vox = 0;
         double tcur = t;
+#if defined(LVX_COUNT) && LVX_COUNT == 2
+        { const uint32_t al = __popc(am); LVX_CNT(13, 1); LVX_CNT(14, al); }
+#endif
         while (__any_sync(LVX_FULL, go)) {
+#if defined(LVX_COUNT) && LVX_COUNT == 2
+            { const uint32_t gl = __popc(__ballot_sync(LVX_FULL, go)); LVX_CNT(15, 1); LVX_CNT(11, gl); }
+#endif
             if (go) {
                 double tent, te;
                 const int st = dda_step<M>(A, S.q, lane, n_vox, ox, oy, oz, dx, dy, dz, inv, t1, tcur, tent, te);
                 if (st == 0) { leaving = true; go = false; }
-                else if (st == 2 && ++n_vox == M) go = false;
+                else if (st == 2 && ++n_vox == Mr) go = false;
             }
         }
 #pragma unroll 1
-        for (int m = n_vox; m < M; m++) S.q.n[m][lane] = 0;
+        for (int m = n_vox; m < Mr; m++) S.q.n[m][lane] = 0;
         __syncwarp();
         // best hit of this lane's ray in this round: lowest ordinal, then min t, then lowest slot
         double cur_t = -1.0;
         uint32_t cur_ms = 0xffffffffu, cur_i = 0;      // (ordinal << 16) | slot
-        run_pairs<M>(A, S.q, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool) {
+        run_pairs<M>(A, S.q, Mr, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool) {
             bool hit = false;
             double ht = 0.0;
             const uint32_t hr = LVX_RS_RAY(rs), hm_ = LVX_RS_ORD(rs);
@@ -734,7 +757,7 @@ k_render_opaque_coop(const RenderArgs A) {
         });
         if (active) {
             // tests the reference would have run: every voxel up to and including the one with the hit
-            const int m_end = cur_t >= 0.0 ? (int)(cur_ms >> 16) : M - 1;
+            const int m_end = cur_t >= 0.0 ? (int)(cur_ms >> 16) : Mr - 1;
             uint32_t cnt = 0;
 #pragma unroll 1
             for (int m = 0; m <= m_end; m++) cnt += S.q.n[m][lane];
@@ -970,7 +993,7 @@ k_render_transparent_coop(const RenderArgs A) {
             __syncwarp();
         };
 
-        run_pairs<M>(A, S.q, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool fin) {
+        run_pairs<M>(A, S.q, M, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool fin) {
             bool hit = false;
             uint32_t hkey = 0;
             double ht = 0.0;
@@ -1054,6 +1077,9 @@ k_render_transparent_coop(const RenderArgs A) {
     n_tests = warp_sum_u64(n_tests);
     if (lane == 0 && n_tests)
         atomicAdd((unsigned long long *)&A.stats[LVX_ST_RAY_TESTS], (unsigned long long)n_tests);
+#if defined(LVX_COUNT) && LVX_COUNT == 3
+    if (threadIdx.x == 0) A.stats[13] = g_dbg_unique;     // (monotone: the last block to finish leaves the total)
+#endif
 }
 
 // Second half of shading on demand: one thread per pixel re-derives its ray (same expressions,
