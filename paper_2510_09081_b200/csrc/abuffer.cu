@@ -369,8 +369,46 @@ k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ curso
         sort_class<3>(__ballot_sync(0xffffffffu, n > 4 && n <= 8), b, n, frags, loose_bits, lane);
         sort_class<4>(__ballot_sync(0xffffffffu, n > 8 && n <= 16), b, n, frags, loose_bits, lane);
         sort_class<5>(__ballot_sync(0xffffffffu, n > 16 && n <= 32), b, n, frags, loose_bits, lane);
-        // long lists one at a time: staged through shared memory, or in place beyond the stage
-        uint32_t work = __ballot_sync(0xffffffffu, n > 32);
+        // lists of 33..64 fragments one at a time, two elements per lane in registers: element i of
+        // the list lives in register i / 32 of lane i % 32, so the j = 32 exchange of the bitonic
+        // network is a register swap and the other 20 stages are one shuffle per register
+        uint32_t mid = __ballot_sync(0xffffffffu, n > 32 && n <= 64);
+        while (mid) {
+            const int s0 = __ffs(mid) - 1;
+            mid &= mid - 1;
+            const uint32_t bb = __shfl_sync(0xffffffffu, b, s0), nn = __shfl_sync(0xffffffffu, n, s0);
+            uint32_t v0 = frags[bb + lane];                                   // nn > 32
+            uint32_t v1 = (uint32_t)lane + 32u < nn ? frags[bb + 32 + lane] : 0xffffffffu;
+#pragma unroll
+            for (int lk = 1; lk <= 6; lk++) {
+#pragma unroll
+                for (int lj = lk - 1; lj >= 0; lj--) {
+                    if (lj == 5) {        // partner = the lane's other register; the 64-block is ascending
+                        const uint32_t lo = min(v0, v1), hi = max(v0, v1);
+                        v0 = lo; v1 = hi;
+                    } else {
+                        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, v0, 1 << lj);
+                        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, v1, 1 << lj);
+                        // index i = lane + 32 r: bits lj < 5 and lk < 6 are lane bits, bit 6 is 0
+                        const bool asc = lk == 6 ? true : ((lane >> lk) & 1) == 0;
+                        const bool low = ((lane >> lj) & 1) == 0;
+                        const bool keep_min = asc == low;
+                        v0 = keep_min ? min(v0, o0) : max(v0, o0);
+                        // register 1 holds indices 32..63: for lk == 5 their bit 5 is set -> descending block
+                        const bool asc1 = lk == 6 ? true : (lk == 5 ? false : asc);
+                        const bool keep_min1 = asc1 == low;
+                        v1 = keep_min1 ? min(v1, o1) : max(v1, o1);
+                    }
+                }
+            }
+            frags[bb + lane] = v0 >> 1;
+            const bool in1 = (uint32_t)lane + 32u < nn;
+            if (in1) frags[bb + 32 + lane] = v1 >> 1;
+            emit_loose(loose_bits, bb, __ballot_sync(0xffffffffu, (v0 & 1u) != 0), lane);
+            emit_loose(loose_bits, bb + 32, __ballot_sync(0xffffffffu, in1 && (v1 & 1u)), lane);
+        }
+        // longer lists one at a time: staged through shared memory, or in place beyond the stage
+        uint32_t work = __ballot_sync(0xffffffffu, n > 64);
         while (work) {
             const int s0 = __ffs(work) - 1;
             work &= work - 1;
