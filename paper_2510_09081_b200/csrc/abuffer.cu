@@ -341,6 +341,52 @@ __device__ __forceinline__ void strip_long(const uint32_t *src, uint32_t *f, uin
     }
 }
 
+// Lists of up to 32 * R fragments (R = 2^LR registers per lane), one list at a time: element i lives
+// in register i / 32 of lane i % 32.  Stages of the bitonic network whose partner distance is >= 32
+// are compare-exchanges between a lane's own registers; the others are one shuffle per register.
+template <int LR>
+__device__ __forceinline__ void sort_regs(uint32_t todo, uint32_t b, uint32_t n, uint32_t *__restrict__ frags,
+                                          uint32_t *__restrict__ loose_bits, int lane) {
+    constexpr int R = 1 << LR, LGN = 5 + LR;
+    while (todo) {
+        const int s0 = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint32_t bb = __shfl_sync(0xffffffffu, b, s0), nn = __shfl_sync(0xffffffffu, n, s0);
+        uint32_t v[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) v[r] = (uint32_t)lane + 32u * r < nn ? frags[bb + 32 * r + lane] : 0xffffffffu;
+#pragma unroll
+        for (int lk = 1; lk <= LGN; lk++) {
+#pragma unroll
+            for (int lj = lk - 1; lj >= 0; lj--) {
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    // bit `bit` of the element index i = lane + 32 r
+                    auto ibit = [&](int bit) { return bit < 5 ? ((lane >> bit) & 1) : ((r >> (bit - 5)) & 1); };
+                    const bool asc = lk == LGN ? true : ibit(lk) == 0;     // direction of the 2^lk block
+                    if (lj >= 5) {
+                        const int pr = r ^ (1 << (lj - 5));                // partner register, same lane
+                        if (pr > r) {
+                            const uint32_t lo = min(v[r], v[pr]), hi = max(v[r], v[pr]);
+                            v[r] = asc ? lo : hi; v[pr] = asc ? hi : lo;
+                        }
+                    } else {
+                        const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], 1 << lj);
+                        const bool keep_min = asc == (ibit(lj) == 0);
+                        v[r] = keep_min ? min(v[r], o) : max(v[r], o);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const bool in = (uint32_t)lane + 32u * r < nn;
+            if (in) frags[bb + 32 * r + lane] = v[r] >> 1;
+            emit_loose(loose_bits, bb + 32 * r, __ballot_sync(0xffffffffu, in && (v[r] & 1u)), lane);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(ORDER_WARPS * 32)
 k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ cursor,
         const uint32_t *__restrict__ vis_list, uint32_t *__restrict__ frags, int64_t cap,
@@ -369,46 +415,11 @@ k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ curso
         sort_class<3>(__ballot_sync(0xffffffffu, n > 4 && n <= 8), b, n, frags, loose_bits, lane);
         sort_class<4>(__ballot_sync(0xffffffffu, n > 8 && n <= 16), b, n, frags, loose_bits, lane);
         sort_class<5>(__ballot_sync(0xffffffffu, n > 16 && n <= 32), b, n, frags, loose_bits, lane);
-        // lists of 33..64 fragments one at a time, two elements per lane in registers: element i of
-        // the list lives in register i / 32 of lane i % 32, so the j = 32 exchange of the bitonic
-        // network is a register swap and the other 20 stages are one shuffle per register
-        uint32_t mid = __ballot_sync(0xffffffffu, n > 32 && n <= 64);
-        while (mid) {
-            const int s0 = __ffs(mid) - 1;
-            mid &= mid - 1;
-            const uint32_t bb = __shfl_sync(0xffffffffu, b, s0), nn = __shfl_sync(0xffffffffu, n, s0);
-            uint32_t v0 = frags[bb + lane];                                   // nn > 32
-            uint32_t v1 = (uint32_t)lane + 32u < nn ? frags[bb + 32 + lane] : 0xffffffffu;
-#pragma unroll
-            for (int lk = 1; lk <= 6; lk++) {
-#pragma unroll
-                for (int lj = lk - 1; lj >= 0; lj--) {
-                    if (lj == 5) {        // partner = the lane's other register; the 64-block is ascending
-                        const uint32_t lo = min(v0, v1), hi = max(v0, v1);
-                        v0 = lo; v1 = hi;
-                    } else {
-                        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, v0, 1 << lj);
-                        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, v1, 1 << lj);
-                        // index i = lane + 32 r: bits lj < 5 and lk < 6 are lane bits, bit 6 is 0
-                        const bool asc = lk == 6 ? true : ((lane >> lk) & 1) == 0;
-                        const bool low = ((lane >> lj) & 1) == 0;
-                        const bool keep_min = asc == low;
-                        v0 = keep_min ? min(v0, o0) : max(v0, o0);
-                        // register 1 holds indices 32..63: for lk == 5 their bit 5 is set -> descending block
-                        const bool asc1 = lk == 6 ? true : (lk == 5 ? false : asc);
-                        const bool keep_min1 = asc1 == low;
-                        v1 = keep_min1 ? min(v1, o1) : max(v1, o1);
-                    }
-                }
-            }
-            frags[bb + lane] = v0 >> 1;
-            const bool in1 = (uint32_t)lane + 32u < nn;
-            if (in1) frags[bb + 32 + lane] = v1 >> 1;
-            emit_loose(loose_bits, bb, __ballot_sync(0xffffffffu, (v0 & 1u) != 0), lane);
-            emit_loose(loose_bits, bb + 32, __ballot_sync(0xffffffffu, in1 && (v1 & 1u)), lane);
-        }
+        // lists of 33..128 fragments one at a time, in registers (see sort_regs)
+        sort_regs<1>(__ballot_sync(0xffffffffu, n > 32 && n <= 64), b, n, frags, loose_bits, lane);
+        sort_regs<2>(__ballot_sync(0xffffffffu, n > 64 && n <= 128), b, n, frags, loose_bits, lane);
         // longer lists one at a time: staged through shared memory, or in place beyond the stage
-        uint32_t work = __ballot_sync(0xffffffffu, n > 64);
+        uint32_t work = __ballot_sync(0xffffffffu, n > 128);
         while (work) {
             const int s0 = __ffs(work) - 1;
             work &= work - 1;
