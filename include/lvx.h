@@ -146,16 +146,18 @@ int lvx_scan(const uint32_t *base, const uint8_t *cull_base, int64_t n_voxels,
 /* second traversal: cursor (V u32 scratch) is initialised from offsets; fragments of each
  * voxel end up in ascending segment order (lv/abuffer.py:313-317 semantics) after the
  * ordering pass, which walks vis_list (the voxels that own fragments).
- * loose_bits (optional, lvx_loose_words(frag_capacity) u32, zeroed here): bit f is set when the
- * capsule of fragment f (radius r_tight = r + 1e-3, voxel units) provably does not reach into the
- * voxel that lists it, so no ray hit can be accepted for it there (lv/raytracer.py:446-452); the
- * ray tracer skips such fragments after reading the bit.  Acceleration only: `frags`, offsets and
- * the ray-test counts are unchanged. */
-int64_t lvx_loose_words(int64_t frag_capacity);
+ * Tight index (optional; pass all three arrays or none): tight_frags (frag_capacity u32),
+ * tight_slot (frag_capacity u16), tight_cnt (V u16).  A fragment is "tight" unless its capsule
+ * (radius r_tight = r + 1e-3, voxel units) provably does not reach into the voxel that lists it --
+ * then no ray hit can be accepted for it there (lv/raytracer.py:446-452).  For every listed voxel v
+ * the ordering pass writes tight_cnt[v] and, at offsets[v] + 0 .. tight_cnt[v], the tight
+ * fragments' segment ids and their slots in the full list.  Acceleration only: `frags`, offsets and
+ * the ray-test counts are the reference's. */
 int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double rt, double r_tight, int res, int method,
                 const uint8_t *cull_flat /* NULL = no culling */, const uint32_t *vis_list,
                 const uint32_t *offsets, uint32_t *cursor, uint32_t *frags, int64_t frag_capacity,
-                uint32_t *loose_bits /* may be NULL */, uint64_t *stats, void *stream);
+                uint32_t *tight_frags, uint16_t *tight_slot, uint16_t *tight_cnt /* may be NULL */,
+                uint64_t *stats, void *stream);
 
 /* ---- shading: lv/shading.py:72-155 _trilinear/_cone_trace/_shading_kernel, 170-185.
  * dirs_host: n_dirs*3 unit vectors (lv/shading.py:32-40); light_host: unit light direction.
@@ -175,9 +177,10 @@ int lvx_march_levels(const uint8_t *bits_flat, int res, uint8_t *march, void *st
 
 /* ---- render: lv/raytracer.py:459-515 _opaque_kernel, 518-645 _transparent_kernel, 94-97 _to_srgb.
  * rgb: h*w*3 f64 linear (may be NULL), srgb: h*w*3 u8 (may be NULL), hit_id: h*w i32.
- * loose_bits: from lvx_scatter, or NULL; valid only if it was built with r_tight >= params.radius. */
+ * tight_*: the tight index from lvx_scatter, or NULL; valid only if it was built with r_tight >= params.radius. */
 int lvx_render(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
-               const uint32_t *loose_bits, const uint8_t *march, int res, const float *ao, const float *shadow,
+               const uint32_t *tight_frags, const uint16_t *tight_slot, const uint16_t *tight_cnt,
+               const uint8_t *march, int res, const float *ao, const float *shadow,
                const lvx_camera *cam_host, const lvx_render_params *params_host,
                double *rgb, uint8_t *srgb, int32_t *hit_id, uint64_t *stats, void *stream);
 
@@ -190,7 +193,8 @@ int lvx_render(const double *verts, const float *verts_f, const double *normals,
  *   lvx_resolve     normal + colour per hit pixel (lv/raytracer.py:486-502), reading ao/shadow only
  *                   where march marks the voxel visible (1.0 elsewhere, lv/shading.py:177-178) */
 int lvx_trace_hits(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
-                   const uint32_t *loose_bits, const uint8_t *march, int res, const lvx_camera *cam_host,
+                   const uint32_t *tight_frags, const uint16_t *tight_slot, const uint16_t *tight_cnt,
+                   const uint8_t *march, int res, const lvx_camera *cam_host,
                    const lvx_render_params *params_host, double *hit_t, int32_t *hit_id, uint32_t *need_bits,
                    uint32_t *need_list, uint64_t *stats, void *stream);
 int lvx_resolve(const double *verts, const double *normals, const uint8_t *march, int res, const float *ao,

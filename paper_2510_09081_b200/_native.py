@@ -57,14 +57,13 @@ SIGNATURES = {
     "lvx_list_words": (_L, [_L]),
     "lvx_scan_scratch_bytes": (_L, [_L]),
     "lvx_scan": (_I, [_P, _P, _L, _P, _P, _P, _P]),
-    "lvx_loose_words": (_L, [_L]),
-    "lvx_scatter": (_I, [_P, _P, _L, _D, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
+    "lvx_scatter": (_I, [_P, _P, _L, _D, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P, _P]),
     "lvx_march_levels": (_I, [_P, _I, _P, _P]),
     "lvx_shade_scratch_bytes": (_L, [_L]),
     "lvx_shade": (_I, [_P, _P, _I, _P, _P, _I, _D, _P, _D, _P, _P, _I, _P, _P]),
-    "lvx_trace_hits": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "lvx_trace_hits": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lvx_resolve": (_I, [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "lvx_render": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "lvx_render": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

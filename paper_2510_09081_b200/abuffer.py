@@ -64,12 +64,12 @@ def scan_offsets(pyramid, culling=None, capacity=None, _stats=None) -> OffsetTab
 class ABuffer:
     """lv/abuffer.py:117-138"""
 
-    def __init__(self, table: OffsetTable, fragments_dev, resolution: int, stats: dict, loose_dev=None,
+    def __init__(self, table: OffsetTable, fragments_dev, resolution: int, stats: dict, tight=None,
                  tight_radius: float = -1.0):
         self.table, self.fragments_dev, self.resolution, self.stats = table, fragments_dev, resolution, stats
-        # 1 bit per fragment: "a capsule of radius <= tight_radius cannot reach into this voxel"
-        # (ray-tracer acceleration, csrc/abuffer.cu); not part of the reference's ABuffer
-        self.loose_dev, self.tight_radius = loose_dev, float(tight_radius)
+        # ops.TightIndex: per voxel, the fragments whose capsule of radius <= tight_radius can reach
+        # into the voxel (ray-tracer acceleration, csrc/abuffer.cu); not part of the reference's ABuffer
+        self.tight, self.tight_radius = tight, float(tight_radius)
         self._frags = None
 
     @property
@@ -107,11 +107,11 @@ def _second_pass(ls, cn, g, pyramid, culling, method, r_world):
     table = scan_offsets(pyramid, culling, _stats=stats)
     rt = ops.footprint_radius(lines.r, pyramid.r_min)
     frags = torch.empty(max(table.total, 1), dtype=torch.int32, device=dev)
-    loose = torch.empty(ops.loose_words(frags.numel()), dtype=torch.int32, device=dev)
+    tight = ops.TightIndex(frags.numel(), res ** 3, dev)
     cursor = torch.empty(res ** 3, dtype=torch.int32, device=dev)
     owners = culling if culling is not None else occupied_bits(pyramid)   # voxels that own fragments
     ops.scatter(lines, rt, res, method, None if culling is None else culling.flat_dev, owners.list_dev,
-                table.offsets_dev, cursor, frags, stats, loose=loose)
+                table.offsets_dev, cursor, frags, stats, tight=tight)
     st = stats.cpu().numpy()
     if pyramid.saturated == 0 and st[N.ST_MISMATCH]:
         raise ABufferError("fragment count mismatch between passes (nondeterministic traversal?)")
@@ -119,7 +119,7 @@ def _second_pass(ls, cn, g, pyramid, culling, method, r_world):
     return ABuffer(table, frags, res, {"incidences": inc, "fragment_touches": 2 * inc,
                                        "fragments": table.total,
                                        "long_lists": int(st[N.ST_LONG_LISTS])},
-                   loose_dev=loose, tight_radius=float(lines.r))
+                   tight=tight, tight_radius=float(lines.r))
 
 
 def build_vsv(ls, cn, g, pyramid, method="capsule", workers=None, r_world=None) -> ABuffer:

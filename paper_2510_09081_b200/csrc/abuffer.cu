@@ -18,9 +18,12 @@
 // fragment whose segment is provably farther than r_tight = r + 1e-3 from the voxel's cube can never
 // yield an accepted hit there.  The scatter pass has the segment in registers and proves this per
 // incidence with a separating-direction lower bound (f32, ~70 flops); the flag rides through the
-// ordering pass in bit 0 of the packed word and ends up in a 1-bit-per-fragment mask the ray
-// tracer consults before it touches the segment's vertices.  `frags` itself stays the reference's
-// array, bit for bit.
+// ordering pass in bit 0 of the packed word, and the ordering pass -- which holds every sorted list
+// in registers anyway -- writes a TIGHT INDEX next to the reference's array: the list's tight
+// fragments compacted to the front of the list's own range in `tfrags` (segment ids) and `tslot`
+// (their slots in the full list, which the transparency keys need), and their number in
+// `tcnt[voxel]`.  The ray tracer enumerates contiguous ranges of that index instead of scanning
+// bit masks.  `frags` itself stays the reference's array, bit for bit.
 #include "lvx_device.cuh"
 
 #ifndef LVX_BATCH
@@ -277,16 +280,24 @@ __device__ __forceinline__ uint32_t group_sort(uint32_t v, int li) {
     return v;
 }
 
+struct TightIndex {
+    uint32_t *frags;     // [capacity] tight segment ids, list v at offsets[v] .. offsets[v] + cnt[v]
+    uint16_t *slot;      // [capacity] their slots (positions in the full, ascending list)
+    uint16_t *cnt;       // [V] tight fragments per voxel
+};
+
 // Short lists, 32 / W of them side by side: lane group g sorts the g-th list of size class W
-// (W/2 < n <= W, or n <= 2 for W = 2) named by the set bits of `cls`; b, n are the per-lane list
-// bounds of the warp's 32 current list entries.  Each group loads its list with one (partial)
-// 128-byte line, sorts it in registers, stores the stripped segment ids and publishes the loose
-// bits of its fragments.
+// (W/2 < n <= W, or n <= 2 for W = 2) named by the set bits of `cls`; b, n, vox are the per-lane
+// list bounds and voxel of the warp's 32 current list entries.  Each group loads its list with one
+// (partial) 128-byte line, sorts it in registers, stores the stripped segment ids and the tight
+// index of its list.
 template <int LG>
-__device__ __forceinline__ void sort_class(uint32_t cls, uint32_t b, uint32_t n, uint32_t *__restrict__ frags,
-                                           uint32_t *__restrict__ loose_bits, int lane) {
+__device__ __forceinline__ void sort_class(uint32_t cls, uint32_t b, uint32_t n, uint32_t vox, uint32_t *__restrict__ frags,
+                                           const TightIndex &T, int lane) {
     constexpr int W = 1 << LG, G = 32 / W;
     const int g = lane >> LG, li = lane & (W - 1);
+    const uint32_t gmask = W == 32 ? 0xffffffffu : (((1u << (W & 31)) - 1u) << (g * W));   // my group's lanes
+    const uint32_t below = gmask & ((1u << lane) - 1u);                                   // ... below me
     while (cls) {
         int src = -1;
 #pragma unroll
@@ -299,59 +310,66 @@ __device__ __forceinline__ void sort_class(uint32_t cls, uint32_t b, uint32_t n,
         }
         const uint32_t bb = __shfl_sync(0xffffffffu, b, src < 0 ? 0 : src);
         const uint32_t nsrc = __shfl_sync(0xffffffffu, n, src < 0 ? 0 : src);   // (all lanes take part)
+        const uint32_t vv = __shfl_sync(0xffffffffu, vox, src < 0 ? 0 : src);
         const uint32_t nn = src < 0 ? 0u : nsrc;
         uint32_t val = 0xffffffffu;
         if ((uint32_t)li < nn) val = frags[bb + li];
         val = group_sort<LG>(val, li);
         const bool mine = (uint32_t)li < nn;
         if (mine) frags[bb + li] = val >> 1;
-        const uint32_t bal = __ballot_sync(0xffffffffu, mine && (val & 1u));
-        if (loose_bits && li == 0 && nn) {
-            const uint32_t gm = W == 32 ? bal : ((bal >> (g * W)) & ((1u << (W & 31)) - 1u));
-            if (gm) {
-                const uint32_t sh = bb & 31u, w = bb >> 5;
-                atomicOr(&loose_bits[w], gm << sh);
-                if (sh && (gm >> (32u - sh))) atomicOr(&loose_bits[w + 1], gm >> (32u - sh));
+        const bool tight = mine && !(val & 1u);
+        const uint32_t bal = __ballot_sync(0xffffffffu, tight);
+        if (T.frags) {
+            if (tight) {
+                const uint32_t k = bb + __popc(bal & below);
+                T.frags[k] = val >> 1;
+                T.slot[k] = (uint16_t)li;
             }
+            if (li == 0 && nn) T.cnt[vv] = (uint16_t)__popc(bal & gmask);
         }
     }
 }
 
-// bit k of `mask` = fragment (b + k) is loose; two lanes publish the (at most two) mask words
-__device__ __forceinline__ void emit_loose(uint32_t *__restrict__ loose_bits, uint32_t b, uint32_t mask, int lane) {
-    if (!loose_bits || !mask) return;
-    const uint32_t sh = b & 31u, w = b >> 5;
-    if (lane == 0) {
-        const uint32_t lo = mask << sh;
-        if (lo) atomicOr(&loose_bits[w], lo);
-    } else if (lane == 1 && sh) {
-        const uint32_t hi = mask >> (32u - sh);
-        if (hi) atomicOr(&loose_bits[w + 1], hi);
+// tight index of the 32 sorted packed words v (valid where `in`) at list positions i0 + lane; `run` = tight
+// fragments of this list emitted so far (warp-uniform)
+__device__ __forceinline__ void emit_tight(const TightIndex &T, uint32_t bb, uint32_t i0, uint32_t v, bool in,
+                                           uint32_t &run, int lane) {
+    const bool tight = in && !(v & 1u);
+    const uint32_t bal = __ballot_sync(0xffffffffu, tight);
+    if (T.frags && tight) {
+        const uint32_t k = bb + run + __popc(bal & ((1u << lane) - 1u));
+        T.frags[k] = v >> 1;
+        T.slot[k] = (uint16_t)(i0 + lane);
     }
+    run += __popc(bal);
 }
 
-// long lists: strip the flag from the sorted packed words in `src` into f[0..nn) and publish the mask
-__device__ __forceinline__ void strip_long(const uint32_t *src, uint32_t *f, uint32_t b, uint32_t nn, int lane,
-                                           uint32_t *__restrict__ loose_bits) {
+// long lists: strip the flag from the sorted packed words in `src` into f[0..nn) and write the tight index
+__device__ __forceinline__ void strip_long(const uint32_t *src, uint32_t *f, uint32_t b, uint32_t nn, uint32_t vv,
+                                           int lane, const TightIndex &T) {
+    uint32_t run = 0;
     for (uint32_t i0 = 0; i0 < nn; i0 += 32) {
         const uint32_t i = i0 + lane;
         const uint32_t v = i < nn ? src[i] : 0u;
+        __syncwarp();
         if (i < nn) f[i] = v >> 1;
-        emit_loose(loose_bits, b + i0, __ballot_sync(0xffffffffu, i < nn && (v & 1u)), lane);
+        emit_tight(T, b, i0, v, i < nn, run, lane);
     }
+    if (T.frags && lane == 0) T.cnt[vv] = (uint16_t)run;
 }
 
 // Lists of up to 32 * R fragments (R = 2^LR registers per lane), one list at a time: element i lives
 // in register i / 32 of lane i % 32.  Stages of the bitonic network whose partner distance is >= 32
 // are compare-exchanges between a lane's own registers; the others are one shuffle per register.
 template <int LR>
-__device__ __forceinline__ void sort_regs(uint32_t todo, uint32_t b, uint32_t n, uint32_t *__restrict__ frags,
-                                          uint32_t *__restrict__ loose_bits, int lane) {
+__device__ __forceinline__ void sort_regs(uint32_t todo, uint32_t b, uint32_t n, uint32_t vox, uint32_t *__restrict__ frags,
+                                          const TightIndex &T, int lane) {
     constexpr int R = 1 << LR, LGN = 5 + LR;
     while (todo) {
         const int s0 = __ffs(todo) - 1;
         todo &= todo - 1;
         const uint32_t bb = __shfl_sync(0xffffffffu, b, s0), nn = __shfl_sync(0xffffffffu, n, s0);
+        const uint32_t vv = __shfl_sync(0xffffffffu, vox, s0);
         uint32_t v[R];
 #pragma unroll
         for (int r = 0; r < R; r++) v[r] = (uint32_t)lane + 32u * r < nn ? frags[bb + 32 * r + lane] : 0xffffffffu;
@@ -378,19 +396,21 @@ __device__ __forceinline__ void sort_regs(uint32_t todo, uint32_t b, uint32_t n,
                 }
             }
         }
+        uint32_t run = 0;
 #pragma unroll
         for (int r = 0; r < R; r++) {
             const bool in = (uint32_t)lane + 32u * r < nn;
             if (in) frags[bb + 32 * r + lane] = v[r] >> 1;
-            emit_loose(loose_bits, bb + 32 * r, __ballot_sync(0xffffffffu, in && (v[r] & 1u)), lane);
+            emit_tight(T, bb, 32u * r, v[r], in, run, lane);
         }
+        if (T.frags && lane == 0) T.cnt[vv] = (uint16_t)run;
     }
 }
 
 __global__ void __launch_bounds__(ORDER_WARPS * 32)
 k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ cursor,
         const uint32_t *__restrict__ vis_list, uint32_t *__restrict__ frags, int64_t cap,
-        uint32_t *__restrict__ loose_bits, uint64_t *__restrict__ stats) {
+        const TightIndex T, uint64_t *__restrict__ stats) {
     __shared__ uint32_t stage[ORDER_WARPS][ORDER_CAP];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n_lists = (int64_t)*reinterpret_cast<const unsigned long long *>(vis_list);
@@ -399,9 +419,10 @@ k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ curso
     uint32_t n_long = 0;
     // each warp takes a contiguous chunk of 32 list entries per step: lane k reads entry k's bounds
     for (int64_t e0 = warp_id * 32; e0 < n_lists; e0 += n_warps * 32) {
-        uint32_t b = 0, n = 0;
+        uint32_t b = 0, n = 0, vox = 0;
         if (e0 + lane < n_lists) {
             const uint32_t v = vis_list[LVX_LIST_HDR + e0 + lane];
+            vox = v;
             b = offsets[v];
             const uint32_t e = offsets[v + 1];
             n = e - b;
@@ -410,31 +431,32 @@ k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ curso
         }
         n_long += __popc(__ballot_sync(0xffffffffu, n > 32));
         // short lists by size class, several lists per warp step
-        sort_class<1>(__ballot_sync(0xffffffffu, n >= 1 && n <= 2), b, n, frags, loose_bits, lane);
-        sort_class<2>(__ballot_sync(0xffffffffu, n > 2 && n <= 4), b, n, frags, loose_bits, lane);
-        sort_class<3>(__ballot_sync(0xffffffffu, n > 4 && n <= 8), b, n, frags, loose_bits, lane);
-        sort_class<4>(__ballot_sync(0xffffffffu, n > 8 && n <= 16), b, n, frags, loose_bits, lane);
-        sort_class<5>(__ballot_sync(0xffffffffu, n > 16 && n <= 32), b, n, frags, loose_bits, lane);
+        sort_class<1>(__ballot_sync(0xffffffffu, n >= 1 && n <= 2), b, n, vox, frags, T, lane);
+        sort_class<2>(__ballot_sync(0xffffffffu, n > 2 && n <= 4), b, n, vox, frags, T, lane);
+        sort_class<3>(__ballot_sync(0xffffffffu, n > 4 && n <= 8), b, n, vox, frags, T, lane);
+        sort_class<4>(__ballot_sync(0xffffffffu, n > 8 && n <= 16), b, n, vox, frags, T, lane);
+        sort_class<5>(__ballot_sync(0xffffffffu, n > 16 && n <= 32), b, n, vox, frags, T, lane);
         // lists of 33..128 fragments one at a time, in registers (see sort_regs)
-        sort_regs<1>(__ballot_sync(0xffffffffu, n > 32 && n <= 64), b, n, frags, loose_bits, lane);
-        sort_regs<2>(__ballot_sync(0xffffffffu, n > 64 && n <= 128), b, n, frags, loose_bits, lane);
+        sort_regs<1>(__ballot_sync(0xffffffffu, n > 32 && n <= 64), b, n, vox, frags, T, lane);
+        sort_regs<2>(__ballot_sync(0xffffffffu, n > 64 && n <= 128), b, n, vox, frags, T, lane);
         // longer lists one at a time: staged through shared memory, or in place beyond the stage
         uint32_t work = __ballot_sync(0xffffffffu, n > 128);
         while (work) {
             const int s0 = __ffs(work) - 1;
             work &= work - 1;
             const uint32_t bb = __shfl_sync(0xffffffffu, b, s0), nn = __shfl_sync(0xffffffffu, n, s0);
+            const uint32_t vv = __shfl_sync(0xffffffffu, vox, s0);
             uint32_t *f = frags + bb;
             if (nn <= ORDER_CAP) {
                 uint32_t *buf = stage[warp];
                 for (uint32_t i = lane; i < nn; i += 32) buf[i] = f[i];
                 __syncwarp();
                 warp_bitonic(buf, nn, lane);
-                strip_long(buf, f, bb, nn, lane, loose_bits);
+                strip_long(buf, f, bb, nn, vv, lane, T);
                 __syncwarp();
             } else {
                 warp_bitonic(f, nn, lane);
-                strip_long(f, f, bb, nn, lane, loose_bits);
+                strip_long(f, f, bb, nn, vv, lane, T);
             }
         }
     }
@@ -481,11 +503,10 @@ int lvx_scan(const uint32_t *base, const uint8_t *cull_base, int64_t n_voxels, u
     return LVX_OK;
 }
 
-int64_t lvx_loose_words(int64_t frag_capacity) { return (frag_capacity + 31) / 32 + 1; }
-
 int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double rt, double r_tight, int res, int method,
                 const uint8_t *cull_flat, const uint32_t *vis_list, const uint32_t *offsets, uint32_t *cursor,
-                uint32_t *frags, int64_t frag_capacity, uint32_t *loose_bits, uint64_t *stats, void *stream) {
+                uint32_t *frags, int64_t frag_capacity, uint32_t *tight_frags, uint16_t *tight_slot, uint16_t *tight_cnt,
+                uint64_t *stats, void *stream) {
     if (!vis_list) return LVX_E_ARG;
     if (!pow2(res) || method < 0 || method > 2) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
@@ -493,8 +514,10 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
     if (V & 3) return LVX_E_ARG;
     if (frag_capacity >= (int64_t)LVX_CURSOR_CULLED) return LVX_E_ARG;
     k_init_cursor<<<blocks_for(V / 4, 256), 256, 0, s>>>(offsets, cull_flat, cursor, V);
-    if (loose_bits) LVX_CUDA(cudaMemsetAsync(loose_bits, 0, (size_t)lvx_loose_words(frag_capacity) * 4, s));
-    else r_tight = -1.0;
+    const bool want_tight = tight_frags != nullptr;
+    if (want_tight != (tight_slot != nullptr) || want_tight != (tight_cnt != nullptr)) return LVX_E_ARG;
+    if (!want_tight) r_tight = -1.0;
+    // (tight_cnt needs no clearing: it is only read for voxels whose list the ordering pass wrote)
     if (n_seg > 0)
         k_scatter<<<blocks_for(n_seg, 128), 128, 0, s>>>(verts, segs, n_seg, rt, (float)r_tight, res, method,
                                                         cursor, frags, frag_capacity);
@@ -502,7 +525,8 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
         unsigned nb = 148 * 8;   // persistent: 148 SMs x 8 CTAs of 8 warps
         const unsigned need = blocks_for((V + 31) / 32, ORDER_WARPS);
         if (nb > need) nb = need;
-        k_order<<<nb, ORDER_WARPS * 32, 0, s>>>(offsets, cursor, vis_list, frags, frag_capacity, loose_bits, stats);
+        const TightIndex T{tight_frags, tight_slot, tight_cnt};
+        k_order<<<nb, ORDER_WARPS * 32, 0, s>>>(offsets, cursor, vis_list, frags, frag_capacity, T, stats);
     }
     LVX_LAUNCH_CHECK();
     return LVX_OK;

@@ -11,7 +11,10 @@ struct RenderArgs {
     const double *verts, *normals;
     const float *verts_f;      // voxel-unit vertices rounded to f32 (conservative pre-test only)
     const uint32_t *offsets, *frags;
-    const uint32_t *loose;     // 1 bit per fragment: this capsule cannot reach into this voxel (may be NULL)
+    // tight index (abuffer.cu; all three NULL = none): per voxel the fragments whose capsule can reach
+    // into the voxel, compacted to the front of the list's range, with their slots in the full list
+    const uint32_t *tfrags;
+    const uint16_t *tslot, *tcnt;
     const uint8_t *march;      // per voxel: 255 = occupied/visible, else the empty level (lvx_march_levels)
     const float *ao, *sh;
     int res;
@@ -302,9 +305,9 @@ __device__ __forceinline__ uint8_t to_srgb8(double v) {   // lv/raytracer.py:94-
 // (lv/raytracer.py:459-515, 518-645) but share the work of a warp's 8x4 pixel tile.  Per round:
 //   1. every unfinished ray marches to its next occupied voxel: one byte of the march table per
 //      DDA step says "occupied" or how large the surrounding empty node is (hierarchical skip);
-//   2./3. stage A: each lane reads the loose-bit words of its voxel's list (abuffer.cu: a set bit
-//      means the capsule cannot reach into this voxel) and the lanes push their remaining (tight)
-//      fragments, one per lane per step, into queue A (ballot + popc compaction);
+//   2./3. stage A: each lane walks the tight ranges of its voxels (abuffer.cu: the fragments whose
+//      capsule can reach into the voxel, compacted by the ordering pass) and the lanes push them,
+//      one per lane per step, into queue A (ballot + popc compaction);
 //   4. stage B: 32 queued pairs at a time read the fragment's segment (f32 copy) and run the cheap
 //      conservative miss test fully converged; survivors are compacted into queue B;
 //   5. stage C: 32 queued pairs at a time run the full clipped f64 ray-capsule routine; accepted
@@ -347,7 +350,8 @@ struct PairQueues {
     float hf[M][32];                // ... and half the parameter length of its stretch there (+ margin)
     int16_t vox[M][3][32];          // res <= 1024
     uint32_t fo[M][32], n[M][32];   // fragment list of voxel m (n = 0: none)
-    uint32_t qa_rs[64], qa_g[64];   // queue A: (ordinal << 21 | ray << 16 | slot), global fragment index
+    uint16_t tn[M][32];             // ... of which the first tn entries of the tight index are worth testing
+    uint32_t qa_rs[64], qa_g[64];   // queue A: (ordinal << 21 | ray << 16 | index in the range), global index
     uint32_t qb_rs[64], qb_i[64];   // queue B: same tag, segment index
 };
 #define LVX_RS_RAY(rs) (((rs) >> 16) & 31u)
@@ -363,9 +367,9 @@ template <int M, class F>
 __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S, int n_ord, int lane, uint32_t lt_mask,
                                           float R2f, F &&stage_c) {
     uint32_t qa = 0, qb = 0;
-    // stage-A cursor: ordinal m, word wi of this lane's list, tight bits left in that word
+    // stage-A cursor of this lane: ordinal m, next global index g of its range, entries left, index in the range
     int m = -1;
-    uint32_t wi = 0, maxw = 0, mask = 0, fo = 0, w0 = 0, nw = 0, last = 0, tag = 0;
+    uint32_t g = 0, left = 0, idx = 0, tag = 0;
     bool a_done = false;
     for (;;) {
         // ---- stage C: full batches, or whatever is left once the producers are done
@@ -388,7 +392,9 @@ __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S,
             uint32_t rs1 = 0, ii = 0;
             if ((uint32_t)lane < take) {
                 rs1 = S.qa_rs[base + lane];
-                ii = A.frags[S.qa_g[base + lane]];
+                const uint32_t g = S.qa_g[base + lane];
+                if (A.tfrags) { ii = A.tfrags[g]; rs1 = (rs1 & 0xFFFF0000u) | A.tslot[g]; }   // slot in the full list
+                else ii = A.frags[g];                                                        // (range index == slot)
                 const uint32_t rr = LVX_RS_RAY(rs1), mm = LVX_RS_ORD(rs1);
                 pass = !surely_misses_f32(S.pf[mm][0][rr], S.pf[mm][1][rr], S.pf[mm][2][rr], S.hf[mm][rr], S.dirf[0][rr],
                                           S.dirf[1][rr], S.dirf[2][rr], A.verts_f, (int64_t)ii, R2f);
@@ -406,50 +412,33 @@ __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S,
             __syncwarp();
             continue;
         }
-        // ---- stage A: every lane walks the loose-bit words of its own lists; in each step all lanes
-        // that still have a tight fragment in their current word push one pair (their lowest bit).
-        // Loose fragments are never enumerated at all.
-        uint32_t ma = __ballot_sync(LVX_FULL, mask != 0);
-        if (ma == 0) {
-            // next word of this ordinal, or the next ordinal
-            if (m >= 0 && wi + 1 < maxw) {
-                wi++;
-            } else {
-                m++;
-                if (m >= n_ord) { a_done = true; continue; }
-                fo = S.fo[m][lane];
-                const uint32_t n = S.n[m][lane];
-                last = fo + n - 1;                                  // valid when n > 0
-                w0 = fo >> 5;
-                nw = n ? (last >> 5) - w0 + 1 : 0;
-                maxw = __reduce_max_sync(LVX_FULL, nw);
-                tag = ((uint32_t)m << 21) | ((uint32_t)lane << 16);
-                wi = 0;
-                if (maxw == 0) continue;
-            }
-            if (wi < nw) {
-                const uint32_t w = w0 + wi;
-                const uint32_t lw = A.loose ? A.loose[w] : 0u;
-                const uint32_t lo = wi == 0 ? (fo & 31u) : 0u;
-                const uint32_t hi = (w == (last >> 5)) ? (last & 31u) : 31u;     // inclusive
-                mask = ~lw & (0xffffffffu >> (31u - hi)) & (0xffffffffu << lo);
-            }
-            continue;
-        }
+        // ---- stage A: every lane walks its own ranges (ordinal after ordinal); in each step all
+        // lanes that still have an entry push one pair.  A lane whose range is used up moves on to
+        // its next ordinal in the same step, so the loop runs max-over-lanes(sum of range lengths)
+        // times, not sum-over-ordinals(max-over-lanes).
+        bool fin;
         do {    // (tight loop: this is the most frequent step of the whole kernel)
-            if (mask) {
-                const uint32_t g = ((w0 + wi) << 5) + (uint32_t)(__ffs(mask) - 1);
-                mask &= mask - 1;
+            if (left == 0 && m < n_ord) {
+                m++;
+                if (m < n_ord) {
+                    g = S.fo[m][lane]; left = S.tn[m][lane]; idx = 0;
+                    tag = ((uint32_t)m << 21) | ((uint32_t)lane << 16);
+                }
+            }
+            const uint32_t ma = __ballot_sync(LVX_FULL, left != 0);
+            if (left) {
                 const uint32_t pos = qa + __popc(ma & lt_mask);
-                S.qa_rs[pos] = tag | (g - fo); S.qa_g[pos] = g;
+                S.qa_rs[pos] = tag | idx; S.qa_g[pos] = g;
+                g++; idx++; left--;
             }
             qa += __popc(ma);
 #if LVX_COUNT != 2
             LVX_CNT(13, __popc(ma));
 #endif
             __syncwarp();
-            ma = __ballot_sync(LVX_FULL, mask != 0);
-        } while (ma != 0 && qa < 32);
+            fin = __ballot_sync(LVX_FULL, m < n_ord) == 0;
+        } while (!fin && qa < 32);
+        if (fin) a_done = true;
     }
 }
 
@@ -501,11 +490,13 @@ __device__ __forceinline__ int dda_step(const RenderArgs &A, PairQueues<M> &S, i
     // trip); they are only used when the voxel turns out to be occupied
     const int lv = A.march[idx];
     const uint32_t fo = A.offsets[idx], fe = A.offsets[idx + 1];
+    const uint32_t tn = A.tcnt ? A.tcnt[idx] : 0u;
     const bool occ = lv == 255;
     const double tx = voxel_exit(ox, oy, oz, dx, dy, dz, inv, x, y, z, occ ? 0 : lv);
     if (occ) {
         S.fo[m][lane] = fo;
         S.n[m][lane] = fe - fo;
+        S.tn[m][lane] = A.tcnt ? (uint16_t)tn : (uint16_t)min(fe - fo, 0xFFFFu);
         S.vox[m][0][lane] = (int16_t)x; S.vox[m][1][lane] = (int16_t)y; S.vox[m][2][lane] = (int16_t)z;
         tent = tcur;
         te = tx;
@@ -717,7 +708,7 @@ k_render_opaque_coop(const RenderArgs A) {
             }
         }
 #pragma unroll 1
-        for (int m = n_vox; m < Mr; m++) S.q.n[m][lane] = 0;
+        for (int m = n_vox; m < Mr; m++) { S.q.n[m][lane] = 0; S.q.tn[m][lane] = 0; }
         __syncwarp();
         // best hit of this lane's ray in this round: lowest ordinal, then min t, then lowest slot
         double cur_t = -1.0;
@@ -914,7 +905,7 @@ k_render_transparent_coop(const RenderArgs A) {
         const int64_t lk0 = repeat_m >= 0 ? last_key : -1;     // key floor of ordinal 0
         if (active && repeat_m >= 0) {
             const int s = repeat_m;                            // own column only: no other lane reads it yet
-            S.q.fo[0][lane] = S.q.fo[s][lane]; S.q.n[0][lane] = S.q.n[s][lane];
+            S.q.fo[0][lane] = S.q.fo[s][lane]; S.q.n[0][lane] = S.q.n[s][lane]; S.q.tn[0][lane] = S.q.tn[s][lane];
 #pragma unroll
             for (int a = 0; a < 3; a++) { S.q.vox[0][a][lane] = S.q.vox[s][a][lane]; S.q.pf[0][a][lane] = S.q.pf[s][a][lane]; }
             S.q.hf[0][lane] = S.q.hf[s][lane];
@@ -949,7 +940,7 @@ k_render_transparent_coop(const RenderArgs A) {
         }
 #pragma unroll 1
         for (int m = 0; m < M; m++) {
-            if (m >= n_vox) S.q.n[m][lane] = 0;
+            if (m >= n_vox) { S.q.n[m][lane] = 0; S.q.tn[m][lane] = 0; }
             kept[m] = 0; accepted[m] = 0;
         }
         __syncwarp();
@@ -1123,12 +1114,16 @@ static unsigned persistent_grid(int tw, int th, int blocks_per_sm) {
             n_sm = 148;
     }
     const int64_t tiles = (int64_t)((tw + 7) / 8) * ((th + 3) / 4);
+#ifdef LVX_GRID_CAP
+    if (blocks_per_sm > LVX_GRID_CAP) blocks_per_sm = LVX_GRID_CAP;
+#endif
     const int64_t need = (tiles + RC_WARPS - 1) / RC_WARPS, fill = (int64_t)n_sm * (blocks_per_sm > 0 ? blocks_per_sm : 1);
     return (unsigned)(need < fill ? need : fill);
 }
 
 static int fill_args(RenderArgs &A, const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets,
-                     const uint32_t *frags, const uint32_t *loose_bits, const uint8_t *march, int res, const float *ao, const float *shadow,
+                     const uint32_t *frags, const uint32_t *tight_frags, const uint16_t *tight_slot, const uint16_t *tight_cnt,
+                     const uint8_t *march, int res, const float *ao, const float *shadow,
                      const lvx_camera *cam_host, const lvx_render_params *params_host, double *rgb, uint8_t *srgb,
                      int32_t *hit_id, uint64_t *stats) {
     if (!pow2(res) || res > 1024 || !cam_host || !params_host || !hit_id || !march) return LVX_E_ARG;
@@ -1137,7 +1132,9 @@ static int fill_args(RenderArgs &A, const double *verts, const float *verts_f, c
     if (cam_host->width <= 0 || cam_host->height <= 0) return LVX_E_ARG;
     if (p.tile_x0 < 0 || p.tile_y0 < 0 || p.tile_x1 > cam_host->width || p.tile_y1 > cam_host->height) return LVX_E_ARG;
     if (p.use_clip && !normals) return LVX_E_ARG;
-    A.verts = verts; A.verts_f = verts_f; A.normals = normals; A.offsets = offsets; A.frags = frags; A.loose = loose_bits; A.march = march;
+    A.verts = verts; A.verts_f = verts_f; A.normals = normals; A.offsets = offsets; A.frags = frags; A.march = march;
+    if ((tight_frags != nullptr) != (tight_slot != nullptr) || (tight_frags != nullptr) != (tight_cnt != nullptr)) return LVX_E_ARG;
+    A.tfrags = tight_frags; A.tslot = tight_slot; A.tcnt = tight_cnt;
     A.ao = ao; A.sh = shadow;
     A.res = res; A.cam = *cam_host; A.p = p;
     A.rgb = rgb; A.srgb = srgb; A.hit_id = hit_id; A.stats = stats;
@@ -1148,11 +1145,12 @@ static int fill_args(RenderArgs &A, const double *verts, const float *verts_f, c
 extern "C" {
 
 int lvx_render(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
-               const uint32_t *loose_bits, const uint8_t *march, int res, const float *ao, const float *shadow,
+               const uint32_t *tight_frags, const uint16_t *tight_slot, const uint16_t *tight_cnt,
+               const uint8_t *march, int res, const float *ao, const float *shadow,
                const lvx_camera *cam_host, const lvx_render_params *params_host, double *rgb, uint8_t *srgb,
                int32_t *hit_id, uint64_t *stats, void *stream) {
     RenderArgs A;
-    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, loose_bits, march, res, ao, shadow, cam_host, params_host,
+    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, tight_frags, tight_slot, tight_cnt, march, res, ao, shadow, cam_host, params_host,
                              rgb, srgb, hit_id, stats);
     if (rc != LVX_OK) return rc;
     if (!verts_f) return LVX_E_ARG;
@@ -1179,11 +1177,12 @@ int lvx_render(const double *verts, const float *verts_f, const double *normals,
 }
 
 int lvx_trace_hits(const double *verts, const float *verts_f, const double *normals, const uint32_t *offsets, const uint32_t *frags,
-                   const uint32_t *loose_bits, const uint8_t *march, int res, const lvx_camera *cam_host,
+                   const uint32_t *tight_frags, const uint16_t *tight_slot, const uint16_t *tight_cnt,
+                   const uint8_t *march, int res, const lvx_camera *cam_host,
                    const lvx_render_params *params_host, double *hit_t, int32_t *hit_id, uint32_t *need_bits,
                    uint32_t *need_list, uint64_t *stats, void *stream) {
     RenderArgs A;
-    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, loose_bits, march, res, nullptr, nullptr, cam_host,
+    const int rc = fill_args(A, verts, verts_f, normals, offsets, frags, tight_frags, tight_slot, tight_cnt, march, res, nullptr, nullptr, cam_host,
                              params_host, nullptr, nullptr, hit_id, stats);
     if (rc != LVX_OK) return rc;
     if (A.p.mode != 0 || !verts_f || !hit_t || !need_bits || !need_list) return LVX_E_ARG;
@@ -1207,7 +1206,7 @@ int lvx_resolve(const double *verts, const double *normals, const uint8_t *march
                 const float *shadow, const lvx_camera *cam_host, const lvx_render_params *params_host,
                 const double *hit_t, const int32_t *hit_id, double *rgb, uint8_t *srgb, void *stream) {
     RenderArgs A;
-    const int rc = fill_args(A, verts, nullptr, normals, nullptr, nullptr, nullptr, march, res, ao, shadow, cam_host, params_host,
+    const int rc = fill_args(A, verts, nullptr, normals, nullptr, nullptr, nullptr, nullptr, nullptr, march, res, ao, shadow, cam_host, params_host,
                              rgb, srgb, const_cast<int32_t *>(hit_id), nullptr);
     if (rc != LVX_OK) return rc;
     if (!hit_t) return LVX_E_ARG;

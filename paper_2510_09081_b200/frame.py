@@ -93,7 +93,7 @@ class FrameEngine:
         self.srgb = t.empty((self.h, self.w, 3), dtype=t.uint8, device=d)
         self.hit_id = t.empty((self.h, self.w), dtype=t.int32, device=d)
         self.frags = t.empty(max(int(frag_capacity), 1), dtype=t.int32, device=d)
-        self.loose = t.empty(ops.loose_words(self.frags.numel()), dtype=t.int32, device=d)
+        self.tight = ops.TightIndex(self.frags.numel(), V, d)
         self.march = t.empty(V, dtype=t.uint8, device=d)
         if self.shading == "demand":
             self.hit_t = t.empty((self.h, self.w), dtype=t.float64, device=d)
@@ -204,7 +204,7 @@ class FrameEngine:
         rt = ops.footprint_radius(self.lines.r, self.r_min)
         ops.scatter(self.lines, rt, self.res, self.method,
                     self.cull_flat if self.strategy == "vcsv" else None, self.vis_list,
-                    self.offsets, self.cursor, self.frags, self.stats, loose=self.loose)
+                    self.offsets, self.cursor, self.frags, self.stats, tight=self.tight)
 
     def _stage_shade(self):
         demand = self.shading == "demand"
@@ -214,12 +214,12 @@ class FrameEngine:
 
     def _stage_trace(self, cam, tile=None):
         p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
-        ops.render(self.lines, self.offsets, self.frags, self.loose, self.march, self.res, self.ao, self.shadow,
+        ops.render(self.lines, self.offsets, self.frags, self.tight, self.march, self.res, self.ao, self.shadow,
                    ops.make_camera_struct(cam, self.grid), p, self.rgb, self.srgb, self.hit_id, self.stats)
 
     def _stage_trace_hits(self, cam, tile=None):
         p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
-        ops.trace_hits(self.lines, self.offsets, self.frags, self.loose, self.march, self.res,
+        ops.trace_hits(self.lines, self.offsets, self.frags, self.tight, self.march, self.res,
                        ops.make_camera_struct(cam, self.grid), p, self.hit_t, self.hit_id, self.need_bits,
                        self.need_list, self.stats)
 
@@ -235,7 +235,7 @@ class FrameEngine:
             if cap >= 2 ** 32:
                 cap = need
             self.frags = self.torch.empty(cap, dtype=self.torch.int32, device=self.dev)
-            self.loose = self.torch.empty(ops.loose_words(cap), dtype=self.torch.int32, device=self.dev)
+            self.tight = ops.TightIndex(cap, self.V, self.dev)
 
     def run(self, cam, grid: GridDesc, r_world: float, tile=None, seg_range=None, after_voxelize=None):
         """One frame on the already loaded vertices.  `after_voxelize(engine)` is the hook where the

@@ -181,19 +181,37 @@ def scan(base, cull_base, offsets, scratch, stats):
 TIGHT_MARGIN = 1e-3   # voxels; see csrc/abuffer.cu "Loose bits"
 
 
-def loose_words(frag_capacity: int) -> int:
-    return int(lib().lvx_loose_words(int(frag_capacity)))
+class TightIndex:
+    """Per-voxel index of the fragments whose capsule can reach into the voxel (csrc/abuffer.cu): the
+    ordering pass compacts them to the front of each list's range.  `frags` i32 [capacity],
+    `slot` i16 [capacity] (position in the full list), `cnt` i16 [V].  An acceleration structure
+    for the ray tracer only; the reference's `fragments` array is untouched."""
+
+    def __init__(self, capacity: int, n_voxels: int, device):
+        import torch
+        self.capacity = int(capacity)
+        self.frags = torch.empty(max(self.capacity, 1), dtype=torch.int32, device=device)
+        self.slot = torch.empty(max(self.capacity, 1), dtype=torch.int16, device=device)
+        self.cnt = torch.empty(int(n_voxels), dtype=torch.int16, device=device)
+
+    def ptrs(self):
+        return _ptr(self.frags), _ptr(self.slot), _ptr(self.cnt)
 
 
-def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, cursor, frags, stats, loose=None):
-    """`loose` (optional int32 tensor of loose_words(frags.numel())): receives the per-fragment
-    "capsule of radius lines.r cannot reach into this voxel" bits for the ray tracer."""
-    if loose is not None and loose.numel() < loose_words(frags.numel()):
-        raise ValueError("loose-bit buffer too small for the fragment buffer")
+def _tight_ptrs(tight):
+    return (None, None, None) if tight is None else tight.ptrs()
+
+
+def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, cursor, frags, stats, tight=None):
+    """`tight` (optional TightIndex with capacity >= frags.numel()) receives the index of the fragments whose
+    capsule of radius lines.r can reach into their voxel, for the ray tracer."""
+    if tight is not None and tight.capacity < frags.numel():
+        raise ValueError("tight index too small for the fragment buffer")
+    tf, ts, tc = _tight_ptrs(tight)
     check(lib().lvx_scatter(_ptr(lines.verts), _ptr(lines.segs), lines.n_segments, float(rt),
                             float(lines.r) + TIGHT_MARGIN, res,
                             METHODS[method], _ptr(cull_flat), _ptr(vis_list), _ptr(offsets), _ptr(cursor),
-                            _ptr(frags), frags.numel(), _ptr(loose), _ptr(stats), _stream()), "lvx_scatter")
+                            _ptr(frags), frags.numel(), tf, ts, tc, _ptr(stats), _stream()), "lvx_scatter")
 
 
 def march_levels(bits_flat, res, march):
@@ -223,17 +241,19 @@ def make_camera_struct(cam, grid) -> N.lvx_camera:
     return c
 
 
-def render(lines: DeviceLines, offsets, frags, loose, march, res, ao, shadow, cam_struct, params, rgb, srgb,
+def render(lines: DeviceLines, offsets, frags, tight, march, res, ao, shadow, cam_struct, params, rgb, srgb,
            hit_id, stats):
+    tf, ts, tc = _tight_ptrs(tight)
     check(lib().lvx_render(_ptr(lines.verts), _ptr(lines.verts_f), _ptr(lines.normals), _ptr(offsets), _ptr(frags),
-                           _ptr(loose), _ptr(march), res, _ptr(ao), _ptr(shadow), C.byref(cam_struct), C.byref(params), _ptr(rgb),
+                           tf, ts, tc, _ptr(march), res, _ptr(ao), _ptr(shadow), C.byref(cam_struct), C.byref(params), _ptr(rgb),
                            _ptr(srgb), _ptr(hit_id), _ptr(stats), _stream()), "lvx_render")
 
 
-def trace_hits(lines: DeviceLines, offsets, frags, loose, march, res, cam_struct, params, hit_t, hit_id, need_bits,
+def trace_hits(lines: DeviceLines, offsets, frags, tight, march, res, cam_struct, params, hit_t, hit_id, need_bits,
                need_list, stats):
+    tf, ts, tc = _tight_ptrs(tight)
     check(lib().lvx_trace_hits(_ptr(lines.verts), _ptr(lines.verts_f), _ptr(lines.normals), _ptr(offsets), _ptr(frags),
-                               _ptr(loose), _ptr(march), res, C.byref(cam_struct), C.byref(params), _ptr(hit_t), _ptr(hit_id),
+                               tf, ts, tc, _ptr(march), res, C.byref(cam_struct), C.byref(params), _ptr(hit_t), _ptr(hit_id),
                                _ptr(need_bits), _ptr(need_list), _ptr(stats), _stream()), "lvx_trace_hits")
 
 

@@ -154,9 +154,9 @@ def render(scene: RenderScene, cam: Camera, settings: RenderSettings, tile=None,
     march = torch.empty(res ** 3, dtype=torch.uint8, device=dev)
     ops.march_levels(bits.flat_dev, res, march)
     abuf = scene.abuf
-    # the loose bits are valid for capsules no thicker than the radius they were built with
-    loose = abuf.loose_dev if getattr(abuf, "loose_dev", None) is not None and lines.r <= abuf.tight_radius else None
-    ops.render(lines, abuf.table.offsets_dev, abuf.fragments_dev, loose, march, res, ao, sh,
+    # the tight index is valid for capsules no thicker than the radius it was built with
+    tight = abuf.tight if getattr(abuf, "tight", None) is not None and lines.r <= abuf.tight_radius else None
+    ops.render(lines, abuf.table.offsets_dev, abuf.fragments_dev, tight, march, res, ao, sh,
                ops.make_camera_struct(cam, g), make_params(settings, lines, light, tile, w, h),
                rgb, srgb, hit, stats)
     return Image(rgb, srgb, hit, stats={"ray_capsule_tests": int(stats[N.ST_RAY_TESTS].item())})
