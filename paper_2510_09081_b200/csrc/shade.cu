@@ -38,9 +38,10 @@ k_nzmask(const uint32_t *__restrict__ base, const double *__restrict__ lvl, int 
         const int x = i % rl, y = (i / rl) % rl, z = i / (rl * rl);
         if (x == rl - 1 || y == rl - 1 || z == rl - 1) any = true;
         else {
+            // (all eight taps are loaded before the first is tested: independent loads, one round trip)
 #pragma unroll
-            for (int k = 0; k < 8 && !any; k++)
-                any = cell_nonzero(base, lvl, l, (x + (k & 1)) + (uint32_t)rl * ((y + ((k >> 1) & 1)) + (uint32_t)rl * (z + (k >> 2))));
+            for (int k = 0; k < 8; k++)
+                any |= cell_nonzero(base, lvl, l, (x + (k & 1)) + (uint32_t)rl * ((y + ((k >> 1) & 1)) + (uint32_t)rl * (z + (k >> 2))));
         }
     }
     const uint32_t m = __ballot_sync(0xffffffffu, any);
