@@ -183,9 +183,11 @@ __device__ void capsule_normal(double px, double py, double pz, const Capsule &c
 // Thm 4.9) makes the second one exact.  (No overflow/underflow here: |n| <= 2048 and a component
 // of a unit vector is either 0 -- axis skipped -- or >= 2^-1074; components below 1e-280 are
 // treated as 0-free by the guarded path.)  5 dependent f64 instructions per axis, branch-free.
-struct RayInv { double ix, iy, iz; };
+struct RayInv { double ix, iy, iz; bool slow; };
 __device__ __forceinline__ RayInv make_inv(double dx, double dy, double dz) {
-    return RayInv{dx != 0.0 ? 1.0 / dx : 0.0, dy != 0.0 ? 1.0 / dy : 0.0, dz != 0.0 ? 1.0 / dz : 0.0};
+    const double tiny = 1e-280;
+    const bool slow = (dx != 0.0 && fabs(dx) <= tiny) || (dy != 0.0 && fabs(dy) <= tiny) || (dz != 0.0 && fabs(dz) <= tiny);
+    return RayInv{dx != 0.0 ? 1.0 / dx : 0.0, dy != 0.0 ? 1.0 / dy : 0.0, dz != 0.0 ? 1.0 / dz : 0.0, slow};
 }
 __device__ __forceinline__ double exact_quot(double n, double d, double y) {
     double q = n * y;
@@ -193,19 +195,29 @@ __device__ __forceinline__ double exact_quot(double n, double d, double y) {
     q = __fma_rn(__fma_rn(-d, q, n), y, q);
     return q;
 }
-__device__ __forceinline__ double voxel_exit(double ox, double oy, double oz, double dx, double dy, double dz,
-                                             const RayInv &inv, int x, int y, int z, int lvl) {
+// the literal form (true divisions), for rays with a denormal-range direction component
+__device__ __noinline__ double voxel_exit_slow(double ox, double oy, double oz, double dx, double dy, double dz,
+                                               int x, int y, int z, int lvl) {
     const int size = 1 << lvl;
     const int bx = (x >> lvl) << lvl, by = (y >> lvl) << lvl, bz = (z >> lvl) << lvl;
-    const double big = 1e30, tiny = 1e-280;
-    const double nx = (double)(dx > 0.0 ? bx + size : bx) - ox;
-    const double ny = (double)(dy > 0.0 ? by + size : by) - oy;
-    const double nz = (double)(dz > 0.0 ? bz + size : bz) - oz;
-    double t = big;
-    if (dx != 0.0) t = fmin(t, fabs(dx) > tiny ? exact_quot(nx, dx, inv.ix) : nx / dx);
-    if (dy != 0.0) t = fmin(t, fabs(dy) > tiny ? exact_quot(ny, dy, inv.iy) : ny / dy);
-    if (dz != 0.0) t = fmin(t, fabs(dz) > tiny ? exact_quot(nz, dz, inv.iz) : nz / dz);
+    double t = 1e30;
+    if (dx != 0.0) t = fmin(t, ((double)(dx > 0.0 ? bx + size : bx) - ox) / dx);
+    if (dy != 0.0) t = fmin(t, ((double)(dy > 0.0 ? by + size : by) - oy) / dy);
+    if (dz != 0.0) t = fmin(t, ((double)(dz > 0.0 ? bz + size : bz) - oz) / dz);
     return t;
+}
+__device__ __forceinline__ double voxel_exit(double ox, double oy, double oz, double dx, double dy, double dz,
+                                             const RayInv &inv, int x, int y, int z, int lvl) {
+    if (inv.slow) return voxel_exit_slow(ox, oy, oz, dx, dy, dz, x, y, z, lvl);
+    // far face of the level-lvl node per axis: ((c >> lvl) + [d > 0]) << lvl
+    const double nx = (double)(((x >> lvl) + (dx > 0.0 ? 1 : 0)) << lvl) - ox;
+    const double ny = (double)(((y >> lvl) + (dy > 0.0 ? 1 : 0)) << lvl) - oy;
+    const double nz = (double)(((z >> lvl) + (dz > 0.0 ? 1 : 0)) << lvl) - oz;
+    const double big = 1e30;
+    const double tx = dx != 0.0 ? exact_quot(nx, dx, inv.ix) : big;
+    const double ty = dy != 0.0 ? exact_quot(ny, dy, inv.iy) : big;
+    const double tz = dz != 0.0 ? exact_quot(nz, dz, inv.iz) : big;
+    return fmin(fmin(fmin(big, tx), ty), tz);
 }
 
 // lv/raytracer.py:368-390 (volumes are f32, widened exactly like the reference's astype(f64)).
@@ -485,7 +497,7 @@ __device__ __forceinline__ int dda_step(const RenderArgs &A, PairQueues<M> &S, i
     const double tm = tcur + 1e-6;
     const int x = (int)floor(ox + dx * tm), y = (int)floor(oy + dy * tm), z = (int)floor(oz + dz * tm);
     if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) return 0;
-    const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
+    const uint32_t idx = (uint32_t)x + (uint32_t)res * ((uint32_t)y + (uint32_t)res * (uint32_t)z);   // res <= 1024
     // the list bounds are fetched together with the march byte (independent loads, one round
     // trip); they are only used when the voxel turns out to be occupied
     const int lv = A.march[idx];
@@ -595,7 +607,7 @@ k_render_opaque_coop(const RenderArgs A) {
     bool has = false, active = false;     // this lane holds a pixel / its ray is still marching
     int px = 0, py = 0;
     double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
-    RayInv inv{0.0, 0.0, 0.0};
+    RayInv inv{0.0, 0.0, 0.0, false};
     double best_t = -1.0;      // final hit of this lane's ray
     int64_t best_i = -1;
     uint64_t n_tests = 0;
@@ -825,7 +837,7 @@ k_render_transparent_coop(const RenderArgs A) {
     bool has = false, active = false;
     int px = 0, py = 0;
     double dx = 0.0, dy = 0.0, dz = 1.0, t = 0.0, t1 = -1.0;
-    RayInv inv{0.0, 0.0, 0.0};
+    RayInv inv{0.0, 0.0, 0.0, false};
     double col_r = 0.0, col_g = 0.0, col_b = 0.0, acc_a = 0.0;
     int64_t first_hit = -1;
     // k-slot buffers, one per ordinal, packed with stride k (local memory)
