@@ -12,6 +12,7 @@ namespace lvx {
 #define LVX_SOLID_Q 4092u
 #define LVX_BRICK 8        // coarse "may contain a blocker" bricks for the visibility march
 #define LVX_SUPER 32       // and a coarser level above them
+#define LVX_SOLID_CAP 1024 // solid voxels listed individually for the per-super-brick shadow test
 
 __host__ __device__ inline int64_t brick_words(int res, int B) {
     const int64_t rb = (res + B - 1) / B;
@@ -30,7 +31,8 @@ __device__ __forceinline__ bool q_solid(const uint32_t *__restrict__ base, int r
 constexpr int SOLID_ITEMS = 4;
 __global__ void __launch_bounds__(256)
 k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restrict__ solid,
-        uint32_t *__restrict__ bricks, uint32_t *__restrict__ occ_list, uint64_t *__restrict__ stats) {
+        uint32_t *__restrict__ bricks, uint32_t *__restrict__ solid_list, uint32_t *__restrict__ occ_list,
+        uint64_t *__restrict__ stats) {
     __shared__ uint32_t s_warp[8];
     __shared__ unsigned long long s_base;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -53,6 +55,9 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
                 q_solid(base, res, x, y - 1, z) && q_solid(base, res, x, y + 1, z) &&
                 q_solid(base, res, x, y, z - 1) && q_solid(base, res, x, y, z + 1);
             if (s) {
+                // (solid voxels are rare: a list of the first LVX_SOLID_CAP of them, word 0 = their number)
+                const uint32_t slot = atomicAdd(&solid_list[0], 1u);
+                if (slot < LVX_SOLID_CAP) solid_list[LVX_LIST_HDR + slot] = (uint32_t)idx;
                 // flag every brick that overlaps this solid voxel dilated by one voxel, at both brick sizes
                 uint32_t *bits = bricks;
 #pragma unroll
@@ -183,12 +188,61 @@ __device__ __forceinline__ bool coarse_may_hit(const uint32_t *__restrict__ bits
     }
 }
 
+// Shadow test per 32^3 super-brick.  A voxel can only be blocked if the segment from its centre
+// to the camera meets a solid voxel, so every voxel of a super-brick B is visible when the convex
+// hull of B and the camera point misses every solid voxel (dilated by 1.5 voxels: far more than
+// the literal march can stray from the geometric segment).  hull(B, c) = union over u in [0, 1] of
+// the boxes c + u (B - c); such a box meets the cube F iff the six per-axis inequalities hold, each
+// linear in u, so the test is an intersection of six u-intervals.  Work: super-bricks x solid
+// voxels (512 x 58 on C2) -- and the per-voxel brick walks then run only inside flagged super-bricks.
+__global__ void __launch_bounds__(128)
+k_superbrick_shadow(const uint32_t *__restrict__ solid_list, int res, float cx, float cy, float cz,
+                    uint8_t *__restrict__ sb_flag) {
+    const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
+    const int sb = blockIdx.x * blockDim.x + threadIdx.x;
+    if (sb >= rs * rs * rs) return;
+    const uint32_t n_all = solid_list[0];
+    if (n_all > LVX_SOLID_CAP) { sb_flag[sb] = 1; return; }      // too many to list: no shortcut
+    const float c[3] = {cx, cy, cz};
+    const int b3[3] = {sb % rs, (sb / rs) % rs, sb / (rs * rs)};
+    float blo[3], bhi[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) { blo[a] = (float)(b3[a] * LVX_SUPER); bhi[a] = fminf((float)((b3[a] + 1) * LVX_SUPER), (float)res); }
+    uint8_t flag = 0;
+    for (uint32_t k = 0; k < n_all && !flag; k++) {
+        const uint32_t v = solid_list[LVX_LIST_HDR + k];
+        const int s3[3] = {(int)(v % res), (int)((v / res) % res), (int)(v / ((uint32_t)res * res))};
+        float u0 = 0.f, u1 = 1.f;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            const float flo = (float)s3[a] - 1.5f, fhi = (float)s3[a] + 2.5f;
+            // c + u (blo - c) <= fhi
+            {
+                const float g0 = c[a], g1 = blo[a];
+                if (g0 > fhi && g1 > fhi) u1 = -1.f;
+                else if (g0 <= fhi && g1 > fhi) u1 = fminf(u1, __fdividef(fhi - g0, g1 - g0) + 1e-3f);
+                else if (g0 > fhi && g1 <= fhi) u0 = fmaxf(u0, __fdividef(fhi - g0, g1 - g0) - 1e-3f);
+            }
+            // c + u (bhi - c) >= flo
+            {
+                const float g0 = c[a], g1 = bhi[a];
+                if (g0 < flo && g1 < flo) u1 = -1.f;
+                else if (g0 >= flo && g1 < flo) u1 = fminf(u1, __fdividef(flo - g0, g1 - g0) + 1e-3f);
+                else if (g0 < flo && g1 >= flo) u0 = fmaxf(u0, __fdividef(flo - g0, g1 - g0) - 1e-3f);
+            }
+        }
+        if (u0 <= u1) flag = 1;
+    }
+    sb_flag[sb] = flag;
+}
+
 // lv/culling.py:191-200.  When the frame has no solid voxel at all nothing can block, so every
 // occupied voxel is visible and the march is skipped (decided on the device, no host sync).
 // Phase A over the compacted occupied voxels: coarse walks only.  Voxels that may be blocked are
 // appended to `march_list`; everything else is visible.
 __global__ void __launch_bounds__(128)
-k_visibility(const uint32_t *__restrict__ bricks, const uint32_t *__restrict__ occ_list, int res,
+k_visibility(const uint32_t *__restrict__ bricks, const uint8_t *__restrict__ sb_flag,
+             const uint32_t *__restrict__ occ_list, int res,
              double cx, double cy, double cz, const uint64_t *__restrict__ stats,
              uint8_t *__restrict__ vis, uint32_t *__restrict__ march_list) {
     const int64_t n = (int64_t)stats[LVX_ST_OCCUPIED];
@@ -201,8 +255,9 @@ k_visibility(const uint32_t *__restrict__ bricks, const uint32_t *__restrict__ o
         uint32_t idx = 0;
         if (e < n) {
             idx = occ_list[e];
-            if (any_solid) {
-                const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
+            const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
+            const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
+            if (any_solid && sb_flag[(x / LVX_SUPER) + rs * ((y / LVX_SUPER) + rs * (z / LVX_SUPER))]) {
                 // Only a solid voxel can block.  Walk the segment centre->camera through the
                 // 32^3-voxel super-bricks, then the 8^3 bricks.
                 const float ox = x + 0.5f, oy = y + 0.5f, oz = z + 0.5f;
@@ -351,7 +406,9 @@ extern "C" {
 int64_t lvx_cull_scratch_words(int res) {
     if (!pow2(res)) return LVX_E_ARG;
     const int64_t V = (int64_t)res * res * res;
-    return (V + 31) / 32 + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER) + V;   // + occupied-voxel list
+    const int64_t rs = (res + LVX_SUPER - 1) / LVX_SUPER;
+    return (V + 31) / 32 + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER)
+           + (LVX_LIST_HDR + LVX_SOLID_CAP) + (rs * rs * rs + 3) / 4 + V;   // + solid list, super-brick flags, occupied-voxel list
 }
 
 int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32_t *solid_bits,
@@ -359,17 +416,23 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     if (!pow2(res)) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
-    // solid_bits scratch layout: [V/32 words of solid bits][8^3-brick flags][32^3-brick flags][V: occupied list]
+    // solid_bits scratch layout: [V/32 words of solid bits][8^3-brick flags][32^3-brick flags][solid list]
+    // [super-brick shadow flags][V: occupied list]
     uint32_t *bricks = solid_bits + (V + 31) / 32;
-    LVX_CUDA(cudaMemsetAsync(bricks, 0, (size_t)(brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER)) * 4, s));
-    uint32_t *occ_list = bricks + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER);
+    uint32_t *solid_list = bricks + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER);
+    LVX_CUDA(cudaMemsetAsync(bricks, 0, (size_t)(brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER) + LVX_LIST_HDR) * 4, s));
+    const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
+    uint8_t *sb_flag = reinterpret_cast<uint8_t *>(solid_list + LVX_LIST_HDR + LVX_SOLID_CAP);
+    uint32_t *occ_list = solid_list + LVX_LIST_HDR + LVX_SOLID_CAP + (rs * rs * rs + 3) / 4;
     LVX_CUDA(cudaMemsetAsync(vis_tmp, 0, (size_t)V, s));
-    k_solid<<<blocks_for(V, SOLID_ITEMS * 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, occ_list, stats);
+    k_solid<<<blocks_for(V, SOLID_ITEMS * 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, solid_list, occ_list, stats);
+    k_superbrick_shadow<<<blocks_for((int64_t)rs * rs * rs, 128), 128, 0, s>>>(solid_list, res, (float)cam_voxel_host[0],
+                                                                          (float)cam_voxel_host[1], (float)cam_voxel_host[2], sb_flag);
     unsigned nb = 148 * 16;
     if (nb > blocks_for(V, 128)) nb = blocks_for(V, 128);
     // vis_list doubles as the "needs the fine march" list until k_dilate refills it
     LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
-    k_visibility<<<nb, 128, 0, s>>>(bricks, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
+    k_visibility<<<nb, 128, 0, s>>>(bricks, sb_flag, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                     cam_voxel_host[2], stats, vis_tmp, vis_list);
     k_march<<<nb, 128, 0, s>>>(solid_bits, vis_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                cam_voxel_host[2], vis_tmp);

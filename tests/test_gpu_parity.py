@@ -241,3 +241,64 @@ def test_long_lists_sorted(lvx, oracle):
     ga = lvx.build_vsv(ls, None, g, gp)
     assert ga.stats["long_lists"] > 0
     assert np.array_equal(ga.fragments, ra.fragments)
+
+
+def _segment_box_distance(a, b, lo):
+    """Distance between segments a->b and unit cubes [lo, lo+1] (rows), by ternary search on the convex
+    function t -> dist(a + t (b - a), cube).  numpy, f64."""
+    t0 = np.zeros(len(a)); t1 = np.ones(len(a))
+
+    def f(t):
+        p = a + t[:, None] * (b - a)
+        d = np.maximum(np.maximum(lo - p, p - (lo + 1.0)), 0.0)
+        return np.sqrt((d * d).sum(axis=1))
+    for _ in range(70):
+        m1 = t0 + (t1 - t0) / 3.0; m2 = t1 - (t1 - t0) / 3.0
+        left = f(m1) <= f(m2)
+        t1 = np.where(left, m2, t1); t0 = np.where(left, t0, m1)
+    return f(0.5 * (t0 + t1))
+
+
+@pytest.mark.parametrize("name", ["c1_vcsv", "diag32_thick_vsv", "walk32_transp_k2"])
+def test_tight_index(lvx, name):
+    """The ray tracer's acceleration index (csrc/abuffer.cu): per listed voxel the first tcnt entries
+    of tfrags/tslot at the list's offset are a subset of the list in list order, and every
+    fragment left out has its capsule provably outside the voxel (so it can never yield an accepted
+    hit there, lv/raytracer.py:446-452)."""
+    sc = Scene(name)
+    cn, pyr, culling, abuf, scene, img = gpu_frame(lvx, sc)
+    assert abuf.tight is not None
+    res = sc.g.resolution
+    off = abuf.table.offsets.astype(np.int64)
+    cnt = abuf.table.counts.astype(np.int64)
+    frags = abuf.fragments.astype(np.int64)
+    tfr = abuf.tight.frags.cpu().numpy().view(np.uint32).astype(np.int64)
+    tsl = abuf.tight.slot.cpu().numpy().view(np.uint16).astype(np.int64)
+    tcn = abuf.tight.cnt.cpu().numpy().view(np.uint16).astype(np.int64)
+    listed = np.nonzero(cnt > 0)[0]
+    assert np.all(tcn[listed] <= cnt[listed])
+    # expand (voxel, j) for j < tcnt
+    reps = tcn[listed]
+    vox_t = np.repeat(listed, reps)
+    j = np.arange(reps.sum()) - np.repeat(np.cumsum(reps) - reps, reps)
+    pos = off[vox_t] + j
+    slot = tsl[pos]
+    assert np.all(slot < cnt[vox_t])
+    assert np.array_equal(frags[off[vox_t] + slot], tfr[pos])          # slot = position in the full list
+    same = vox_t[1:] == vox_t[:-1]
+    assert np.all(slot[1:][same] > slot[:-1][same])                    # list order kept (ascending ids)
+    # fragments left out: capsule of radius r farther than r from the voxel cube
+    is_tight = np.zeros(len(frags), dtype=bool)
+    is_tight[off[vox_t] + slot] = True
+    vox_all = np.repeat(listed, cnt[listed])
+    loose = ~is_tight
+    assert loose.sum() > 0
+    verts = (sc.ls.vertices.astype(np.float64) - sc.g.world_min) / sc.g.voxel_size       # lv/voxelizer.py:440
+    a = verts[frags[loose]]; b = verts[frags[loose] + 1]      # a fragment is its segment's start-vertex index
+    v = vox_all[loose]
+    lo = np.stack([v % res, (v // res) % res, v // (res * res)], axis=1).astype(np.float64)
+    d = _segment_box_distance(a, b, lo)
+    r = sc.r_world / sc.g.voxel_size
+    assert d.min() > r + 5e-4, f"a loose fragment comes within {d.min() - r:.2e} of its voxel"
+    if r < 0.5:
+        assert is_tight.mean() < 0.6      # the index is worth having for thin lines
