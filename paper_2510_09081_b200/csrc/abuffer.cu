@@ -407,7 +407,10 @@ __device__ __forceinline__ void sort_regs(uint32_t todo, uint32_t b, uint32_t n,
     }
 }
 
-__global__ void __launch_bounds__(ORDER_WARPS * 32)
+#ifndef LVX_ORDER_MINB
+#define LVX_ORDER_MINB 8   // 32 registers: the rare 4-elements-per-lane path spills a little, every other path gains occupancy
+#endif
+__global__ void __launch_bounds__(ORDER_WARPS * 32, LVX_ORDER_MINB)
 k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ cursor,
         const uint32_t *__restrict__ vis_list, uint32_t *__restrict__ frags, int64_t cap,
         const TightIndex T, uint64_t *__restrict__ stats) {
