@@ -1,8 +1,8 @@
 #!/usr/bin/env python3
 """bench.py -- frames/s and per-stage ms of the per-frame pipeline on BASELINE.json's C2 workload
 (synthetic tractography bundles, ~1 M segments, 256^3 grid, 1920x1080 opaque + cone-traced AO,
-strategy vcsv), full rebuild every frame (upload -> voxelize -> mips -> cull -> scan ->
-scatter/order -> shade -> trace).
+strategy vcsv), full rebuild every frame (upload + clip normals + grid refit -> voxelize -> mips ->
+cull -> scan -> scatter/order -> shade -> trace).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload c1|c2|c3|c4]
 
@@ -160,13 +160,19 @@ def run_gpu(args):
     out_srgb = torch.empty((h, w, 3), dtype=torch.uint8).pin_memory()
     out_hit = torch.empty((h, w), dtype=torch.int32).pin_memory()
 
+    def refit(e):
+        """a3 of the hot path, every frame: AABB of the new vertices on the device (24-byte read-back),
+        fit_grid and the orbit camera on the host (lv/pipeline.py:68-87, 40-47)."""
+        g_i, rw_i = e.fit(radius_voxels=R_VOXELS)
+        return lvx.make_camera(cfg, g_i), g_i, rw_i
+
     def step_resident(i):
         eng.load_vertices(dev[i % n_variants])          # D2D: inputs are resident in HBM
-        return eng.run(cam, g, r_world)
+        return eng.run(*refit(eng))
 
     def step_e2e(i):
         eng.load_vertices(host[i % n_variants])         # H2D from pinned memory
-        r = eng.run(cam, g, r_world)
+        r = eng.run(*refit(eng))
         out_srgb.copy_(eng.srgb, non_blocking=True)     # D2H result
         out_hit.copy_(eng.hit_id, non_blocking=True)
         torch.cuda.current_stream().synchronize()
@@ -233,7 +239,7 @@ def run_gpu(args):
                         e0.record(main)
                         streams[k].wait_event(e0)
                     engines[k].load_vertices(src[i % n_variants])
-                    engines[k].submit(cam, g, r_world)
+                    engines[k].submit(*refit(engines[k]))
                     if e2e:
                         out_bufs[k][0].copy_(engines[k].srgb, non_blocking=True)
                         out_bufs[k][1].copy_(engines[k].hit_id, non_blocking=True)
@@ -308,7 +314,7 @@ def run_gpu(args):
         "e2e": {"value": round(fps_e2e, 3), "unit": "frames/s", "ms_per_step": round(ms_e2e / args.steps, 4),
                 "h2d_bytes_per_step": int(host[0].numel() * 4),
                 "d2h_bytes_per_step": int(out_srgb.numel() + out_hit.numel() * 4 + 128)},
-        "gpu_launches": int(eng.kernel_launches_per_frame() * args.steps),
+        "gpu_launches": int((eng.kernel_launches_per_frame() + 3) * args.steps),   # + the 3 AABB kernels of the refit
         "roofline": {"bound": "hbm", "kernel": kernel_of[top], "stage": top,
                      "achieved": round(top_gbs, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(top_gbs / peak, 4), "traffic": traffic, "kernel_ms": round(top_ms, 4),

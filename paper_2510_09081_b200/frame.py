@@ -119,9 +119,9 @@ class FrameEngine:
         n = 1 + 1                                   # stats_reset, upload
         n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
         n += levels - 1                             # mips
-        n += (4 if self.strategy == "vcsv" else 1) + (levels - 1)   # solid, visibility, march, dilate | occupied; or-mips
+        n += (5 if self.strategy == "vcsv" else 1) + (levels - 1)   # solid, super-brick shadow, visibility, march, dilate | occupied; or-mips
         n += 1                                      # scan
-        n += 3 + 1                                  # cursor copy, scatter, order; march table
+        n += 3 + 1                                  # cursor init, scatter, order; march table
         n += levels + 1                             # non-empty masks, shade
         if self.shading == "demand":
             n += 2                                  # trace_hits, resolve
