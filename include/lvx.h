@@ -91,6 +91,15 @@ int lvx_upload(const float *verts_f32, const int64_t *poly_off, int64_t n_verts,
                const double *world_min_host, double voxel_size,
                double *verts, float *verts_f, double *normals, int32_t *segs, uint64_t *stats, void *stream);
 
+/* Processing order for lvx_voxelize* / lvx_scatter: `order` = the entries of `segs` grouped by the
+ * brick (brick^3 voxels, brick a power of two) of their start vertex.  Both consumers produce the same
+ * output for any order of the segments (the reference's results are independent of its chunking,
+ * lv/voxelizer.py:461-463); grouping makes neighbouring threads touch the same sectors.
+ * scratch: lvx_segment_order_scratch_words(n_seg, res, brick) u32. */
+int64_t lvx_segment_order_scratch_words(int64_t n_seg, int res, int brick);
+int lvx_segment_order(const double *verts, const int32_t *segs, int64_t n_seg, int res, int brick,
+                      int32_t *order, uint32_t *scratch, void *stream);
+
 /* lv/lineset.py:81-82 LineSet.aabb(): out6 = {min xyz, max xyz} as f32 (device). */
 int lvx_aabb(const float *verts_f32, int64_t n_verts, float *out6, void *stream);
 

@@ -118,6 +118,81 @@ __global__ void k_stats_reset(uint64_t *stats) {
     if (threadIdx.x < LVX_STATS_WORDS) stats[threadIdx.x] = 0;
 }
 
+
+// ----------------------------------------------------------------------------- processing order
+// Voxelization and the A-buffer scatter produce the same output for any processing order of the
+// segments (integer atomics; the ordering pass sorts every list).  Handing neighbouring threads
+// segments of the same brick makes their atomics and 4-byte fragment stores fall into the same
+// sectors at the same time: on C4 (10 M segments, 3.7 GB of fragments) the scatter's DRAM traffic
+// was 11x the fragment bytes in polyline order.  One counting sort per frame: rank inside the
+// brick from the histogram atomic, a single-block scan of the (few thousand) bins, a scatter.
+__device__ __forceinline__ uint32_t brick_of(const double *__restrict__ verts, int64_t v, int res, int brick, int nb) {
+    const int bx = min(max((int)floor(verts[3 * v]), 0), res - 1) / brick;
+    const int by = min(max((int)floor(verts[3 * v + 1]), 0), res - 1) / brick;
+    const int bz = min(max((int)floor(verts[3 * v + 2]), 0), res - 1) / brick;
+    return (uint32_t)bx + (uint32_t)nb * ((uint32_t)by + (uint32_t)nb * (uint32_t)bz);
+}
+
+__global__ void __launch_bounds__(256)
+k_order_hist(const double *__restrict__ verts, const int32_t *__restrict__ segs, int64_t n_seg, int res, int brick,
+             int nb, uint32_t *__restrict__ hist, uint32_t *__restrict__ rank) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // consecutive segments of a polyline mostly share their brick: one atomic per group of equal keys
+    const uint32_t key = i < n_seg ? brick_of(verts, segs[i], res, brick, nb) : 0xffffffffu;
+    const uint32_t same = __match_any_sync(0xffffffffu, key);
+    const int lane = threadIdx.x & 31, leader = __ffs(same) - 1;
+    uint32_t base = 0;
+    if (lane == leader && i < n_seg) base = atomicAdd(&hist[key], (uint32_t)__popc(same));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (i < n_seg) rank[i] = base + __popc(same & ((1u << lane) - 1u));
+}
+
+// exclusive scan of n <= 2^20 bins by one block of 1024 threads (n is a few thousand)
+__global__ void __launch_bounds__(1024)
+k_order_scan(uint32_t *__restrict__ hist, int n) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_carry;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += 1024) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < n ? hist[i] : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) s_warp[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = s_warp[lane], wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += u;
+            }
+            s_warp[lane] = wi - w;
+        }
+        __syncthreads();
+        const uint32_t carry = s_carry;
+        if (i < n) hist[i] = carry + s_warp[warp] + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) s_carry = carry + s_warp[warp] + inc;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_order_scatter(const double *__restrict__ verts, const int32_t *__restrict__ segs, int64_t n_seg, int res, int brick,
+                int nb, const uint32_t *__restrict__ start, const uint32_t *__restrict__ rank, int32_t *__restrict__ order) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_seg) return;
+    const int32_t v = segs[i];
+    order[start[brick_of(verts, v, res, brick, nb)] + rank[i]] = v;
+}
+
 }  // namespace lvx
 
 using namespace lvx;
@@ -170,6 +245,29 @@ int lvx_aabb(const float *verts_f32, int64_t n_verts, float *out6, void *stream)
     if (nb > 148 * 8) nb = 148 * 8;
     k_aabb<<<nb, 256, 0, s>>>(verts_f32, n_verts, (uint32_t *)out6);
     k_aabb_finish<<<1, 32, 0, s>>>((uint32_t *)out6);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int64_t lvx_segment_order_scratch_words(int64_t n_seg, int res, int brick) {
+    if (!pow2(res) || brick < 1 || !pow2(brick) || brick > res) return LVX_E_ARG;
+    const int64_t nb = res / brick;
+    return nb * nb * nb + n_seg;
+}
+
+int lvx_segment_order(const double *verts, const int32_t *segs, int64_t n_seg, int res, int brick, int32_t *order,
+                      uint32_t *scratch, void *stream) {
+    if (!pow2(res) || brick < 1 || (brick & (brick - 1)) || brick > res || n_seg < 0 || n_seg > 0x7fffffffLL) return LVX_E_ARG;
+    if (n_seg == 0) return LVX_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int nb = res / brick;
+    const int64_t bins = (int64_t)nb * nb * nb;
+    if (bins > (1 << 20)) return LVX_E_ARG;
+    uint32_t *hist = scratch, *rank = scratch + bins;
+    LVX_CUDA(cudaMemsetAsync(hist, 0, (size_t)bins * 4, s));
+    k_order_hist<<<blocks_for(n_seg, 256), 256, 0, s>>>(verts, segs, n_seg, res, brick, nb, hist, rank);
+    k_order_scan<<<1, 1024, 0, s>>>(hist, (int)bins);
+    k_order_scatter<<<blocks_for(n_seg, 256), 256, 0, s>>>(verts, segs, n_seg, res, brick, nb, hist, rank, order);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -110,6 +110,10 @@ class FrameEngine:
         # C3 (B200) the two only slow each other down (scatter 1.8 -> 4.4 ms, shade 2.9 -> 3.7 ms), the
         # frame time does not change and the per-stage times stop being readable.
         self.overlap_shading = False
+        # brick size of the segment processing order (0 = polyline order).  Measured on B200: 8..32 are
+        # within 2 % of each other on C2 (256^3), 32 is best on C4 (512^3): res / 16
+        import os
+        self.order_brick = min(int(os.environ.get("LVX_ORDER_BRICK", str(max(8, self.res // 16)))), self.res)
         self._stats_host = self._done = self._side = self._ev_side = self._pending = None
         self._overlapped = False
 
@@ -117,6 +121,7 @@ class FrameEngine:
         """Number of lvx kernels one `run` enqueues (csrc/*.cu), for bench.py's `gpu_launches`."""
         levels = int(self.res).bit_length()
         n = 1 + 1                                   # stats_reset, upload
+        n += 3 if self.order_brick > 0 else 0       # processing order: histogram, scan, scatter
         n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
         n += levels - 1                             # mips
         n += (5 if self.strategy == "vcsv" else 1) + (levels - 1)   # solid, super-brick shadow, visibility, march, dilate | occupied; or-mips
@@ -139,6 +144,10 @@ class FrameEngine:
         self._vertsf = t.empty((int(n_vertices), 3), dtype=t.float32, device=self.dev)
         self._normals = t.empty((int(n_vertices), 3), dtype=t.float64, device=self.dev) if self.clip else None
         self._segs = t.empty(int(n_vertices) - (len(polyline_offsets) - 1), dtype=t.int32, device=self.dev)
+        # processing order of the segments (grouped by brick, csrc/upload.cu); results do not depend on it
+        self._order = t.empty_like(self._segs) if self.order_brick > 0 else None
+        self._order_scratch = (t.empty(ops.segment_order_scratch_words(self._segs.numel(), self.res, self.order_brick),
+                                       dtype=t.int32, device=self.dev) if self.order_brick > 0 else None)
 
     def load_vertices(self, verts):
         """verts: (N,3) f32 -- pinned host tensor / numpy (H2D on the current stream) or cuda tensor."""
@@ -170,6 +179,8 @@ class FrameEngine:
                                      int(self._verts32.shape[0]), int(self._poly_off.shape[0]) - 1,
                                      float(r_world) / float(grid.voxel_size), grid, float(r_world))
         self.grid = grid
+        if self._order is not None:
+            ops.segment_order(self.lines, self.res, self.order_brick, self._order, self._order_scratch)
 
     def _stage_voxelize(self, seg_range=None):
         b, e = (0, self.lines.n_segments) if seg_range is None else seg_range

@@ -65,6 +65,11 @@ class DeviceLines:
     r: float              # capsule radius, voxel units
     grid: "object"
     r_world: float
+    order: "object" = None   # (N,) i32: `segs` grouped by brick (segment_order), the order the kernels process them in
+
+    @property
+    def proc_segs(self):
+        return self.segs if self.order is None else self.order
 
     @property
     def n_segments(self) -> int:
@@ -105,6 +110,17 @@ def aabb(verts32):
     return h[:3], h[3:]
 
 
+def segment_order_scratch_words(n_seg: int, res: int, brick: int) -> int:
+    return int(lib().lvx_segment_order_scratch_words(int(n_seg), int(res), int(brick)))
+
+
+def segment_order(lines: DeviceLines, res: int, brick: int, order, scratch):
+    """Fills `order` (i32, n_segments) with lines.segs grouped by brick and makes it the processing order."""
+    check(lib().lvx_segment_order(_ptr(lines.verts), _ptr(lines.segs), lines.n_segments, int(res), int(brick),
+                                  _ptr(order), _ptr(scratch), _stream()), "lvx_segment_order")
+    lines.order = order
+
+
 def footprint_radius(r: float, r_min: float = 0.5) -> float:
     """lv/voxelizer.py:450-458"""
     return max(r, r_min) + 0.5
@@ -118,7 +134,7 @@ def voxelize(lines: DeviceLines, res, r_min, method, base, occ_sat, stats, seg_b
     """lvx_voxelize into zeroed `base` (V i32) / `occ_sat` (V/32 i32)."""
     seg_end = lines.n_segments if seg_end is None else seg_end
     r = lines.r
-    check(lib().lvx_voxelize(_ptr(lines.verts), _ptr(lines.normals), _ptr(lines.segs), seg_begin, seg_end,
+    check(lib().lvx_voxelize(_ptr(lines.verts), _ptr(lines.normals), _ptr(lines.proc_segs), seg_begin, seg_end,
                              int(lines.use_clip), r, footprint_radius(r, r_min), float(r_min), res,
                              METHODS[method], _ptr(base), _ptr(occ_sat), _ptr(stats), _stream()),
           "lvx_voxelize")
@@ -127,7 +143,7 @@ def voxelize(lines: DeviceLines, res, r_min, method, base, occ_sat, stats, seg_b
 def voxelize_wide(lines: DeviceLines, res, r_min, method, wide, stats, seg_begin=0, seg_end=None):
     seg_end = lines.n_segments if seg_end is None else seg_end
     r = lines.r
-    check(lib().lvx_voxelize_wide(_ptr(lines.verts), _ptr(lines.normals), _ptr(lines.segs), seg_begin,
+    check(lib().lvx_voxelize_wide(_ptr(lines.verts), _ptr(lines.normals), _ptr(lines.proc_segs), seg_begin,
                                   seg_end, int(lines.use_clip), r, footprint_radius(r, r_min), float(r_min),
                                   res, METHODS[method], _ptr(wide), _ptr(stats), _stream()),
           "lvx_voxelize_wide")
@@ -208,7 +224,7 @@ def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, c
     if tight is not None and tight.capacity < frags.numel():
         raise ValueError("tight index too small for the fragment buffer")
     tf, ts, tc = _tight_ptrs(tight)
-    check(lib().lvx_scatter(_ptr(lines.verts), _ptr(lines.segs), lines.n_segments, float(rt),
+    check(lib().lvx_scatter(_ptr(lines.verts), _ptr(lines.proc_segs), lines.n_segments, float(rt),
                             float(lines.r) + TIGHT_MARGIN, res,
                             METHODS[method], _ptr(cull_flat), _ptr(vis_list), _ptr(offsets), _ptr(cursor),
                             _ptr(frags), frags.numel(), tf, ts, tc, _ptr(stats), _stream()), "lvx_scatter")
