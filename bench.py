@@ -36,7 +36,11 @@ WORKLOADS = {
     "c2": (dict(kind="bundles", seed=0, n_bundles=40, fibers=250, verts=101), 256, 1920, 1080, "vcsv", "opaque", 1.0),
     "c3": (dict(kind="bundles", seed=0, n_bundles=40, fibers=250, verts=101), 256, 1920, 1080, "vsv", "transparent", 0.3),
     "c4": (dict(kind="bundles", seed=1, n_bundles=400, fibers=250, verts=101), 512, 1920, 1080, "vcsv", "opaque", 1.0),
+    # unsteady-flow pathline sequence: every frame is a different time step (its own generator seed)
+    "c5": (dict(kind="random_streamlines", seed=0, polylines=20000, verts_per_line=101, domain=128.0, curl=0.3),
+           256, 1920, 1080, "vcsv", "opaque", 1.0),
 }
+C5_TIME_STEPS = 2      # distinct time steps generated on the host (~20 s each); the sequence cycles through them
 R_VOXELS = 0.2
 R_MIN = 0.5
 LIGHT = "-0.5,-0.3,-0.8"
@@ -155,7 +159,14 @@ def run_gpu(args):
     eng.set_topology(ls.polyline_offsets, ls.n_vertices)
     # a dynamic sequence: every step gets its own deformed vertex set (rank r renders frames r, r+world, ...)
     n_variants = 4
-    host = [torch.from_numpy(deform(ls.vertices, rank + world * i, g.voxel_size)).pin_memory() for i in range(n_variants)]
+    if args.workload == "c5":   # time steps = independent line sets of the same topology
+        n_variants = C5_TIME_STEPS
+        gen = dict(WORKLOADS["c5"][0]); kind = gen.pop("kind"); gen.pop("seed")
+        host = [torch.from_numpy(ls.vertices if rank + world * i == 0 else
+                                 lvx.generate(kind, seed=rank + world * i, **gen).vertices).pin_memory()
+                for i in range(n_variants)]
+    else:
+        host = [torch.from_numpy(deform(ls.vertices, rank + world * i, g.voxel_size)).pin_memory() for i in range(n_variants)]
     dev = [hv.cuda() for hv in host]
     out_srgb = torch.empty((h, w, 3), dtype=torch.uint8).pin_memory()
     out_hit = torch.empty((h, w), dtype=torch.int32).pin_memory()
