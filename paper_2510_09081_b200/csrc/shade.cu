@@ -11,6 +11,7 @@ namespace lvx {
 struct ShadeParams {
     double dirs[15][3];
     double shadow_dir[3];   // -light
+    double inv_dirs[15][3], inv_shadow[3];   // 1/d per component (0 where d == 0), for the t_safe bound only
     double tan_ao, tan_shadow, w;
     uint32_t mip_off[16];   // element offset of level l (l >= 1) inside `mips`
     uint32_t mask_off[16];  // word offset of level l inside the non-empty masks
@@ -80,18 +81,20 @@ __device__ __forceinline__ double trilinear(const uint32_t *__restrict__ base, c
 __device__ __forceinline__ double cone_trace(const uint32_t *__restrict__ base, const double *__restrict__ mips,
                                              const uint32_t *__restrict__ masks, const ShadeParams &P,
                                              double ox, double oy, double oz,
-                                             double dx, double dy, double dz, double tan_half) {
+                                             double dx, double dy, double dz, const double *inv_d, double tan_half) {
     const double R = (double)P.res;
     if (ox < 0.0 || oy < 0.0 || oz < 0.0 || ox > R || oy > R || oz > R) return 0.0;
     // while t <= t_safe the sample point is inside [1e-3, R-1e-3]^3 for certain, so the exact
-    // six-way bounds test (line 122 of the reference) cannot fire and is not evaluated
+    // six-way bounds test (line 122 of the reference) cannot fire and is not evaluated.  t_safe is
+    // only this gate, so it is formed with the host's reciprocals (a product instead of three
+    // divisions per cone); the 1e-3-voxel margin covers the rounding of the product many times over.
     double t_safe = 1e30;
     {
         const double o[3] = {ox, oy, oz}, d[3] = {dx, dy, dz};
 #pragma unroll
         for (int a = 0; a < 3; a++) {
-            if (d[a] > 0.0) t_safe = fmin(t_safe, (R - 1e-3 - o[a]) / d[a]);
-            else if (d[a] < 0.0) t_safe = fmin(t_safe, (1e-3 - o[a]) / d[a]);
+            if (d[a] > 0.0) t_safe = fmin(t_safe, (R - 1e-3 - o[a]) * inv_d[a]);
+            else if (d[a] < 0.0) t_safe = fmin(t_safe, (1e-3 - o[a]) * inv_d[a]);
         }
     }
     double occ = 0.0, t = 1.0;
@@ -150,9 +153,10 @@ k_shade(const uint32_t *__restrict__ base, const double *__restrict__ mips,
         const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
         double acc = 0.0;
         for (int c = 0; c < P.n_dirs; c++)
-            acc += P.w * cone_trace(base, mips, masks, P, ox, oy, oz, P.dirs[c][0], P.dirs[c][1], P.dirs[c][2], P.tan_ao);
+            acc += P.w * cone_trace(base, mips, masks, P, ox, oy, oz, P.dirs[c][0], P.dirs[c][1], P.dirs[c][2], P.inv_dirs[c],
+                                    P.tan_ao);
         const double sh = cone_trace(base, mips, masks, P, ox, oy, oz, P.shadow_dir[0], P.shadow_dir[1], P.shadow_dir[2],
-                                     P.tan_shadow);
+                                     P.inv_shadow, P.tan_shadow);
         double a = 1.0 - acc, s = 1.0 - sh;
         a = a < 0.0 ? 0.0 : (a > 1.0 ? 1.0 : a);     // lv/shading.py:183-184
         s = s < 0.0 ? 0.0 : (s > 1.0 ? 1.0 : s);
@@ -184,6 +188,9 @@ int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t 
     for (int c = 0; c < n_dirs; c++)
         for (int a = 0; a < 3; a++) P.dirs[c][a] = dirs_host[3 * c + a];
     for (int a = 0; a < 3; a++) P.shadow_dir[a] = -light_host[a];   // lv/shading.py:154-155
+    for (int c = 0; c < 15; c++)
+        for (int a = 0; a < 3; a++) P.inv_dirs[c][a] = (c < n_dirs && P.dirs[c][a] != 0.0) ? 1.0 / P.dirs[c][a] : 0.0;
+    for (int a = 0; a < 3; a++) P.inv_shadow[a] = P.shadow_dir[a] != 0.0 ? 1.0 / P.shadow_dir[a] : 0.0;
     P.tan_ao = tan_ao; P.tan_shadow = tan_shadow; P.w = 1.0 / n_dirs;
     const LevelOffsets L = make_level_offsets(res);
     uint32_t mw = 0;
