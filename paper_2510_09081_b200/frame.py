@@ -100,7 +100,12 @@ class FrameEngine:
             self.need_bits = t.empty(max(V // 32, 1), dtype=t.int32, device=d)
             self.need_list = t.empty(ops.list_words(V), dtype=t.int32, device=d)
         self.wide = None
-        self.use_wide = False
+        # Accumulate into 64-bit (count << 32 | occ) words and pack afterwards (lvx_voxelize_wide +
+        # lvx_pack_wide) instead of the packed 32-bit word with carry repair (lvx_voxelize).  The wide
+        # form never needs the atomic's return value, so it compiles to fire-and-forget RED.64: measured
+        # on B200, C2 voxelize 0.81 -> 0.68 ms and C4 12.8 -> 9.5 ms including the clear and the pack.
+        # Same result bit for bit (per-field saturation, lv/voxelizer.py:490-495); False selects the packed path.
+        self.use_wide = True
         self.lines = None
         self.grid = None
         self._verts32 = self._poly_off = None
