@@ -195,21 +195,21 @@ __device__ __forceinline__ bool coarse_may_hit(const uint32_t *__restrict__ bits
 // the boxes c + u (B - c); such a box meets the cube F iff the six per-axis inequalities hold, each
 // linear in u, so the test is an intersection of six u-intervals.  Work: super-bricks x solid
 // voxels (512 x 58 on C2) -- and the per-voxel brick walks then run only inside flagged super-bricks.
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(64)
 k_superbrick_shadow(const uint32_t *__restrict__ solid_list, int res, float cx, float cy, float cz,
                     uint8_t *__restrict__ sb_flag) {
+    // one block of 64 threads per super-brick, the solid voxels dealt out to the threads
     const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
-    const int sb = blockIdx.x * blockDim.x + threadIdx.x;
-    if (sb >= rs * rs * rs) return;
+    const int sb = blockIdx.x;
     const uint32_t n_all = solid_list[0];
-    if (n_all > LVX_SOLID_CAP) { sb_flag[sb] = 1; return; }      // too many to list: no shortcut
+    if (n_all > LVX_SOLID_CAP) { if (threadIdx.x == 0) sb_flag[sb] = 1; return; }      // too many to list: no shortcut
     const float c[3] = {cx, cy, cz};
     const int b3[3] = {sb % rs, (sb / rs) % rs, sb / (rs * rs)};
     float blo[3], bhi[3];
 #pragma unroll
     for (int a = 0; a < 3; a++) { blo[a] = (float)(b3[a] * LVX_SUPER); bhi[a] = fminf((float)((b3[a] + 1) * LVX_SUPER), (float)res); }
-    uint8_t flag = 0;
-    for (uint32_t k = 0; k < n_all && !flag; k++) {
+    int flag = 0;
+    for (uint32_t k = threadIdx.x; k < n_all; k += blockDim.x) {
         const uint32_t v = solid_list[LVX_LIST_HDR + k];
         const int s3[3] = {(int)(v % res), (int)((v / res) % res), (int)(v / ((uint32_t)res * res))};
         float u0 = 0.f, u1 = 1.f;
@@ -233,7 +233,8 @@ k_superbrick_shadow(const uint32_t *__restrict__ solid_list, int res, float cx, 
         }
         if (u0 <= u1) flag = 1;
     }
-    sb_flag[sb] = flag;
+    flag = __syncthreads_or(flag);
+    if (threadIdx.x == 0) sb_flag[sb] = (uint8_t)(flag != 0);
 }
 
 // lv/culling.py:191-200.  When the frame has no solid voxel at all nothing can block, so every
@@ -426,7 +427,7 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     uint32_t *occ_list = solid_list + LVX_LIST_HDR + LVX_SOLID_CAP + (rs * rs * rs + 3) / 4;
     LVX_CUDA(cudaMemsetAsync(vis_tmp, 0, (size_t)V, s));
     k_solid<<<blocks_for(V, SOLID_ITEMS * 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, solid_list, occ_list, stats);
-    k_superbrick_shadow<<<blocks_for((int64_t)rs * rs * rs, 128), 128, 0, s>>>(solid_list, res, (float)cam_voxel_host[0],
+    k_superbrick_shadow<<<(unsigned)(rs * rs * rs), 64, 0, s>>>(solid_list, res, (float)cam_voxel_host[0],
                                                                           (float)cam_voxel_host[1], (float)cam_voxel_host[2], sb_flag);
     unsigned nb = 148 * 16;
     if (nb > blocks_for(V, 128)) nb = blocks_for(V, 128);

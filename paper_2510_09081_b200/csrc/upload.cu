@@ -103,11 +103,19 @@ k_aabb(const float *__restrict__ v, int64_t n_verts, uint32_t *__restrict__ acc)
             mn[a] = fminf(mn[a], __shfl_xor_sync(0xffffffffu, mn[a], o));
             mx[a] = fmaxf(mx[a], __shfl_xor_sync(0xffffffffu, mx[a], o));
         }
-    if ((threadIdx.x & 31) == 0)
-        for (int a = 0; a < 3; a++) {
-            atomicMin(&acc[a], f2o(mn[a]));
-            atomicMax(&acc[3 + a], f2o(mx[a]));
-        }
+    // one set of six atomics per block (the six target words are shared by the whole grid)
+    __shared__ float s_mn[8][3], s_mx[8][3];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0)
+        for (int a = 0; a < 3; a++) { s_mn[warp][a] = mn[a]; s_mx[warp][a] = mx[a]; }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int a = threadIdx.x;
+        float lo = s_mn[0][a], hi = s_mx[0][a];
+        for (int w = 1; w < 8; w++) { lo = fminf(lo, s_mn[w][a]); hi = fmaxf(hi, s_mx[w][a]); }
+        atomicMin(&acc[a], f2o(lo));
+        atomicMax(&acc[3 + a], f2o(hi));
+    }
 }
 
 __global__ void k_aabb_finish(uint32_t *acc) {
@@ -241,8 +249,9 @@ int lvx_aabb(const float *verts_f32, int64_t n_verts, float *out6, void *stream)
     if (n_verts < 1) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     k_aabb_init<<<1, 32, 0, s>>>((uint32_t *)out6);
-    unsigned nb = blocks_for(n_verts, 256);
-    if (nb > 148 * 8) nb = 148 * 8;
+    unsigned nb = blocks_for(n_verts, 256 * 4);       // >= 4 vertices per thread
+    if (nb > 148 * 4) nb = 148 * 4;
+    if (nb < 1) nb = 1;
     k_aabb<<<nb, 256, 0, s>>>(verts_f32, n_verts, (uint32_t *)out6);
     k_aabb_finish<<<1, 32, 0, s>>>((uint32_t *)out6);
     LVX_LAUNCH_CHECK();
