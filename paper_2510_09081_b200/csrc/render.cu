@@ -342,7 +342,8 @@ constexpr int RC_WARPS = 4;
 #define LVX_CNT(slot, n) do { } while (0)
 #endif
 #ifndef LVX_SPEC
-#define LVX_SPEC 2      // occupied voxels a ray walks ahead per round (opaque)
+#define LVX_SPEC 5      // occupied voxels a ray walks ahead per round (opaque).  Measured on C2 with the tight
+                        // index: 2 -> 2.39 ms, 3 -> 2.27, 4 -> 1.96, 5 -> 1.91, 6 -> 1.93, 8 -> 1.96 (at 5 CTAs/SM)
 #endif
 #ifndef LVX_SPEC_T
 #define LVX_SPEC_T 4    // ... per round (transparent: rays rarely stop early, so deeper is cheap)
@@ -573,10 +574,8 @@ __device__ __forceinline__ bool assign_pixels(const RenderArgs &A, TileQueue &Q,
 
 // ----------------------------------------------------------------------------- opaque
 #ifndef LVX_SPEC_MAX
-#define LVX_SPEC_MAX LVX_SPEC   // look-ahead when only a few rays of the tile are still marching.  Measured on C2:
-                                // 4 -> trace 2.80 ms, 8 -> 4.3 ms against 2.76 ms for a fixed depth of 2 (the
-                                // extra ordinals are mostly wasted behind the first hit, and the larger
-                                // queues cost a resident CTA), so the depth stays fixed.
+#define LVX_SPEC_MAX LVX_SPEC   // look-ahead when only a few rays of the tile are still marching: same as the
+                                // fixed depth (a deeper look-ahead for sparse rounds was measured and did not pay)
 #endif
 struct WarpShared {
     PairQueues<LVX_SPEC_MAX> q;
@@ -585,7 +584,7 @@ struct WarpShared {
 };
 
 #ifndef LVX_RC_MINB
-#define LVX_RC_MINB 6
+#define LVX_RC_MINB 5   // 96 registers, no spills (6 CTAs/SM = 80 registers spills in the march loop: 2.39 vs 2.20 ms)
 #endif
 template <bool DEFER>
 __global__ void __launch_bounds__(RC_WARPS * 32, LVX_RC_MINB)
