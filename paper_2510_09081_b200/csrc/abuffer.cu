@@ -172,7 +172,10 @@ __device__ __forceinline__ bool segment_misses_cube(float ax, float ay, float az
 // above any fragment capacity, so the position their atomic returns fails the capacity test and
 // nothing is stored -- one dependent memory round trip per cell (the atomic) instead of two.
 #define LVX_CURSOR_CULLED 0xF0000000u
-__global__ void __launch_bounds__(128)
+#ifndef LVX_SCAT_MINB
+#define LVX_SCAT_MINB 1
+#endif
+__global__ void __launch_bounds__(128, LVX_SCAT_MINB)
 k_scatter(const double *__restrict__ verts, const int32_t *__restrict__ segs, int64_t n_seg, double rt,
           float r_tight, int res, int method, uint32_t *__restrict__ cursor,
           uint32_t *__restrict__ frags, int64_t cap) {

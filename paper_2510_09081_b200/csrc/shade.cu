@@ -140,7 +140,10 @@ k_shade_fill(int64_t n4, float4 *__restrict__ ao, float4 *__restrict__ shadow) {
 // lanes fall on consecutive addresses (or the same address at coarse levels) -- a few L1
 // wavefronts per load instead of one per lane.  The 12 AO cones are folded in cone order in a
 // register (lv/shading.py:150-152), so the f64 sum has the reference's rounding.
-__global__ void __launch_bounds__(128)
+#ifndef LVX_SHADE_MINB
+#define LVX_SHADE_MINB 6
+#endif
+__global__ void __launch_bounds__(128, LVX_SHADE_MINB)
 k_shade(const uint32_t *__restrict__ base, const double *__restrict__ mips,
         const uint32_t *__restrict__ masks, const ShadeParams P, const uint32_t *__restrict__ vis_list,
         float *__restrict__ ao, float *__restrict__ shadow) {
