@@ -7,7 +7,7 @@ timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -5 > $O/${TAG}_tests_gp
 timeout 900 python bench.py --steps 20 --warmup 3 > $O/${TAG}_bench_c2.json 2> $O/${TAG}_bench_c2.err
 timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > $O/${TAG}_bench_c2_reference.json 2> $O/${TAG}_bench_c2_reference.err
 timeout 600 python bench.py --steps 20 --warmup 3 --pipeline 1 --no-cpu > $O/${TAG}_bench_c2_serial.json 2>> $O/${TAG}_bench_c2.err
-for w in c3 c4 c1; do
+for w in c3 c4 c1 c5; do
   timeout 900 python bench.py --workload $w --steps 20 --warmup 3 --no-cpu > $O/${TAG}_bench_$w.json 2> $O/${TAG}_bench_$w.err
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file $O/${TAG}_launches_c2.csv \
