@@ -302,3 +302,60 @@ def test_tight_index(lvx, name):
     assert d.min() > r + 5e-4, f"a loose fragment comes within {d.min() - r:.2e} of its voxel"
     if r < 0.5:
         assert is_tight.mean() < 0.6      # the index is worth having for thin lines
+
+
+def test_engine_variants_identical(lvx, oracle):
+    """FrameEngine's internal choices -- segment processing order (brick-sorted vs polyline order), 64-bit
+    vs packed accumulation, frames submitted to two engines on two streams -- never change an output."""
+    import torch
+    ls = lvx.generate("random_streamlines", seed=12, polylines=120, verts_per_line=50)
+    res = 64
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=0.3)
+    cfg = lvx.PipelineConfig(res=res, width=160, height=96, strategy="vcsv")
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vcsv")
+
+    def engine(order_brick, wide):
+        e = lvx.FrameEngine(res, 160, 96, strategy="vcsv", keep_rgb=True)
+        e.order_brick, e.use_wide = order_brick, wide
+        e.set_topology(ls.polyline_offsets, ls.n_vertices)
+        return e
+
+    outs = []
+    for order_brick, wide in [(0, False), (8, True), (16, False), (4, True)]:
+        e = engine(order_brick, wide)
+        e.load_vertices(ls.vertices)
+        out = e.run(cam, g, r_world)
+        n = out.stats["fragments"]
+        assert np.array_equal(e.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
+        assert n == ref.abuf.total
+        assert np.array_equal(e.frags[:n].cpu().numpy().view(np.uint32), ref.abuf.fragments)
+        assert np.array_equal(e.cull_flat.cpu().numpy(), ref.culling.flat)
+        assert np.array_equal(e.hit_id.cpu().numpy(), ref.image.hit_id)
+        assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
+        assert out.stats["ray_capsule_tests"] == ref.image.stats["ray_capsule_tests"]
+        assert out.stats["voxels_visited"] == ref.pyramid.visited
+        if order_brick:
+            order = e._order.cpu().numpy()
+            assert np.array_equal(np.sort(order), e._segs.cpu().numpy())          # a permutation of segs
+            v = e._verts64.cpu().numpy()[order]
+            nb = res // order_brick
+            c = np.clip(np.floor(v), 0, res - 1).astype(np.int64) // order_brick
+            key = c[:, 0] + nb * (c[:, 1] + nb * c[:, 2])
+            assert np.all(np.diff(key) >= 0)                                      # grouped by brick
+        outs.append(e)
+    # two frames in flight on two streams (submit/collect)
+    ea, eb = engine(8, True), engine(8, True)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(sa):
+        ea.load_vertices(ls.vertices); ea.submit(cam, g, r_world)
+    with torch.cuda.stream(sb):
+        eb.load_vertices(ls.vertices); eb.submit(cam, g, r_world)
+    with torch.cuda.stream(sa):
+        ra = ea.collect()
+    with torch.cuda.stream(sb):
+        rb = eb.collect()
+    torch.cuda.synchronize()
+    for e, r in ((ea, ra), (eb, rb)):
+        assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
+        assert r.stats["fragments"] == ref.abuf.total
