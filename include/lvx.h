@@ -119,7 +119,9 @@ int lvx_voxelize_wide(const double *verts, const double *normals, const int32_t 
 /* packed (+occ_sat) -> wide, so that per-GPU partial grids can be all-reduced with a plain sum */
 int lvx_widen(const uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, uint64_t *wide, void *stream);
 /* wide -> packed with per-field saturation (lv/voxelizer.py:493-495); adds to LVX_ST_SATURATED */
-int lvx_pack_wide(const uint64_t *wide, int64_t n_voxels, uint32_t *base, uint64_t *stats, void *stream);
+int lvx_pack_wide(const uint64_t *wide, int64_t n_voxels, uint32_t *base,
+                  uint32_t *nz_bits /* may be NULL; n_voxels/32 u32: bit = occupancy field non-zero, for lvx_shade */,
+                  uint64_t *stats, void *stream);
 /* applies occ_sat to `base` in place (occ field := 0xFFFF where flagged) */
 int lvx_finalize_base(uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, uint64_t *stats, void *stream);
 
@@ -172,11 +174,13 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
  * dirs_host: n_dirs*3 unit vectors (lv/shading.py:32-40); light_host: unit light direction.
  * ao/shadow: V f32; with fill_ones != 0 every voxel not in vis_list is set to 1.0 (the reference's
  * volumes), with 0 only listed voxels are written (shading on demand, see lvx_trace_hits).  n_dirs <= 15.  scratch: lvx_shade_scratch_bytes(V)
- * (per-level non-empty masks). */
+ * (per-level non-empty masks).  nz_bits: the per-voxel bits from lvx_pack_wide, or NULL (the level-0
+ * mask is then derived from `base`). */
 int64_t lvx_shade_scratch_bytes(int64_t n_voxels);
 int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t *vis_list,
               const double *dirs_host, int n_dirs, double tan_ao, const double *light_host,
-              double tan_shadow, float *ao, float *shadow, int fill_ones, void *scratch, void *stream);
+              double tan_shadow, float *ao, float *shadow, int fill_ones, const uint32_t *nz_bits,
+              void *scratch, void *stream);
 
 /* ---- march table: lv/raytracer.py:316-326 _empty_level evaluated once per voxel.  march[i] (V u8) =
  * 255 where bits_flat's level-0 bit is set, else the level _empty_level returns there; the ray

@@ -48,7 +48,7 @@ SIGNATURES = {
     "lvx_voxelize": (_I, [_P, _P, _P, _L, _L, _I, _D, _D, _D, _I, _I, _P, _P, _P, _P]),
     "lvx_voxelize_wide": (_I, [_P, _P, _P, _L, _L, _I, _D, _D, _D, _I, _I, _P, _P, _P]),
     "lvx_widen": (_I, [_P, _P, _L, _P, _P]),
-    "lvx_pack_wide": (_I, [_P, _L, _P, _P, _P]),
+    "lvx_pack_wide": (_I, [_P, _L, _P, _P, _P, _P]),
     "lvx_finalize_base": (_I, [_P, _P, _L, _P, _P]),
     "lvx_build_mips": (_I, [_P, _I, _P, _P]),
     "lvx_cull_scratch_words": (_L, [_I]),
@@ -62,7 +62,7 @@ SIGNATURES = {
     "lvx_scatter": (_I, [_P, _P, _L, _D, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P, _P]),
     "lvx_march_levels": (_I, [_P, _I, _P, _P]),
     "lvx_shade_scratch_bytes": (_L, [_L]),
-    "lvx_shade": (_I, [_P, _P, _I, _P, _P, _I, _D, _P, _D, _P, _P, _I, _P, _P]),
+    "lvx_shade": (_I, [_P, _P, _I, _P, _P, _I, _D, _P, _D, _P, _P, _I, _P, _P, _P]),
     "lvx_trace_hits": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lvx_resolve": (_I, [_P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "lvx_render": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P]),

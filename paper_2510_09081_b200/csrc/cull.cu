@@ -287,45 +287,103 @@ k_march(const uint32_t *__restrict__ solid, const uint32_t *__restrict__ march_l
     }
 }
 
-// lv/culling.py:130-140 dilate_bits, then `& occ_bits` (224)
+// Appends the set bits of the per-thread masks (bit k = voxel first + k of this thread, ITEMS voxels per
+// thread, threads in voxel order) to `list` in ascending voxel order inside the block's chunk: block
+// scan of the per-thread counts, ONE atomic on the list counter per block.  Called by all 256 threads.
+template <int ITEMS>
+__device__ __forceinline__ void list_append_items(uint32_t *list, uint32_t mask, uint32_t first,
+                                                  unsigned long long *counter2) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t c = __popc(mask);
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < 8 ? s_warp[lane] : 0;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += v;
+        }
+        if (lane < 8) s_warp[lane] = wi - w;
+        if (lane == 7 && wi) {
+            s_base = atomicAdd(reinterpret_cast<unsigned long long *>(list), (unsigned long long)wi);
+            if (counter2) atomicAdd(counter2, (unsigned long long)wi);
+        }
+    }
+    __syncthreads();
+    if (c) {
+        uint64_t slot = LVX_LIST_HDR + s_base + s_warp[warp] + (inc - c);
+#pragma unroll
+        for (int k = 0; k < ITEMS; k++)
+            if ((mask >> k) & 1u) list[slot++] = first + k;
+    }
+}
+
+// lv/culling.py:130-140 dilate_bits, then `& occ_bits` (224).  Four x-adjacent voxels per thread
+// (128-bit load of the packed words, 32-bit load/store of the byte masks); the 26-neighbour search
+// only runs for occupied voxels that are not visible themselves while anything is solid at all.
 __global__ void __launch_bounds__(256)
 k_dilate(const uint32_t *__restrict__ base, const uint8_t *__restrict__ vis, int res, int64_t V,
          uint8_t *__restrict__ out, uint32_t *__restrict__ vis_list, uint64_t *__restrict__ stats) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool v = false;
-    if (idx < V && (base[idx] >> 16) != 0) {
-        v = vis[idx] != 0;
-        if (!v && stats[LVX_ST_SOLID] != 0) {
-            const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
-            for (int dz = -1; dz <= 1 && !v; dz++) {
-                const int Z = z + dz;
-                if (Z < 0 || Z >= res) continue;
-                for (int dy = -1; dy <= 1 && !v; dy++) {
-                    const int Y = y + dy;
-                    if (Y < 0 || Y >= res) continue;
-                    for (int dx = -1; dx <= 1; dx++) {
-                        const int X = x + dx;
-                        if (X < 0 || X >= res) continue;
-                        if (vis[X + (int64_t)res * (Y + (int64_t)res * Z)]) { v = true; break; }
+    const int64_t idx0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;     // V is a multiple of 4 (res >= 2)
+    uint32_t mask = 0;
+    if (idx0 < V) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(base + idx0);
+        const uchar4 vv = *reinterpret_cast<const uchar4 *>(vis + idx0);
+        const uint32_t occ[4] = {w.x >> 16, w.y >> 16, w.z >> 16, w.w >> 16};
+        const uint8_t vs[4] = {vv.x, vv.y, vv.z, vv.w};
+        const bool any_solid = stats[LVX_ST_SOLID] != 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (!occ[k]) continue;
+            bool v = vs[k] != 0;
+            if (!v && any_solid) {
+                const int64_t idx = idx0 + k;
+                const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
+                for (int dz = -1; dz <= 1 && !v; dz++) {
+                    const int Z = z + dz;
+                    if (Z < 0 || Z >= res) continue;
+                    for (int dy = -1; dy <= 1 && !v; dy++) {
+                        const int Y = y + dy;
+                        if (Y < 0 || Y >= res) continue;
+                        for (int dx = -1; dx <= 1; dx++) {
+                            const int X = x + dx;
+                            if (X < 0 || X >= res) continue;
+                            if (vis[X + (int64_t)res * (Y + (int64_t)res * Z)]) { v = true; break; }
+                        }
                     }
                 }
             }
+            if (v) mask |= 1u << k;
         }
+        *reinterpret_cast<uchar4 *>(out + idx0) = make_uchar4(mask & 1u, (mask >> 1) & 1u, (mask >> 2) & 1u, (mask >> 3) & 1u);
     }
-    if (idx < V) out[idx] = v ? 1 : 0;
-    list_append_block(vis_list, v, (uint32_t)idx, (unsigned long long *)&stats[LVX_ST_VISIBLE]);
+    list_append_items<4>(vis_list, mask, (uint32_t)idx0, (unsigned long long *)&stats[LVX_ST_VISIBLE]);
 }
 
 __global__ void __launch_bounds__(256)
 k_occupied(const uint32_t *__restrict__ base, int64_t V, uint8_t *__restrict__ out, uint32_t *__restrict__ vis_list,
            uint64_t *__restrict__ stats) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool v = idx < V && (base[idx] >> 16) != 0;
-    if (idx < V) out[idx] = v ? 1 : 0;
-    const uint32_t m = __ballot_sync(0xffffffffu, v);
-    if ((threadIdx.x & 31) == 0 && m)
-        atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)__popc(m));
-    list_append_block(vis_list, v, (uint32_t)idx, (unsigned long long *)&stats[LVX_ST_VISIBLE]);
+    const int64_t idx0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    uint32_t mask = 0;
+    if (idx0 < V) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(base + idx0);
+        mask = ((w.x >> 16) ? 1u : 0u) | ((w.y >> 16) ? 2u : 0u) | ((w.z >> 16) ? 4u : 0u) | ((w.w >> 16) ? 8u : 0u);
+        *reinterpret_cast<uchar4 *>(out + idx0) = make_uchar4(mask & 1u, (mask >> 1) & 1u, (mask >> 2) & 1u, (mask >> 3) & 1u);
+    }
+    const uint32_t wm = __reduce_add_sync(0xffffffffu, __popc(mask));
+    if ((threadIdx.x & 31) == 0 && wm)
+        atomicAdd((unsigned long long *)&stats[LVX_ST_OCCUPIED], (unsigned long long)wm);
+    list_append_items<4>(vis_list, mask, (uint32_t)idx0, (unsigned long long *)&stats[LVX_ST_VISIBLE]);
 }
 
 // lv/culling.py:103-109: parent = OR of its 8 children
@@ -438,7 +496,7 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     k_march<<<nb, 128, 0, s>>>(solid_bits, vis_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                cam_voxel_host[2], vis_tmp);
     LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
-    k_dilate<<<blocks_for(V, 256), 256, 0, s>>>(base, vis_tmp, res, V, cull_flat, vis_list, stats);
+    k_dilate<<<blocks_for(V / 4, 256), 256, 0, s>>>(base, vis_tmp, res, V, cull_flat, vis_list, stats);
     LVX_LAUNCH_CHECK();
     return or_mips(cull_flat, res, s);
 }
@@ -449,7 +507,7 @@ int lvx_occupied_pyramid(const uint32_t *base, int res, uint8_t *cull_flat, uint
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
     LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
-    k_occupied<<<blocks_for(V, 256), 256, 0, s>>>(base, V, cull_flat, vis_list, stats);
+    k_occupied<<<blocks_for(V / 4, 256), 256, 0, s>>>(base, V, cull_flat, vis_list, stats);
     LVX_LAUNCH_CHECK();
     return or_mips(cull_flat, res, s);
 }

@@ -49,6 +49,32 @@ k_nzmask(const uint32_t *__restrict__ base, const double *__restrict__ lvl, int 
     if ((threadIdx.x & 31) == 0 && i < n) mask[i >> 5] = m;
 }
 
+// Level-0 footprint mask from the one-bit-per-voxel "occupancy non-zero" words (lvx_pack_wide):
+// one thread per 32 cells.  Same result as k_nzmask at level 0 (rl a multiple of 32).
+__global__ void __launch_bounds__(256)
+k_nzmask_bits(const uint32_t *__restrict__ nz, int rl, uint32_t *__restrict__ mask) {
+    const int wpr = rl >> 5;                                   // words per x-row
+    const uint32_t n_words = (uint32_t)wpr * rl * rl;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_words) return;
+    const int w = i % wpr, y = (i / wpr) % rl, z = i / (wpr * rl);
+    uint32_t m = 0xffffffffu;                                  // last row / slice: always set
+    if (y < rl - 1 && z < rl - 1) {
+        m = 0;
+#pragma unroll
+        for (int dz = 0; dz < 2; dz++)
+#pragma unroll
+            for (int dy = 0; dy < 2; dy++) {
+                const uint32_t r = (uint32_t)w + (uint32_t)wpr * ((uint32_t)(y + dy) + (uint32_t)rl * (uint32_t)(z + dz));
+                const uint32_t a = nz[r];
+                const uint32_t nx = w + 1 < wpr ? nz[r + 1] : 0u;
+                m |= a | (a >> 1) | (nx << 31);
+            }
+        if (w == wpr - 1) m |= 0x80000000u;                    // x = rl - 1: always set
+    }
+    mask[i] = m;
+}
+
 // lv/shading.py:72-109; level 0 is read straight from the packed base words
 template <bool CLAMP>
 __device__ __forceinline__ double trilinear(const uint32_t *__restrict__ base, const double *__restrict__ lvl,
@@ -183,7 +209,7 @@ int64_t lvx_shade_scratch_bytes(int64_t n_voxels) {
 
 int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t *vis_list,
               const double *dirs_host, int n_dirs, double tan_ao, const double *light_host, double tan_shadow,
-              float *ao, float *shadow, int fill_ones, void *scratch, void *stream) {
+              float *ao, float *shadow, int fill_ones, const uint32_t *nz_bits, void *scratch, void *stream) {
     if (!pow2(res) || n_dirs < 1 || n_dirs > 15) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
@@ -207,6 +233,10 @@ int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t 
     uint32_t *masks = (uint32_t *)scratch;
     for (int l = 0; l < L.n_levels; l++) {
         const int rl = res >> l;
+        if (l == 0 && nz_bits && rl >= 32) {
+            k_nzmask_bits<<<blocks_for((int64_t)(rl >> 5) * rl * rl, 256), 256, 0, s>>>(nz_bits, rl, masks + P.mask_off[0]);
+            continue;
+        }
         k_nzmask<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(base, mips + P.mip_off[l], l, rl,
                                                                        masks + P.mask_off[l]);
     }

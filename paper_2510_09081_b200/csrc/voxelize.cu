@@ -119,16 +119,22 @@ k_widen(const uint32_t *__restrict__ base, const uint32_t *__restrict__ occ_sat,
 
 __global__ void __launch_bounds__(256)
 k_pack_wide(const unsigned long long *__restrict__ wide, int64_t n, uint32_t *__restrict__ base,
-            uint64_t *__restrict__ stats) {
+            uint32_t *__restrict__ nz_bits, uint64_t *__restrict__ stats) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint64_t sat = 0;
+    bool nz = false;
     if (i < n) {
         const unsigned long long w = wide[i];
         uint64_t c = w >> 32, o = w & 0xFFFFFFFFull;
         if (c > 0xFFFF) { sat = c - 0xFFFF; c = 0xFFFF; }   // lv/voxelizer.py:333-336, 493
         if (o > 0xFFFF) o = 0xFFFF;                          // lv/voxelizer.py:494
         base[i] = (uint32_t)((c << 16) | o);
+        nz = o != 0;
     }
+    // one bit per voxel "level-0 occupancy is non-zero" (32 x-adjacent voxels per word): the cone
+    // tracer's level-0 footprint masks are built from these bits instead of re-reading `base`
+    const uint32_t m = __ballot_sync(0xffffffffu, nz);
+    if (nz_bits && (threadIdx.x & 31) == 0 && i < n) nz_bits[i >> 5] = m;
     sat = warp_sum_u64(sat);
     if ((threadIdx.x & 31) == 0 && sat)
         atomicAdd((unsigned long long *)&stats[LVX_ST_SATURATED], (unsigned long long)sat);
@@ -229,9 +235,10 @@ int lvx_widen(const uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, u
     return LVX_OK;
 }
 
-int lvx_pack_wide(const uint64_t *wide, int64_t n_voxels, uint32_t *base, uint64_t *stats, void *stream) {
+int lvx_pack_wide(const uint64_t *wide, int64_t n_voxels, uint32_t *base, uint32_t *nz_bits, uint64_t *stats, void *stream) {
+    if (nz_bits && (n_voxels & 31)) return LVX_E_ARG;
     k_pack_wide<<<blocks_for(n_voxels, 256), 256, 0, (cudaStream_t)stream>>>(
-        (const unsigned long long *)wide, n_voxels, base, stats);
+        (const unsigned long long *)wide, n_voxels, base, nz_bits, stats);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -100,6 +100,8 @@ class FrameEngine:
             self.need_bits = t.empty(max(V // 32, 1), dtype=t.int32, device=d)
             self.need_list = t.empty(ops.list_words(V), dtype=t.int32, device=d)
         self.wide = None
+        self.nz_bits = None          # per-voxel "occupancy non-zero" bits from the pack pass (level-0 shading mask)
+        self._nz_valid = False
         # Accumulate into 64-bit (count << 32 | occ) words and pack afterwards (lvx_voxelize_wide +
         # lvx_pack_wide) instead of the packed 32-bit word with carry repair (lvx_voxelize).  The wide
         # form never needs the atomic's return value, so it compiles to fire-and-forget RED.64: measured
@@ -194,8 +196,12 @@ class FrameEngine:
                 self.wide = self.torch.empty(self.V, dtype=self.torch.int64, device=self.dev)
             ops.clear(self.wide)
             ops.voxelize_wide(self.lines, self.res, self.r_min, self.method, self.wide, self.stats, b, e)
-            ops.pack_wide(self.wide, self.base, self.stats)
+            if self.nz_bits is None and self.res >= 32:
+                self.nz_bits = self.torch.empty(self.V // 32, dtype=self.torch.int32, device=self.dev)
+            ops.pack_wide(self.wide, self.base, self.stats, self.nz_bits)
+            self._nz_valid = self.nz_bits is not None
         else:
+            self._nz_valid = False
             ops.clear(self.base)
             ops.clear(self.occ_sat)
             ops.voxelize(self.lines, self.res, self.r_min, self.method, self.base, self.occ_sat, self.stats, b, e)
@@ -226,7 +232,7 @@ class FrameEngine:
         demand = self.shading == "demand"
         ops.shade(self.base, self.mips, self.res, self.need_list if demand else self.vis_list, self.dirs,
                   np.tan(AO_HALF_ANGLE), self.light, np.tan(SHADOW_HALF_ANGLE), self.ao, self.shadow,
-                  self.shade_scratch, fill_ones=not demand)
+                  self.shade_scratch, fill_ones=not demand, nz_bits=self.nz_bits if self._nz_valid else None)
 
     def _stage_trace(self, cam, tile=None):
         p = make_params(self.settings, self.lines, self.light, tile, self.w, self.h)
@@ -279,6 +285,7 @@ class FrameEngine:
         self._stage_voxelize(seg_range)
         if after_voxelize is not None:
             after_voxelize(self)
+            self._nz_valid = False          # the hook may replace `base` (multi-GPU merge)
         ev[2].record()
         self._stage_mips(); ev[3].record()
         self._stage_cull(cam); ev[4].record()

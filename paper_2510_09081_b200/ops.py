@@ -153,8 +153,9 @@ def widen(base, occ_sat, wide):
     check(lib().lvx_widen(_ptr(base), _ptr(occ_sat), base.numel(), _ptr(wide), _stream()), "lvx_widen")
 
 
-def pack_wide(wide, base, stats):
-    check(lib().lvx_pack_wide(_ptr(wide), wide.numel(), _ptr(base), _ptr(stats), _stream()), "lvx_pack_wide")
+def pack_wide(wide, base, stats, nz_bits=None):
+    """`nz_bits` (optional i32, V/32): receives one bit per voxel "occupancy non-zero" for `shade`."""
+    check(lib().lvx_pack_wide(_ptr(wide), wide.numel(), _ptr(base), _ptr(nz_bits), _ptr(stats), _stream()), "lvx_pack_wide")
 
 
 def finalize_base(base, occ_sat, stats):
@@ -238,12 +239,12 @@ def shade_scratch_bytes(n_voxels: int) -> int:
     return int(lib().lvx_shade_scratch_bytes(n_voxels))
 
 
-def shade(base, mips, res, vis_list, dirs, tan_ao, light, tan_shadow, ao, shadow, scratch, fill_ones=True):
+def shade(base, mips, res, vis_list, dirs, tan_ao, light, tan_shadow, ao, shadow, scratch, fill_ones=True, nz_bits=None):
     d = np.ascontiguousarray(dirs, dtype=np.float64)
     l, l_p = _dbl3(light)
     check(lib().lvx_shade(_ptr(base), _ptr(mips), res, _ptr(vis_list), d.ctypes.data_as(C.c_void_p),
                           int(d.shape[0]), float(tan_ao), l_p, float(tan_shadow), _ptr(ao), _ptr(shadow),
-                          int(bool(fill_ones)), _ptr(scratch), _stream()), "lvx_shade")
+                          int(bool(fill_ones)), _ptr(nz_bits), _ptr(scratch), _stream()), "lvx_shade")
 
 
 def make_camera_struct(cam, grid) -> N.lvx_camera:
