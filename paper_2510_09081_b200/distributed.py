@@ -85,6 +85,10 @@ class TiledFrame:
         self.tiles = tile_rects(engine.w, engine.h, self.world)
 
     def _merge(self, eng):
+        if eng.use_wide:     # the engine's 64-bit accumulators are sum-reducible as they are; it packs afterwards
+            import torch.distributed as dist
+            dist.all_reduce(eng.wide, op=dist.ReduceOp.SUM, group=self.group)
+            return
         merged, _ = merge_partial_grids(eng.base, self.group)
         eng.base.copy_(merged)
 

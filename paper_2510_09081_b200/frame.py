@@ -189,13 +189,18 @@ class FrameEngine:
         if self._order is not None:
             ops.segment_order(self.lines, self.res, self.order_brick, self._order, self._order_scratch)
 
-    def _stage_voxelize(self, seg_range=None):
+    def _stage_voxelize(self, seg_range=None, after_voxelize=None):
+        """`after_voxelize(engine)`: the multi-GPU exchange hook.  On the 64-bit path it runs between
+        accumulation and packing and sums `engine.wide` across ranks (exact: per-field saturation
+        comes after the sum, lv/voxelizer.py:490-495); on the packed path it runs on the finished `base`."""
         b, e = (0, self.lines.n_segments) if seg_range is None else seg_range
         if self.use_wide:
             if self.wide is None:
                 self.wide = self.torch.empty(self.V, dtype=self.torch.int64, device=self.dev)
             ops.clear(self.wide)
             ops.voxelize_wide(self.lines, self.res, self.r_min, self.method, self.wide, self.stats, b, e)
+            if after_voxelize is not None:
+                after_voxelize(self)
             if self.nz_bits is None and self.res >= 32:
                 self.nz_bits = self.torch.empty(self.V // 32, dtype=self.torch.int32, device=self.dev)
             ops.pack_wide(self.wide, self.base, self.stats, self.nz_bits)
@@ -206,6 +211,8 @@ class FrameEngine:
             ops.clear(self.occ_sat)
             ops.voxelize(self.lines, self.res, self.r_min, self.method, self.base, self.occ_sat, self.stats, b, e)
             ops.finalize_base(self.base, self.occ_sat, self.stats)
+            if after_voxelize is not None:
+                after_voxelize(self)
 
     def _stage_mips(self):
         ops.build_mips(self.base, self.res, self.mips)
@@ -282,10 +289,7 @@ class FrameEngine:
         ops.stats_reset(self.stats)
         ev[0].record()
         self._stage_upload(grid, r_world); ev[1].record()
-        self._stage_voxelize(seg_range)
-        if after_voxelize is not None:
-            after_voxelize(self)
-            self._nz_valid = False          # the hook may replace `base` (multi-GPU merge)
+        self._stage_voxelize(seg_range, after_voxelize)
         ev[2].record()
         self._stage_mips(); ev[3].record()
         self._stage_cull(cam); ev[4].record()

@@ -130,11 +130,20 @@ def clear(t):
     check(lib().lvx_clear(_ptr(t), t.numel() * t.element_size(), _stream()), "lvx_clear")
 
 
+def _shard_segs(lines: DeviceLines, seg_begin, seg_end):
+    """The array a [seg_begin, seg_end) shard indexes.  The brick-grouped processing order is a
+    different permutation on every rank (its ranks inside a brick come from atomics), so shards of a
+    multi-GPU voxelization are cut from the canonical ascending `segs`; only a whole-set pass uses the
+    processing order."""
+    whole = seg_begin == 0 and seg_end == lines.n_segments
+    return lines.proc_segs if whole else lines.segs
+
+
 def voxelize(lines: DeviceLines, res, r_min, method, base, occ_sat, stats, seg_begin=0, seg_end=None):
     """lvx_voxelize into zeroed `base` (V i32) / `occ_sat` (V/32 i32)."""
     seg_end = lines.n_segments if seg_end is None else seg_end
     r = lines.r
-    check(lib().lvx_voxelize(_ptr(lines.verts), _ptr(lines.normals), _ptr(lines.proc_segs), seg_begin, seg_end,
+    check(lib().lvx_voxelize(_ptr(lines.verts), _ptr(lines.normals), _ptr(_shard_segs(lines, seg_begin, seg_end)), seg_begin, seg_end,
                              int(lines.use_clip), r, footprint_radius(r, r_min), float(r_min), res,
                              METHODS[method], _ptr(base), _ptr(occ_sat), _ptr(stats), _stream()),
           "lvx_voxelize")
@@ -143,7 +152,7 @@ def voxelize(lines: DeviceLines, res, r_min, method, base, occ_sat, stats, seg_b
 def voxelize_wide(lines: DeviceLines, res, r_min, method, wide, stats, seg_begin=0, seg_end=None):
     seg_end = lines.n_segments if seg_end is None else seg_end
     r = lines.r
-    check(lib().lvx_voxelize_wide(_ptr(lines.verts), _ptr(lines.normals), _ptr(lines.proc_segs), seg_begin,
+    check(lib().lvx_voxelize_wide(_ptr(lines.verts), _ptr(lines.normals), _ptr(_shard_segs(lines, seg_begin, seg_end)), seg_begin,
                                   seg_end, int(lines.use_clip), r, footprint_radius(r, r_min), float(r_min),
                                   res, METHODS[method], _ptr(wide), _ptr(stats), _stream()),
           "lvx_voxelize_wide")

@@ -359,3 +359,44 @@ def test_engine_variants_identical(lvx, oracle):
     for e, r in ((ea, ra), (eb, rb)):
         assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
         assert r.stats["fragments"] == ref.abuf.total
+
+
+def test_segment_shards_merge_on_engine(lvx, oracle):
+    """Multi-GPU voxelization emulated on one GPU: two engines accumulate disjoint segment shards, the
+    `after_voxelize` hook sums the 64-bit accumulators (what TiledFrame's all-reduce does) and the rest
+    of the frame runs replicated -- the result is the single-GPU frame, bit for bit."""
+    from paper_2510_09081_b200 import distributed as D
+    ls = lvx.generate("grid_diagonals", count=300, length=14.0, domain=20.0)
+    ls = lvx.LineSet(ls.vertices, ls.polyline_offsets, 1.1)
+    res = 32
+    g, r_world = lvx.fit_grid(ls, res)
+    cfg = lvx.PipelineConfig(res=res, width=96, height=64, strategy="vcsv")
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vcsv")
+    b = D.shard_bounds(ls.n_segments, 2)
+    partial = {}
+
+    def engine():
+        e = lvx.FrameEngine(res, 96, 64, strategy="vcsv", keep_rgb=True)
+        e.set_topology(ls.polyline_offsets, ls.n_vertices)
+        e.load_vertices(ls.vertices)
+        return e
+
+    from paper_2510_09081_b200 import ops
+    for rank in range(2):       # what each rank accumulates on its own (upload + voxelize stages only)
+        e = engine()
+        assert e.use_wide
+        ops.stats_reset(e.stats)
+        e._stage_upload(g, r_world)
+        e._stage_voxelize((int(b[rank]), int(b[rank + 1])),
+                          lambda eng, rank=rank: partial.__setitem__(rank, eng.wide.clone()))
+    e = engine()
+    out = e.run(cam, g, r_world, seg_range=(int(b[0]), int(b[1])),
+                after_voxelize=lambda eng: eng.wide.copy_(partial[0] + partial[1]))
+    assert np.array_equal(e.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
+    n = out.stats["fragments"]
+    assert n == ref.abuf.total
+    assert np.array_equal(e.frags[:n].cpu().numpy().view(np.uint32), ref.abuf.fragments)
+    assert np.array_equal(e.cull_flat.cpu().numpy(), ref.culling.flat)
+    assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
+    assert np.array_equal(e.hit_id.cpu().numpy(), ref.image.hit_id)
