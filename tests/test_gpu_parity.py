@@ -400,3 +400,29 @@ def test_segment_shards_merge_on_engine(lvx, oracle):
     assert np.array_equal(e.cull_flat.cpu().numpy(), ref.culling.flat)
     assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
     assert np.array_equal(e.hit_id.cpu().numpy(), ref.image.hit_id)
+
+
+@pytest.mark.parametrize("mode", ["opaque", "transparent"])
+def test_screen_tiles_make_the_full_image(lvx, oracle, mode):
+    """Screen-tile sharding (lvx_render_params.tile_*): tracing the tiles of a 3-way split one after the
+    other fills exactly the image of a single full-frame trace, and the test counts add up."""
+    from paper_2510_09081_b200 import distributed as D
+    ls = lvx.generate("random_streamlines", seed=21, polylines=90, verts_per_line=40)
+    res, w, h = 32, 150, 101          # sizes that are not multiples of the 8x4 warp tile
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=0.35)
+    strategy = "vcsv" if mode == "opaque" else "vsv"
+    cfg = lvx.PipelineConfig(res=res, width=w, height=h, strategy=strategy, mode=mode, alpha=0.4)
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy=strategy, mode=mode, alpha=0.4)
+    e = lvx.FrameEngine(res, w, h, strategy=strategy, mode=mode, alpha=0.4, keep_rgb=True)
+    e.set_topology(ls.polyline_offsets, ls.n_vertices)
+    e.load_vertices(ls.vertices)
+    rgb = np.zeros((h, w, 3)); hit = np.full((h, w), -7, np.int32); tests = 0
+    for (x0, y0, x1, y1) in D.tile_rects(w, h, 3):
+        out = e.run(cam, g, r_world, tile=(x0, y0, x1, y1))
+        rgb[y0:y1, x0:x1] = e.rgb.cpu().numpy()[y0:y1, x0:x1]
+        hit[y0:y1, x0:x1] = e.hit_id.cpu().numpy()[y0:y1, x0:x1]
+        tests += out.stats["ray_capsule_tests"]
+    assert np.array_equal(hit, ref.image.hit_id)
+    assert np.array_equal(rgb, ref.image.rgb)
+    assert tests == ref.image.stats["ray_capsule_tests"]
