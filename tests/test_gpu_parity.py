@@ -426,3 +426,27 @@ def test_screen_tiles_make_the_full_image(lvx, oracle, mode):
     assert np.array_equal(hit, ref.image.hit_id)
     assert np.array_equal(rgb, ref.image.rgb)
     assert tests == ref.image.stats["ray_capsule_tests"]
+
+
+@pytest.mark.parametrize("res,mode", [(4, "opaque"), (8, "transparent"), (16, "opaque")])
+def test_engine_tiny_inputs(lvx, oracle, res, mode):
+    """FrameEngine at the small end: one or two segments, grids below the brick / bit-mask granularity
+    (res < 32), images smaller than one 8x4 warp tile."""
+    v = np.array([[0.1, 0.2, 0.3], [0.9, 0.8, 0.6], [0.5, 0.1, 0.9]], np.float32)
+    ls = lvx.LineSet(v, np.array([0, 3], np.int64), 0.05)
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=0.3) if res > 4 else (lvx.GridDesc(4, np.array([-0.5, -0.5, -0.5]), 0.5), 0.1)
+    strategy = "vcsv" if mode == "opaque" else "vsv"
+    cfg = lvx.PipelineConfig(res=res, width=5, height=3, strategy=strategy, mode=mode, alpha=0.5)
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy=strategy, mode=mode, alpha=0.5)
+    e = lvx.FrameEngine(res, 5, 3, strategy=strategy, mode=mode, alpha=0.5, keep_rgb=True)
+    e.set_topology(ls.polyline_offsets, ls.n_vertices)
+    e.load_vertices(ls.vertices)
+    out = e.run(cam, g, r_world)
+    assert np.array_equal(e.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
+    n = out.stats["fragments"]
+    assert n == ref.abuf.total
+    assert np.array_equal(e.frags[:n].cpu().numpy().view(np.uint32), ref.abuf.fragments)
+    assert np.array_equal(e.hit_id.cpu().numpy(), ref.image.hit_id)
+    assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
+    assert out.stats["ray_capsule_tests"] == ref.image.stats["ray_capsule_tests"]
