@@ -633,9 +633,9 @@ k_render_opaque_coop(const RenderArgs A) {
                     }
                 } else {
                     // Shading on demand: record the hit, and request AO/shadow for the (visible) voxels
-                    // its trilinear lookup will read (lv/raytracer.py:368-390).
-                    uint32_t items[8];
-                    int n_items = 0;
+                    // its trilinear lookup will read (lv/raytracer.py:368-390).  The request is a bit
+                    // per voxel set with a fire-and-forget atomic; k_need_list compacts the bits into
+                    // the list the cone tracer walks.
                     if (done) {
                         const int64_t pix = (int64_t)py * w + px;
                         A.hit_t[pix] = best_t;
@@ -649,34 +649,9 @@ k_render_opaque_coop(const RenderArgs A) {
                                 const int Y = min(max(iy + ((k >> 1) & 1), 0), res - 1);
                                 const int Z = min(max(iz + (k >> 2), 0), res - 1);
                                 const uint32_t idx = (uint32_t)X + (uint32_t)res * ((uint32_t)Y + (uint32_t)res * (uint32_t)Z);
-                                bool fresh = false;
-                                if (A.march[idx] == 255) {
-                                    const uint32_t bit = 1u << (idx & 31);
-                                    fresh = (atomicOr(&A.need_bits[idx >> 5], bit) & bit) == 0;
-                                }
-                                items[k] = idx;
-                                if (fresh) n_items |= 1 << k;
+                                if (A.march[idx] == 255) atomicOr(&A.need_bits[idx >> 5], 1u << (idx & 31));
                             }
                         }
-                    }
-                    // one global atomic per warp: exclusive scan of the per-lane counts
-                    const uint32_t mine = __popc((uint32_t)n_items);
-                    uint32_t incl = mine;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t v = __shfl_up_sync(LVX_FULL, incl, o);
-                        if (lane >= o) incl += v;
-                    }
-                    const uint32_t total = __shfl_sync(LVX_FULL, incl, 31);
-                    if (total) {
-                        unsigned long long b = 0;
-                        if (lane == 0)
-                            b = atomicAdd(reinterpret_cast<unsigned long long *>(A.need_list), (unsigned long long)total);
-                        b = __shfl_sync(LVX_FULL, b, 0);
-                        uint32_t pos = (uint32_t)b + incl - mine;
-#pragma unroll
-                        for (int k = 0; k < 8; k++)
-                            if (n_items & (1 << k)) A.need_list[LVX_LIST_HDR + pos++] = items[k];
                     }
                 }
                 if (done) has = false;
@@ -1084,6 +1059,46 @@ k_render_transparent_coop(const RenderArgs A) {
 #endif
 }
 
+// Requested voxels (one bit each) -> list, ascending inside every block's chunk: block scan of the
+// per-thread popcounts, one atomic on the list counter per block.
+__global__ void __launch_bounds__(256)
+k_need_list(const uint32_t *__restrict__ need_bits, int64_t n_words, uint32_t *__restrict__ need_list) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ unsigned long long s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t m = i < n_words ? need_bits[i] : 0u;
+    const uint32_t c = __popc(m);
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(LVX_FULL, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t wv = lane < 8 ? s_warp[lane] : 0;
+        uint32_t wi = wv;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(LVX_FULL, wi, o);
+            if (lane >= o) wi += v;
+        }
+        if (lane < 8) s_warp[lane] = wi - wv;
+        if (lane == 7 && wi) s_base = atomicAdd(reinterpret_cast<unsigned long long *>(need_list), (unsigned long long)wi);
+    }
+    __syncthreads();
+    if (c) {
+        uint64_t slot = LVX_LIST_HDR + s_base + s_warp[warp] + (inc - c);
+        while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            need_list[slot++] = (uint32_t)(i * 32 + bit);
+        }
+    }
+}
+
 // Second half of shading on demand: one thread per pixel re-derives its ray (same expressions,
 // hence the same bits, as the trace kernel), and shades the recorded hit.
 __global__ void __launch_bounds__(128)
@@ -1209,6 +1224,10 @@ int lvx_trace_hits(const double *verts, const float *verts_f, const double *norm
     static int per_sm = 0;
     if (!per_sm) LVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_opaque_coop<true>, RC_WARPS * 32, 0));
     k_render_opaque_coop<true><<<persistent_grid(tw, th, per_sm), RC_WARPS * 32, 0, s>>>(A);
+    {
+        const int64_t n_words = (V + 31) / 32;
+        k_need_list<<<blocks_for(n_words, 256), 256, 0, s>>>(need_bits, n_words, need_list);
+    }
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }
