@@ -218,7 +218,9 @@ class TightIndex:
         self.capacity = int(capacity)
         self.frags = torch.empty(max(self.capacity, 1), dtype=torch.int32, device=device)
         self.slot = torch.empty(max(self.capacity, 1), dtype=torch.int16, device=device)
-        self.cnt = torch.empty(int(n_voxels), dtype=torch.int16, device=device)
+        # zeroed once: the tracer fetches cnt[v] together with the march byte of EVERY voxel it steps through
+        # and only uses it where the voxel is listed (which the ordering pass has written)
+        self.cnt = torch.zeros(int(n_voxels), dtype=torch.int16, device=device)
 
     def ptrs(self):
         return _ptr(self.frags), _ptr(self.slot), _ptr(self.cnt)
