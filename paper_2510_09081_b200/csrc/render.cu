@@ -78,7 +78,12 @@ __device__ __forceinline__ bool surely_misses_f32(float Cx, float Cy, float Cz, 
 // The candidate loops are deliberately NOT unrolled: the routine is executed by few lanes at a time and
 // the cooperative kernels were stalling on instruction fetch (ncu: 26 % no_instruction stalls at
 // ~7000 SASS instructions per kernel); rolled loops execute the same operations in the same order.
-__device__ double ray_capsule(double ox, double oy, double oz, double dx, double dy, double dz, const Capsule &c) {
+// `sub` < 0: all candidate surfaces.  `sub` = 0 / 1: only the first / second candidate of each pair
+// (near / far cylinder root, end sphere a / b, clip plane a / b) -- two lanes then share one test and
+// the smaller of their results is the routine's result (a minimum does not depend on the order).
+__device__ double ray_capsule(double ox, double oy, double oz, double dx, double dy, double dz, const Capsule &c,
+                              int sub = -1) {
+    const int k0 = sub < 0 ? 0 : sub, k1 = sub < 0 ? 2 : sub + 1;
     const double ax = c.a.x, ay = c.a.y, az = c.a.z, bx = c.b.x, by = c.b.y, bz = c.b.z, r = c.r;
     const double bax = bx - ax, bay = by - ay, baz = bz - az;
     const double oax = ox - ax, oay = oy - ay, oaz = oz - az;
@@ -98,7 +103,7 @@ __device__ double ray_capsule(double ox, double oy, double oz, double dx, double
             if (disc >= 0.0) {
                 const double sq = sqrt(disc);
 #pragma unroll 1
-                for (int k = 0; k < 2; k++) {
+                for (int k = k0; k < k1; k++) {
                     const double t = (-b_ + (k ? sq : -sq)) / a_;
                     if (t >= 0.0) {
                         const double y = baoa + t * bard;
@@ -112,7 +117,7 @@ __device__ double ray_capsule(double ox, double oy, double oz, double dx, double
         }
     }
 #pragma unroll 1
-    for (int cap = 0; cap < 2; cap++) {
+    for (int cap = k0; cap < k1; cap++) {
         const double cx = cap ? bx : ax, cy = cap ? by : ay, cz = cap ? bz : az;
         const double ocx = ox - cx, ocy = oy - cy, ocz = oz - cz;
         const double bq = ocx * dx + ocy * dy + ocz * dz;
@@ -133,7 +138,7 @@ __device__ double ray_capsule(double ox, double oy, double oz, double dx, double
     }
     if (c.clip) {
 #pragma unroll 1
-        for (int pl = 0; pl < 2; pl++) {
+        for (int pl = k0; pl < k1; pl++) {
             const double nx = pl ? c.n1.x : c.n0.x, ny = pl ? c.n1.y : c.n0.y, nz = pl ? c.n1.z : c.n0.z;
             const double qx = pl ? bx : ax, qy = pl ? by : ay, qz = pl ? bz : az;
             const double dn = dx * nx + dy * ny + dz * nz;
@@ -372,8 +377,9 @@ struct PairQueues {
 #define LVX_RS_SLOT(rs) ((rs) & 0xFFFFu)
 
 // Runs stages A-C for one round over the lists S.fo/S.n[0..n_ord) of every lane (n_ord <= M);
-// `stage_c(valid, rs, seg, last)` is called with 32 (or fewer, at the end) queue-B entries; the
-// final call has last = true (and possibly no valid entry at all).
+// `stage_c(valid, rs, seg, last, sub)` is called with 32 (or fewer, at the end) queue-B entries; the
+// final call has last = true (and possibly no valid entry at all).  sub >= 0: lanes 2e and 2e+1 both
+// hold entry e and evaluate candidate subset `sub` (see ray_capsule); the callee merges the pair.
 // Written as one loop with a single call site per stage: the stages are large (stage C inlines the
 // f64 intersection routine), and every extra inlined copy costs instruction-cache capacity.
 template <int M, class F>
@@ -389,12 +395,16 @@ __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S,
         const bool tail = a_done && qa == 0;
         if (qb >= 32 || tail) {
             const uint32_t take = qb < 32 ? qb : 32, base = qb - take;
-            const bool valid = (uint32_t)lane < take;
-            const uint32_t rs = valid ? S.qb_rs[base + lane] : 0, ii = valid ? S.qb_i[base + lane] : 0;
+            // a batch of at most 16 pairs is spread over two lanes per pair: each lane evaluates half
+            // of the candidate surfaces of the f64 routine (ray_capsule's `sub`)
+            const bool split = take <= 16;
+            const uint32_t e = split ? (uint32_t)lane >> 1 : (uint32_t)lane;
+            const bool valid = e < take;
+            const uint32_t rs = valid ? S.qb_rs[base + e] : 0, ii = valid ? S.qb_i[base + e] : 0;
             qb = base;
             __syncwarp();
             const bool fin = tail && qb == 0;
-            stage_c(valid, rs, ii, fin);
+            stage_c(valid, rs, ii, fin, split ? (lane & 1) : -1);
             if (fin) break;
             continue;
         }
@@ -699,14 +709,22 @@ k_render_opaque_coop(const RenderArgs A) {
         // best hit of this lane's ray in this round: lowest ordinal, then min t, then lowest slot
         double cur_t = -1.0;
         uint32_t cur_ms = 0xffffffffu, cur_i = 0;      // (ordinal << 16) | slot
-        run_pairs<M>(A, S.q, Mr, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool) {
+        run_pairs<M>(A, S.q, Mr, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool, int sub) {
             bool hit = false;
-            double ht = 0.0;
+            double ht = -1.0;
             const uint32_t hr = LVX_RS_RAY(rs), hm_ = LVX_RS_ORD(rs);
+            double ddx = 0.0, ddy = 0.0, ddz = 1.0;
             if (valid) {
-                const double ddx = S.q.dir[0][hr], ddy = S.q.dir[1][hr], ddz = S.q.dir[2][hr];
+                ddx = S.q.dir[0][hr]; ddy = S.q.dir[1][hr]; ddz = S.q.dir[2][hr];
                 const Capsule c = load_capsule(A.verts, A.normals, (int64_t)ii, r, clip);
-                ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
+                ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c, sub);
+            }
+            if (sub >= 0) {     // two lanes per pair: the smaller admissible t of the two halves, kept on the even lane
+                const double other = __shfl_xor_sync(LVX_FULL, ht, 1);
+                ht = ht < 0.0 ? other : (other < 0.0 ? ht : fmin(ht, other));
+                if (lane & 1) valid = false;
+            }
+            if (valid) {
                 if (ht >= 0.0) {   // lv/raytracer.py:446-452: the hit must lie in the voxel being visited
                     const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
                     hit = hx == S.q.vox[hm_][0][hr] && hy == S.q.vox[hm_][1][hr] && hz == S.q.vox[hm_][2][hr];
@@ -970,15 +988,23 @@ k_render_transparent_coop(const RenderArgs A) {
             __syncwarp();
         };
 
-        run_pairs<M>(A, S.q, M, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool fin) {
+        run_pairs<M>(A, S.q, M, lane, lt_mask, R2f, [&](bool valid, uint32_t rs, uint32_t ii, bool fin, int sub) {
             bool hit = false;
             uint32_t hkey = 0;
-            double ht = 0.0;
+            double ht = -1.0;
             const uint32_t hr = LVX_RS_RAY(rs), hm_ = LVX_RS_ORD(rs);
+            double ddx = 0.0, ddy = 0.0, ddz = 1.0;
             if (valid) {
-                const double ddx = S.q.dir[0][hr], ddy = S.q.dir[1][hr], ddz = S.q.dir[2][hr];
+                ddx = S.q.dir[0][hr]; ddy = S.q.dir[1][hr]; ddz = S.q.dir[2][hr];
                 const Capsule c = load_capsule(A.verts, A.normals, (int64_t)ii, r, clip);
-                ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c);
+                ht = ray_capsule(ox, oy, oz, ddx, ddy, ddz, c, sub);
+            }
+            if (sub >= 0) {     // two lanes per pair (see run_pairs): merge, keep the even lane
+                const double other = __shfl_xor_sync(LVX_FULL, ht, 1);
+                ht = ht < 0.0 ? other : (other < 0.0 ? ht : fmin(ht, other));
+                if (lane & 1) valid = false;
+            }
+            if (valid) {
                 if (ht >= 0.0) {
                     const int hx = (int)floor(ox + ddx * ht), hy = (int)floor(oy + ddy * ht), hz = (int)floor(oz + ddz * ht);
                     hit = hx == S.q.vox[hm_][0][hr] && hy == S.q.vox[hm_][1][hr] && hz == S.q.vox[hm_][2][hr];
