@@ -583,12 +583,8 @@ __device__ __forceinline__ bool assign_pixels(const RenderArgs &A, TileQueue &Q,
 }
 
 // ----------------------------------------------------------------------------- opaque
-#ifndef LVX_SPEC_MAX
-#define LVX_SPEC_MAX LVX_SPEC   // look-ahead when only a few rays of the tile are still marching: same as the
-                                // fixed depth (a deeper look-ahead for sparse rounds was measured and did not pay)
-#endif
 struct WarpShared {
-    PairQueues<LVX_SPEC_MAX> q;
+    PairQueues<LVX_SPEC> q;
     double hit_t[32];
     uint32_t hit_rs[32], hit_i[32];
 };
@@ -599,7 +595,7 @@ struct WarpShared {
 template <bool DEFER>
 __global__ void __launch_bounds__(RC_WARPS * 32, LVX_RC_MINB)
 k_render_opaque_coop(const RenderArgs A) {
-    constexpr int M = LVX_SPEC_MAX;
+    constexpr int M = LVX_SPEC;
     __shared__ __align__(16) unsigned char smem_raw[sizeof(WarpShared) * RC_WARPS];
     uint32_t lane_u = threadIdx.x & 31u, soff = (threadIdx.x >> 5) * (uint32_t)sizeof(WarpShared);
     LVX_PIN(lane_u); LVX_PIN(soff);
@@ -682,10 +678,8 @@ k_render_opaque_coop(const RenderArgs A) {
             }
         }
         // ---- 1. record the next Mr occupied voxels (lv/raytracer.py:475-482, 506-509); every lane
-        // steps its own DDA until it has Mr of them or leaves the grid.  A round has fixed costs
-        // (a partly filled f64 batch above all), so the fewer rays are left, the deeper they look ahead.
-        const int n_act = __popc(am);
-        const int Mr = n_act > 16 ? LVX_SPEC : (n_act > 8 ? min(2 * LVX_SPEC, M) : M);
+        // steps its own DDA until it has Mr of them or leaves the grid
+        constexpr int Mr = M;
         bool leaving = false, go = active;
         int n_vox = 0;
         double tcur = t;
