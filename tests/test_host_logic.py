@@ -91,3 +91,16 @@ def test_grid_desc_rules():
     g = lvx.GridDesc(64, np.array([1.0, 2.0, 3.0]), 0.5)
     assert g.n_levels == 7 and g.flat_index(1, 2, 3) == 1 + 64 * (2 + 64 * 3)
     assert np.allclose(g.to_world(g.to_voxel([2.0, 3.0, 4.0])), [2.0, 3.0, 4.0])
+
+
+def test_shards_index_the_canonical_segment_array():
+    """A multi-GPU shard [b, e) must mean the same segments on every rank: the brick-grouped processing
+    order is a per-rank permutation, so only a whole-set pass may use it (ops._shard_segs)."""
+    from paper_2510_09081_b200 import ops
+    lines = ops.DeviceLines(None, None, None, None, None, "SEGS", 110, 10, 0.2, None, 0.1, order="ORDER")
+    assert lines.n_segments == 100
+    assert ops._shard_segs(lines, 0, 100) == "ORDER"
+    assert ops._shard_segs(lines, 0, 50) == "SEGS"
+    assert ops._shard_segs(lines, 50, 100) == "SEGS"
+    lines.order = None
+    assert ops._shard_segs(lines, 0, 100) == "SEGS"
