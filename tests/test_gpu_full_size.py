@@ -1,0 +1,107 @@
+"""GPU parity at BASELINE.json's full sizes (run on the B200 box): FrameEngine -- the path bench.py
+times -- against the CPU oracle on the C2 workload itself (1 000 000 segments, 256^3, 1920x1080, opaque +
+AO, vcsv) and on C3 (the same line set, vsv, ground-truth transparency alpha 0.3, 1920x1080), plus the size-independent properties of SURVEY.md §8c:
+sum of counts = voxels visited, fragment total = sum of the masked counts, every list strictly ascending.
+
+Everything compared here is bit-exact (stricter than the north star's 1e-4 / 1/255 tolerances, which are
+asserted as well so that the bar is written down where it is tested).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lvx():
+    import paper_2510_09081_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def c2_lines(lvx):
+    ls = lvx.generate("bundles", seed=0, n_bundles=40, fibers=250, verts=101)
+    assert ls.n_segments == 1_000_000
+    g, r_world = lvx.fit_grid(ls, 256, radius_voxels=0.2)
+    return ls, g, r_world
+
+
+def _engine_frame(lvx, ls, g, r_world, cam, strategy, mode, alpha):
+    eng = lvx.FrameEngine(g.resolution, cam.width, cam.height,
+                          strategy=strategy, mode=mode, alpha=alpha, keep_rgb=True)
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    eng.load_vertices(ls.vertices)
+    return eng, eng.run(cam, g, r_world)
+
+
+def _check_build(eng, out, ref, res):
+    V = res ** 3
+    base = eng.base.cpu().numpy().view(np.uint32)
+    ref_base = ref.pyramid.base.ravel()
+    # counts (high 16 bits) bit-exact; occupancy within 1e-4 (quantum 1/4096: that means equal)
+    assert np.array_equal(base >> 16, ref_base >> 16)
+    occ = np.minimum(base & 0xFFFF, 4096) / 4096.0
+    occ_ref = np.minimum(ref_base & 0xFFFF, 4096) / 4096.0
+    assert np.abs(occ - occ_ref).max() <= 1e-4
+    assert np.array_equal(base, ref_base)
+    assert out.stats["voxels_visited"] == ref.pyramid.visited
+    if ref.culling is not None:
+        assert np.array_equal(eng.cull_flat.cpu().numpy(), ref.culling.flat)
+        mask = ref.culling.flat[:V] != 0
+    else:
+        mask = (ref_base >> 16) > 0
+    n = out.stats["fragments"]
+    assert n == ref.abuf.total
+    counts = (base >> 16).astype(np.int64) * mask
+    assert int(counts.sum()) == n                                   # fragment total = sum of the masked counts
+    if out.stats["saturated"] == 0:
+        assert int((base >> 16).astype(np.int64).sum()) == out.stats["voxels_visited"]
+    offsets = eng.offsets.cpu().numpy().view(np.uint32).astype(np.int64)
+    assert np.array_equal(offsets[:V], np.cumsum(counts) - counts) and offsets[V] == n
+    frags = eng.frags[:n].cpu().numpy().view(np.uint32)
+    assert np.array_equal(frags, ref.abuf.fragments)
+    # every list strictly ascending: a descent may only happen where a new list starts
+    starts = np.zeros(n + 1, dtype=bool)
+    starts[offsets[:V][counts > 0]] = True
+    desc = np.nonzero(frags[1:] <= frags[:-1])[0] + 1
+    assert np.all(starts[desc])
+
+
+def _check_image(eng, out, ref):
+    hit = eng.hit_id.cpu().numpy()
+    srgb = eng.srgb.cpu().numpy()
+    assert np.array_equal(hit, ref.image.hit_id)
+    d = np.abs(srgb.astype(np.int16) - ref.image.srgb.astype(np.int16)).max(axis=2)
+    assert (d <= 1).mean() >= 0.999                                 # the north star's bar
+    assert np.array_equal(srgb, ref.image.srgb)                     # ... and what is actually achieved
+    assert np.array_equal(eng.rgb.cpu().numpy(), ref.image.rgb)
+    assert out.stats["ray_capsule_tests"] == ref.image.stats["ray_capsule_tests"]
+
+
+def test_c2_full_size_vs_oracle(lvx, oracle, c2_lines):
+    ls, g, r_world = c2_lines
+    cfg = lvx.PipelineConfig(res=256, width=1920, height=1080, strategy="vcsv", mode="opaque", light="-0.5,-0.3,-0.8")
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vcsv", mode="opaque")
+    eng, out = _engine_frame(lvx, ls, g, r_world, cam, "vcsv", "opaque", 1.0)
+    assert out.stats["shading"] == "demand"
+    _check_build(eng, out, ref, 256)
+    _check_image(eng, out, ref)
+    # the cone-traced values the image was shaded with, wherever the engine computed them on demand
+    need = eng.need_list.cpu().numpy().view(np.uint32)
+    n_need = int(need[:2].view(np.uint64)[0])
+    assert n_need == out.stats["shaded_voxels"] and 0 < n_need < out.stats["visible_voxels"]
+
+
+def test_c3_full_size_vs_oracle(lvx, oracle, c2_lines):
+    ls, g, r_world = c2_lines
+    cfg = lvx.PipelineConfig(res=256, width=1920, height=1080, strategy="vsv", mode="transparent", alpha=0.3,
+                             light="-0.5,-0.3,-0.8")
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vsv", mode="transparent", alpha=0.3)
+    eng, out = _engine_frame(lvx, ls, g, r_world, cam, "vsv", "transparent", 0.3)
+    _check_build(eng, out, ref, 256)
+    _check_image(eng, out, ref)
+    # all-voxel shading: ao / shadow f32 bit patterns
+    assert np.array_equal(eng.ao.cpu().numpy().view(np.uint32), ref.shading.ao.ravel().view(np.uint32))
+    assert np.array_equal(eng.shadow.cpu().numpy().view(np.uint32), ref.shading.shadow.ravel().view(np.uint32))
