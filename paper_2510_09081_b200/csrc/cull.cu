@@ -13,6 +13,8 @@ namespace lvx {
 #define LVX_BRICK 8        // coarse "may contain a blocker" bricks for the visibility march
 #define LVX_SUPER 32       // and a coarser level above them
 #define LVX_SOLID_CAP 1024 // solid voxels listed individually for the per-super-brick shadow test
+#define LVX_SB_ROW 128     // words per super-brick row: [number of shadowing solid voxels][up to 127 of them]
+#define LVX_SB_CAP (LVX_SB_ROW - 1)
 
 __host__ __device__ inline int64_t brick_words(int res, int B) {
     const int64_t rb = (res + B - 1) / B;
@@ -197,18 +199,24 @@ __device__ __forceinline__ bool coarse_may_hit(const uint32_t *__restrict__ bits
 // voxels (512 x 58 on C2) -- and the per-voxel brick walks then run only inside flagged super-bricks.
 __global__ void __launch_bounds__(64)
 k_superbrick_shadow(const uint32_t *__restrict__ solid_list, int res, float cx, float cy, float cz,
-                    uint8_t *__restrict__ sb_flag) {
+                    uint8_t *__restrict__ sb_flag, uint32_t *__restrict__ sb_rows) {
     // one block of 64 threads per super-brick, the solid voxels dealt out to the threads
+    __shared__ uint32_t s_n;
     const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
     const int sb = blockIdx.x;
+    uint32_t *row = sb_rows + (size_t)sb * LVX_SB_ROW;
     const uint32_t n_all = solid_list[0];
-    if (n_all > LVX_SOLID_CAP) { if (threadIdx.x == 0) sb_flag[sb] = 1; return; }      // too many to list: no shortcut
+    if (n_all > LVX_SOLID_CAP) {      // too many to list: no shortcut
+        if (threadIdx.x == 0) { sb_flag[sb] = 1; row[0] = 0xFFFFFFFFu; }
+        return;
+    }
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
     const float c[3] = {cx, cy, cz};
     const int b3[3] = {sb % rs, (sb / rs) % rs, sb / (rs * rs)};
     float blo[3], bhi[3];
 #pragma unroll
     for (int a = 0; a < 3; a++) { blo[a] = (float)(b3[a] * LVX_SUPER); bhi[a] = fminf((float)((b3[a] + 1) * LVX_SUPER), (float)res); }
-    int flag = 0;
     for (uint32_t k = threadIdx.x; k < n_all; k += blockDim.x) {
         const uint32_t v = solid_list[LVX_LIST_HDR + k];
         const int s3[3] = {(int)(v % res), (int)((v / res) % res), (int)(v / ((uint32_t)res * res))};
@@ -231,10 +239,76 @@ k_superbrick_shadow(const uint32_t *__restrict__ solid_list, int res, float cx, 
                 else if (g0 < flo && g1 >= flo) u0 = fmaxf(u0, __fdividef(flo - g0, g1 - g0) - 1e-3f);
             }
         }
-        if (u0 <= u1) flag = 1;
+        if (u0 <= u1) {     // this solid voxel's shadow reaches into the super-brick: keep it for the per-voxel test
+            const uint32_t slot = atomicAdd(&s_n, 1u);
+            if (slot < LVX_SB_CAP) row[1 + slot] = v;
+        }
     }
-    flag = __syncthreads_or(flag);
-    if (threadIdx.x == 0) sb_flag[sb] = (uint8_t)(flag != 0);
+    __syncthreads();
+    if (threadIdx.x == 0) { sb_flag[sb] = (uint8_t)(s_n != 0); row[0] = s_n; }
+}
+
+// Per-voxel test against the solid voxels kept for the voxel's super-brick.  Returns 0 = visible,
+// 1 = blocked, 2 = undecided (the literal march decides).
+//  * The literal march (march_blocked) can only be stopped by a solid voxel S that it visits, and every
+//    voxel it visits touches the segment centre -> camera: an f32 slab test against S dilated by 1.5
+//    voxels (the margin of the super-brick test) discards the solid voxels that cannot matter.
+//  * For the others the segment o + t (c - o) is clipped in f64 against S shrunk and S grown by 1e-6.
+//    If it meets the shrunk cube before t = 1 - 1e-9 it stays inside S for a parameter interval of
+//    >= 1e-9, a thousand times the rounding the march's accumulated crossing parameters can carry
+//    (<= ~600 additions of ulp-accurate terms), so the march is in S after the step that enters it --
+//    and it cannot have ended earlier: it leaves the grid or reaches the camera's voxel only after S
+//    (S is in the grid, and the segment ends inside the camera's voxel).  If it misses the grown cube
+//    (or only meets it beyond t = 1 + 1e-9) the march cannot visit S.  In between: undecided.
+//    S = the voxel itself and S = the camera's voxel never block (lv/culling.py:176-186).
+__device__ __forceinline__ int listed_solid_blocks(const uint32_t *__restrict__ row, uint32_t n, int res,
+                                                   int x, int y, int z, double cx, double cy, double cz) {
+    const float of[3] = {x + 0.5f, y + 0.5f, z + 0.5f};
+    const float df[3] = {(float)cx - of[0], (float)cy - of[1], (float)cz - of[2]};
+    float inv[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) inv[a] = df[a] != 0.f ? __fdividef(1.f, df[a]) : 0.f;
+    const int self3[3] = {x, y, z};
+    const int cam3[3] = {(int)floor(cx), (int)floor(cy), (int)floor(cz)};
+    const double o[3] = {x + 0.5, y + 0.5, z + 0.5};
+    const double d[3] = {cx - o[0], cy - o[1], cz - o[2]};
+    int result = 0;
+    for (uint32_t k = 0; k < n; k++) {
+        const uint32_t v = row[1 + k];
+        const int s3[3] = {(int)(v % res), (int)((v / res) % res), (int)(v / ((uint32_t)res * res))};
+        float t0 = 0.f, t1 = 1.f;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            const float lo = (float)s3[a] - 1.5f - of[a], hi = (float)s3[a] + 2.5f - of[a];
+            if (df[a] == 0.f) { if (lo > 0.f || hi < 0.f) t1 = -1.f; }
+            else {
+                const float ta = lo * inv[a], tb = hi * inv[a];
+                t0 = fmaxf(t0, fminf(ta, tb)); t1 = fminf(t1, fmaxf(ta, tb));
+            }
+        }
+        if (!(t0 <= t1 + 1e-3f)) continue;                     // the march cannot come near S
+        if (s3[0] == self3[0] && s3[1] == self3[1] && s3[2] == self3[2]) continue;
+        if (s3[0] == cam3[0] && s3[1] == cam3[1] && s3[2] == cam3[2]) continue;
+        // f64: entry/exit parameters for the shrunk (sure) and the grown (maybe) cube
+        double si = 0.0, so = 1.0 - 1e-9, gi = 0.0, go = 1.0 + 1e-9;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+            const double lo = (double)s3[a] - o[a], hi = lo + 1.0;
+            if (d[a] == 0.0) {
+                if (!(lo + 1e-6 < 0.0 && 0.0 < hi - 1e-6)) so = -1.0;
+                if (!(lo - 1e-6 < 0.0 && 0.0 < hi + 1e-6)) go = -1.0;
+            } else {
+                const double id = 1.0 / d[a];
+                const double sa = (lo + 1e-6) * id, sb = (hi - 1e-6) * id;
+                const double ga = (lo - 1e-6) * id, gb = (hi + 1e-6) * id;
+                si = fmax(si, fmin(sa, sb)); so = fmin(so, fmax(sa, sb));
+                gi = fmax(gi, fmin(ga, gb)); go = fmin(go, fmax(ga, gb));
+            }
+        }
+        if (si <= so) return 1;
+        if (gi <= go) result = 2;
+    }
+    return result;
 }
 
 // lv/culling.py:191-200.  When the frame has no solid voxel at all nothing can block, so every
@@ -243,7 +317,7 @@ k_superbrick_shadow(const uint32_t *__restrict__ solid_list, int res, float cx, 
 // appended to `march_list`; everything else is visible.
 __global__ void __launch_bounds__(128)
 k_visibility(const uint32_t *__restrict__ bricks, const uint8_t *__restrict__ sb_flag,
-             const uint32_t *__restrict__ occ_list, int res,
+             const uint32_t *__restrict__ sb_rows, const uint32_t *__restrict__ occ_list, int res,
              double cx, double cy, double cz, const uint64_t *__restrict__ stats,
              uint8_t *__restrict__ vis, uint32_t *__restrict__ march_list) {
     const int64_t n = (int64_t)stats[LVX_ST_OCCUPIED];
@@ -252,23 +326,33 @@ k_visibility(const uint32_t *__restrict__ bricks, const uint8_t *__restrict__ sb
     const int64_t n_iter = (n + stride - 1) / stride;
     for (int64_t it = 0; it < n_iter; it++) {
         const int64_t e = it * stride + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        bool may_hit = false;
+        bool may_hit = false, blocked = false;
         uint32_t idx = 0;
         if (e < n) {
             idx = occ_list[e];
             const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
             const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
-            if (any_solid && sb_flag[(x / LVX_SUPER) + rs * ((y / LVX_SUPER) + rs * (z / LVX_SUPER))]) {
-                // Only a solid voxel can block.  Walk the segment centre->camera through the
-                // 32^3-voxel super-bricks, then the 8^3 bricks.
+            const int sb = (x / LVX_SUPER) + rs * ((y / LVX_SUPER) + rs * (z / LVX_SUPER));
+            if (any_solid && sb_flag[sb]) {
+                // Only a solid voxel can block.
                 const float ox = x + 0.5f, oy = y + 0.5f, oz = z + 0.5f;
-                may_hit = coarse_may_hit(bricks + brick_words(res, LVX_BRICK), (res + LVX_SUPER - 1) / LVX_SUPER,
-                                         LVX_SUPER, ox, oy, oz, (float)cx, (float)cy, (float)cz);
-                if (may_hit)
-                    may_hit = coarse_may_hit(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz,
-                                             (float)cx, (float)cy, (float)cz);
+                const uint32_t *row = sb_rows + (size_t)sb * LVX_SB_ROW;
+                const uint32_t n_row = row[0];
+                if (n_row <= LVX_SB_CAP) {
+                    // few solid voxels shadow this super-brick: decide against each of them in closed form
+                    const int r = listed_solid_blocks(row, n_row, res, x, y, z, cx, cy, cz);
+                    blocked = r == 1;
+                    may_hit = r == 2;
+                } else {
+                    // walk the segment centre->camera through the 32^3-voxel super-bricks, then the 8^3 bricks
+                    may_hit = coarse_may_hit(bricks + brick_words(res, LVX_BRICK), (res + LVX_SUPER - 1) / LVX_SUPER,
+                                             LVX_SUPER, ox, oy, oz, (float)cx, (float)cy, (float)cz);
+                    if (may_hit)
+                        may_hit = coarse_may_hit(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz,
+                                                 (float)cx, (float)cy, (float)cz);
+                }
             }
-            if (!may_hit) vis[idx] = 1;
+            if (!may_hit && !blocked) vis[idx] = 1;
         }
         list_append_block(march_list, may_hit, idx);
     }
@@ -467,7 +551,8 @@ int64_t lvx_cull_scratch_words(int res) {
     const int64_t V = (int64_t)res * res * res;
     const int64_t rs = (res + LVX_SUPER - 1) / LVX_SUPER;
     return (V + 31) / 32 + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER)
-           + (LVX_LIST_HDR + LVX_SOLID_CAP) + (rs * rs * rs + 3) / 4 + V;   // + solid list, super-brick flags, occupied-voxel list
+           + (LVX_LIST_HDR + LVX_SOLID_CAP) + (rs * rs * rs + 3) / 4 + V    // + solid list, super-brick flags, occupied-voxel list
+           + rs * rs * rs * LVX_SB_ROW;                                     // + solid voxels shadowing each super-brick
 }
 
 int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32_t *solid_bits,
@@ -476,22 +561,23 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
     // solid_bits scratch layout: [V/32 words of solid bits][8^3-brick flags][32^3-brick flags][solid list]
-    // [super-brick shadow flags][V: occupied list]
+    // [super-brick shadow flags][V: occupied list][super-brick rows]
     uint32_t *bricks = solid_bits + (V + 31) / 32;
     uint32_t *solid_list = bricks + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER);
     LVX_CUDA(cudaMemsetAsync(bricks, 0, (size_t)(brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER) + LVX_LIST_HDR) * 4, s));
     const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
     uint8_t *sb_flag = reinterpret_cast<uint8_t *>(solid_list + LVX_LIST_HDR + LVX_SOLID_CAP);
     uint32_t *occ_list = solid_list + LVX_LIST_HDR + LVX_SOLID_CAP + (rs * rs * rs + 3) / 4;
+    uint32_t *sb_rows = occ_list + V;
     LVX_CUDA(cudaMemsetAsync(vis_tmp, 0, (size_t)V, s));
     k_solid<<<blocks_for(V, SOLID_ITEMS * 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, solid_list, occ_list, stats);
     k_superbrick_shadow<<<(unsigned)(rs * rs * rs), 64, 0, s>>>(solid_list, res, (float)cam_voxel_host[0],
-                                                                          (float)cam_voxel_host[1], (float)cam_voxel_host[2], sb_flag);
+                                                                          (float)cam_voxel_host[1], (float)cam_voxel_host[2], sb_flag, sb_rows);
     unsigned nb = 148 * 16;
     if (nb > blocks_for(V, 128)) nb = blocks_for(V, 128);
     // vis_list doubles as the "needs the fine march" list until k_dilate refills it
     LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
-    k_visibility<<<nb, 128, 0, s>>>(bricks, sb_flag, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
+    k_visibility<<<nb, 128, 0, s>>>(bricks, sb_flag, sb_rows, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                     cam_voxel_host[2], stats, vis_tmp, vis_list);
     k_march<<<nb, 128, 0, s>>>(solid_bits, vis_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                cam_voxel_host[2], vis_tmp);

@@ -450,3 +450,49 @@ def test_engine_tiny_inputs(lvx, oracle, res, mode):
     assert np.array_equal(e.hit_id.cpu().numpy(), ref.image.hit_id)
     assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
     assert out.stats["ray_capsule_tests"] == ref.image.stats["ray_capsule_tests"]
+
+
+@pytest.mark.parametrize("kind,kw,res,r,az", [
+    ("bundles", dict(seed=2, n_bundles=2, fibers=40, verts=41, domain=40.0), 64, 0.6, 35.0),
+    ("bundles", dict(seed=5, n_bundles=3, fibers=30, verts=41, domain=40.0), 64, 0.7, 35.0),
+    ("bundles", dict(seed=5, n_bundles=3, fibers=30, verts=41, domain=40.0), 64, 0.7, 200.0),
+    ("grid_diagonals", dict(count=6, length=20, domain=26), 64, 1.6, 35.0),
+    ("grid_diagonals", dict(count=12, length=14, domain=26), 32, 1.6, 120.0),
+])
+def test_culling_with_few_solid_voxels(lvx, oracle, kind, kw, res, r, az):
+    """1..1024 solid voxels: every super-brick keeps the solid voxels that shadow it and each occupied
+    voxel is decided against them in closed form (blocked / visible / undecided -> literal march,
+    csrc/cull.cu listed_solid_blocks).  The masks must equal the oracle's literal march bit for bit."""
+    ls = lvx.generate(kind, **kw)
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=r)
+    cfg = lvx.PipelineConfig(res=res, width=64, height=64, strategy="vcsv", cam_azimuth=az)
+    cam = lvx.make_camera(cfg, g)
+    cn = oracle.compute_clip_normals(ls)
+    pyr = oracle.voxelize(ls, cn, g, r_world=r_world)
+    er = oracle.erode(pyr.occ_levels[0])
+    n_solid = int((er >= 0.999).sum())
+    assert 0 < n_solid <= 1024                       # the listed-solid path, not the brick-walk fallback
+    ref = oracle.compute_visibility(er, g, cam, pyr.counts() > 0)
+    gp = lvx.voxelize(ls, lvx.compute_clip_normals(ls), g, r_world=r_world)
+    got = lvx.compute_visibility(lvx.erode(gp), g, cam)
+    occupied = int((pyr.counts() > 0).sum())
+    visible = int((ref.flat[:res ** 3] != 0).sum())
+    assert visible < occupied                        # something is really culled
+    for a, b in zip(got.levels, ref.levels):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+    # the same through the engine, from a camera inside the grid as well
+    for position in (None, "inside"):
+        c = cam
+        if position == "inside":
+            centre = np.asarray(g.world_min) + 0.5 * g.resolution * g.voxel_size
+            c = lvx.Camera(centre + np.array([0.13, -0.21, 0.07]) * g.voxel_size, cam.forward, cam.up, cam.fov,
+                           cam.width, cam.height)
+            ref_c = oracle.compute_visibility(er, g, c, pyr.counts() > 0)
+        else:
+            ref_c = ref
+        eng = lvx.FrameEngine(res, 64, 64, strategy="vcsv")
+        eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+        eng.load_vertices(ls.vertices)
+        out = eng.run(c, g, r_world)
+        assert out.stats["solid_voxels"] == n_solid
+        assert np.array_equal(eng.cull_flat.cpu().numpy(), ref_c.flat)
