@@ -190,6 +190,33 @@ __device__ __forceinline__ bool coarse_may_hit(const uint32_t *__restrict__ bits
     }
 }
 
+// hull(B, c) = union over u in [0, 1] of the boxes c + u (B - c), B = [blo, bhi]; such a box meets the
+// cube F (solid voxel v dilated by 1.5 voxels) iff six per-axis inequalities hold, each linear in u, so
+// the test is an intersection of six u-intervals.  True when a voxel of B may be shadowed by v.
+__device__ __forceinline__ bool shadow_reaches(const float c[3], const float blo[3], const float bhi[3], uint32_t v, int res) {
+    const int s3[3] = {(int)(v % res), (int)((v / res) % res), (int)(v / ((uint32_t)res * res))};
+    float u0 = 0.f, u1 = 1.f;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const float flo = (float)s3[a] - 1.5f, fhi = (float)s3[a] + 2.5f;
+        // c + u (blo - c) <= fhi
+        {
+            const float g0 = c[a], g1 = blo[a];
+            if (g0 > fhi && g1 > fhi) u1 = -1.f;
+            else if (g0 <= fhi && g1 > fhi) u1 = fminf(u1, __fdividef(fhi - g0, g1 - g0) + 1e-3f);
+            else if (g0 > fhi && g1 <= fhi) u0 = fmaxf(u0, __fdividef(fhi - g0, g1 - g0) - 1e-3f);
+        }
+        // c + u (bhi - c) >= flo
+        {
+            const float g0 = c[a], g1 = bhi[a];
+            if (g0 < flo && g1 < flo) u1 = -1.f;
+            else if (g0 >= flo && g1 < flo) u1 = fminf(u1, __fdividef(flo - g0, g1 - g0) + 1e-3f);
+            else if (g0 < flo && g1 >= flo) u0 = fmaxf(u0, __fdividef(flo - g0, g1 - g0) - 1e-3f);
+        }
+    }
+    return u0 <= u1;
+}
+
 // Shadow test per 32^3 super-brick.  A voxel can only be blocked if the segment from its centre
 // to the camera meets a solid voxel, so every voxel of a super-brick B is visible when the convex
 // hull of B and the camera point misses every solid voxel (dilated by 1.5 voxels: far more than
@@ -219,27 +246,8 @@ k_superbrick_shadow(const uint32_t *__restrict__ solid_list, int res, float cx, 
     for (int a = 0; a < 3; a++) { blo[a] = (float)(b3[a] * LVX_SUPER); bhi[a] = fminf((float)((b3[a] + 1) * LVX_SUPER), (float)res); }
     for (uint32_t k = threadIdx.x; k < n_all; k += blockDim.x) {
         const uint32_t v = solid_list[LVX_LIST_HDR + k];
-        const int s3[3] = {(int)(v % res), (int)((v / res) % res), (int)(v / ((uint32_t)res * res))};
-        float u0 = 0.f, u1 = 1.f;
-#pragma unroll
-        for (int a = 0; a < 3; a++) {
-            const float flo = (float)s3[a] - 1.5f, fhi = (float)s3[a] + 2.5f;
-            // c + u (blo - c) <= fhi
-            {
-                const float g0 = c[a], g1 = blo[a];
-                if (g0 > fhi && g1 > fhi) u1 = -1.f;
-                else if (g0 <= fhi && g1 > fhi) u1 = fminf(u1, __fdividef(fhi - g0, g1 - g0) + 1e-3f);
-                else if (g0 > fhi && g1 <= fhi) u0 = fmaxf(u0, __fdividef(fhi - g0, g1 - g0) - 1e-3f);
-            }
-            // c + u (bhi - c) >= flo
-            {
-                const float g0 = c[a], g1 = bhi[a];
-                if (g0 < flo && g1 < flo) u1 = -1.f;
-                else if (g0 >= flo && g1 < flo) u1 = fminf(u1, __fdividef(flo - g0, g1 - g0) + 1e-3f);
-                else if (g0 < flo && g1 >= flo) u0 = fmaxf(u0, __fdividef(flo - g0, g1 - g0) - 1e-3f);
-            }
-        }
-        if (u0 <= u1) {     // this solid voxel's shadow reaches into the super-brick: keep it for the per-voxel test
+        const bool reaches = shadow_reaches(c, blo, bhi, v, res);
+        if (reaches) {      // this solid voxel's shadow reaches into the super-brick: keep it for the per-voxel test
             const uint32_t slot = atomicAdd(&s_n, 1u);
             if (slot < LVX_SB_CAP) row[1 + slot] = v;
         }
@@ -261,7 +269,7 @@ k_superbrick_shadow(const uint32_t *__restrict__ solid_list, int res, float cx, 
 //    (S is in the grid, and the segment ends inside the camera's voxel).  If it misses the grown cube
 //    (or only meets it beyond t = 1 + 1e-9) the march cannot visit S.  In between: undecided.
 //    S = the voxel itself and S = the camera's voxel never block (lv/culling.py:176-186).
-__device__ __forceinline__ int listed_solid_blocks(const uint32_t *__restrict__ row, uint32_t n, int res,
+__device__ __forceinline__ int listed_solid_blocks(const uint32_t *list, uint32_t n, int res,
                                                    int x, int y, int z, double cx, double cy, double cz) {
     const float of[3] = {x + 0.5f, y + 0.5f, z + 0.5f};
     const float df[3] = {(float)cx - of[0], (float)cy - of[1], (float)cz - of[2]};
@@ -274,7 +282,7 @@ __device__ __forceinline__ int listed_solid_blocks(const uint32_t *__restrict__ 
     const double d[3] = {cx - o[0], cy - o[1], cz - o[2]};
     int result = 0;
     for (uint32_t k = 0; k < n; k++) {
-        const uint32_t v = row[1 + k];
+        const uint32_t v = list[k];
         const int s3[3] = {(int)(v % res), (int)((v / res) % res), (int)(v / ((uint32_t)res * res))};
         float t0 = 0.f, t1 = 1.f;
 #pragma unroll
@@ -317,43 +325,87 @@ __device__ __forceinline__ int listed_solid_blocks(const uint32_t *__restrict__ 
 // appended to `march_list`; everything else is visible.
 __global__ void __launch_bounds__(128)
 k_visibility(const uint32_t *__restrict__ bricks, const uint8_t *__restrict__ sb_flag,
-             const uint32_t *__restrict__ sb_rows, const uint32_t *__restrict__ occ_list, int res,
+             const uint32_t *__restrict__ sb_rows, const uint32_t *__restrict__ solid_list,
+             const uint32_t *__restrict__ occ_list, int res,
              double cx, double cy, double cz, const uint64_t *__restrict__ stats,
              uint8_t *__restrict__ vis, uint32_t *__restrict__ march_list) {
+    __shared__ uint32_t s_cand[4][LVX_SB_ROW];   // per warp: the solid voxels that can matter to its 32 voxels
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n = (int64_t)stats[LVX_ST_OCCUPIED];
     const bool any_solid = stats[LVX_ST_SOLID] != 0;
+    if (!any_solid) return;        // nothing can block: k_dilate treats every occupied voxel as visible
+    const uint32_t n_all = solid_list[0];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t n_iter = (n + stride - 1) / stride;
+    const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
+    const float cf[3] = {(float)cx, (float)cy, (float)cz};
     for (int64_t it = 0; it < n_iter; it++) {
         const int64_t e = it * stride + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        bool may_hit = false, blocked = false;
+        bool may_hit = false, blocked = false, flagged = false;
         uint32_t idx = 0;
+        int x = 0, y = 0, z = 0, sb = 0;
         if (e < n) {
             idx = occ_list[e];
-            const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
-            const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
-            const int sb = (x / LVX_SUPER) + rs * ((y / LVX_SUPER) + rs * (z / LVX_SUPER));
-            if (any_solid && sb_flag[sb]) {
-                // Only a solid voxel can block.
-                const float ox = x + 0.5f, oy = y + 0.5f, oz = z + 0.5f;
-                const uint32_t *row = sb_rows + (size_t)sb * LVX_SB_ROW;
-                const uint32_t n_row = row[0];
-                if (n_row <= LVX_SB_CAP) {
-                    // few solid voxels shadow this super-brick: decide against each of them in closed form
-                    const int r = listed_solid_blocks(row, n_row, res, x, y, z, cx, cy, cz);
+            x = (int)(idx % res); y = (int)((idx / res) % res); z = (int)(idx / ((uint32_t)res * res));
+            sb = (x / LVX_SUPER) + rs * ((y / LVX_SUPER) + rs * (z / LVX_SUPER));
+            flagged = any_solid && sb_flag[sb];       // only a solid voxel can block
+        }
+        const uint32_t fm = __ballot_sync(0xffffffffu, flagged);
+        if (fm) {
+            // The warp's voxels are consecutive entries of the occupied list: neighbours in a row, mostly.
+            // The listed solid voxels (those shadowing the super-brick if all lanes share one, else all of
+            // them) are first tested, one per lane, against the hull of the warp's bounding box and the
+            // camera; the few that remain are what every lane then decides against in closed form.
+            const int sb0 = __shfl_sync(0xffffffffu, sb, __ffs(fm) - 1);
+            const bool same = __all_sync(0xffffffffu, !flagged || sb == sb0);
+            const uint32_t *row = sb_rows + (size_t)sb0 * LVX_SB_ROW;
+            const uint32_t n_row = row[0];
+            const bool use_row = same && n_row <= LVX_SB_CAP;
+            const uint32_t *src = use_row ? row + 1 : solid_list + LVX_LIST_HDR;
+            const uint32_t cnt = use_row ? n_row : n_all;
+            bool walk = n_all > LVX_SOLID_CAP;        // nothing listed: coarse walks below
+            bool full = false;
+            uint32_t nc = 0;
+            if (!walk) {
+                const int big = 1 << 30;
+                const float blo[3] = {(float)__reduce_min_sync(0xffffffffu, flagged ? x : big),
+                                      (float)__reduce_min_sync(0xffffffffu, flagged ? y : big),
+                                      (float)__reduce_min_sync(0xffffffffu, flagged ? z : big)};
+                const float bhi[3] = {(float)(__reduce_max_sync(0xffffffffu, flagged ? x : -big) + 1),
+                                      (float)(__reduce_max_sync(0xffffffffu, flagged ? y : -big) + 1),
+                                      (float)(__reduce_max_sync(0xffffffffu, flagged ? z : -big) + 1)};
+                for (uint32_t k0 = 0; k0 < cnt && !full; k0 += 32) {
+                    const uint32_t k = k0 + lane;
+                    uint32_t v = 0;
+                    bool reaches = false;
+                    if (k < cnt) { v = src[k]; reaches = shadow_reaches(cf, blo, bhi, v, res); }
+                    const uint32_t hm = __ballot_sync(0xffffffffu, reaches);
+                    if (nc + __popc(hm) > LVX_SB_ROW) full = true;      // too many remain: every lane takes the whole list
+                    else {
+                        if (reaches) s_cand[warp][nc + __popc(hm & ((1u << lane) - 1u))] = v;
+                        nc += __popc(hm);
+                    }
+                }
+                __syncwarp();
+            }
+            if (flagged) {
+                if (!walk) {
+                    const int r = full ? listed_solid_blocks(src, cnt, res, x, y, z, cx, cy, cz)
+                                       : listed_solid_blocks(s_cand[warp], nc, res, x, y, z, cx, cy, cz);
                     blocked = r == 1;
                     may_hit = r == 2;
                 } else {
                     // walk the segment centre->camera through the 32^3-voxel super-bricks, then the 8^3 bricks
-                    may_hit = coarse_may_hit(bricks + brick_words(res, LVX_BRICK), (res + LVX_SUPER - 1) / LVX_SUPER,
-                                             LVX_SUPER, ox, oy, oz, (float)cx, (float)cy, (float)cz);
+                    const float ox = x + 0.5f, oy = y + 0.5f, oz = z + 0.5f;
+                    may_hit = coarse_may_hit(bricks + brick_words(res, LVX_BRICK), rs, LVX_SUPER, ox, oy, oz, cf[0], cf[1], cf[2]);
                     if (may_hit)
                         may_hit = coarse_may_hit(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz,
-                                                 (float)cx, (float)cy, (float)cz);
+                                                 cf[0], cf[1], cf[2]);
                 }
             }
-            if (!may_hit && !blocked) vis[idx] = 1;
+            __syncwarp();      // s_cand is rewritten in the next iteration
         }
+        if (e < n && !may_hit && !blocked) vis[idx] = 1;
         list_append_block(march_list, may_hit, idx);
     }
 }
@@ -429,8 +481,8 @@ k_dilate(const uint32_t *__restrict__ base, const uint8_t *__restrict__ vis, int
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             if (!occ[k]) continue;
-            bool v = vs[k] != 0;
-            if (!v && any_solid) {
+            bool v = vs[k] != 0 || !any_solid;     // (k_visibility does not run when nothing is solid)
+            if (!v) {
                 const int64_t idx = idx0 + k;
                 const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((int64_t)res * res));
                 for (int dz = -1; dz <= 1 && !v; dz++) {
@@ -512,13 +564,19 @@ k_march_levels(const uint8_t *__restrict__ flat, const MarchOffsets O, int res, 
             const uint32_t i1 = O.off[1] + ((uint32_t)x0 >> 1) + r1 * (((uint32_t)y >> 1) + r1 * ((uint32_t)z >> 1));
             p1a = flat[i1]; p1b = flat[i1 + 1];
             if (!(p1a && p1b)) {
-                up = 1;
-                while (up < n_levels - 1) {
-                    const int nl = up + 1;
-                    const uint32_t rl = (uint32_t)res >> nl;
-                    if (flat[O.off[nl] + ((uint32_t)x0 >> nl) + rl * (((uint32_t)y >> nl) + rl * ((uint32_t)z >> nl))] != 0) break;
-                    up = nl;
+                // In an OR pyramid a set node has set ancestors only, so "ancestors 1..l all clear" holds
+                // for l up to the highest clear ancestor: all levels are loaded at once (independent
+                // loads, one round trip) and the clear ones counted, instead of a dependent walk upwards.
+                uint32_t clear = 0;
+#pragma unroll
+                for (int nl = 2; nl < 11; nl++) {     // res <= 1024: at most 11 levels
+                    if (nl < n_levels) {
+                        const uint32_t rl = (uint32_t)res >> nl;
+                        if (flat[O.off[nl] + ((uint32_t)x0 >> nl) + rl * (((uint32_t)y >> nl) + rl * ((uint32_t)z >> nl))] == 0)
+                            clear |= 1u << nl;
+                    }
                 }
+                up = __ffs(~(clear | 3u)) - 2;        // the level below the first set ancestor (>= 1)
             }
         }
         const uint8_t la = p1a ? 0 : (uint8_t)up, lb = p1b ? 0 : (uint8_t)up;
@@ -577,7 +635,7 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     if (nb > blocks_for(V, 128)) nb = blocks_for(V, 128);
     // vis_list doubles as the "needs the fine march" list until k_dilate refills it
     LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
-    k_visibility<<<nb, 128, 0, s>>>(bricks, sb_flag, sb_rows, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
+    k_visibility<<<nb, 128, 0, s>>>(bricks, sb_flag, sb_rows, solid_list, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                     cam_voxel_host[2], stats, vis_tmp, vis_list);
     k_march<<<nb, 128, 0, s>>>(solid_bits, vis_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                cam_voxel_host[2], vis_tmp);
