@@ -588,10 +588,41 @@ k_march_levels(const uint8_t *__restrict__ flat, const MarchOffsets O, int res, 
     *reinterpret_cast<uchar4 *>(skip + 4 * g) = out;
 }
 
+// The top of the OR pyramid (levels of <= 16^3 nodes) in one launch: a single CTA, level after level.
+struct OrTail { int64_t off[16]; int first, n_levels, res; };
+__global__ void __launch_bounds__(1024)
+k_ormip_tail(uint8_t *__restrict__ flat, const OrTail T) {
+    for (int l = T.first; l < T.n_levels; l++) {
+        const int rsrc = T.res >> (l - 1), rl = T.res >> l;
+        const uint8_t *src = flat + T.off[l - 1];
+        uint8_t *out = flat + T.off[l];
+        for (int i = threadIdx.x; i < rl * rl * rl; i += blockDim.x) {
+            const int x = i % rl, y = (i / rl) % rl, z = i / (rl * rl);
+            uint32_t m = 0;
+#pragma unroll
+            for (int dz = 0; dz < 2; dz++)
+#pragma unroll
+                for (int dy = 0; dy < 2; dy++) {
+                    const uchar2 w = *reinterpret_cast<const uchar2 *>(src + (2 * x + rsrc * ((2 * y + dy) + rsrc * (2 * z + dz))));
+                    m |= w.x | w.y;
+                }
+            out[i] = m ? 1 : 0;
+        }
+        __syncthreads();
+    }
+}
+
 static int or_mips(uint8_t *flat, int res, cudaStream_t s) {
     const LevelOffsets L = make_level_offsets(res);
     for (int l = 1; l < L.n_levels; l++) {
         const int rsrc = res >> (l - 1), rl = res >> l;
+        if (rl <= 16) {     // this level and everything above it: one launch
+            OrTail T;
+            for (int k = 0; k < 16; k++) T.off[k] = k < L.n_levels ? L.off[k] : 0;
+            T.first = l; T.n_levels = L.n_levels; T.res = res;
+            k_ormip_tail<<<1, 1024, 0, s>>>(flat, T);
+            break;
+        }
         k_ormip<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(flat + L.off[l - 1], rsrc, flat + L.off[l]);
     }
     LVX_LAUNCH_CHECK();

@@ -49,6 +49,33 @@ k_nzmask(const uint32_t *__restrict__ base, const double *__restrict__ lvl, int 
     if ((threadIdx.x & 31) == 0 && i < n) mask[i >> 5] = m;
 }
 
+// The masks of all levels with <= 16^3 cells in one launch (a single CTA; the levels are independent).
+struct NzTail { uint32_t mip_off[16], mask_off[16]; int first, n_levels, res; };
+__global__ void __launch_bounds__(1024)
+k_nzmask_tail(const double *__restrict__ mips, const NzTail T, uint32_t *__restrict__ masks) {
+    const int lane = threadIdx.x & 31;
+    for (int l = T.first; l < T.n_levels; l++) {
+        const int rl = T.res >> l;
+        const int n = rl * rl * rl;
+        const double *lvl = mips + T.mip_off[l];
+        for (int i0 = threadIdx.x - lane; i0 < n; i0 += blockDim.x) {      // warp-uniform trip count
+            const int i = i0 + lane;
+            bool any = false;
+            if (i < n) {
+                const int x = i % rl, y = (i / rl) % rl, z = i / (rl * rl);
+                if (x == rl - 1 || y == rl - 1 || z == rl - 1) any = true;
+                else {
+#pragma unroll
+                    for (int k = 0; k < 8; k++)
+                        any |= lvl[(x + (k & 1)) + rl * ((y + ((k >> 1) & 1)) + rl * (z + (k >> 2)))] != 0.0;
+                }
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, any);
+            if (lane == 0) masks[T.mask_off[l] + (i >> 5)] = m;
+        }
+    }
+}
+
 // Level-0 footprint mask from the one-bit-per-voxel "occupancy non-zero" words (lvx_pack_wide):
 // one thread per 32 cells.  Same result as k_nzmask at level 0 (rl a multiple of 32).
 __global__ void __launch_bounds__(256)
@@ -236,6 +263,13 @@ int lvx_shade(const uint32_t *base, const double *mips, int res, const uint32_t 
         if (l == 0 && nz_bits && rl >= 32) {
             k_nzmask_bits<<<blocks_for((int64_t)(rl >> 5) * rl * rl, 256), 256, 0, s>>>(nz_bits, rl, masks + P.mask_off[0]);
             continue;
+        }
+        if (l >= 1 && rl <= 16) {     // this level and everything above it: one launch
+            NzTail T;
+            for (int k = 0; k < 16; k++) { T.mip_off[k] = P.mip_off[k]; T.mask_off[k] = P.mask_off[k]; }
+            T.first = l; T.n_levels = L.n_levels; T.res = res;
+            k_nzmask_tail<<<1, 1024, 0, s>>>(mips, T, masks);
+            break;
         }
         k_nzmask<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(base, mips + P.mip_off[l], l, rl,
                                                                        masks + P.mask_off[l]);

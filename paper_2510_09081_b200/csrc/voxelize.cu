@@ -188,6 +188,31 @@ k_mip_next(const double *__restrict__ src, int rsrc, double *__restrict__ out) {
     out[i] = s * 0.125;
 }
 
+// The top of the pyramid (levels of <= 16^3 nodes) in ONE launch: a single CTA builds level after
+// level with a block barrier in between, instead of one tiny launch per level.
+struct MipTail { int64_t off[16]; int first, n_levels, res; };   // off[l] = element offset of level l inside `mips`
+__global__ void __launch_bounds__(1024)
+k_mip_tail(double *__restrict__ mips, const MipTail T) {
+    for (int l = T.first; l < T.n_levels; l++) {
+        const int rsrc = T.res >> (l - 1), rl = T.res >> l;
+        const double *src = mips + T.off[l - 1];
+        double *out = mips + T.off[l];
+        for (int i = threadIdx.x; i < rl * rl * rl; i += blockDim.x) {
+            const int x = i % rl, y = (i / rl) % rl, z = i / (rl * rl);
+            double s = 0.0;
+#pragma unroll
+            for (int dz = 0; dz < 2; dz++)
+#pragma unroll
+                for (int dy = 0; dy < 2; dy++) {
+                    const double2 w = *reinterpret_cast<const double2 *>(src + (2 * x + rsrc * ((2 * y + dy) + rsrc * (2 * z + dz))));
+                    s += w.x + w.y;
+                }
+            out[i] = s * 0.125;
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace lvx
 
 using namespace lvx;
@@ -261,6 +286,13 @@ int lvx_build_mips(const uint32_t *base, int res, double *mips, void *stream) {
     }
     for (int l = 2; l < L.n_levels; l++) {
         const int rsrc = res >> (l - 1), rl = res >> l;
+        if (rl <= 16) {     // this level and everything above it: one launch
+            MipTail T;
+            for (int k = 0; k < 16; k++) T.off[k] = (k >= 1 && k < L.n_levels) ? L.off[k] - V : 0;
+            T.first = l; T.n_levels = L.n_levels; T.res = res;
+            k_mip_tail<<<1, 1024, 0, s>>>(mips, T);
+            break;
+        }
         k_mip_next<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(mips + (L.off[l - 1] - V), rsrc,
                                                                         mips + (L.off[l] - V));
     }

@@ -127,14 +127,18 @@ class FrameEngine:
     def kernel_launches_per_frame(self) -> int:
         """Number of lvx kernels one `run` enqueues (csrc/*.cu), for bench.py's `gpu_launches`."""
         levels = int(self.res).bit_length()
+
+        def pyramid(first):     # one launch per level of more than 16^3 nodes, one for all the levels above
+            big = sum(1 for l in range(first, levels) if (self.res >> l) > 16)
+            return big + (1 if big < levels - first else 0)
         n = 1 + 1                                   # stats_reset, upload
         n += 3 if self.order_brick > 0 else 0       # processing order: histogram, scan, scatter
         n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
-        n += levels - 1                             # mips
-        n += (5 if self.strategy == "vcsv" else 1) + (levels - 1)   # solid, super-brick shadow, visibility, march, dilate | occupied; or-mips
+        n += 1 + pyramid(2)                         # mips: level 1 from the packed grid, then the rest
+        n += (5 if self.strategy == "vcsv" else 1) + pyramid(1)   # solid, super-brick shadow, visibility, march, dilate | occupied; or-mips
         n += 1                                      # scan
         n += 3 + 1                                  # cursor init, scatter, order; march table
-        n += levels + 1                             # non-empty masks, shade
+        n += 1 + pyramid(1) + 1                     # non-empty masks (level 0, the rest), shade
         if self.shading == "demand":
             n += 2                                  # trace_hits, resolve
         else:
