@@ -140,7 +140,7 @@ class FrameEngine:
         n += 3 + 1                                  # cursor init, scatter, order; march table
         n += 1 + pyramid(1) + 1                     # non-empty masks (level 0, the rest), shade
         if self.shading == "demand":
-            n += 2                                  # trace_hits, resolve
+            n += 3                                  # trace_hits, need list, resolve
         else:
             n += 1 + 1                              # shade fill, render
         return n
