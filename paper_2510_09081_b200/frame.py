@@ -315,7 +315,7 @@ class FrameEngine:
             self._stage_trace_hits(cam, tile); ev[7].record()
             self._stage_shade(); ev[8].record()
             self._stage_resolve(cam, tile); ev[9].record()
-            self._stats_host[N.STATS_WORDS:].copy_(self.need_list[:4].view(t.int64), non_blocking=True)
+            self._stats_host[N.STATS_WORDS:N.STATS_WORDS + 1].copy_(self.need_list[:2].view(t.int64), non_blocking=True)
         else:
             if overlap:
                 main.wait_event(self._ev_side[1])
