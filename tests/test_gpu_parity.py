@@ -496,3 +496,30 @@ def test_culling_with_few_solid_voxels(lvx, oracle, kind, kw, res, r, az):
         out = eng.run(c, g, r_world)
         assert out.stats["solid_voxels"] == n_solid
         assert np.array_equal(eng.cull_flat.cpu().numpy(), ref_c.flat)
+
+
+@pytest.mark.parametrize("res,strategy,mode", [(64, "vcsv", "opaque"), (256, "vcsv", "opaque"), (64, "vsv", "transparent")])
+def test_launch_count_is_what_the_engine_claims(lvx, res, strategy, mode):
+    """bench.py's `gpu_launches` comes from FrameEngine.kernel_launches_per_frame(); CUPTI (torch.profiler)
+    counts the lvx kernels one frame really launches."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    ls = lvx.generate("random_streamlines", seed=8, polylines=60, verts_per_line=40)
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=0.3)
+    cfg = lvx.PipelineConfig(res=res, width=96, height=64, strategy=strategy, mode=mode, alpha=0.4)
+    cam = lvx.make_camera(cfg, g)
+    eng = lvx.FrameEngine(res, 96, 64, strategy=strategy, mode=mode, alpha=0.4)
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    eng.load_vertices(ls.vertices)
+    eng.run(cam, g, r_world)                       # sizes the fragment buffer
+    torch.cuda.synchronize()
+    try:
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            eng.run(cam, g, r_world)
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if "lvx::" in e.name]
+    except Exception as e:                         # no CUPTI in this environment
+        pytest.skip(f"torch.profiler unavailable: {e}")
+    if not names:
+        pytest.skip("the profiler recorded no device activity")
+    assert len(names) == eng.kernel_launches_per_frame(), sorted(names)
