@@ -2,6 +2,7 @@
 times -- against the CPU oracle on the C2 workload itself (1 000 000 segments, 256^3, 1920x1080, opaque +
 AO, vcsv) and on C3 (the same line set, vsv, ground-truth transparency alpha 0.3, 1920x1080), plus the size-independent properties of SURVEY.md §8c:
 sum of counts = voxels visited, fragment total = sum of the masked counts, every list strictly ascending.
+C4 (10 000 000 segments, 512^3) gets the properties and an engine-variant identity check (no oracle: too slow).
 
 Everything compared here is bit-exact (stricter than the north star's 1e-4 / 1/255 tolerances, which are
 asserted as well so that the bar is written down where it is tested).
@@ -105,3 +106,60 @@ def test_c3_full_size_vs_oracle(lvx, oracle, c2_lines):
     # all-voxel shading: ao / shadow f32 bit patterns
     assert np.array_equal(eng.ao.cpu().numpy().view(np.uint32), ref.shading.ao.ravel().view(np.uint32))
     assert np.array_equal(eng.shadow.cpu().numpy().view(np.uint32), ref.shading.shadow.ravel().view(np.uint32))
+
+
+def test_c4_full_size_properties(lvx):
+    """C4 (10 000 000 segments, 512^3, 1920x1080, vcsv opaque): too large for the CPU oracle inside a test,
+    so the size-independent properties are checked on the device, and a second engine with the other
+    internal choices (polyline processing order, packed 32-bit accumulation) must give identical arrays."""
+    import torch
+    res, w, h = 512, 1920, 1080
+    ls = lvx.generate("bundles", seed=1, n_bundles=400, fibers=250, verts=101)
+    assert ls.n_segments == 10_000_000
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=0.2)
+    cfg = lvx.PipelineConfig(res=res, width=w, height=h, strategy="vcsv", mode="opaque", light="-0.5,-0.3,-0.8")
+    cam = lvx.make_camera(cfg, g)
+    V = res ** 3
+
+    def frame(order_brick, wide):
+        e = lvx.FrameEngine(res, w, h, strategy="vcsv", mode="opaque")
+        if order_brick is not None:
+            e.order_brick = order_brick
+        e.use_wide = wide
+        e.set_topology(ls.polyline_offsets, ls.n_vertices)
+        e.load_vertices(ls.vertices)
+        return e, e.run(cam, g, r_world)
+
+    e1, o1 = frame(None, True)
+    n = o1.stats["fragments"]
+    base = e1.base.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    counts = base >> 16
+    assert o1.stats["saturated"] == 0
+    assert int(counts.sum().item()) == o1.stats["voxels_visited"]          # sum of counts = incidences
+    vis = e1.cull_flat[:V] != 0
+    masked = counts * vis
+    assert int(masked.sum().item()) == n                                   # fragment total = sum of the masked counts
+    assert int((counts > 0).sum().item()) == o1.stats["occupied_voxels"]
+    assert int(vis.sum().item()) == o1.stats["visible_voxels"]
+    offs = e1.offsets.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    excl = torch.cumsum(masked, 0) - masked
+    assert torch.equal(offs[:V], excl) and int(offs[V].item()) == n        # offsets = exclusive scan
+    del excl, base
+    frags = e1.frags[:n]
+    assert int(frags.min().item()) >= 0 and int(frags.max().item()) < ls.n_vertices
+    starts = torch.zeros(n + 1, dtype=torch.bool, device=frags.device)
+    starts[offs[:V][masked > 0]] = True
+    descents = frags[1:] <= frags[:-1]
+    assert not bool((descents & ~starts[1:n]).any().item())               # every list strictly ascending
+    del descents, starts, offs, masked, counts
+    torch.cuda.empty_cache()
+    # the other internal choices: same arrays, same image
+    e2, o2 = frame(0, False)
+    assert o2.stats["fragments"] == n and o2.stats["voxels_visited"] == o1.stats["voxels_visited"]
+    assert o2.stats["ray_capsule_tests"] == o1.stats["ray_capsule_tests"]
+    assert torch.equal(e1.base, e2.base)
+    assert torch.equal(e1.cull_flat, e2.cull_flat)
+    assert torch.equal(e1.offsets, e2.offsets)
+    assert torch.equal(e1.frags[:n], e2.frags[:n])
+    assert torch.equal(e1.hit_id, e2.hit_id)
+    assert torch.equal(e1.srgb, e2.srgb)
