@@ -410,9 +410,15 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--bundles", type=int, default=0, help="c2/c3/c4 only: number of fibre bundles (25 000 segments "
+                                                           "each) instead of the workload's own, for segment-count sweeps")
     ap.add_argument("--pipeline", type=int, default=3, help="frames in flight per GPU (engines on separate streams); "
                                                              "1 = strictly one frame after the other")
     args = ap.parse_args()
+    if args.bundles > 0:
+        if WORKLOADS[args.workload][0]["kind"] != "bundles":
+            ap.error("--bundles needs a bundles workload (c2, c3, c4)")
+        WORKLOADS[args.workload][0]["n_bundles"] = args.bundles
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     if args.impl == "reference":
         run_reference(args)
