@@ -12,7 +12,7 @@ namespace lvx {
 #define LVX_SOLID_Q 4092u
 #define LVX_BRICK 8        // coarse "may contain a blocker" bricks for the visibility march
 #define LVX_SUPER 32       // and a coarser level above them
-#define LVX_SOLID_CAP 1024 // solid voxels listed individually for the per-super-brick shadow test
+#define LVX_SOLID_CAP 16384 // solid voxels listed individually for the per-super-brick shadow test
 #define LVX_SB_ROW 128     // words per super-brick row: [number of shadowing solid voxels][up to 127 of them]
 #define LVX_SB_CAP (LVX_SB_ROW - 1)
 
@@ -363,7 +363,9 @@ k_visibility(const uint32_t *__restrict__ bricks, const uint8_t *__restrict__ sb
             const bool use_row = same && n_row <= LVX_SB_CAP;
             const uint32_t *src = use_row ? row + 1 : solid_list + LVX_LIST_HDR;
             const uint32_t cnt = use_row ? n_row : n_all;
-            bool walk = n_all > LVX_SOLID_CAP;        // nothing listed: coarse walks below
+            // no short list for this warp (too many solid voxels shadow the super-brick, or the lanes
+            // straddle super-bricks in a frame with many solid voxels): coarse walks below
+            bool walk = n_all > LVX_SOLID_CAP || (!use_row && n_all > 1024u);
             bool full = false;
             uint32_t nc = 0;
             if (!walk) {

@@ -452,15 +452,19 @@ def test_engine_tiny_inputs(lvx, oracle, res, mode):
     assert out.stats["ray_capsule_tests"] == ref.image.stats["ray_capsule_tests"]
 
 
-@pytest.mark.parametrize("kind,kw,res,r,az", [
-    ("bundles", dict(seed=2, n_bundles=2, fibers=40, verts=41, domain=40.0), 64, 0.6, 35.0),
-    ("bundles", dict(seed=5, n_bundles=3, fibers=30, verts=41, domain=40.0), 64, 0.7, 35.0),
-    ("bundles", dict(seed=5, n_bundles=3, fibers=30, verts=41, domain=40.0), 64, 0.7, 200.0),
-    ("grid_diagonals", dict(count=6, length=20, domain=26), 64, 1.6, 35.0),
-    ("grid_diagonals", dict(count=12, length=14, domain=26), 32, 1.6, 120.0),
+@pytest.mark.parametrize("kind,kw,res,r,az,lo,hi", [
+    ("bundles", dict(seed=2, n_bundles=2, fibers=40, verts=41, domain=40.0), 64, 0.6, 35.0, 0, 1024),
+    ("bundles", dict(seed=5, n_bundles=3, fibers=30, verts=41, domain=40.0), 64, 0.7, 35.0, 0, 1024),
+    ("bundles", dict(seed=5, n_bundles=3, fibers=30, verts=41, domain=40.0), 64, 0.7, 200.0, 0, 1024),
+    ("grid_diagonals", dict(count=6, length=20, domain=26), 64, 1.6, 35.0, 0, 1024),
+    ("grid_diagonals", dict(count=12, length=14, domain=26), 32, 1.6, 120.0, 0, 1024),
+    # 1025..16384 solid voxels: super-bricks with a short row use it, the others walk the brick flags
+    ("grid_diagonals", dict(count=60, length=20, domain=26), 64, 1.5, 35.0, 1024, 16384),
+    ("random_streamlines", dict(seed=4, polylines=60, verts_per_line=40), 64, 1.8, 35.0, 1024, 16384),
+    ("bundles", dict(seed=2, n_bundles=3, fibers=60, verts=41, domain=40.0), 64, 0.6, 300.0, 1024, 16384),
 ])
-def test_culling_with_few_solid_voxels(lvx, oracle, kind, kw, res, r, az):
-    """1..1024 solid voxels: every super-brick keeps the solid voxels that shadow it and each occupied
+def test_culling_with_few_solid_voxels(lvx, oracle, kind, kw, res, r, az, lo, hi):
+    """1..16384 solid voxels: every super-brick keeps the solid voxels that shadow it and each occupied
     voxel is decided against them in closed form (blocked / visible / undecided -> literal march,
     csrc/cull.cu listed_solid_blocks).  The masks must equal the oracle's literal march bit for bit."""
     ls = lvx.generate(kind, **kw)
@@ -471,7 +475,7 @@ def test_culling_with_few_solid_voxels(lvx, oracle, kind, kw, res, r, az):
     pyr = oracle.voxelize(ls, cn, g, r_world=r_world)
     er = oracle.erode(pyr.occ_levels[0])
     n_solid = int((er >= 0.999).sum())
-    assert 0 < n_solid <= 1024                       # the listed-solid path, not the brick-walk fallback
+    assert lo < n_solid <= hi                        # the listed-solid path, not the all-walk fallback
     ref = oracle.compute_visibility(er, g, cam, pyr.counts() > 0)
     gp = lvx.voxelize(ls, lvx.compute_clip_normals(ls), g, r_world=r_world)
     got = lvx.compute_visibility(lvx.erode(gp), g, cam)
