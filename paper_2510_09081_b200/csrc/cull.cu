@@ -117,8 +117,10 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
 }
 
 // lv/culling.py:143-188, literally: Amanatides-Woo from the voxel centre to the camera point.
+// `t_stop`: a parameter beyond which the caller has PROVED that the walk cannot meet a solid voxel (see
+// coarse_last_flagged); there the reference's loop can only run on to one of its `return False` exits.
 __device__ __forceinline__ bool march_blocked(const uint32_t *__restrict__ solid, int res, int x, int y, int z,
-                                              double cx, double cy, double cz) {
+                                              double cx, double cy, double cz, double t_stop = 2.0) {
     const double ox = x + 0.5, oy = y + 0.5, oz = z + 0.5;
     const double dx = cx - ox, dy = cy - oy, dz = cz - oz;
     const int ex = (int)floor(cx), ey = (int)floor(cy), ez = (int)floor(cz);
@@ -136,6 +138,7 @@ __device__ __forceinline__ bool march_blocked(const uint32_t *__restrict__ solid
         else if (tmy <= tmz) { y += sy; t = tmy; tmy += tdy; }
         else { z += sz; t = tmz; tmz += tdz; }
         if (t >= 1.0) return false;                                               // reached the camera
+        if (t > t_stop) return false;                                             // nothing solid from here on
         if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) return false;  // left the grid
         if (x == ex && y == ey && z == ez) return false;                          // camera's own voxel
         const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
@@ -187,6 +190,51 @@ __device__ __forceinline__ bool coarse_may_hit(const uint32_t *__restrict__ bits
         else { c[2] += st[2]; t = tm[2]; tm[2] += td[2]; }
         if (t > t1 + 1e-4f) return false;
         if (c[0] < 0 || c[1] < 0 || c[2] < 0 || c[0] >= rb || c[1] >= rb || c[2] >= rb) return false;
+    }
+}
+
+// The same brick walk run to the end of the segment: returns the parameter at which the walk leaves the
+// LAST flagged brick (< 0: none is flagged).  Beyond that parameter (plus the caller's margin of two
+// voxels) every voxel within one voxel of the segment lies in unflagged bricks, i.e. is not solid.
+__device__ __forceinline__ float coarse_last_flagged(const uint32_t *__restrict__ bits, int rb, int brick,
+                                                     float ox, float oy, float oz, float cx, float cy, float cz) {
+    const float inv = 1.0f / (float)brick;
+    const float o[3] = {ox * inv, oy * inv, oz * inv};
+    const float d[3] = {(cx - ox) * inv, (cy - oy) * inv, (cz - oz) * inv};
+    float t0 = 0.0f, t1 = 1.0f;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        if (d[a] == 0.0f) { if (o[a] < 0.0f || o[a] > (float)rb) return -1.0f; }
+        else {
+            const float id = __fdividef(1.0f, d[a]);
+            float ta = (0.0f - o[a]) * id, tb = ((float)rb - o[a]) * id;
+            if (ta > tb) { const float tmp = ta; ta = tb; tb = tmp; }
+            t0 = fmaxf(t0, ta); t1 = fminf(t1, tb);
+        }
+    }
+    if (t0 > t1 + 1e-4f) return -1.0f;
+    int c[3], st[3];
+    float tm[3], td[3];
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const float p = o[a] + d[a] * t0;
+        c[a] = min(max((int)floorf(p), 0), rb - 1);
+        st[a] = d[a] > 0 ? 1 : -1;
+        const float id = d[a] != 0.0f ? __fdividef(1.0f, d[a]) : 0.0f;
+        tm[a] = d[a] != 0.0f ? ((float)(c[a] + (d[a] > 0 ? 1 : 0)) - o[a]) * id : 1e30f;
+        td[a] = d[a] != 0.0f ? fabsf(id) : 1e30f;
+    }
+    float last = -1.0f;
+    for (;;) {
+        const int bi = c[0] + rb * (c[1] + rb * c[2]);
+        const bool flagged = (bits[bi >> 5] >> (bi & 31)) & 1u;
+        float t;
+        if (tm[0] <= tm[1] && tm[0] <= tm[2]) { c[0] += st[0]; t = tm[0]; tm[0] += td[0]; }
+        else if (tm[1] <= tm[2]) { c[1] += st[1]; t = tm[1]; tm[1] += td[1]; }
+        else { c[2] += st[2]; t = tm[2]; tm[2] += td[2]; }
+        if (flagged) last = fminf(t, 1.0f);
+        if (t > t1 + 1e-4f) return last;
+        if (c[0] < 0 || c[1] < 0 || c[2] < 0 || c[0] >= rb || c[1] >= rb || c[2] >= rb) return last;
     }
 }
 
@@ -414,14 +462,27 @@ k_visibility(const uint32_t *__restrict__ bricks, const uint8_t *__restrict__ sb
 
 // Phase B: the literal fine march (lv/culling.py:143-188) decides for the remaining candidates.
 __global__ void __launch_bounds__(128)
-k_march(const uint32_t *__restrict__ solid, const uint32_t *__restrict__ march_list, int res,
-        double cx, double cy, double cz, uint8_t *__restrict__ vis) {
+k_march(const uint32_t *__restrict__ solid, const uint32_t *__restrict__ bricks, const uint32_t *__restrict__ march_list,
+        int res, double cx, double cy, double cz, uint8_t *__restrict__ vis) {
     const int64_t n = (int64_t)*reinterpret_cast<const unsigned long long *>(march_list);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
         const uint32_t idx = march_list[LVX_LIST_HDR + e];
         const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
-        vis[idx] = march_blocked(solid, res, x, y, z, cx, cy, cz) ? 0 : 1;
+        // Most candidates are visible, and their literal walk would run on to the camera or the grid's
+        // boundary long after the last place a solid voxel can be.  A brick walk over the whole segment
+        // (f32, conservative: flags cover the solid voxels dilated by a voxel) gives the parameter where
+        // the segment leaves the last flagged 8^3 brick; two voxels later the literal walk may stop.
+        const float ox = x + 0.5f, oy = y + 0.5f, oz = z + 0.5f;
+        const float tl = coarse_last_flagged(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz,
+                                             (float)cx, (float)cy, (float)cz);
+        bool blocked = false;
+        if (tl >= 0.0f) {
+            const float dmax = fmaxf(fmaxf(fabsf((float)cx - ox), fabsf((float)cy - oy)), fabsf((float)cz - oz));
+            const double t_stop = dmax > 0.f ? (double)tl * 1.0001 + 2.0 / (double)dmax + 1e-4 : 2.0;
+            blocked = march_blocked(solid, res, x, y, z, cx, cy, cz, t_stop);
+        }
+        vis[idx] = blocked ? 0 : 1;
     }
 }
 
@@ -670,7 +731,7 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
     k_visibility<<<nb, 128, 0, s>>>(bricks, sb_flag, sb_rows, solid_list, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                     cam_voxel_host[2], stats, vis_tmp, vis_list);
-    k_march<<<nb, 128, 0, s>>>(solid_bits, vis_list, res, cam_voxel_host[0], cam_voxel_host[1],
+    k_march<<<nb, 128, 0, s>>>(solid_bits, bricks, vis_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                cam_voxel_host[2], vis_tmp);
     LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
     k_dilate<<<blocks_for(V / 4, 256), 256, 0, s>>>(base, vis_tmp, res, V, cull_flat, vis_list, stats);
