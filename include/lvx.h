@@ -164,6 +164,8 @@ int lvx_scan(const uint32_t *base, const uint8_t *cull_base, int64_t n_voxels,
  * the ordering pass writes tight_cnt[v] and, at offsets[v] + 0 .. tight_cnt[v], the tight
  * fragments' segment ids and their slots in the full list.  Acceleration only: `frags`, offsets and
  * the ray-test counts are the reference's. */
+/* largest frag_capacity (and fragment total) lvx_scatter accepts; larger -> LVX_E_ARG */
+int64_t lvx_max_fragments(void);
 int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double rt, double r_tight, int res, int method,
                 const uint8_t *cull_flat /* NULL = no culling */, const uint32_t *vis_list,
                 const uint32_t *offsets, uint32_t *cursor, uint32_t *frags, int64_t frag_capacity,

@@ -57,6 +57,7 @@ SIGNATURES = {
     "lvx_list_words": (_L, [_L]),
     "lvx_scan_scratch_bytes": (_L, [_L]),
     "lvx_scan": (_I, [_P, _P, _L, _P, _P, _P, _P]),
+    "lvx_max_fragments": (_L, []),
     "lvx_segment_order_scratch_words": (_L, [_L, _I, _I]),
     "lvx_segment_order": (_I, [_P, _P, _L, _I, _I, _P, _P, _P]),
     "lvx_scatter": (_I, [_P, _P, _L, _D, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P, _P]),

@@ -56,8 +56,8 @@ def scan_offsets(pyramid, culling=None, capacity=None, _stats=None) -> OffsetTab
     total = int(stats[N.ST_FRAG_TOTAL].item())
     if capacity is not None and total > capacity:
         raise ABufferError(f"fragment total {total} exceeds capacity {capacity}")
-    if total >= 2 ** 32:
-        raise ABufferError(f"fragment total {total} exceeds the 32-bit offset range")
+    if total > ops.max_fragments():
+        raise ABufferError(f"fragment total {total} exceeds the A-buffer limit of {ops.max_fragments()} fragments")
     return OffsetTable(offsets, total)
 
 

@@ -509,6 +509,8 @@ int lvx_scan(const uint32_t *base, const uint8_t *cull_base, int64_t n_voxels, u
     return LVX_OK;
 }
 
+int64_t lvx_max_fragments(void) { return (int64_t)LVX_CURSOR_CULLED - 1; }
+
 int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double rt, double r_tight, int res, int method,
                 const uint8_t *cull_flat, const uint32_t *vis_list, const uint32_t *offsets, uint32_t *cursor,
                 uint32_t *frags, int64_t frag_capacity, uint32_t *tight_frags, uint16_t *tight_slot, uint16_t *tight_cnt,

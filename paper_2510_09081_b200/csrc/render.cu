@@ -60,6 +60,10 @@ __device__ __forceinline__ bool surely_misses_f32(float Cx, float Cy, float Cz, 
     const float dw = fmaf(Dx, wx, fmaf(Dy, wy, Dz * wz)), de = fmaf(Dx, ex, fmaf(Dy, ey, Dz * ez));
     const float ee = fmaf(ex, ex, fmaf(ey, ey, ez * ez)), ew = fmaf(ex, wx, fmaf(ey, wy, ez * wz));
     const float den = fmaf(-de, de, ee);                    // |D| = 1
+    // Nearly parallel ray and segment: den = ee sin^2(angle) carries ~1e-7 ee of rounding, so below
+    // sin^2 = 1e-4 the closest-pair parameter would be noise and the distance an OVER-estimate of up to
+    // ~2e-3 voxel^2 -- more than the margin.  Such pairs go to the exact f64 test instead.
+    if (ee > 1e-12f && !(den > 1e-4f * ee)) return false;
     float sr = 0.f;                                         // parameter on the ray stretch
     if (den > 1e-12f) sr = fminf(fmaxf(__fdividef(fmaf(dw, ee, -de * ew), den), -h), h);
     float u = 0.f;                                          // parameter on the segment

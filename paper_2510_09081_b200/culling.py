@@ -106,6 +106,7 @@ class ErodedField:
     def __init__(self, base_dev, resolution):
         self.base_dev, self.resolution = base_dev, resolution
         self.shape = (resolution,) * 3
+        self.has_counts = True      # False for a plain occupancy field: `occupied` must then be given
 
 
 def erode(field) -> ErodedField:
@@ -118,9 +119,14 @@ def erode(field) -> ErodedField:
     res = f.shape[0]
     if f.shape != (res, res, res):
         raise ValueError("field must be cubic")
-    q = np.rint(np.clip(f, 0.0, 1.0) * 4096.0).astype(np.int32)
+    # Only `eroded >= THETA_BLOCK` is ever consumed (lv/culling.py:186) and erosion (a neighbourhood min)
+    # commutes with any monotone quantisation, so an arbitrary field is mapped onto the kernel's integer
+    # predicate occ_q >= 4092 exactly: >= 0.999 -> 4096, below -> at most 4091.
+    q = np.where(f >= THETA_BLOCK, 4096.0, np.minimum(np.floor(np.clip(f, 0.0, 1.0) * 4096.0), 4091.0)).astype(np.int32)
     dev = torch.device("cuda", torch.cuda.current_device())
-    return ErodedField(torch.from_numpy(q.reshape(-1)).to(dev), res)
+    out = ErodedField(torch.from_numpy(q.reshape(-1)).to(dev), res)
+    out.has_counts = False
+    return out
 
 
 def compute_visibility(eroded, g: GridDesc, cam: Camera, occupied=None) -> CullingPyramid:
@@ -133,6 +139,9 @@ def compute_visibility(eroded, g: GridDesc, cam: Camera, occupied=None) -> Culli
         eroded = erode(eroded)
     if eroded.resolution != res or (occupied is not None and tuple(occupied.shape) != (res,) * 3):
         raise ValueError("field shape does not match grid")
+    if occupied is None and not eroded.has_counts:
+        raise ValueError("compute_visibility: `occupied` is required when `eroded` is a plain field "
+                         "(lv/culling.py:203); only a pyramid handle carries the counts")
     base = eroded.base_dev
     dev = base.device
     if occupied is not None:

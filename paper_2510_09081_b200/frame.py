@@ -62,6 +62,8 @@ class FrameEngine:
         self.shading = ("demand" if mode == "opaque" else "all") if shading == "auto" else shading
         if self.shading == "demand" and mode != "opaque":
             raise ValueError("shading on demand needs opaque mode")
+        if int(res) < 4 or int(res) & (int(res) - 1):
+            raise ValueError(f"FrameEngine needs a power-of-two grid resolution >= 4, got {res}")
         self.torch = torch
         self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.res, self.w, self.h = int(res), int(width), int(height)
@@ -122,6 +124,7 @@ class FrameEngine:
         import os
         self.order_brick = min(int(os.environ.get("LVX_ORDER_BRICK", str(max(8, self.res // 16)))), self.res)
         self._stats_host = self._done = self._side = self._ev_side = self._pending = None
+        self._geom_stats = self._geom_ms = None
         self._overlapped = False
 
     def kernel_launches_per_frame(self) -> int:
@@ -168,11 +171,15 @@ class FrameEngine:
         self._verts32.copy_(verts, non_blocking=True)
 
     def fit(self, radius_voxels=None, radius_world=None):
-        """fit_grid with the AABB reduced on the GPU (one 24-byte read-back)."""
+        """lv/grid.py:51-80 fit_grid with LineSet.aabb() (lv/lineset.py:81-82) reduced on the GPU (one
+        24-byte read-back).  Exactly one of `radius_voxels` (the radius is re-derived from the voxel
+        size) and `radius_world` (the line set's own radius) must be given."""
+        if (radius_voxels is None) == (radius_world is None):
+            raise ValueError("fit() needs exactly one of radius_voxels and radius_world")
         lo, hi = ops.aabb(self._verts32)
 
         class _L:
-            radius = radius_world if radius_world is not None else 1.0
+            radius = radius_world
         return fit_grid(_L, self.res, radius_voxels=radius_voxels, aabb=(lo, hi))
 
     # ------------------------------------------------------------------ stages
@@ -263,39 +270,83 @@ class FrameEngine:
 
     # ------------------------------------------------------------------ frame
     def _ensure_capacity(self, need: int):
+        limit = ops.max_fragments()
+        if need > limit:
+            raise ABufferError(f"fragment total {need} exceeds the A-buffer limit of {limit} fragments")
         if need > self.frags.numel():
-            cap = int(need * 1.25) + 1024
-            if cap >= 2 ** 32:
-                cap = need
+            cap = min(int(need * 1.25) + 1024, limit)      # head-room never pushes a valid total over the limit
             self.frags = self.torch.empty(cap, dtype=self.torch.int32, device=self.dev)
             self.tight = ops.TightIndex(cap, self.V, self.dev)
 
-    def run(self, cam, grid: GridDesc, r_world: float, tile=None, seg_range=None, after_voxelize=None):
+    def run(self, cam, grid: GridDesc, r_world: float, tile=None, seg_range=None, after_voxelize=None,
+            geometry=True):
         """One frame on the already loaded vertices.  `after_voxelize(engine)` is the hook where the
-        multi-GPU path all-reduces the occupancy grid (distributed.py).  Returns FrameResult."""
-        self.submit(cam, grid, r_world, tile, seg_range, after_voxelize)
+        multi-GPU path all-reduces the occupancy grid (distributed.py).  `geometry=False` keeps the
+        grid, pyramid and uploaded line set of the previous frame and redoes only the camera-dependent
+        stages (cull -> trace), like lv/pipeline.py:89-136 without cfg.revoxelize.  Returns FrameResult."""
+        self.submit(cam, grid, r_world, tile, seg_range, after_voxelize, geometry)
         return self.collect()
 
-    def submit(self, cam, grid: GridDesc, r_world: float, tile=None, seg_range=None, after_voxelize=None):
-        """Enqueue one frame on the current CUDA stream without waiting for it (`collect` does).
-        Two engines on two streams can so keep two frames of a sequence in flight: the stages are
-        latency-bound walks that leave issue slots free, and a second frame's kernels fill them."""
-        if cam.width != self.w or cam.height != self.h:
-            raise ValueError("camera size does not match the engine's image size")
+    def run_geometry(self, grid: GridDesc, r_world: float, seg_range=None, after_voxelize=None):
+        """lv/pipeline.py:68-87 build_geometry on the loaded vertices: upload + voxelize + mips, one
+        sync.  Returns {"voxels_visited", "saturated", "upload_ms", "voxelize_ms", "mips_ms"}; later
+        `run(..., geometry=False)` frames reuse the result."""
+        t = self.torch
+        self._prepare_host()
+        ev = self._ev
+        ops.stats_reset(self.stats)
+        ev[0].record()
+        self._stage_upload(grid, r_world); ev[1].record()
+        self._stage_voxelize(seg_range, after_voxelize); ev[2].record()
+        self._stage_mips(); ev[3].record()
+        self._stats_host[:N.STATS_WORDS].copy_(self.stats, non_blocking=True)
+        self._done.record()
+        self._done.synchronize()
+        st = self._stats_host.numpy().copy()
+        if st[N.ST_NEED_WIDE] and not self.use_wide:
+            self.use_wide = True
+            return self.run_geometry(grid, r_world, seg_range, after_voxelize)
+        self._check_lines(st)
+        self._geom_stats = st[:N.STATS_WORDS].copy()
+        self._geom_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
+        return {"voxels_visited": int(st[N.ST_VISITED]), "saturated": int(st[N.ST_SATURATED]),
+                "upload_ms": self._geom_ms[0], "voxelize_ms": self._geom_ms[1], "mips_ms": self._geom_ms[2]}
+
+    def _prepare_host(self):
         t = self.torch
         if self._stats_host is None:
             self._stats_host = t.empty(N.STATS_WORDS + 2, dtype=t.int64).pin_memory()
             self._done = t.cuda.Event()
             self._side = t.cuda.Stream(device=self.dev)
             self._ev_side = [t.cuda.Event(enable_timing=True) for _ in range(2)]
-        self._pending = (cam, grid, r_world, tile, seg_range, after_voxelize)
+
+    @staticmethod
+    def _check_lines(st):
+        if st[N.ST_DEGENERATE]:
+            from .lineset import LineSetError
+            raise LineSetError(f"degenerate polyline {int(st[N.ST_DEGENERATE]) - 1}: all vertices coincide")
+
+    def submit(self, cam, grid: GridDesc, r_world: float, tile=None, seg_range=None, after_voxelize=None,
+               geometry=True):
+        """Enqueue one frame on the current CUDA stream without waiting for it (`collect` does).
+        Two engines on two streams can so keep two frames of a sequence in flight: the stages are
+        latency-bound walks that leave issue slots free, and a second frame's kernels fill them."""
+        if cam.width != self.w or cam.height != self.h:
+            raise ValueError("camera size does not match the engine's image size")
+        if not geometry and (self.lines is None or self._geom_stats is None):
+            raise ValueError("geometry=False needs a previous run_geometry() / full frame")
+        t = self.torch
+        self._prepare_host()
+        self._pending = (cam, grid, r_world, tile, seg_range, after_voxelize, geometry)
         ev = self._ev
         ops.stats_reset(self.stats)
-        ev[0].record()
-        self._stage_upload(grid, r_world); ev[1].record()
-        self._stage_voxelize(seg_range, after_voxelize)
-        ev[2].record()
-        self._stage_mips(); ev[3].record()
+        if geometry:
+            ev[0].record()
+            self._stage_upload(grid, r_world); ev[1].record()
+            self._stage_voxelize(seg_range, after_voxelize)
+            ev[2].record()
+            self._stage_mips()
+        ev[3].record()
         self._stage_cull(cam); ev[4].record()
         overlap = self.shading == "all" and self.overlap_shading
         if overlap:
@@ -334,13 +385,17 @@ class FrameEngine:
         for attempt in range(4):
             self._done.synchronize()           # the frame's only mandatory sync
             st = self._stats_host.numpy().copy()
+            geometry = self._pending[6]
+            if geometry:
+                self._geom_stats = st[:N.STATS_WORDS].copy()
+            else:       # the voxelize-stage words of the frame that built the geometry
+                for w in (N.ST_VISITED, N.ST_SATURATED, N.ST_NEED_WIDE, N.ST_DEGENERATE, N.ST_OCC_SAT):
+                    st[w] = self._geom_stats[w]
             if st[N.ST_NEED_WIDE] and not self.use_wide:
                 self.use_wide = True               # a 16-bit count wrapped: exact 64-bit path from now on
                 self.submit(*self._pending)
                 continue
             total = int(st[N.ST_FRAG_TOTAL])
-            if total >= 2 ** 32:
-                raise ABufferError(f"fragment total {total} exceeds the 32-bit offset range")
             if total > self.frags.numel():
                 self._ensure_capacity(total)
                 self.submit(*self._pending)
@@ -348,13 +403,14 @@ class FrameEngine:
             break
         else:
             raise RuntimeError("frame did not converge")
-        if st[N.ST_DEGENERATE]:
-            from .lineset import LineSetError
-            raise LineSetError(f"degenerate polyline {int(st[N.ST_DEGENERATE]) - 1}: all vertices coincide")
+        self._check_lines(st)
         if st[N.ST_MISMATCH] and st[N.ST_SATURATED] == 0:
             raise ABufferError("fragment count mismatch between passes (nondeterministic traversal?)")
         out = FrameResult(self)
-        out.stage_ms = {s: ev[i].elapsed_time(ev[i + 1]) for i, s in enumerate(STAGES)}
+        if geometry:
+            self._geom_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
+        out.stage_ms = {s: (ev[i].elapsed_time(ev[i + 1]) if i >= 3 else (self._geom_ms[i] if geometry else 0.0))
+                        for i, s in enumerate(STAGES)}
         out.trace_kernel_ms = out.stage_ms["trace"]
         if self.shading == "demand":   # events 6..9 bracket trace_hits, shade, resolve
             out.stage_ms["trace"] = ev[6].elapsed_time(ev[7]) + ev[8].elapsed_time(ev[9])

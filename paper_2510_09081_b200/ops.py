@@ -207,6 +207,11 @@ def scan(base, cull_base, offsets, scratch, stats):
 TIGHT_MARGIN = 1e-3   # voxels; see csrc/abuffer.cu "Loose bits"
 
 
+def max_fragments() -> int:
+    """Largest fragment total / capacity lvx_scatter accepts (cursor values above it mark culled voxels)."""
+    return int(lib().lvx_max_fragments())
+
+
 class TightIndex:
     """Per-voxel index of the fragments whose capsule can reach into the voxel (csrc/abuffer.cu): the
     ordering pass compacts them to the front of each list's range.  `frags` i32 [capacity],

@@ -29,8 +29,18 @@ def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+def _fingerprint(a: np.ndarray) -> bytes:
+    """Content hash of a host array (blake2b, ~1 GB/s): the device copy of a LineSet is reused only while
+    the host vertices are byte-identical, so in-place edits of `ls.vertices` are never missed."""
+    import hashlib
+    return hashlib.blake2b(np.ascontiguousarray(a).view(np.uint8).reshape(-1), digest_size=16).digest()
+
+
 def upload_lineset(ls: LineSet, g: GridDesc, r_world=None, cn="device", stats=None) -> ops.DeviceLines:
-    """Host LineSet -> DeviceLines (cached on the LineSet per grid/radius/normal mode).
+    """Host LineSet -> DeviceLines.  The reference recomputes segment_arrays on every call
+    (lv/voxelizer.py:480, lv/abuffer.py:284, lv/raytracer.py:675); here the device copy is kept on the
+    LineSet and reused while grid, radius, the clip-normal array (same object) and the CONTENT of
+    `ls.vertices` / `ls.polyline_offsets` are unchanged.
 
     cn: "device" computes clip normals on the GPU (lv/lineset.py:213-242); None disables
     clipping (lv/voxelizer.py:440-442); an (N,3) array (numpy or cuda tensor) is used as given.
@@ -38,15 +48,19 @@ def upload_lineset(ls: LineSet, g: GridDesc, r_world=None, cn="device", stats=No
     torch = N.require_cuda()
     dev = _device()
     r_world = float(ls.radius if r_world is None else r_world)
-    mode = "device" if isinstance(cn, str) else ("none" if cn is None else id(cn))
-    key = (dev.index, g.resolution, g.voxel_size, tuple(float(x) for x in g.world_min), r_world, mode)
+    mode = "device" if isinstance(cn, str) else ("none" if cn is None else "given")
+    key = (dev.index, g.resolution, g.voxel_size, tuple(float(x) for x in g.world_min), r_world, mode,
+           _fingerprint(ls.vertices), _fingerprint(ls.polyline_offsets))
     cache = ls.__dict__.setdefault("_lvx_device_cache", {})
-    if key in cache:
-        return cache[key]
+    hit = cache.get("entry")
+    # the entry holds a reference to the normals array it was built from: `is` cannot be fooled by a
+    # recycled id(), and a host array's content is part of the key
+    if hit is not None and hit[0] == key and (mode != "given" or (hit[1] is cn and hit[2] == _cn_fingerprint(cn))):
+        return hit[3]
     v32 = torch.from_numpy(ls.vertices).to(dev, non_blocking=True)
     off = torch.from_numpy(ls.polyline_offsets).to(dev, non_blocking=True)
     normals = None
-    if not isinstance(cn, str) and cn is not None:
+    if mode == "given":
         normals = cn if torch.is_tensor(cn) else torch.from_numpy(np.ascontiguousarray(cn, dtype=np.float64))
         normals = normals.to(dev, dtype=torch.float64).contiguous()
         if tuple(normals.shape) != (ls.n_vertices, 3):
@@ -60,9 +74,17 @@ def upload_lineset(ls: LineSet, g: GridDesc, r_world=None, cn="device", stats=No
         if bad:
             from .lineset import LineSetError
             raise LineSetError(f"degenerate polyline {bad - 1}: all vertices coincide")
-    cache.clear()          # one entry: a LineSet is re-gridded rarely and the arrays are big
-    cache[key] = lines
+    # one entry: a LineSet is re-gridded rarely and the arrays are big
+    cache["entry"] = (key, cn if mode == "given" else None, _cn_fingerprint(cn) if mode == "given" else None, lines)
     return lines
+
+
+def _cn_fingerprint(cn):
+    """Host normals are hashed; device tensors are identified by storage pointer + version counter
+    (bumped by every in-place torch op)."""
+    if hasattr(cn, "data_ptr"):
+        return (cn.data_ptr(), cn._version, tuple(cn.shape))
+    return _fingerprint(np.asarray(cn))
 
 
 def compute_clip_normals(ls: LineSet):

@@ -157,10 +157,44 @@ def unit_vectors():
     print("unit_vectors", n, flush=True)
 
 
+def dumps_and_stats():
+    """On-disk formats either side of the path and the frame entry's `stats`:
+    the reference's own writers (VOXP lv/voxelizer.py:414-419, CULP lv/culling.py:97-100, ABUF
+    lv/abuffer.py:133-138, PPM/HITI lv/raytracer.py:85-91) are run on golden scenes and the sha256 + size
+    of every file is committed, together with the non-timing `stats` of `run_once` (lv/pipeline.py:153-156)
+    and `LineSet.aabb()` (lv/lineset.py:81-82)."""
+    import tempfile
+    out = {}
+    for name in ("helix32_vsv", "walk32_inside_cam", "diag32_thick_vsv", "walk32_transp_k2", "helix64_vcsv", "diag_vcsv"):
+        kw, _ = SCENES[name]
+        pipe = lv.ScenePipeline(lv.PipelineConfig(**kw))
+        img = pipe.render_frame()
+        files = {}
+        with tempfile.TemporaryDirectory() as d:
+            pre = os.path.join(d, "f")
+            pipe.dump_intermediates(pre)
+            img.save_ppm(pre + ".ppm")
+            img.save_hit_ids(pre + ".hiti")
+            for ext in ("voxp", "culp", "abuf", "ppm", "hiti"):
+                if os.path.exists(f"{pre}.{ext}"):
+                    b = open(f"{pre}.{ext}", "rb").read()
+                    files[ext] = {"sha256": hashlib.sha256(b).hexdigest(), "bytes": len(b)}
+        lo, hi = pipe.ls.aabb()
+        stats = {k: v for k, v in pipe.stats.items() if not k.endswith("_ms")}
+        stats["culled_fraction"] = float(stats["culled_fraction"]).hex()
+        out[name] = {"files": files, "stats": stats, "stats_keys": sorted(pipe.stats),
+                     "aabb": {"lo": [float(x).hex() for x in lo], "hi": [float(x).hex() for x in hi]}}
+        print("dumps", name, {k: v["bytes"] for k, v in files.items()}, stats, flush=True)
+    with open(os.path.join(OUT, "dumps.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
 if __name__ == "__main__":
     only = sys.argv[1:]
     if not only or "unit" in only:
         unit_vectors()
+    if not only or "dumps" in only:
+        dumps_and_stats()
     for name, (kw, full) in SCENES.items():
         if only and name not in only:
             continue
