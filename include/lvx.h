@@ -51,6 +51,7 @@ enum {
     LVX_ST_OCCUPIED = 10,    /* voxels with count > 0 */
     LVX_ST_OCC_SAT = 11,     /* voxels whose 16-bit occupancy sum saturated */
     LVX_ST_TILE_CURSOR = 12, /* scratch: pixel-tile queue of the persistent trace kernels (reset by every launch) */
+    LVX_ST_OWNED = 13,       /* voxels a screen tile owns (lvx_tile_owners) */
     LVX_STATS_WORDS = 16
 };
 
@@ -146,6 +147,18 @@ int lvx_occupied_pyramid(const uint32_t *base, int res, uint8_t *cull_flat, uint
  * bits (u64), entries (flat voxel indices, unordered) from word 16.  The A-buffer ordering pass
  * and the shading kernel iterate this list instead of the whole volume. */
 int64_t lvx_list_words(int64_t n_voxels);
+
+/* ---- screen-tile ownership (multi-GPU screen tiles; no counterpart in the reference, whose only
+ * decomposition is by segment chunk, lv/voxelizer.py:461-463).  owner_flat (lvx_pyramid_elems(res) u8,
+ * all levels) / owner_list (lvx_list_words(V)) = the set bits of cull_flat's level 0 whose voxel cube,
+ * grown by `margin` voxels, meets the sub-frustum of the pixel rect [x0,x1) x [y0,y1) of `cam`
+ * (conservative).  A rank that traces only this rect passes them to lvx_scan / lvx_scatter / lvx_shade
+ * in place of the culling pyramid and keeps the FULL pyramid for lvx_march_levels: its rays then step
+ * exactly as on one GPU and find the reference's fragment lists in every voxel they visit.  margin
+ * >= 1.5 also covers the 8 trilinear AO/shadow taps of any hit (lv/raytracer.py:368-390). */
+int lvx_tile_owners(const uint8_t *cull_flat, int res, const lvx_camera *cam_host, int tile_x0, int tile_y0,
+                    int tile_x1, int tile_y1, double margin, uint8_t *owner_flat, uint32_t *owner_list,
+                    uint64_t *stats, void *stream);
 
 /* ---- A-buffer: lv/abuffer.py:104-114 scan_offsets; 195-255 _chunk_count_kernel/_write_kernel.
  * offsets has V+1 entries (u32): offsets[i] = exclusive scan of the culling-masked counts,

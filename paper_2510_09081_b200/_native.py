@@ -16,6 +16,7 @@ LIB_PATH = os.environ.get("LVX_LIB") or os.path.join(_HERE, "liblvx_b200.so")
 # stats block indices (include/lvx.h)
 ST_VISITED, ST_SATURATED, ST_NEED_WIDE, ST_SOLID, ST_FRAG_TOTAL, ST_MISMATCH, ST_RAY_TESTS, \
     ST_LONG_LISTS, ST_DEGENERATE, ST_VISIBLE, ST_OCCUPIED, ST_OCC_SAT = range(12)
+ST_OWNED = 13
 STATS_WORDS = 16
 
 
@@ -55,6 +56,7 @@ SIGNATURES = {
     "lvx_cull": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "lvx_occupied_pyramid": (_I, [_P, _I, _P, _P, _P, _P]),
     "lvx_list_words": (_L, [_L]),
+    "lvx_tile_owners": (_I, [_P, _I, _P, _I, _I, _I, _I, _D, _P, _P, _P, _P]),
     "lvx_scan_scratch_bytes": (_L, [_L]),
     "lvx_scan": (_I, [_P, _P, _L, _P, _P, _P, _P]),
     "lvx_max_fragments": (_L, []),

@@ -175,14 +175,46 @@ __device__ __forceinline__ bool segment_misses_cube(float ax, float ay, float az
 #ifndef LVX_SCAT_MINB
 #define LVX_SCAT_MINB 1
 #endif
+// lv/abuffer.py:145-181 _segment_visible: does the segment's inflated voxel box
+// floor(min - rt) .. floor(max + rt) overlap a set voxel of the culling pyramid?  The reference runs a
+// depth-first search from the root; here the box is looked up at the finest level where it spans at
+// most two nodes per axis (<= 8 byte loads from a level that is a few KiB..MiB and stays in L1/L2).
+// The answer may be "yes" where the reference's exact search says "no" -- never the other way round --
+// and the per-cell culled test below then skips every cell of such a segment, so `fragments` is the
+// reference's array either way (the reference itself treats this test as an acceleration, 252-253).
+struct PyrOffsets { uint32_t off[12]; int n_levels; };
+__device__ __forceinline__ bool segment_visible(const uint8_t *__restrict__ flat, const PyrOffsets &O, int res,
+                                                const d3 &a, const d3 &b, double rt) {
+    int lo[3], hi[3];
+    lo[0] = (int)floor(fmin(a.x, b.x) - rt); hi[0] = (int)floor(fmax(a.x, b.x) + rt);
+    lo[1] = (int)floor(fmin(a.y, b.y) - rt); hi[1] = (int)floor(fmax(a.y, b.y) + rt);
+    lo[2] = (int)floor(fmin(a.z, b.z) - rt); hi[2] = (int)floor(fmax(a.z, b.z) + rt);
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        lo[k] = max(lo[k], 0); hi[k] = min(hi[k], res - 1);
+        if (hi[k] < lo[k]) return false;                  // entirely outside the grid: no cell at all
+    }
+    int l = 0;
+    while (l < O.n_levels - 1 && (((hi[0] >> l) - (lo[0] >> l)) > 1 || ((hi[1] >> l) - (lo[1] >> l)) > 1 ||
+                                  ((hi[2] >> l) - (lo[2] >> l)) > 1)) l++;
+    const uint32_t rl = (uint32_t)res >> l;
+    const uint8_t *lev = flat + O.off[l];
+    for (int z = lo[2] >> l; z <= hi[2] >> l; z++)
+        for (int y = lo[1] >> l; y <= hi[1] >> l; y++)
+            for (int x = lo[0] >> l; x <= hi[0] >> l; x++)
+                if (lev[(uint32_t)x + rl * ((uint32_t)y + rl * (uint32_t)z)]) return true;
+    return false;
+}
+
 __global__ void __launch_bounds__(128, LVX_SCAT_MINB)
 k_scatter(const double *__restrict__ verts, const int32_t *__restrict__ segs, int64_t n_seg, double rt,
-          float r_tight, int res, int method, uint32_t *__restrict__ cursor,
-          uint32_t *__restrict__ frags, int64_t cap) {
+          float r_tight, int res, int method, const uint8_t *__restrict__ own_flat, const PyrOffsets O,
+          uint32_t *__restrict__ cursor, uint32_t *__restrict__ frags, int64_t cap) {
     const int64_t si = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (si >= n_seg) return;
     const int64_t i = segs[si];
     const d3 a = ld3(verts + 3 * i), b = ld3(verts + 3 * i + 3);
+    if (own_flat && !segment_visible(own_flat, O, res, a, b, rt)) return;
     const int64_t res64 = res;
     // f32 view of the segment for the loose test.  Cells whose centre is farther than
     // r_tight + sqrt(3)/2 from the segment are loose without the separating-direction search.
@@ -433,7 +465,10 @@ k_order(const uint32_t *__restrict__ offsets, const uint32_t *__restrict__ curso
             const uint32_t e = offsets[v + 1];
             n = e - b;
             if (cursor[v] != e) stats[LVX_ST_MISMATCH] = 1;   // lv/abuffer.py:310-311
-            if ((int64_t)e > cap) n = 0;                      // never touch memory past the buffer
+            if ((int64_t)e > cap) {                           // never touch memory past the buffer; the frame is
+                n = 0;                                        // redone with a larger one, but the tracer of THIS
+                if (T.cnt) T.cnt[v] = 0;                      // frame still runs: no stale tight count for it
+            }
         }
         n_long += __popc(__ballot_sync(0xffffffffu, n > 32));
         // short lists by size class, several lists per warp step
@@ -526,9 +561,16 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
     if (want_tight != (tight_slot != nullptr) || want_tight != (tight_cnt != nullptr)) return LVX_E_ARG;
     if (!want_tight) r_tight = -1.0;
     // (tight_cnt needs no clearing: it is only read for voxels whose list the ordering pass wrote)
+    PyrOffsets O;
+    {
+        const LevelOffsets L = make_level_offsets(res);
+        if (L.n_levels > 12) return LVX_E_ARG;
+        for (int l = 0; l < 12; l++) O.off[l] = l < L.n_levels ? (uint32_t)L.off[l] : 0u;
+        O.n_levels = L.n_levels;
+    }
     if (n_seg > 0)
         k_scatter<<<blocks_for(n_seg, 128), 128, 0, s>>>(verts, segs, n_seg, rt, (float)r_tight, res, method,
-                                                        cursor, frags, frag_capacity);
+                                                        cull_flat, O, cursor, frags, frag_capacity);
     {
         unsigned nb = 148 * 8;   // persistent: 148 SMs x 8 CTAs of 8 warps
         const unsigned need = blocks_for((V + 31) / 32, ORDER_WARPS);

@@ -585,6 +585,42 @@ k_occupied(const uint32_t *__restrict__ base, int64_t V, uint8_t *__restrict__ o
     list_append_items<4>(vis_list, mask, (uint32_t)idx0, (unsigned long long *)&stats[LVX_ST_VISIBLE]);
 }
 
+// Screen-tile ownership (multi-GPU screen tiles): owner = visible AND the voxel's cube,
+// grown by `margin`, meets the tile's sub-frustum -- the pyramid whose apex is the camera and whose four
+// side planes pass through the tile's pixel EDGES (every pixel-centre ray of the tile lies inside).  A
+// cube [c - h, c + h] meets the half-space {q : q.n >= 0} (q relative to the apex) iff
+// (c - apex).n + h |n|_1 >= 0; passing all four tests is the usual conservative box/frustum test (it may
+// keep a few cubes outside, never drops one that a ray can visit).  The A-buffer build of a rank is
+// restricted to its owners; the MARCH bits stay the full culling pyramid, so every ray steps exactly as
+// it does on one GPU and only ever visits voxels its rank owns.
+struct TilePlanes { double apex[3]; double n[4][3]; double h; };
+__global__ void __launch_bounds__(256)
+k_owner(const uint8_t *__restrict__ cull0, int res, int64_t V, const TilePlanes P, uint8_t *__restrict__ out,
+        uint32_t *__restrict__ list, uint64_t *__restrict__ stats) {
+    const int64_t idx0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    uint32_t mask = 0;
+    if (idx0 < V) {
+        const uchar4 c = *reinterpret_cast<const uchar4 *>(cull0 + idx0);
+        const uint8_t vs[4] = {c.x, c.y, c.z, c.w};
+        const int x0 = (int)(idx0 % res), y = (int)((idx0 / res) % res), z = (int)(idx0 / ((int64_t)res * res));
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (!vs[k]) continue;
+            const double qx = (x0 + k) + 0.5 - P.apex[0], qy = y + 0.5 - P.apex[1], qz = z + 0.5 - P.apex[2];
+            bool in = true;
+#pragma unroll
+            for (int p = 0; p < 4; p++) {
+                const double d = qx * P.n[p][0] + qy * P.n[p][1] + qz * P.n[p][2]
+                                 + P.h * (fabs(P.n[p][0]) + fabs(P.n[p][1]) + fabs(P.n[p][2]));
+                in = in && d >= 0.0;
+            }
+            if (in) mask |= 1u << k;
+        }
+        *reinterpret_cast<uchar4 *>(out + idx0) = make_uchar4(mask & 1u, (mask >> 1) & 1u, (mask >> 2) & 1u, (mask >> 3) & 1u);
+    }
+    list_append_items<4>(list, mask, (uint32_t)idx0, (unsigned long long *)&stats[LVX_ST_OWNED]);
+}
+
 // lv/culling.py:103-109: parent = OR of its 8 children
 __global__ void __launch_bounds__(256)
 k_ormip(const uint8_t *__restrict__ src, int rsrc, uint8_t *__restrict__ out) {
@@ -748,6 +784,34 @@ int lvx_occupied_pyramid(const uint32_t *base, int res, uint8_t *cull_flat, uint
     k_occupied<<<blocks_for(V / 4, 256), 256, 0, s>>>(base, V, cull_flat, vis_list, stats);
     LVX_LAUNCH_CHECK();
     return or_mips(cull_flat, res, s);
+}
+
+int lvx_tile_owners(const uint8_t *cull_flat, int res, const lvx_camera *cam, int tile_x0, int tile_y0, int tile_x1,
+                    int tile_y1, double margin, uint8_t *owner_flat, uint32_t *owner_list, uint64_t *stats, void *stream) {
+    if (!pow2(res) || !cull_flat || !cam || !owner_flat || !owner_list) return LVX_E_ARG;
+    if (cam->width <= 0 || cam->height <= 0 || tile_x0 < 0 || tile_y0 < 0 || tile_x1 > cam->width || tile_y1 > cam->height ||
+        tile_x0 > tile_x1 || tile_y0 > tile_y1 || !(margin >= 0.0)) return LVX_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t V = (int64_t)res * res * res;
+    if (V & 3) return LVX_E_ARG;
+    // lv/raytracer.py:414-423 _pixel_ray: u = (2 (px + .5) / w - 1) aspect tan, v = (1 - 2 (py + .5) / h) tan.
+    // Pixel EDGES: px + .5 -> tile_x0 and tile_x1 (a half pixel wider than the outermost centres).
+    const double aspect = (double)cam->width / (double)cam->height, tf = cam->tan_half_fov;
+    const double u_lo = (2.0 * tile_x0 / cam->width - 1.0) * aspect * tf, u_hi = (2.0 * tile_x1 / cam->width - 1.0) * aspect * tf;
+    const double v_hi = (1.0 - 2.0 * tile_y0 / cam->height) * tf, v_lo = (1.0 - 2.0 * tile_y1 / cam->height) * tf;
+    TilePlanes P;
+    for (int a = 0; a < 3; a++) {
+        P.apex[a] = cam->pos[a];
+        P.n[0][a] = cam->right[a] - u_lo * cam->fwd[a];     // q.right >= u_lo q.fwd
+        P.n[1][a] = u_hi * cam->fwd[a] - cam->right[a];     // q.right <= u_hi q.fwd
+        P.n[2][a] = cam->up[a] - v_lo * cam->fwd[a];
+        P.n[3][a] = v_hi * cam->fwd[a] - cam->up[a];
+    }
+    P.h = 0.5 + margin;
+    LVX_CUDA(cudaMemsetAsync(owner_list, 0, 8, s));
+    k_owner<<<blocks_for(V / 4, 256), 256, 0, s>>>(cull_flat, res, V, P, owner_flat, owner_list, stats);
+    LVX_LAUNCH_CHECK();
+    return or_mips(owner_flat, res, s);
 }
 
 int lvx_march_levels(const uint8_t *bits_flat, int res, uint8_t *march, void *stream) {

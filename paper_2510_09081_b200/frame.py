@@ -125,6 +125,11 @@ class FrameEngine:
         self.order_brick = min(int(os.environ.get("LVX_ORDER_BRICK", str(max(8, self.res // 16)))), self.res)
         self._stats_host = self._done = self._side = self._ev_side = self._pending = None
         self._geom_stats = self._geom_ms = None
+        # tiled frames (`run(..., tile=rect)`): build the A-buffer only for the voxels the tile's rays can
+        # visit (see _stage_owners).  False = replicate the whole build on every rank.
+        self.tile_build = True
+        self._owned = False
+        self.owner_flat = self.owner_list = None
         self._overlapped = False
 
     def kernel_launches_per_frame(self) -> int:
@@ -139,6 +144,7 @@ class FrameEngine:
         n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
         n += 1 + pyramid(2)                         # mips: level 1 from the packed grid, then the rest
         n += (5 if self.strategy == "vcsv" else 1) + pyramid(1)   # solid, super-brick shadow, visibility, march, dilate | occupied; or-mips
+        n += 1 + pyramid(1) if self._owned else 0   # tile owners + their OR pyramid
         n += 1                                      # scan
         n += 3 + 1                                  # cursor init, scatter, order; march table
         n += 1 + pyramid(1) + 1                     # non-empty masks (level 0, the rest), shade
@@ -236,19 +242,40 @@ class FrameEngine:
             ops.occupied_pyramid(self.base, self.res, self.cull_flat, self.vis_list, self.stats)
         ops.march_levels(self.cull_flat, self.res, self.march)
 
+    def _stage_owners(self, cam, tile):
+        """Screen-tile ownership (multi-GPU screen tiles): the A-buffer build and all-voxel shading of
+        this frame are restricted to the visible voxels the tile's rays can visit (lvx_tile_owners); the
+        march bits stay the full culling pyramid, so the tile's pixels are the single-GPU frame's."""
+        full = tile is None or tuple(tile) == (0, 0, self.w, self.h)
+        self._owned = self.tile_build and not full
+        if not self._owned:
+            return
+        t = self.torch
+        if self.owner_flat is None:
+            self.owner_flat = t.empty_like(self.cull_flat)
+            self.owner_list = t.empty_like(self.vis_list)
+        ops.tile_owners(self.cull_flat, self.res, ops.make_camera_struct(cam, self.grid), tile,
+                        self.owner_flat, self.owner_list, self.stats)
+
+    def _owner_bits(self):
+        """(pyramid, list) of the voxels that own fragments this frame; pyramid None = every occupied voxel."""
+        if self._owned:
+            return self.owner_flat, self.owner_list
+        return (self.cull_flat if self.strategy == "vcsv" else None), self.vis_list
+
     def _stage_scan(self):
-        cull_base = self.cull_flat[:self.V] if self.strategy == "vcsv" else None
-        ops.scan(self.base, cull_base, self.offsets, self.scan_scratch, self.stats)
+        flat, _ = self._owner_bits()
+        ops.scan(self.base, None if flat is None else flat[:self.V], self.offsets, self.scan_scratch, self.stats)
 
     def _stage_scatter(self):
         rt = ops.footprint_radius(self.lines.r, self.r_min)
-        ops.scatter(self.lines, rt, self.res, self.method,
-                    self.cull_flat if self.strategy == "vcsv" else None, self.vis_list,
+        flat, lst = self._owner_bits()
+        ops.scatter(self.lines, rt, self.res, self.method, flat, lst,
                     self.offsets, self.cursor, self.frags, self.stats, tight=self.tight)
 
     def _stage_shade(self):
         demand = self.shading == "demand"
-        ops.shade(self.base, self.mips, self.res, self.need_list if demand else self.vis_list, self.dirs,
+        ops.shade(self.base, self.mips, self.res, self.need_list if demand else self._owner_bits()[1], self.dirs,
                   np.tan(AO_HALF_ANGLE), self.light, np.tan(SHADOW_HALF_ANGLE), self.ao, self.shadow,
                   self.shade_scratch, fill_ones=not demand, nz_bits=self.nz_bits if self._nz_valid else None)
 
@@ -347,7 +374,8 @@ class FrameEngine:
             ev[2].record()
             self._stage_mips()
         ev[3].record()
-        self._stage_cull(cam); ev[4].record()
+        self._stage_cull(cam)
+        self._stage_owners(cam, tile); ev[4].record()
         overlap = self.shading == "all" and self.overlap_shading
         if overlap:
             # cone tracing needs the pyramid and the visible-voxel list only: it runs beside the
@@ -420,7 +448,7 @@ class FrameEngine:
         else:
             if self._overlapped:   # shade ran beside scan+scatter: its own duration, and the join wait is not a stage
                 out.stage_ms["shade"] = self._ev_side[0].elapsed_time(self._ev_side[1])
-            shaded = int(st[N.ST_VISIBLE])
+            shaded = int(st[N.ST_OWNED]) if self._owned else int(st[N.ST_VISIBLE])
         occ = int(st[N.ST_OCCUPIED])
         out.stats = {
             "segments": self.lines.n_segments, "vertices": self.lines.n_vertices, "resolution": self.res,
@@ -431,5 +459,6 @@ class FrameEngine:
             "ray_capsule_tests": int(st[N.ST_RAY_TESTS]), "long_lists": int(st[N.ST_LONG_LISTS]),
             "occ_saturated_voxels": int(st[N.ST_OCC_SAT]), "wide_path": bool(self.use_wide),
             "shaded_voxels": shaded, "shading": self.shading,
+            "owned_voxels": int(st[N.ST_OWNED]) if self._owned else int(st[N.ST_VISIBLE]),
         }
         return out

@@ -195,6 +195,16 @@ def occupied_pyramid(base, res, cull_flat, vis_list, stats):
                                      _stream()), "lvx_occupied_pyramid")
 
 
+TILE_MARGIN = 1.5 + 1e-3   # voxels: the visited voxel's cube + the 8 trilinear AO/shadow taps of a hit in it
+
+
+def tile_owners(cull_flat, res, cam_struct, tile, owner_flat, owner_list, stats, margin=TILE_MARGIN):
+    """lvx_tile_owners: the visible voxels a rank tracing pixel rect `tile` = (x0, y0, x1, y1) needs."""
+    x0, y0, x1, y1 = (int(v) for v in tile)
+    check(lib().lvx_tile_owners(_ptr(cull_flat), res, C.byref(cam_struct), x0, y0, x1, y1, float(margin),
+                                _ptr(owner_flat), _ptr(owner_list), _ptr(stats), _stream()), "lvx_tile_owners")
+
+
 def scan_scratch_bytes(n_voxels: int) -> int:
     return int(lib().lvx_scan_scratch_bytes(n_voxels))
 

@@ -417,12 +417,73 @@ def test_screen_tiles_make_the_full_image(lvx, oracle, mode):
     e = lvx.FrameEngine(res, w, h, strategy=strategy, mode=mode, alpha=0.4, keep_rgb=True)
     e.set_topology(ls.polyline_offsets, ls.n_vertices)
     e.load_vertices(ls.vertices)
+    full = e.run(cam, g, r_world)
+    for tile_build in (True, False):
+        e.tile_build = tile_build
+        rgb = np.zeros((h, w, 3)); hit = np.full((h, w), -7, np.int32); tests = 0; frag_sum = 0
+        for (x0, y0, x1, y1) in D.tile_rects(w, h, 3):
+            out = e.run(cam, g, r_world, tile=(x0, y0, x1, y1))
+            rgb[y0:y1, x0:x1] = e.rgb.cpu().numpy()[y0:y1, x0:x1]
+            hit[y0:y1, x0:x1] = e.hit_id.cpu().numpy()[y0:y1, x0:x1]
+            tests += out.stats["ray_capsule_tests"]
+            frag_sum += out.stats["fragments"]
+            if tile_build:      # the build of a tile is restricted to the voxels its rays can visit
+                assert out.stats["owned_voxels"] < full.stats["visible_voxels"]
+                assert out.stats["fragments"] < full.stats["fragments"]
+            else:
+                assert out.stats["fragments"] == full.stats["fragments"]
+        assert np.array_equal(hit, ref.image.hit_id)
+        assert np.array_equal(rgb, ref.image.rgb)
+        assert tests == ref.image.stats["ray_capsule_tests"]
+        if tile_build:
+            assert frag_sum < 2 * full.stats["fragments"]       # three tiles together: little more than one full build
+
+
+@pytest.mark.parametrize("mode,inside", [("opaque", False), ("opaque", True), ("transparent", False), ("transparent", True)])
+def test_tile_owner_build_is_exact_on_rect_tiles(lvx, oracle, mode, inside):
+    """lvx_tile_owners on a 3 x 2 grid of pixel rects (all four frustum planes in play), camera outside and
+    inside the grid: per tile, the owners' lists are the reference's lists, every voxel the full frame's
+    rays of that tile hit is owned, and the assembled image is the oracle's."""
+    ls = lvx.generate("random_streamlines", seed=33, polylines=70, verts_per_line=50)
+    res, w, h = 64, 133, 94
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=0.45)
+    strategy = "vcsv" if mode == "opaque" else "vsv"
+    cfg = lvx.PipelineConfig(res=res, width=w, height=h, strategy=strategy, mode=mode, alpha=0.35)
+    cam = lvx.make_camera(cfg, g)
+    if inside:
+        centre = np.asarray(g.world_min) + 0.5 * res * g.voxel_size
+        cam = lvx.Camera(centre + np.array([1.3, -2.1, 0.7]) * g.voxel_size, np.array([0.3, 1.0, -0.2]),
+                         np.array([0.0, 0.0, 1.0]), np.deg2rad(70.0), w, h)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy=strategy, mode=mode, alpha=0.35)
+    e = lvx.FrameEngine(res, w, h, strategy=strategy, mode=mode, alpha=0.35, keep_rgb=True)
+    e.set_topology(ls.polyline_offsets, ls.n_vertices)
+    e.load_vertices(ls.vertices)
+    xs, ys = [0, 40, 41, w], [0, 50, h]       # one tile is a single pixel column
     rgb = np.zeros((h, w, 3)); hit = np.full((h, w), -7, np.int32); tests = 0
-    for (x0, y0, x1, y1) in D.tile_rects(w, h, 3):
-        out = e.run(cam, g, r_world, tile=(x0, y0, x1, y1))
-        rgb[y0:y1, x0:x1] = e.rgb.cpu().numpy()[y0:y1, x0:x1]
-        hit[y0:y1, x0:x1] = e.hit_id.cpu().numpy()[y0:y1, x0:x1]
-        tests += out.stats["ray_capsule_tests"]
+    ref_off = ref.abuf.table.offsets; ref_cnt = ref.abuf.table.counts
+    V = res ** 3
+    for y0, y1 in zip(ys[:-1], ys[1:]):
+        for x0, x1 in zip(xs[:-1], xs[1:]):
+            out = e.run(cam, g, r_world, tile=(x0, y0, x1, y1))
+            rgb[y0:y1, x0:x1] = e.rgb.cpu().numpy()[y0:y1, x0:x1]
+            hit[y0:y1, x0:x1] = e.hit_id.cpu().numpy()[y0:y1, x0:x1]
+            tests += out.stats["ray_capsule_tests"]
+            own = e.owner_flat[:V].cpu().numpy() != 0
+            assert own.sum() == out.stats["owned_voxels"]
+            vis = ref.culling.flat[:V] != 0 if ref.culling is not None else ref_cnt > 0
+            assert not (own & ~vis).any()                                    # owners are visible voxels
+            # the owners' lists are the reference's lists
+            offs = e.offsets.cpu().numpy().view(np.uint32).astype(np.int64)
+            cnt = np.diff(offs)
+            assert np.array_equal(cnt, np.where(own, ref_cnt, 0))
+            fr = e.frags[:out.stats["fragments"]].cpu().numpy().view(np.uint32)
+            idx = np.nonzero(own & (ref_cnt > 0))[0]
+            pick = idx[:: max(1, len(idx) // 400)]
+            for v in pick:
+                assert np.array_equal(fr[offs[v]:offs[v] + cnt[v]], ref.abuf.fragments[ref_off[v]:ref_off[v] + ref_cnt[v]])
+            # the OR pyramid above the owners
+            lv = oracle.culling_from_bits(own.reshape(res, res, res).astype(np.uint8))
+            assert np.array_equal(e.owner_flat.cpu().numpy(), lv.flat)
     assert np.array_equal(hit, ref.image.hit_id)
     assert np.array_equal(rgb, ref.image.rgb)
     assert tests == ref.image.stats["ray_capsule_tests"]

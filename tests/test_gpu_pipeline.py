@@ -406,3 +406,32 @@ def test_upload_cache_sees_in_place_edits(lvx, oracle):
     p4 = lvx.voxelize(ls, cn, g, r_world=rw)
     assert np.array_equal(p4.base, oracle.voxelize(ls, cn, g, r_world=rw).base)
     assert not np.array_equal(p3.base, p4.base)
+
+
+def test_fragment_buffer_overflow_is_redone_exactly(lvx, oracle):
+    """A frame whose fragment total exceeds the buffer sized by earlier frames: the overflowing attempt's
+    tracer must not follow stale tight counts past the buffer, and the redone frame equals the oracle."""
+    ls = lvx.generate("random_streamlines", seed=17, polylines=60, verts_per_line=40)
+    res = 32
+    g, rw = lvx.fit_grid(ls, res, radius_voxels=0.2)
+    cfg = lvx.PipelineConfig(res=res, width=64, height=48, strategy="vsv")
+    cam = lvx.make_camera(cfg, g)
+    eng = lvx.FrameEngine(res, 64, 48, strategy="vsv", keep_rgb=True)
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    eng.load_vertices(ls.vertices)
+    small = eng.run(cam, g, rw)
+    cap = eng.frags.numel()
+    # the same lines four times as thick (same grid): far more incidences than the buffer holds
+    big = eng.run(cam, g, 6.0 * rw)
+    assert big.stats["fragments"] > cap > small.stats["fragments"] and eng.frags.numel() >= big.stats["fragments"]
+    ref = oracle.run_frame(ls, g, 6.0 * rw, cam, cfg.light_vector(), strategy="vsv")
+    n = big.stats["fragments"]
+    assert n == ref.abuf.total
+    assert np.array_equal(eng.frags[:n].cpu().numpy().view(np.uint32), ref.abuf.fragments)
+    assert np.array_equal(eng.hit_id.cpu().numpy(), ref.image.hit_id)
+    assert np.array_equal(eng.rgb.cpu().numpy(), ref.image.rgb)
+    # and back: the thin frame after the thick one (stale tight counts of voxels that lost fragments)
+    again = eng.run(cam, g, rw)
+    ref0 = oracle.run_frame(ls, g, rw, cam, cfg.light_vector(), strategy="vsv")
+    assert again.stats["fragments"] == ref0.abuf.total
+    assert np.array_equal(eng.rgb.cpu().numpy(), ref0.image.rgb)
