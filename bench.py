@@ -11,14 +11,25 @@ HBM; `e2e` = the same with pinned-host vertices copied in and the sRGB image + h
 out every step.  By default three frames of the dynamic sequence are in flight per GPU (three
 engines on three streams, `--pipeline 3`): every frame runs the complete pipeline, the next
 frame's build fills the issue slots this frame's latency-bound trace leaves free.  The per-stage
-times, the roofline numbers and `config.serial_frames_per_s` come from a strictly serial pass
-(`--pipeline 1` makes that the headline as well).  N > 1: every rank renders its own frames of a dynamic sequence (frame
-sharding, no data-path collective; "weak").  `--impl reference` times the CPU oracle port
-(the reference is Python+numba and cannot travel to the GPU box) on all host threads.
+times, the roofline numbers and `run.serial_frames_per_s` come from a strictly serial pass
+(`--pipeline 1` makes that the headline as well).
+
+N > 1 (`--gpus N`: under torchrun WORLD_SIZE must equal N; without torchrun the script spawns the N ranks
+itself): `--multi frames` (default) -- every rank renders its own frames of a dynamic sequence (frame
+sharding, no data-path collective; "weak"); `--multi tiled` -- all ranks render EVERY frame together
+(TiledFrame: segment-sharded voxelization, NCCL all-reduce of the 64-bit occupancy accumulators,
+tile-restricted build, per-rank screen tile, gather on rank 0; "strong").  `--emulate-world G` plays the G
+ranks of a tiled job one after the other on ONE GPU (no exchange) and prints their per-rank stage times.
+
+`--impl reference` times the CPU oracle port (the reference is Python+numba and cannot travel to the
+GPU box) on all host threads: the whole workload for C1/C2/C3/C5, a stated sample for C4.
 """
 import argparse
+import glob
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -40,10 +51,18 @@ WORKLOADS = {
     "c5": (dict(kind="random_streamlines", seed=0, polylines=20000, verts_per_line=101, domain=128.0, curl=0.3),
            256, 1920, 1080, "vcsv", "opaque", 1.0),
 }
+# culling-active variant of C2: the same bundles drawn as thick tubes (radius 0.6 voxel), so that bundle
+# interiors become solid (eroded occupancy >= 0.999) and the voxels behind them are culled
+WORKLOADS["c2thick"] = WORKLOADS["c2"]
 C5_TIME_STEPS = 2      # distinct time steps generated on the host (~20 s each); the sequence cycles through them
 R_VOXELS = 0.2
+R_VOXELS_OF = {"c2thick": 0.6}
 R_MIN = 0.5
 LIGHT = "-0.5,-0.3,-0.8"
+
+
+def radius_of(name):
+    return R_VOXELS_OF.get(name, R_VOXELS)
 
 
 def describe(name, ls):
@@ -51,7 +70,22 @@ def describe(name, ls):
     g = ",".join(f"{k}={v}" for k, v in gen.items() if k != "kind")
     return (f"{name.upper()}: {gen['kind']}({g}) = {ls.n_segments} segments / {ls.n_vertices} vertices, "
             f"{res}^3 grid, {w}x{h}, {mode}" + (f" alpha={alpha}" if mode == "transparent" else "")
-            + f" + AO, strategy {strat}, r={R_VOXELS} voxel, full rebuild per frame")
+            + f" + AO, strategy {strat}, r={radius_of(name)} voxel, full rebuild per frame")
+
+
+def workload_config(name, ls):
+    """`config` of the JSON line: names the workload only, identical in the GPU and the reference arm."""
+    _, res, w, h, *_ = WORKLOADS[name]
+    l2 = ("no explicit flush: every frame streams more than L2 (126 MB) of grid and fragment data between reuses"
+          if res >= 256 else "no flush; this small parity config fits in L2 and is not a bench line")
+    return {"workload": describe(name, ls), "segments": ls.n_segments, "grid": res, "image": [w, h], "l2": l2}
+
+
+def csrc_sha16():
+    hsh = hashlib.sha256()
+    for f in sorted(glob.glob(os.path.join(ROOT, "paper_2510_09081_b200", "csrc", "*.cu*"))):
+        hsh.update(open(f, "rb").read())
+    return hsh.hexdigest()[:16]
 
 
 def make_workload(name, bundle_fraction=1.0):
@@ -60,7 +94,7 @@ def make_workload(name, bundle_fraction=1.0):
     gen = dict(gen)
     kind = gen.pop("kind")
     full = lvx.generate(kind, **gen)
-    g, r_world = lvx.fit_grid(full, res, radius_voxels=R_VOXELS)
+    g, r_world = lvx.fit_grid(full, res, radius_voxels=radius_of(name))
     ls = full
     if bundle_fraction < 1.0:
         keep = max(1, int(round(full.n_polylines * bundle_fraction)))
@@ -139,6 +173,23 @@ def algorithmic_bytes(stats, n_verts, V, pixels):
     }
 
 
+def load_traffic(workload, kernel):
+    """DRAM bytes per launch of `kernel` from the committed `ncu --set full` capture (profiles/ncu_traffic.json,
+    written by tools/ncu_summary.py together with the hash of csrc/ it was taken on).  A capture of other
+    kernel sources is refused: (None, why)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        j = json.load(open(path))
+        names = kernel.split("+")
+        val = sum(int(j[workload][k]) for k in names)
+    except Exception as e:
+        return None, f"no capture for {workload}/{kernel} in profiles/ncu_traffic.json ({type(e).__name__})"
+    have, now = (j.get("_csrc_sha16") or {}).get(workload), csrc_sha16()
+    if have != now:
+        return None, f"stale: profiles/ncu_traffic.json[{workload}] was captured on csrc {have}, this build is {now}"
+    return val, f"profiles/ncu_traffic.json (ncu --set full, dram read+write of one launch, csrc {now})"
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -155,6 +206,9 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     full, ls, g, r_world, cam, cfg = make_workload(args.workload)
     _, res, w, h, strat, mode, alpha = WORKLOADS[args.workload]
+    rv = radius_of(args.workload)
+    if args.multi == "tiled" or args.emulate_world > 1:
+        return run_tiled(args, lvx, torch, dist, rank, world, local, ls, g, cfg)
     eng = lvx.FrameEngine(res, w, h, strategy=strat, mode=mode, alpha=alpha, light=cfg.light_vector())
     eng.set_topology(ls.polyline_offsets, ls.n_vertices)
     # a dynamic sequence: every step gets its own deformed vertex set (rank r renders frames r, r+world, ...)
@@ -174,7 +228,7 @@ def run_gpu(args):
     def refit(e):
         """a3 of the hot path, every frame: AABB of the new vertices on the device (24-byte read-back),
         fit_grid and the orbit camera on the host (lv/pipeline.py:68-87, 40-47)."""
-        g_i, rw_i = e.fit(radius_voxels=R_VOXELS)
+        g_i, rw_i = e.fit(radius_voxels=rv)
         return lvx.make_camera(cfg, g_i), g_i, rw_i
 
     def step_resident(i):
@@ -301,11 +355,7 @@ def run_gpu(args):
     # the dominant kernel, timed alone with CUDA events on its stream (trace kernel: events 6->7)
     top_ms = stage_ms["_trace_kernel"] if top == "trace" else stage_ms[top]
     top_gbs = ab[top] / (top_ms * 1e-3) / 1e9
-    traffic = None
-    try:   # DRAM bytes per launch of that kernel from the committed `ncu --set full` capture
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[args.workload][kernel_of[top]]
-    except Exception:
-        pass
+    traffic, traffic_source = load_traffic(args.workload, kernel_of[top])
     fps = world * args.steps / (ms * 1e-3)
     fps_e2e = world * args.steps / (ms_e2e * 1e-3)
     line = {
@@ -313,11 +363,11 @@ def run_gpu(args):
         "value": round(fps, 3), "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": describe(args.workload, ls), "segments": ls.n_segments, "grid": res,
-                   "image": [w, h], "multi_gpu": "frame-sharded dynamic sequence, no collective",
-                   "frames_in_flight": depth, "serial_frames_per_s": round(world * args.steps / (ms_serial * 1e-3), 3),
-                   "l2": "no explicit flush: each frame streams > L2 (126 MB) of grid/fragment data "
-                         f"({round((sum(ab.values())) / 1e6)} MB algorithmic) between reuses"},
+        "config": workload_config(args.workload, ls),
+        "run": {"multi_gpu": "frame-sharded dynamic sequence, no collective", "frames_in_flight": depth,
+                "serial_frames_per_s": round(world * args.steps / (ms_serial * 1e-3), 3),
+                "serial_ms_per_step": round(ms_serial / args.steps, 4),
+                "algorithmic_mb_per_frame": round(sum(ab.values()) / 1e6)},
         "stages_ms": {s: round(v, 4) for s, v in stage_ms.items() if not s.startswith("_")},
         "frame_stats": {k: last.stats[k] for k in ("voxels_visited", "fragments", "occupied_voxels", "visible_voxels",
                                                    "solid_voxels", "ray_capsule_tests", "culled_fraction", "long_lists",
@@ -328,7 +378,8 @@ def run_gpu(args):
         "gpu_launches": int((eng.kernel_launches_per_frame() + 3) * args.steps),   # + the 3 AABB kernels of the refit
         "roofline": {"bound": "hbm", "kernel": kernel_of[top], "stage": top,
                      "achieved": round(top_gbs, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(top_gbs / peak, 4), "traffic": traffic, "kernel_ms": round(top_ms, 4),
+                     "frac": round(top_gbs / peak, 4), "traffic": traffic, "traffic_source": traffic_source,
+                     "kernel_ms": round(top_ms, 4),
                      "algorithmic_bytes": int(ab[top]), "peak_source": peak_kind,
                      "per_stage": stage_roof},
         "clocks": clocks,
@@ -340,33 +391,144 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+def run_tiled(args, lvx, torch, dist, rank, world, local, ls, g, cfg):
+    """All ranks render every frame together (SURVEY.md §8e 1+2, C4's multi-GPU mode): rank r voxelizes its
+    segment shard, the 64-bit accumulators are all-reduced (NCCL), every rank culls on the merged grid, builds
+    the A-buffer and the shading for the voxels of its own screen strip and traces it; rank 0 gathers the
+    strips.  `--emulate-world G` (one process, one GPU) plays the G ranks in turn without the exchange."""
+    from paper_2510_09081_b200 import distributed as D
+    from paper_2510_09081_b200.frame import STAGES
+    _, res, w, h, strat, mode, alpha = WORKLOADS[args.workload]
+    rv = radius_of(args.workload)
+    emu = args.emulate_world if args.emulate_world > 1 else 0
+    if emu and world > 1:
+        raise SystemExit("bench.py: --emulate-world runs in one process on one GPU")
+    eng = lvx.FrameEngine(res, w, h, strategy=strat, mode=mode, alpha=alpha, light=cfg.light_vector())
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    n_variants = 4          # every rank holds the same deformed vertex sets: all ranks work on the same frame
+    host = [torch.from_numpy(deform(ls.vertices, i, g.voxel_size)).pin_memory() for i in range(n_variants)]
+    dev = [hv.cuda() for hv in host]
+    out_srgb = torch.empty((h, w, 3), dtype=torch.uint8).pin_memory()
+    out_hit = torch.empty((h, w), dtype=torch.int32).pin_memory()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def frame(tf, i, e2e):
+        eng.load_vertices((host if e2e else dev)[i % n_variants])
+        g_i, rw_i = eng.fit(radius_voxels=rv)
+        r = tf.run(lvx.make_camera(cfg, g_i), g_i, rw_i)
+        srgb, hit = tf.gather_image()
+        if e2e and srgb is not None:
+            out_srgb[:srgb.shape[0]].copy_(srgb, non_blocking=True)
+            out_hit[:hit.shape[0]].copy_(hit, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        return r
+
+    def timed(tf, e2e):
+        for i in range(args.warmup):
+            frame(tf, i, e2e)
+        barrier()
+        stage, last = {}, None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.steps):
+            last = frame(tf, args.warmup + i, e2e)
+            for k, v in last.stage_ms.items():
+                stage[k] = stage.get(k, 0.0) + v / args.steps
+        e1.record()
+        barrier()
+        return e0.elapsed_time(e1), stage, last
+
+    keys = ("fragments", "owned_voxels", "visible_voxels", "ray_capsule_tests", "voxels_visited", "shaded_voxels")
+    sampler = ClockSampler(local) if rank == 0 else None
+    if emu:
+        per_rank = []
+        for r in range(emu):
+            tf = D.TiledFrame(eng, comm=D.EmulatedComm(r, emu))
+            ms, stage, last = timed(tf, False)
+            own = sum(v for k, v in stage.items() if k != "emulated_peers")
+            per_rank.append({"rank": r, "tile": list(tf.tiles[r]), "segments": list(tf.seg_range()),
+                             "own_stage_ms_sum": round(own, 4), "stages_ms": {k: round(v, 4) for k, v in stage.items()},
+                             "stats": {k: last.stats[k] for k in keys}})
+        clocks = sampler.stop()
+        worst = max(p["own_stage_ms_sum"] for p in per_rank)
+        line = {
+            "metric": "frames/sec (voxelize+cull+build+shade+trace, full rebuild per frame) at 1920x1080",
+            "value": round(1e3 / worst, 3), "unit": "frames/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(worst, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": workload_config(args.workload, ls),
+            "emulated": {"world": emu, "note": "ONE GPU plays the ranks of a tiled job in turn; value = 1 / (largest per-rank "
+                         "sum of the rank's own stage times); the all-reduce of the accumulators (exchange_bytes per rank) "
+                         "and the gather of the strips are NOT included", "exchange_bytes": 8 * res ** 3,
+                         "ranks": per_rank},
+            "gpu_launches": int((eng.kernel_launches_per_frame() + 3) * args.steps * emu), "clocks": clocks}
+        print(json.dumps(line))
+        return
+
+    tf = D.TiledFrame(eng)
+    ms, stage, last = timed(tf, False)
+    clocks = sampler.stop() if sampler else None
+    ms_e2e, _, _ = timed(tf, True)
+    t = torch.tensor([ms, ms_e2e], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, ms_e2e = (float(x) for x in t.tolist())
+    mine = {"rank": rank, "tile": list(tf.tiles[rank]), "segments": list(tf.seg_range()),
+            "stages_ms": {k: round(v, 4) for k, v in stage.items()}, "stats": {k: last.stats[k] for k in keys}}
+    ranks = [mine]
+    if world > 1:
+        ranks = [None] * world
+        dist.all_gather_object(ranks, mine)
+    if rank == 0:
+        xb = tf.exchange_bytes if world > 1 else 0
+        xms = max((p["stages_ms"].get("exchange", 0.0) for p in ranks), default=0.0)
+        line = {
+            "metric": "frames/sec (voxelize+cull+build+shade+trace, full rebuild per frame) at 1920x1080",
+            "value": round(args.steps / (ms * 1e-3), 3), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args.workload, ls),
+            "run": {"multi_gpu": "tiled: segment-sharded voxelize + all-reduce of the 64-bit accumulators + per-rank "
+                                 "screen strip (tile-restricted build) + gather on rank 0", "frames_in_flight": 1},
+            "exchange": {"all_reduce_bytes_per_rank": xb, "all_reduce_ms_max": round(xms, 4),
+                         "bus_gbs": round(2 * (world - 1) / world * xb / (xms * 1e-3) / 1e9, 1) if xms > 0 else None,
+                         "gather_bytes": int(out_srgb.numel() + out_hit.numel() * 4)},
+            "ranks": ranks,
+            "e2e": {"value": round(args.steps / (ms_e2e * 1e-3), 3), "unit": "frames/s",
+                    "ms_per_step": round(ms_e2e / args.steps, 4),
+                    "h2d_bytes_per_step": int(host[0].numel() * 4) * world,
+                    "d2h_bytes_per_step": int(out_srgb.numel() + out_hit.numel() * 4 + 128 * world)},
+            "gpu_launches": int((eng.kernel_launches_per_frame() + 3) * args.steps * world), "clocks": clocks}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def cpu_baseline(workload, steps, warmup, fraction=None):
-    """The CPU oracle port (oracle/, C + OpenMP, all host threads) on a bounded sample of the
-    workload: the first `fraction` of the bundles at the full grid/image; bundles are spatially
-    separate, so every stage's work scales with the fraction and frames/s is scaled by it."""
+    """The CPU oracle port (oracle/, C + OpenMP, all host threads).  C1/C2/C3/C5: the WHOLE workload, every
+    step one full frame, value = 1 / measured seconds per frame.  C4 (10 M segments at 512^3 needs tens of
+    seconds and tens of GB per frame on the host): a stated sample -- the first 1/8 of the bundles at the full
+    grid and image; bundles are spatially separate, so the build work scales with the fraction while the
+    per-voxel / per-pixel sweeps do not, and value = fraction / seconds is an upper bound for the CPU."""
     from oracle import oracle as orc
     orc.build()
+    orc.set_threads(len(os.sched_getaffinity(0)))     # all host threads (torchrun exports OMP_NUM_THREADS=1)
     cores = orc.max_threads()
     _, res, w, h, strat, mode, alpha = WORKLOADS[workload]
     if fraction is None:
-        fraction = 1.0
-        if workload != "c1":
-            # calibrate on 1/16 of the bundles, then take the largest sample that keeps the whole
-            # run near `budget` seconds of CPU wall time
-            budget = 25.0 if steps + warmup <= 1 else 150.0
-            _, ls0, g0, rw0, cam0, cfg0 = make_workload(workload, 1.0 / 16)
-            t0 = time.perf_counter()
-            orc.run_frame(ls0, g0, rw0, cam0, cfg0.light_vector(), strategy=strat, mode=mode, alpha=alpha)
-            est_full = 16.0 * (time.perf_counter() - t0)
-            fraction = min(1.0, budget / ((steps + warmup) * est_full))
-            fraction = max(fraction, 1.0 / 64)
+        fraction = 0.125 if workload == "c4" else 1.0
     full, ls, g, r_world, cam, cfg = make_workload(workload, fraction)
     stage = {}
     times = []
     for i in range(warmup + steps):
         tm = {}
+        # a dynamic sequence like the GPU arm's: every step has its own deformed vertex set
+        ls_i = type(ls)(deform(ls.vertices, i, g.voxel_size), ls.polyline_offsets, ls.radius) if workload != "c5" else ls
         t0 = time.perf_counter()
-        orc.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy=strat, mode=mode, alpha=alpha, timings=tm)
+        orc.run_frame(ls_i, g, r_world, cam, cfg.light_vector(), strategy=strat, mode=mode, alpha=alpha, timings=tm)
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
@@ -374,10 +536,27 @@ def cpu_baseline(workload, steps, warmup, fraction=None):
                 stage[k] = stage.get(k, 0.0) + v / steps
     sec = float(np.mean(times))
     frac = ls.n_segments / full.n_segments
+    whole = ls.n_segments == full.n_segments
+    sample = (f"the whole workload: {ls.n_segments} segments, {res}^3 grid, {w}x{h} image; {len(times)} frame(s) of "
+              f"{sec:.2f} s each, value = 1 / seconds per frame" if whole else
+              f"{ls.n_segments} of {full.n_segments} segments (first {frac:.3f} of the polylines), full "
+              f"{res}^3 grid and {w}x{h} image; {sec:.2f} s per sample frame, value = fraction / seconds")
     return {"value": round(frac / sec, 5), "unit": "frames/s", "cores": cores, "kind": "port",
-            "sample": f"{ls.n_segments} of {full.n_segments} segments (first {frac:.3f} of the polylines), full "
-                      f"{res}^3 grid and {w}x{h} image; {sec:.2f} s per sample frame, value = fraction / seconds",
-            "sample_seconds": round(sec, 3), "stages_ms_sample": {k: round(v, 1) for k, v in stage.items()}}
+            "sample": sample, "whole_workload": whole, "sample_seconds": round(sec, 3),
+            "total_seconds": round(float(np.sum(times)), 2),
+            "stages_ms_sample": {k: round(v, 1) for k, v in stage.items()}}
+
+
+def reference_package_probe():
+    """Whether the reference's own package could run on this host (it needs numba); recorded, not required."""
+    out = {}
+    try:
+        import numba
+        out["numba"] = numba.__version__
+    except Exception as e:
+        out["numba"] = f"not importable ({type(e).__name__})"
+    out["baseline_ref_present"] = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "linevox"))
+    return out
 
 
 def run_reference(args):
@@ -386,20 +565,39 @@ def run_reference(args):
         return
     cb = cpu_baseline(args.workload, steps=args.steps, warmup=args.warmup)
     full, ls, *_ = make_workload(args.workload)
-    _, res, w, h, strat, mode, alpha = WORKLOADS[args.workload]
+    ms_step = 1e3 * cb["sample_seconds"] if cb["whole_workload"] else 1e3 / cb["value"]
     line = {
         "impl": "reference",
         "metric": "frames/sec (voxelize+cull+build+shade+trace, full rebuild per frame) at 1920x1080",
         "value": cb["value"], "unit": "frames/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 / cb["value"], 2), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(ms_step, 2), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": describe(args.workload, ls), "segments": ls.n_segments, "grid": res, "image": [w, h]},
+        "config": workload_config(args.workload, ls),
         "cpu_baseline": cb,
+        "reference_package": reference_package_probe(),
         "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line))
+
+
+def free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: start the N ranks exactly as the driver would."""
+    if "--impl" not in sys.argv or "reference" not in sys.argv:
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            raise SystemExit(f"bench.py: --gpus {n} but this host has {have} CUDA device(s)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
 
 
 def main():
@@ -414,7 +612,25 @@ def main():
                                                            "each) instead of the workload's own, for segment-count sweeps")
     ap.add_argument("--pipeline", type=int, default=3, help="frames in flight per GPU (engines on separate streams); "
                                                              "1 = strictly one frame after the other")
+    ap.add_argument("--multi", default="frames", choices=["frames", "tiled"],
+                    help="N > 1: frames = every rank renders its own frames (weak); tiled = all ranks render every "
+                         "frame together: sharded voxelize + all-reduce + screen strips (strong)")
+    ap.add_argument("--emulate-world", type=int, default=0, help="one GPU plays the G ranks of a tiled job in turn")
+    ap.add_argument("--alpha", type=float, default=None, help="opacity of a transparent workload (c3: 0.1 .. 0.5)")
     args = ap.parse_args()
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if env_world is None and args.gpus > 1:
+        spawn_ranks(args.gpus)
+    if env_world is not None and int(env_world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={env_world} ranks; "
+                         "pass --gpus equal to the number of ranks")
+    if args.alpha is not None:
+        wl = WORKLOADS[args.workload]
+        if wl[5] != "transparent" or not 0.0 < args.alpha <= 1.0:
+            ap.error("--alpha needs a transparent workload (c3) and a value in (0, 1]")
+        WORKLOADS[args.workload] = wl[:6] + (args.alpha,)
     if args.bundles > 0:
         if WORKLOADS[args.workload][0]["kind"] != "bundles":
             ap.error("--bundles needs a bundles workload (c2, c3, c4)")

@@ -4,16 +4,23 @@ The path shards in three independent ways; only the first has a
 exchange:
 
 1. **Segment-sharded voxelization** -- rank g voxelizes segments ``[bounds[g], bounds[g+1])``
-   (the reference's own chunking, lv/voxelizer.py:461-463) into its private packed grid; the grids
-   are merged with ONE all-reduce.  A plain sum of packed u32 words would let the 16-bit occupancy
+   (the reference's own chunking, lv/voxelizer.py:461-463) into its private grid; the grids are
+   merged with ONE all-reduce.  A plain sum of packed u32 words would let the 16-bit occupancy
    field carry into the count field, and the reference saturates each field separately
    (lv/voxelizer.py:490-495), so the exchange format is one int64 per voxel,
    ``(count << 32) | occ_q`` -- sum-reducible and exact -- re-packed with per-field saturation
    afterwards.  The result equals the reference's worker-count-invariant grid.
-2. **Screen-tile tracing** -- after the merge every rank holds the full pyramid, builds culling /
-   A-buffer / shading locally (replicated) and traces only its pixel rectangle; tiles are gathered.
+2. **Screen-tile tracing** -- after the merge every rank holds the full pyramid and the full culling
+   pyramid (march bits), builds the A-buffer and the shading only for the voxels its own pixel
+   rectangle's rays can visit (lvx_tile_owners) and traces that rectangle; tiles are gathered.
 3. **Frame-sharded sequences** -- frames of a dynamic sequence are independent: rank g renders
-   frames g, g+G, ...; no communication (this is what ``bench.py --gpus N`` measures).
+   frames g, g+G, ...; no communication (``bench.py --gpus N`` default).
+
+`TiledFrame` (1 + 2) talks to its peers through a small `Comm` object: `TorchComm` is
+torch.distributed (NCCL on GPUs, gloo in the CPU tests), `EmulatedComm` plays one rank of a G-rank
+job on a single device -- the peers' contribution to the all-reduce is produced by voxelizing their
+segment shards locally -- so that the per-rank work of a G-GPU frame can be tested and timed on
+the one GPU this project's runs have.
 
 `merge_partial_grids` is written with device-agnostic torch ops so that the same code runs under
 NCCL on GPUs and under gloo in the CPU tests (tests/test_distributed_cpu.py).
@@ -23,7 +30,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["shard_bounds", "tile_rects", "frames_for_rank", "widen_packed", "pack_wide",
-           "merge_partial_grids", "TiledFrame"]
+           "merge_partial_grids", "TiledFrame", "Comm", "TorchComm", "EmulatedComm"]
 
 
 def shard_bounds(n_segments: int, world: int) -> np.ndarray:
@@ -63,47 +70,159 @@ def pack_wide(wide_i64):
     return packed, visited
 
 
-def merge_partial_grids(base_i32, group=None):
+class Comm:
+    """What a TiledFrame needs from its peers.  This base class is the single-rank job."""
+    rank, world = 0, 1
+
+    def all_reduce_sum(self, t):
+        """In-place sum of `t` over all ranks."""
+
+    def gather(self, t):
+        """Rank 0 gets [t of rank 0, t of rank 1, ...] (equal shapes); other ranks get None."""
+        return [t]
+
+    def barrier(self):
+        pass
+
+
+class TorchComm(Comm):
+    """torch.distributed: NCCL over NVLink on GPUs, gloo in the CPU tests."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        if not (dist.is_available() and dist.is_initialized()):
+            raise RuntimeError("TorchComm needs an initialised torch.distributed process group")
+        self.dist, self.group = dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+    def all_reduce_sum(self, t):
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def gather(self, t):
+        import torch
+        if self.world == 1:
+            return [t]
+        outs = [torch.empty_like(t) for _ in range(self.world)] if self.rank == 0 else None
+        self.dist.gather(t, outs, dst=0, group=self.group)
+        return outs
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier(group=self.group)
+
+
+class EmulatedComm(Comm):
+    """Rank `rank` of a `world`-rank job played on one device.  The all-reduce of the occupancy
+    accumulators is replaced by `peers(t)`, a callback installed by TiledFrame that adds what the
+    other ranks would have contributed (their segment shards, voxelized here); `gather` returns only
+    this rank's piece.  Every kernel this rank would launch in the real job runs with the same
+    arguments; only the NVLink exchange is missing, and its cost is reported as absent, not as zero."""
+    emulated = True
+
+    def __init__(self, rank: int, world: int):
+        if not 0 <= int(rank) < int(world):
+            raise ValueError("rank must be in [0, world)")
+        self.rank, self.world = int(rank), int(world)
+        self.peers = None
+
+    def all_reduce_sum(self, t):
+        if self.world > 1:
+            if self.peers is None:
+                raise RuntimeError("EmulatedComm has no peer contribution installed")
+            self.peers(t)
+
+    def gather(self, t):
+        return [t] if self.rank == 0 else None
+
+
+def merge_partial_grids(base_i32, group=None, comm=None):
     """All-reduce the per-rank packed grids exactly.  `base_i32`: this rank's finalized packed grid
     (int32 bit patterns, any device).  Returns (merged packed int32 grid, total visited)."""
     import torch.distributed as dist
     wide = widen_packed(base_i32)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if comm is not None:
+        comm.all_reduce_sum(wide)
+    elif dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(wide, op=dist.ReduceOp.SUM, group=group)
     return pack_wide(wide)
 
 
 class TiledFrame:
-    """One frame rendered cooperatively by all ranks: segment-sharded voxelization + all-reduce,
-    replicated build, per-rank screen tile, gather to rank 0.  Wraps a FrameEngine."""
+    """One frame rendered cooperatively by all ranks: segment-sharded voxelization + all-reduce of the
+    occupancy accumulators, per-rank screen tile (tile-restricted A-buffer build and shading), gather
+    of the tiles on rank 0.  Wraps a FrameEngine (or anything with its `run` signature and buffers).
 
-    def __init__(self, engine, group=None):
-        import torch.distributed as dist
-        self.engine, self.group = engine, group
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+    After `run`, `exchange_ms` is the device time of the all-reduce (None under emulation, where the
+    time of the locally voxelized peer shards is reported as stage "emulated_peers" instead) and
+    `exchange_bytes` the size of the buffer every rank contributed."""
+
+    def __init__(self, engine, group=None, comm=None):
+        if comm is None:
+            import torch.distributed as dist
+            comm = TorchComm(group) if (dist.is_available() and dist.is_initialized()) else Comm()
+        self.engine, self.comm = engine, comm
+        self.rank, self.world = comm.rank, comm.world
         self.tiles = tile_rects(engine.w, engine.h, self.world)
+        self.exchange_ms = None
+        self.exchange_bytes = 0
+        self._ev = None
+        if getattr(comm, "emulated", False):
+            comm.peers = self._voxelize_peers
+
+    def seg_range(self):
+        b = shard_bounds(self.engine._segs.numel(), self.world)
+        return (int(b[self.rank]), int(b[self.rank + 1])) if self.rank < len(b) - 1 else (0, 0)
+
+    def _voxelize_peers(self, wide):
+        """EmulatedComm: what the other ranks' shards add to the accumulators (and to the incidence
+        count, which the real job all-reduces with the grid)."""
+        from . import ops
+        eng = self.engine
+        b = shard_bounds(eng._segs.numel(), self.world)
+        for r in range(len(b) - 1):
+            if r != self.rank and b[r + 1] > b[r]:
+                ops.voxelize_wide(eng.lines, eng.res, eng.r_min, eng.method, wide, eng.stats, int(b[r]), int(b[r + 1]))
 
     def _merge(self, eng):
+        import torch
+        timed = eng.stats.is_cuda
+        if timed:
+            if self._ev is None:
+                self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            self._ev[0].record()
         if eng.use_wide:     # the engine's 64-bit accumulators are sum-reducible as they are; it packs afterwards
-            import torch.distributed as dist
-            dist.all_reduce(eng.wide, op=dist.ReduceOp.SUM, group=self.group)
-            return
-        merged, _ = merge_partial_grids(eng.base, self.group)
-        eng.base.copy_(merged)
+            self.exchange_bytes = eng.wide.numel() * 8
+            self.comm.all_reduce_sum(eng.wide)
+        else:
+            self.exchange_bytes = eng.base.numel() * 8
+            merged, _ = merge_partial_grids(eng.base, comm=self.comm)
+            eng.base.copy_(merged)
+        if not getattr(self.comm, "emulated", False):
+            from . import _native as N       # Σ incidences over the shards = `visited` of the whole set
+            self.comm.all_reduce_sum(eng.stats[N.ST_VISITED:N.ST_VISITED + 1])
+        if timed:
+            self._ev[1].record()
 
     def run(self, cam, grid, r_world):
+        """This rank's part of the frame.  Returns the engine's FrameResult; its `stage_ms` gets an
+        "exchange" entry (taken out of "voxelize") when the all-reduce was timed."""
         eng = self.engine
-        n_seg = eng._segs.numel()
-        b = shard_bounds(n_seg, self.world)
-        lo, hi = (int(b[self.rank]), int(b[self.rank + 1])) if self.rank < len(b) - 1 else (0, 0)
-        return eng.run(cam, grid, r_world, tile=self.tiles[self.rank], seg_range=(lo, hi),
-                       after_voxelize=self._merge if self.world > 1 else None)
+        out = eng.run(cam, grid, r_world, tile=self.tiles[self.rank], seg_range=self.seg_range(),
+                      after_voxelize=self._merge if self.world > 1 else None)
+        self.exchange_ms = None
+        if self.world > 1 and self._ev is not None:
+            ms = self._ev[0].elapsed_time(self._ev[1])
+            out.stage_ms["voxelize"] = max(0.0, out.stage_ms["voxelize"] - ms)
+            if getattr(self.comm, "emulated", False):     # the peers' shards voxelized here: not this rank's work
+                out.stage_ms["emulated_peers"] = ms
+            else:
+                out.stage_ms["exchange"] = self.exchange_ms = ms
+        return out
 
     def gather_image(self):
         """Rank 0 receives the full sRGB image and hit ids (H, W, 3) u8 / (H, W) i32; others None."""
         import torch
-        import torch.distributed as dist
         eng = self.engine
         x0, y0, x1, y1 = self.tiles[self.rank]
         if self.world == 1:
@@ -113,12 +232,12 @@ class TiledFrame:
         pad_h = torch.zeros((rows, eng.w), dtype=torch.int32, device=eng.srgb.device)
         pad_s[:y1 - y0] = eng.srgb[y0:y1]
         pad_h[:y1 - y0] = eng.hit_id[y0:y1]
-        outs = [torch.empty_like(pad_s) for _ in range(self.world)] if self.rank == 0 else None
-        outh = [torch.empty_like(pad_h) for _ in range(self.world)] if self.rank == 0 else None
-        dist.gather(pad_s, outs, dst=0, group=self.group)
-        dist.gather(pad_h, outh, dst=0, group=self.group)
+        outs = self.comm.gather(pad_s)
+        outh = self.comm.gather(pad_h)
         if self.rank != 0:
             return None, None
+        if getattr(self.comm, "emulated", False):       # only this rank's strip exists
+            return pad_s[:y1 - y0], pad_h[:y1 - y0]
         srgb = torch.cat([o[:t[3] - t[1]] for o, t in zip(outs, self.tiles)], dim=0)
         hit = torch.cat([o[:t[3] - t[1]] for o, t in zip(outh, self.tiles)], dim=0)
         return srgb, hit

@@ -47,6 +47,100 @@ def _worker(rank, world, port, scene_name, out_dir):
         dist.destroy_process_group()
 
 
+class OracleEngine:
+    """Stand-in for FrameEngine on a host without a GPU: the same `run(cam, grid, r_world, tile, seg_range,
+    after_voxelize)` contract and buffers (`wide`, `stats`, `srgb`, `hit_id`), every stage computed by the CPU
+    oracle.  It lets the gloo test drive TiledFrame.run / gather_image through a real 2-process exchange."""
+    use_wide = True
+
+    def __init__(self, orc, sc):
+        self.orc, self.sc = orc, sc
+        self.w, self.h = sc.cam.width, sc.cam.height
+        self._segs = torch.arange(sc.ls.n_segments, dtype=torch.int32)
+        self.stats = torch.zeros(16, dtype=torch.int64)
+        self.srgb = torch.zeros((self.h, self.w, 3), dtype=torch.uint8)
+        self.hit_id = torch.full((self.h, self.w), -9, dtype=torch.int32)
+        self.wide = None
+        self.merged_base = None
+
+    def run(self, cam, grid, r_world, tile=None, seg_range=None, after_voxelize=None):
+        from types import SimpleNamespace
+        orc, sc = self.orc, self.sc
+        cn = orc.compute_clip_normals(sc.ls)
+        part = orc.voxelize(sc.ls, cn, grid, r_min=sc.r_min, r_world=r_world, seg_range=seg_range)
+        self.stats[0] = int(part.visited)
+        self.wide = D.widen_packed(torch.from_numpy(part.base.view(np.int32).reshape(-1).copy()))
+        if after_voxelize is not None:
+            after_voxelize(self)
+        packed, _ = D.pack_wide(self.wide)
+        self.merged_base = packed.numpy().view(np.uint32).reshape(part.base.shape)
+        # the rest of the frame is replicated; this rank keeps only the rows of its tile
+        ref = orc.run_frame(sc.ls, grid, r_world, cam, sc.light, strategy=sc.strategy, mode=sc.mode,
+                            alpha=sc.alpha, k=sc.k)
+        assert np.array_equal(self.merged_base, ref.pyramid.base), "merged grid differs from the whole-set grid"
+        x0, y0, x1, y1 = tile
+        self.srgb[y0:y1, x0:x1] = torch.from_numpy(ref.image.srgb[y0:y1, x0:x1])
+        self.hit_id[y0:y1, x0:x1] = torch.from_numpy(ref.image.hit_id[y0:y1, x0:x1])
+        return SimpleNamespace(stats={"voxels_visited": int(self.stats[0])}, stage_ms={"voxelize": 0.0})
+
+
+def _tiled_worker(rank, world, port, scene_name, out_dir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from helpers import Scene
+        from oracle import oracle as orc
+        orc.set_threads(2)
+        sc = Scene(scene_name)
+        eng = OracleEngine(orc, sc)
+        tf = D.TiledFrame(eng)                       # TorchComm over the gloo group
+        assert (tf.rank, tf.world) == (rank, world) and isinstance(tf.comm, D.TorchComm)
+        lo, hi = tf.seg_range()
+        out = tf.run(sc.cam, sc.g, sc.r_world)
+        srgb, hit = tf.gather_image()
+        ref = orc.run_frame(sc.ls, sc.g, sc.r_world, sc.cam, sc.light, strategy=sc.strategy, mode=sc.mode,
+                            alpha=sc.alpha, k=sc.k)
+        ok = out.stats["voxels_visited"] == ref.pyramid.visited and tf.exchange_bytes == 8 * sc.g.resolution ** 3
+        ok = ok and 0 <= lo < hi <= sc.ls.n_segments
+        if rank == 0:
+            ok = ok and np.array_equal(srgb.numpy(), ref.image.srgb) and np.array_equal(hit.numpy(), ref.image.hit_id)
+        else:
+            ok = ok and srgb is None and hit is None
+        np.save(os.path.join(out_dir, f"tiled{rank}.npy"), np.array([ok, lo, hi]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scene", ["helix32_vsv", "walk32_transp_k2"])
+def test_tiled_frame_runs_and_gathers_over_gloo(scene, tmp_path, oracle):
+    """TiledFrame.run + gather_image across two real processes (gloo): segment shards, the exact all-reduce
+    of the 64-bit accumulators and of the incidence count, per-rank tiles, gather on rank 0."""
+    world = 2
+    mp.spawn(_tiled_worker, args=(world, _free_port(), scene, str(tmp_path)), nprocs=world, join=True)
+    r = [np.load(tmp_path / f"tiled{k}.npy") for k in range(world)]
+    assert all(x[0] for x in r)
+    assert r[0][1] == 0 and r[0][2] == r[1][1] and r[1][2] > r[1][1]      # the shards tile [0, n)
+
+
+def test_emulated_comm_contract():
+    c = D.EmulatedComm(1, 4)
+    assert (c.rank, c.world) == (1, 4) and c.gather(torch.zeros(1)) is None
+    with pytest.raises(RuntimeError):
+        c.all_reduce_sum(torch.zeros(1))
+    with pytest.raises(ValueError):
+        D.EmulatedComm(4, 4)
+    seen = []
+    c.peers = seen.append
+    t = torch.ones(2)
+    c.all_reduce_sum(t)
+    assert seen and seen[0] is t
+    one = D.Comm()
+    assert (one.rank, one.world) == (0, 1) and one.gather(t) == [t]
+
+
 @pytest.mark.parametrize("scene", ["helix64_vcsv", "diag_vcsv"])   # diag: 16-bit occupancy saturates
 def test_sharded_voxelize_merge_gloo(scene, tmp_path, oracle):
     world = 2

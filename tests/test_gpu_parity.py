@@ -489,6 +489,61 @@ def test_tile_owner_build_is_exact_on_rect_tiles(lvx, oracle, mode, inside):
     assert tests == ref.image.stats["ray_capsule_tests"]
 
 
+@pytest.mark.parametrize("kind,mode", [("walk", "opaque"), ("walk", "transparent"), ("diag", "opaque")])
+def test_tiled_frame_emulated_ranks_make_the_frame(lvx, oracle, kind, mode):
+    """Every rank of a 3-rank TiledFrame job, played one after the other on this GPU (EmulatedComm: the
+    peers' shards are voxelized locally in place of the all-reduce; everything else is what the rank runs in
+    the real job): each rank ends up with the whole-set grid and incidence count, builds only its tile's
+    voxels, and the gathered strips are the oracle's image.  `diag` saturates the 16-bit occupancy field, so
+    the per-field saturation after the sum is exercised."""
+    from paper_2510_09081_b200 import distributed as D
+    if kind == "walk":
+        ls = lvx.generate("random_streamlines", seed=44, polylines=80, verts_per_line=45)
+        res, w, h = 64, 150, 101
+        g, r_world = lvx.fit_grid(ls, res, radius_voxels=0.4)
+    else:
+        ls = lvx.generate("grid_diagonals", count=300, length=14.0, domain=20.0)
+        ls = lvx.LineSet(ls.vertices, ls.polyline_offsets, 1.1)
+        res, w, h = 32, 96, 64
+        g, r_world = lvx.fit_grid(ls, res)
+    strategy = "vcsv" if mode == "opaque" else "vsv"
+    cfg = lvx.PipelineConfig(res=res, width=w, height=h, strategy=strategy, mode=mode, alpha=0.3)
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy=strategy, mode=mode, alpha=0.3)
+    if kind == "diag":
+        assert (ref.pyramid.base & 0xFFFF).max() == 0xFFFF
+    world = 3
+    srgb = np.zeros((h, w, 3), np.uint8); hit = np.full((h, w), -7, np.int32); tests = 0; frags = 0
+    for rank in range(world):
+        e = lvx.FrameEngine(res, w, h, strategy=strategy, mode=mode, alpha=0.3)
+        e.set_topology(ls.polyline_offsets, ls.n_vertices)
+        e.load_vertices(ls.vertices)
+        tf = D.TiledFrame(e, comm=D.EmulatedComm(rank, world))
+        lo, hi = tf.seg_range()
+        assert hi - lo in (ls.n_segments // world, ls.n_segments // world + 1)
+        out = tf.run(cam, g, r_world)
+        assert tf.exchange_ms is None and tf.exchange_bytes == 8 * res ** 3
+        assert np.array_equal(e.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
+        assert out.stats["voxels_visited"] == ref.pyramid.visited
+        if ref.culling is not None:
+            assert np.array_equal(e.cull_flat.cpu().numpy(), ref.culling.flat)
+        assert out.stats["fragments"] < ref.abuf.total
+        s, hh = tf.gather_image()
+        x0, y0, x1, y1 = tf.tiles[rank]
+        if rank == 0:
+            assert s.shape == (y1 - y0, w, 3)
+        else:
+            assert s is None and hh is None
+        srgb[y0:y1] = e.srgb.cpu().numpy()[y0:y1]
+        hit[y0:y1] = e.hit_id.cpu().numpy()[y0:y1]
+        tests += out.stats["ray_capsule_tests"]
+        frags += out.stats["fragments"]
+    assert np.array_equal(hit, ref.image.hit_id)
+    assert np.array_equal(srgb, ref.image.srgb)
+    assert tests == ref.image.stats["ray_capsule_tests"]
+    assert frags < 2 * ref.abuf.total
+
+
 @pytest.mark.parametrize("res,mode", [(4, "opaque"), (8, "transparent"), (16, "opaque")])
 def test_engine_tiny_inputs(lvx, oracle, res, mode):
     """FrameEngine at the small end: one or two segments, grids below the brick / bit-mask granularity

@@ -1,7 +1,10 @@
 """Host-side logic (no GPU): generators, grid fit and camera reproduce the reference bit for bit
 (checked against the golden fixtures made from the live reference), configuration rules, .lns I/O."""
 import numpy as np
+import os
 import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 import paper_2510_09081_b200 as lvx
 from helpers import SCENES, Scene, h
@@ -104,3 +107,36 @@ def test_shards_index_the_canonical_segment_array():
     assert ops._shard_segs(lines, 50, 100) == "SEGS"
     lines.order = None
     assert ops._shard_segs(lines, 0, 100) == "SEGS"
+
+
+def test_bench_traffic_is_refused_when_stale(tmp_path, monkeypatch):
+    """bench.py reads roofline.traffic from the committed ncu capture only if it was taken on these kernel
+    sources (tools/ncu_summary.py stores the hash of csrc/)."""
+    import json
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    prof = tmp_path / "profiles"
+    prof.mkdir()
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    monkeypatch.setattr(bench, "csrc_sha16", lambda: "abc")
+    (prof / "ncu_traffic.json").write_text(json.dumps({"c2": {"k_a": 5, "k_b": 7}, "_csrc_sha16": {"c2": "abc"}}))
+    v, src = bench.load_traffic("c2", "k_a+k_b")
+    assert v == 12 and "csrc abc" in src
+    (prof / "ncu_traffic.json").write_text(json.dumps({"c2": {"k_a": 5}, "_csrc_sha16": {"c2": "old"}}))
+    v, src = bench.load_traffic("c2", "k_a")
+    assert v is None and src.startswith("stale")
+    v, src = bench.load_traffic("c3", "k_a")
+    assert v is None and "no capture" in src
+
+
+def test_bench_config_is_the_same_in_both_arms():
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2510_09081_b200 as lvx
+    ls = lvx.generate("random_streamlines", seed=0, polylines=100, verts_per_line=101)
+    c = bench.workload_config("c1", ls)
+    assert set(c) == {"workload", "segments", "grid", "image", "l2"} and c["segments"] == 10000
+    assert "10000 segments" in c["workload"] and "r=0.2" in c["workload"]
+    assert "r=0.6" in bench.describe("c2thick", ls)

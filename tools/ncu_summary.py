@@ -43,5 +43,11 @@ if len(sys.argv) > 3:
     except Exception:
         j = {}
     j[wl] = traffic
+    import glob, hashlib, os
+    hsh = hashlib.sha256()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for f in sorted(glob.glob(os.path.join(root, "paper_2510_09081_b200", "csrc", "*.cu*"))):
+        hsh.update(open(f, "rb").read())
+    j.setdefault("_csrc_sha16", {})[wl] = hsh.hexdigest()[:16]     # bench.py refuses the numbers on other sources
     j["_source"] = "ncu --set full --clock-control none, first launch of each kernel in bench.py --workload <w> --steps 1 --warmup 3 --pipeline 1; see profiles/*_ncu_full_*_summary.txt"
     json.dump(j, open(path, "w"), indent=1)
