@@ -123,6 +123,10 @@ int lvx_widen(const uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, u
 int lvx_pack_wide(const uint64_t *wide, int64_t n_voxels, uint32_t *base,
                   uint32_t *nz_bits /* may be NULL; n_voxels/32 u32: bit = occupancy field non-zero, for lvx_shade */,
                   uint64_t *stats, void *stream);
+/* lvx_pack_wide and level 1 of lvx_build_mips in one read of the accumulators (res >= 64, else LVX_E_ARG):
+ * `mips` receives level 1 at its start, exactly as lvx_build_mips writes it; follow with lvx_build_mips_upper. */
+int lvx_pack_wide_mip1(const uint64_t *wide, int res, uint32_t *base, uint32_t *nz_bits /* may be NULL */,
+                       double *mips, uint64_t *stats, void *stream);
 /* applies occ_sat to `base` in place (occ field := 0xFFFF where flagged) */
 int lvx_finalize_base(uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, uint64_t *stats, void *stream);
 
@@ -130,6 +134,8 @@ int lvx_finalize_base(uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels,
  * (min(occ_q,4096)/4096); `mips` receives levels 1.. as f64, flat, level 1 first
  * (lvx_pyramid_elems(res) - res^3 elements).  Values are exact dyadic rationals. */
 int lvx_build_mips(const uint32_t *base, int res, double *mips, void *stream);
+/* levels 2.. from a level 1 that is already in `mips` (lvx_pack_wide_mip1) */
+int lvx_build_mips_upper(int res, double *mips, void *stream);
 
 /* ---- culling: lv/culling.py:112-127 erode, 143-200 _march_blocked/_visibility_kernel,
  * 130-140 dilate_bits, 103-109 or_mips.  cull_flat (lvx_pyramid_elems(res) bytes) receives the
@@ -163,11 +169,14 @@ int lvx_tile_owners(const uint8_t *cull_flat, int res, const lvx_camera *cam_hos
 /* ---- A-buffer: lv/abuffer.py:104-114 scan_offsets; 195-255 _chunk_count_kernel/_write_kernel.
  * offsets has V+1 entries (u32): offsets[i] = exclusive scan of the culling-masked counts,
  * offsets[V] = total, so count(i) = offsets[i+1]-offsets[i].  cull_base may be NULL (VSV).
- * The total is also written to stats[LVX_ST_FRAG_TOTAL]. */
+ * The total is also written to stats[LVX_ST_FRAG_TOTAL].  cursor (V u32, may be NULL): when given, the scan
+ * also writes lvx_scatter's cursors in the same pass (list start per visible voxel, a parking value per
+ * culled one); pass cursor_ready = 1 to lvx_scatter then. */
 int64_t lvx_scan_scratch_bytes(int64_t n_voxels);
 int lvx_scan(const uint32_t *base, const uint8_t *cull_base, int64_t n_voxels,
-             uint32_t *offsets, void *scratch, uint64_t *stats, void *stream);
-/* second traversal: cursor (V u32 scratch) is initialised from offsets; fragments of each
+             uint32_t *offsets, void *scratch, uint64_t *stats, uint32_t *cursor, void *stream);
+/* second traversal: cursor (V u32 scratch) is initialised from offsets (unless cursor_ready != 0: lvx_scan
+ * with the same culling mask has already written it); fragments of each
  * voxel end up in ascending segment order (lv/abuffer.py:313-317 semantics) after the
  * ordering pass, which walks vis_list (the voxels that own fragments).
  * Tight index (optional; pass all three arrays or none): tight_frags (frag_capacity u32),
@@ -183,7 +192,7 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
                 const uint8_t *cull_flat /* NULL = no culling */, const uint32_t *vis_list,
                 const uint32_t *offsets, uint32_t *cursor, uint32_t *frags, int64_t frag_capacity,
                 uint32_t *tight_frags, uint16_t *tight_slot, uint16_t *tight_cnt /* may be NULL */,
-                uint64_t *stats, void *stream);
+                int cursor_ready, uint64_t *stats, void *stream);
 
 /* ---- shading: lv/shading.py:72-155 _trilinear/_cone_trace/_shading_kernel, 170-185.
  * dirs_host: n_dirs*3 unit vectors (lv/shading.py:32-40); light_host: unit light direction.

@@ -50,19 +50,21 @@ SIGNATURES = {
     "lvx_voxelize_wide": (_I, [_P, _P, _P, _L, _L, _I, _D, _D, _D, _I, _I, _P, _P, _P]),
     "lvx_widen": (_I, [_P, _P, _L, _P, _P]),
     "lvx_pack_wide": (_I, [_P, _L, _P, _P, _P, _P]),
+    "lvx_pack_wide_mip1": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "lvx_finalize_base": (_I, [_P, _P, _L, _P, _P]),
     "lvx_build_mips": (_I, [_P, _I, _P, _P]),
+    "lvx_build_mips_upper": (_I, [_I, _P, _P]),
     "lvx_cull_scratch_words": (_L, [_I]),
     "lvx_cull": (_I, [_P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "lvx_occupied_pyramid": (_I, [_P, _I, _P, _P, _P, _P]),
     "lvx_list_words": (_L, [_L]),
     "lvx_tile_owners": (_I, [_P, _I, _P, _I, _I, _I, _I, _D, _P, _P, _P, _P]),
     "lvx_scan_scratch_bytes": (_L, [_L]),
-    "lvx_scan": (_I, [_P, _P, _L, _P, _P, _P, _P]),
+    "lvx_scan": (_I, [_P, _P, _L, _P, _P, _P, _P, _P]),
     "lvx_max_fragments": (_L, []),
     "lvx_segment_order_scratch_words": (_L, [_L, _I, _I]),
     "lvx_segment_order": (_I, [_P, _P, _L, _I, _I, _P, _P, _P]),
-    "lvx_scatter": (_I, [_P, _P, _L, _D, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P, _P]),
+    "lvx_scatter": (_I, [_P, _P, _L, _D, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P, _I, _P, _P]),
     "lvx_march_levels": (_I, [_P, _I, _P, _P]),
     "lvx_shade_scratch_bytes": (_L, [_L]),
     "lvx_shade": (_I, [_P, _P, _I, _P, _P, _I, _D, _P, _D, _P, _P, _I, _P, _P, _P]),

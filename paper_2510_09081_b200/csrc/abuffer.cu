@@ -30,6 +30,9 @@
 #define LVX_BATCH 4   // cells of a traversal row whose atomics are issued back to back
 #endif
 
+// cursor value of a culled voxel: far above any fragment capacity (see k_scatter)
+#define LVX_CURSOR_CULLED 0xF0000000u
+
 namespace lvx {
 
 // ----------------------------------------------------------------------------- scan
@@ -40,7 +43,8 @@ constexpr uint64_t FLAG_AGG = 1ull << 62, FLAG_INC = 2ull << 62, VAL_MASK = (1ul
 
 __global__ void __launch_bounds__(SCAN_THREADS)
 k_scan(const uint32_t *__restrict__ base, const uint8_t *__restrict__ cull, int64_t V,
-       uint32_t *__restrict__ offsets, unsigned long long *__restrict__ state, uint64_t *__restrict__ stats) {
+       uint32_t *__restrict__ offsets, uint32_t *__restrict__ cursor, unsigned long long *__restrict__ state,
+       uint64_t *__restrict__ stats) {
     __shared__ uint32_t s_tile;
     __shared__ uint32_t s_warp[SCAN_THREADS / 32];
     __shared__ uint64_t s_prefix;
@@ -54,6 +58,7 @@ k_scan(const uint32_t *__restrict__ base, const uint8_t *__restrict__ cull, int6
     const int64_t i0 = tile * SCAN_TILE + (int64_t)tid * SCAN_ITEMS;
 
     uint32_t c[SCAN_ITEMS];
+    uint32_t culled = 0;       // bit k: voxel i0 + k is culled
 #pragma unroll
     for (int k = 0; k < SCAN_ITEMS; k++) c[k] = 0;
     if (i0 < V) {   // V is a multiple of 8, so a thread's 8 items are all in or all out
@@ -65,8 +70,8 @@ k_scan(const uint32_t *__restrict__ base, const uint8_t *__restrict__ cull, int6
             const uint2 m = *reinterpret_cast<const uint2 *>(cull + i0);
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-                if (((m.x >> (8 * k)) & 0xFFu) == 0) c[k] = 0;
-                if (((m.y >> (8 * k)) & 0xFFu) == 0) c[4 + k] = 0;
+                if (((m.x >> (8 * k)) & 0xFFu) == 0) { c[k] = 0; culled |= 1u << k; }
+                if (((m.y >> (8 * k)) & 0xFFu) == 0) { c[4 + k] = 0; culled |= 16u << k; }
             }
         }
     }
@@ -133,6 +138,13 @@ k_scan(const uint32_t *__restrict__ base, const uint8_t *__restrict__ cull, int6
         for (int k = 0; k < SCAN_ITEMS; k++) { o[k] = run; run += c[k]; }
         *reinterpret_cast<uint4 *>(offsets + i0) = make_uint4(o[0], o[1], o[2], o[3]);
         *reinterpret_cast<uint4 *>(offsets + i0 + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+        if (cursor) {   // the scatter pass's cursors (see k_init_cursor): list start, or the parking value of a culled voxel
+#pragma unroll
+            for (int k = 0; k < SCAN_ITEMS; k++)
+                if ((culled >> k) & 1u) o[k] = LVX_CURSOR_CULLED;
+            *reinterpret_cast<uint4 *>(cursor + i0) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4 *>(cursor + i0 + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+        }
     }
 }
 
@@ -171,7 +183,6 @@ __device__ __forceinline__ bool segment_misses_cube(float ax, float ay, float az
 // Culled voxels are not looked up: k_init_cursor parks their cursor at LVX_CURSOR_CULLED, far
 // above any fragment capacity, so the position their atomic returns fails the capacity test and
 // nothing is stored -- one dependent memory round trip per cell (the atomic) instead of two.
-#define LVX_CURSOR_CULLED 0xF0000000u
 #ifndef LVX_SCAT_MINB
 #define LVX_SCAT_MINB 1
 #endif
@@ -253,6 +264,109 @@ k_scatter(const double *__restrict__ verts, const int32_t *__restrict__ segs, in
                 if (on[k] && (int64_t)pos[k] < cap) frags[pos[k]] = word[k];
         }
     });
+}
+
+// Row-pooled form of k_scatter (capsule method).  One thread still owns one segment, but only for the
+// cheap part -- stepping its traversal (RowGen) -- and the warp steps its 32 traversals in lockstep.  The rows
+// they produce (3-4 cells each) go into a per-warp queue in shared memory, and whenever 32 rows are queued
+// every lane takes ONE row, whoever's it is: the loose test, the cursor atomics and the fragment stores of
+// 32 rows are then issued by 32 lanes, instead of by the 16-17 lanes that are still inside their own
+// traversal at any given moment (segments differ a lot in their number of rows).  The f32 view of the
+// owner's segment is read from shared memory.  Same cells, same words: the fragment lists do not change.
+constexpr int SR_WARPS = 4;
+struct ScatterWarp {
+    int ox[32], oy[32], oz[32];
+    float ax[32], ay[32], az[32], ex[32], ey[32], ez[32], inv_ee[32];
+    uint32_t seg[32];
+    uint32_t q_xyz[64], q_meta[64];      // x | y << 10 | z << 20 | axis << 30 ;  len | owner << 16
+};
+
+__global__ void __launch_bounds__(SR_WARPS * 32, LVX_SCAT_MINB)
+k_scatter_rows(const double *__restrict__ verts, const int32_t *__restrict__ segs, int64_t n_seg, double rt,
+               float r_tight, int res, const uint8_t *__restrict__ own_flat, const PyrOffsets O,
+               uint32_t *__restrict__ cursor, uint32_t *__restrict__ frags, int64_t cap) {
+    __shared__ ScatterWarp s_w[SR_WARPS];
+    const int lane = threadIdx.x & 31;
+    ScatterWarp &W = s_w[threadIdx.x >> 5];
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    const int64_t si = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    RowGen g;
+    g.done = true; g.j = 1; g.j_max = 0;
+    if (si < n_seg) {
+        const int64_t i = segs[si];
+        const d3 a = ld3(verts + 3 * i), b = ld3(verts + 3 * i + 3);
+        if (!own_flat || segment_visible(own_flat, O, res, a, b, rt)) {
+            g.init(a, b, rt, res);
+            const SegF sf = make_segf(a, b);
+            W.ox[lane] = sf.ox; W.oy[lane] = sf.oy; W.oz[lane] = sf.oz;
+            W.ax[lane] = sf.ax; W.ay[lane] = sf.ay; W.az[lane] = sf.az;
+            W.ex[lane] = sf.ex; W.ey[lane] = sf.ey; W.ez[lane] = sf.ez; W.inv_ee[lane] = sf.inv_ee;
+            W.seg[lane] = (uint32_t)i;
+        }
+    }
+    __syncwarp();
+    const float far2 = (r_tight + 0.8661f) * (r_tight + 0.8661f) * 1.001f + 1e-4f;
+    const uint32_t res_u = (uint32_t)res;
+    uint32_t qn = 0;
+    for (;;) {
+        const bool more = __any_sync(0xffffffffu, !g.finished());
+        if (more) {
+            int x = 0, y = 0, z = 0, axis = 0, len = 0;
+            const bool have = g.next(x, y, z, axis, len);
+            const uint32_t m = __ballot_sync(0xffffffffu, have);
+            if (have) {
+                const uint32_t pos = qn + __popc(m & lt_mask);
+                W.q_xyz[pos] = (uint32_t)x | ((uint32_t)y << 10) | ((uint32_t)z << 20) | ((uint32_t)axis << 30);
+                W.q_meta[pos] = (uint32_t)len | ((uint32_t)lane << 16);
+            }
+            qn += __popc(m);
+            __syncwarp();
+            if (qn < 32) continue;
+        } else if (qn == 0) break;
+        // ---- 32 rows (or the rest), one per lane
+        const uint32_t take = qn < 32 ? qn : 32;
+        qn -= take;
+        if ((uint32_t)lane < take) {
+            const uint32_t xyz = W.q_xyz[qn + lane], meta = W.q_meta[qn + lane];
+            const int x = (int)(xyz & 1023u), y = (int)((xyz >> 10) & 1023u), z = (int)((xyz >> 20) & 1023u);
+            const int axis = (int)(xyz >> 30), len = (int)(meta & 0xFFFFu), o = (int)(meta >> 16);
+            SegF sf;
+            sf.ox = W.ox[o]; sf.oy = W.oy[o]; sf.oz = W.oz[o];
+            sf.ax = W.ax[o]; sf.ay = W.ay[o]; sf.az = W.az[o];
+            sf.ex = W.ex[o]; sf.ey = W.ey[o]; sf.ez = W.ez[o]; sf.inv_ee = W.inv_ee[o];
+            const uint32_t seg2 = W.seg[o] << 1;
+            const float bfx = sf.ax + sf.ex, bfy = sf.ay + sf.ey, bfz = sf.az + sf.ez;
+            const uint32_t stride = axis == 0 ? 1u : (axis == 1 ? res_u : res_u * res_u);
+            const uint32_t idx0 = (uint32_t)x + res_u * ((uint32_t)y + res_u * (uint32_t)z);
+            const float sx = axis == 0 ? 1.f : 0.f, sy = axis == 1 ? 1.f : 0.f, sz = axis == 2 ? 1.f : 0.f;
+            const float fx = (float)(x - sf.ox) + 0.5f, fy = (float)(y - sf.oy) + 0.5f, fz = (float)(z - sf.oz) + 0.5f;
+            for (int u0 = 0; u0 < len; u0 += LVX_BATCH) {
+                uint32_t word[LVX_BATCH], pos[LVX_BATCH];
+                bool on[LVX_BATCH];
+#pragma unroll
+                for (int k = 0; k < LVX_BATCH; k++) {
+                    const int u = u0 + k;
+                    on[k] = u < len;
+                    word[k] = 0;
+                    if (on[k]) {
+                        const float cx = fx + (float)u * sx, cy = fy + (float)u * sy, cz = fz + (float)u * sz;
+                        bool loose = false;
+                        if (r_tight >= 0.f) {
+                            loose = segf_dist2(sf, cx, cy, cz) > far2 ||
+                                    segment_misses_cube(sf.ax - cx, sf.ay - cy, sf.az - cz, bfx - cx, bfy - cy, bfz - cz, r_tight);
+                        }
+                        word[k] = seg2 | (loose ? 1u : 0u);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < LVX_BATCH; k++) pos[k] = on[k] ? atomicAdd(&cursor[idx0 + (uint32_t)(u0 + k) * stride], 1u) : 0u;
+#pragma unroll
+                for (int k = 0; k < LVX_BATCH; k++)
+                    if (on[k] && (int64_t)pos[k] < cap) frags[pos[k]] = word[k];
+            }
+        }
+        __syncwarp();
+    }
 }
 
 // ----------------------------------------------------------------------------- ordering
@@ -533,12 +647,12 @@ int64_t lvx_scan_scratch_bytes(int64_t n_voxels) {
 }
 
 int lvx_scan(const uint32_t *base, const uint8_t *cull_base, int64_t n_voxels, uint32_t *offsets,
-             void *scratch, uint64_t *stats, void *stream) {
+             void *scratch, uint64_t *stats, uint32_t *cursor, void *stream) {
     if (n_voxels < 8 || (n_voxels & 7)) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t tiles = (n_voxels + SCAN_TILE - 1) / SCAN_TILE;
     LVX_CUDA(cudaMemsetAsync(scratch, 0, (size_t)lvx_scan_scratch_bytes(n_voxels), s));
-    k_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(base, cull_base, n_voxels, offsets,
+    k_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(base, cull_base, n_voxels, offsets, cursor,
                                                    (unsigned long long *)scratch, stats);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
@@ -549,14 +663,14 @@ int64_t lvx_max_fragments(void) { return (int64_t)LVX_CURSOR_CULLED - 1; }
 int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double rt, double r_tight, int res, int method,
                 const uint8_t *cull_flat, const uint32_t *vis_list, const uint32_t *offsets, uint32_t *cursor,
                 uint32_t *frags, int64_t frag_capacity, uint32_t *tight_frags, uint16_t *tight_slot, uint16_t *tight_cnt,
-                uint64_t *stats, void *stream) {
+                int cursor_ready, uint64_t *stats, void *stream) {
     if (!vis_list) return LVX_E_ARG;
     if (!pow2(res) || method < 0 || method > 2) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t V = (int64_t)res * res * res;
     if (V & 3) return LVX_E_ARG;
     if (frag_capacity >= (int64_t)LVX_CURSOR_CULLED) return LVX_E_ARG;
-    k_init_cursor<<<blocks_for(V / 4, 256), 256, 0, s>>>(offsets, cull_flat, cursor, V);
+    if (!cursor_ready) k_init_cursor<<<blocks_for(V / 4, 256), 256, 0, s>>>(offsets, cull_flat, cursor, V);
     const bool want_tight = tight_frags != nullptr;
     if (want_tight != (tight_slot != nullptr) || want_tight != (tight_cnt != nullptr)) return LVX_E_ARG;
     if (!want_tight) r_tight = -1.0;
@@ -568,7 +682,11 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
         for (int l = 0; l < 12; l++) O.off[l] = l < L.n_levels ? (uint32_t)L.off[l] : 0u;
         O.n_levels = L.n_levels;
     }
-    if (n_seg > 0)
+    static const bool old_scatter = getenv("LVX_SCATTER_OLD") != nullptr;
+    if (n_seg > 0 && method == 1 && !old_scatter)       // capsule traversal: rows pooled per warp
+        k_scatter_rows<<<blocks_for(n_seg, SR_WARPS * 32), SR_WARPS * 32, 0, s>>>(verts, segs, n_seg, rt, (float)r_tight, res,
+                                                                                 cull_flat, O, cursor, frags, frag_capacity);
+    else if (n_seg > 0)
         k_scatter<<<blocks_for(n_seg, 128), 128, 0, s>>>(verts, segs, n_seg, rt, (float)r_tight, res, method,
                                                         cull_flat, O, cursor, frags, frag_capacity);
     {

@@ -57,10 +57,9 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
                 q_solid(base, res, x, y - 1, z) && q_solid(base, res, x, y + 1, z) &&
                 q_solid(base, res, x, y, z - 1) && q_solid(base, res, x, y, z + 1);
             if (s) {
-                // (solid voxels are rare: a list of the first LVX_SOLID_CAP of them, word 0 = their number)
-                const uint32_t slot = atomicAdd(&solid_list[0], 1u);
-                if (slot < LVX_SOLID_CAP) solid_list[LVX_LIST_HDR + slot] = (uint32_t)idx;
-                // flag every brick that overlaps this solid voxel dilated by one voxel, at both brick sizes
+                // flag every brick that overlaps this solid voxel dilated by one voxel, at both brick sizes.
+                // In a frame with many solid voxels most flags are already set: look before the atomic
+                // (a stale zero only costs a redundant atomicOr).
                 uint32_t *bits = bricks;
 #pragma unroll
                 for (int lvl = 0; lvl < 2; lvl++) {
@@ -73,7 +72,8 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
                         for (int by = by0; by <= by1; by++)
                             for (int bx = bx0; bx <= bx1; bx++) {
                                 const int bi = bx + rb * (by + rb * bz);
-                                atomicOr(&bits[bi >> 5], 1u << (bi & 31));
+                                const uint32_t bit = 1u << (bi & 31);
+                                if (!(*reinterpret_cast<volatile uint32_t *>(&bits[bi >> 5]) & bit)) atomicOr(&bits[bi >> 5], bit);
                             }
                     bits += brick_words(res, B);
                 }
@@ -83,6 +83,21 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
         if (lane == 0 && idx < V) {
             solid[idx >> 5] = m;
             if (m) atomicAdd((unsigned long long *)&stats[LVX_ST_SOLID], (unsigned long long)__popc(m));
+        }
+        // (solid voxels are rare in thin-line frames: a list of the first LVX_SOLID_CAP of them, word 0 = their
+        // number.  One counter atomic per warp; once the counter is past the cap -- nobody reads the list then,
+        // only "more than the cap" -- the appends stop, so a frame full of solid voxels does not queue up on it)
+        if (m) {
+            uint32_t slot0 = 0;
+            if (lane == 0) {
+                slot0 = *reinterpret_cast<volatile uint32_t *>(&solid_list[0]);
+                if (slot0 <= LVX_SOLID_CAP) slot0 = atomicAdd(&solid_list[0], (uint32_t)__popc(m));
+            }
+            slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+            if (s) {
+                const uint32_t slot = slot0 + __popc(m & ((1u << lane) - 1u));
+                if (slot < LVX_SOLID_CAP) solid_list[LVX_LIST_HDR + slot] = (uint32_t)idx;
+            }
         }
     }
     // compacted list of occupied voxels (the march kernels then run on dense warps): block scan of
@@ -474,13 +489,18 @@ k_march(const uint32_t *__restrict__ solid, const uint32_t *__restrict__ bricks,
         // (f32, conservative: flags cover the solid voxels dilated by a voxel) gives the parameter where
         // the segment leaves the last flagged 8^3 brick; two voxels later the literal walk may stop.
         const float ox = x + 0.5f, oy = y + 0.5f, oz = z + 0.5f;
-        const float tl = coarse_last_flagged(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz,
-                                             (float)cx, (float)cy, (float)cz);
-        bool blocked = false;
-        if (tl >= 0.0f) {
-            const float dmax = fmaxf(fmaxf(fabsf((float)cx - ox), fabsf((float)cy - oy)), fabsf((float)cz - oz));
-            const double t_stop = dmax > 0.f ? (double)tl * 1.0001 + 2.0 / (double)dmax + 1e-4 : 2.0;
-            blocked = march_blocked(solid, res, x, y, z, cx, cy, cz, t_stop);
+        const float dmax = fmaxf(fmaxf(fabsf((float)cx - ox), fabsf((float)cy - oy)), fabsf((float)cz - oz));
+        // In a frame with many solid voxels most candidates sit inside the solid mass and their walk ends in a
+        // blocker within a few steps: probe the first ~6 voxels of the literal walk before paying for the brick
+        // walk.  (A "true" of the truncated walk is a "true" of the full one; a "false" decides nothing.)
+        bool blocked = dmax > 0.f && march_blocked(solid, res, x, y, z, cx, cy, cz, 6.0 / (double)dmax);
+        if (!blocked) {
+            const float tl = coarse_last_flagged(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz,
+                                                 (float)cx, (float)cy, (float)cz);
+            if (tl >= 0.0f) {
+                const double t_stop = dmax > 0.f ? (double)tl * 1.0001 + 2.0 / (double)dmax + 1e-4 : 2.0;
+                blocked = march_blocked(solid, res, x, y, z, cx, cy, cz, t_stop);
+            }
         }
         vis[idx] = blocked ? 0 : 1;
     }

@@ -118,6 +118,93 @@ __device__ __forceinline__ void rows_capsule(const d3 &a, const d3 &b, double r,
     }
 }
 
+// The same traversal as a state machine: next() hands out the rows of rows_capsule (zero-length
+// segments: rows_aabb) one at a time, in the same order, from the same arithmetic.  A warp can so step
+// the traversals of its 32 segments in lockstep and pool their rows (k_scatter_rows).
+struct RowGen {
+    double t_min, t_max, e1, e2, s1, s2, r1, r2;     // constants of the segment (capsule form)
+    double t0, p0_1, p0_2;                           // slab state
+    int lo_j, hi_j, lo_k, hi_k, res;
+    int a0, a1, a2;
+    int ci, j, j_max, k_min, len;                    // rows j..j_max of the current slab
+    bool box, done;
+
+    __device__ __forceinline__ void init(const d3 &a, const d3 &b, double r, int res_) {
+        res = res_; done = false; j = 1; j_max = 0; ci = 0; k_min = 0; len = 0;
+        const d3 d{b.x - a.x, b.y - a.y, b.z - a.z};
+        box = d.x == 0.0 && d.y == 0.0 && d.z == 0.0;
+        if (box) {      // rows_aabb: slabs = z, rows = y, cells along x
+            int x0 = (int)floor(fmin(a.x, b.x) - r), x1 = (int)floor(fmax(a.x, b.x) + r);
+            int y0 = (int)floor(fmin(a.y, b.y) - r), y1 = (int)floor(fmax(a.y, b.y) + r);
+            int z0 = (int)floor(fmin(a.z, b.z) - r), z1 = (int)floor(fmax(a.z, b.z) + r);
+            x0 = max(x0, 0); y0 = max(y0, 0); z0 = max(z0, 0);
+            x1 = min(x1, res - 1); y1 = min(y1, res - 1); z1 = min(z1, res - 1);
+            a0 = 2; a1 = 1; a2 = 0;
+            lo_j = y0; hi_j = y1; lo_k = x0; hi_k = x1;
+            ci = z0 - 1; t0 = (double)z1;            // (t0 doubles as the last slab here)
+            if (x1 < x0) done = true;
+            t_min = t_max = e1 = e2 = s1 = s2 = r1 = r2 = p0_1 = p0_2 = 0.0;
+            return;
+        }
+        rank3(fabs(d.x), fabs(d.y), fabs(d.z), a0, a1, a2);
+        double d0 = sel(d, a0), d1 = sel(d, a1), d2 = sel(d, a2);
+        double v0_0 = sel(a, a0), v0_1 = sel(a, a1), v0_2 = sel(a, a2);
+        double v1_0 = sel(b, a0), v1_1 = sel(b, a1), v1_2 = sel(b, a2);
+        if (d0 < 0.0) {
+            double t;
+            t = v0_0; v0_0 = v1_0; v1_0 = t;
+            t = v0_1; v0_1 = v1_1; v1_1 = t;
+            t = v0_2; v0_2 = v1_2; v1_2 = t;
+            d0 = -d0; d1 = -d1; d2 = -d2;
+        }
+        s1 = d1 / d0; s2 = d2 / d0;
+        t_min = v0_0 - 1.0 * r;
+        t_max = v1_0 + 1.0 * r;
+        e1 = v0_1 - s1 * r; e2 = v0_2 - s2 * r;
+        r1 = r * sqrt(1.0 + s1 * s1);
+        r2 = r * sqrt(1.0 + s2 * s2);
+        lo_j = (int)floor(fmin(v0_1, v1_1) - r); hi_j = (int)floor(fmax(v0_1, v1_1) + r);
+        lo_k = (int)floor(fmin(v0_2, v1_2) - r); hi_k = (int)floor(fmax(v0_2, v1_2) + r);
+        lo_j = max(lo_j, 0); lo_k = max(lo_k, 0);
+        hi_j = min(hi_j, res - 1); hi_k = min(hi_k, res - 1);
+        t0 = t_min; p0_1 = e1; p0_2 = e2;
+    }
+    __device__ __forceinline__ bool finished() const { return done && j > j_max; }
+    __device__ __forceinline__ void advance() {
+        j = 1; j_max = 0;
+        if (box) {
+            if ((double)ci >= t0) { done = true; return; }
+            ci++;
+            if (hi_j >= lo_j) { j = lo_j; j_max = hi_j; k_min = lo_k; len = hi_k - lo_k + 1; }
+            return;
+        }
+        if (!(t0 < t_max)) { done = true; return; }
+        const double t1 = fmin(t_max, floor(t0 + 1.0));
+        const double dt = t1 - t_min;
+        const double p1_1 = e1 + s1 * dt, p1_2 = e2 + s2 * dt;
+        ci = (int)floor(t0);
+        if (ci >= 0 && ci < res) {
+            const int j_min = max((int)floor(fmin(p0_1, p1_1) - r1), lo_j);
+            const int jm = min((int)floor(fmax(p0_1, p1_1) + r1), hi_j);
+            const int km = max((int)floor(fmin(p0_2, p1_2) - r2), lo_k);
+            const int k_max = min((int)floor(fmax(p0_2, p1_2) + r2), hi_k);
+            if (k_max >= km) { j = j_min; j_max = jm; k_min = km; len = k_max - km + 1; }
+        }
+        t0 = t1; p0_1 = p1_1; p0_2 = p1_2;
+    }
+    // one step: at most one slab advance, at most one row (x, y, z) + u * e_axis, u in [0, n)
+    __device__ __forceinline__ bool next(int &x, int &y, int &z, int &axis, int &n) {
+        if (j > j_max && !done) advance();
+        if (j > j_max) return false;
+        x = a0 == 0 ? ci : (a1 == 0 ? j : k_min);
+        y = a0 == 1 ? ci : (a1 == 1 ? j : k_min);
+        z = a0 == 2 ? ci : (a1 == 2 ? j : k_min);
+        axis = a2; n = len;
+        j++;
+        return true;
+    }
+};
+
 template <class F>
 __device__ __forceinline__ void cells_aabb(const d3 &v0, const d3 &v1, double r, int res, F &&f) {
     rows_aabb(v0, v1, r, res, [&](int x, int y, int z, int, int len) { for (int u = 0; u < len; u++) f(x + u, y, z); });

@@ -140,6 +140,49 @@ k_pack_wide(const unsigned long long *__restrict__ wide, int64_t n, uint32_t *__
         atomicAdd((unsigned long long *)&stats[LVX_ST_SATURATED], (unsigned long long)sat);
 }
 
+// Pack + level 1 of the pyramid in one read of the accumulators (res >= 64).  One thread per level-1
+// cell: its 2x2x2 children are four 16-byte loads (two x-adjacent accumulators each; a warp reads 512
+// contiguous bytes per row), four 8-byte stores of packed words, one f64 store of the parent.  The
+// "occupancy non-zero" bits of a row's 64 voxels are two ballots interleaved by lanes 0 and 16.
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {     // bit k -> bit 2k
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+__global__ void __launch_bounds__(256)
+k_pack_mip1(const ulonglong2 *__restrict__ wide2, int res, uint32_t *__restrict__ base, uint32_t *__restrict__ nz_bits,
+            double *__restrict__ mip1, uint64_t *__restrict__ stats) {
+    const int rl = res >> 1;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;    // rl^3 is a multiple of the block size
+    const int lane = threadIdx.x & 31;
+    const int x = (int)(i % rl), y = (int)((i / rl) % rl), z = (int)(i / ((int64_t)rl * rl));
+    ulonglong2 w[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+        w[k] = wide2[(2 * x + (int64_t)res * ((2 * y + (k & 1)) + (int64_t)res * (2 * z + (k >> 1)))) >> 1];
+    uint64_t sat = 0;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int64_t v = 2 * x + (int64_t)res * ((2 * y + (k & 1)) + (int64_t)res * (2 * z + (k >> 1)));
+        uint64_t c0 = w[k].x >> 32, o0 = w[k].x & 0xFFFFFFFFull, c1 = w[k].y >> 32, o1 = w[k].y & 0xFFFFFFFFull;
+        if (c0 > 0xFFFF) { sat += c0 - 0xFFFF; c0 = 0xFFFF; }     // lv/voxelizer.py:333-336, 493
+        if (c1 > 0xFFFF) { sat += c1 - 0xFFFF; c1 = 0xFFFF; }
+        if (o0 > 0xFFFF) o0 = 0xFFFF;                              // lv/voxelizer.py:494
+        if (o1 > 0xFFFF) o1 = 0xFFFF;
+        *reinterpret_cast<uint2 *>(base + v) = make_uint2((uint32_t)((c0 << 16) | o0), (uint32_t)((c1 << 16) | o1));
+        s += min((uint32_t)o0, 4096u) + min((uint32_t)o1, 4096u);   // lv/voxelizer.py:496
+        const uint32_t be = __ballot_sync(0xffffffffu, o0 != 0), bo = __ballot_sync(0xffffffffu, o1 != 0);
+        if (nz_bits && (lane & 15) == 0)
+            nz_bits[v >> 5] = spread16((be >> lane) & 0xFFFFu) | (spread16((bo >> lane) & 0xFFFFu) << 1);
+    }
+    mip1[i] = (double)s * (1.0 / 32768.0);   // (sum / 4096) / 8, exact
+    sat = warp_sum_u64(sat);
+    if (lane == 0 && sat) atomicAdd((unsigned long long *)&stats[LVX_ST_SATURATED], (unsigned long long)sat);
+}
+
 // ----------------------------------------------------------------------------- mips
 // Level sums are exact dyadic rationals (multiples of 2^-(12+3l) below 2^53 ulps), so any
 // summation order gives the reference's bits.
@@ -275,12 +318,22 @@ int lvx_finalize_base(uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels,
     return LVX_OK;
 }
 
-int lvx_build_mips(const uint32_t *base, int res, double *mips, void *stream) {
+int lvx_pack_wide_mip1(const uint64_t *wide, int res, uint32_t *base, uint32_t *nz_bits, double *mips,
+                       uint64_t *stats, void *stream) {
+    if (!pow2(res) || res < 64 || !mips) return LVX_E_ARG;
+    const int rl = res >> 1;
+    k_pack_mip1<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const ulonglong2 *)wide, res, base, nz_bits, mips, stats);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+static int build_mips_from(const uint32_t *base, int res, double *mips, void *stream) {
     if (!pow2(res)) return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     const LevelOffsets L = make_level_offsets(res);
     const int64_t V = L.off[1];
-    {
+    if (base) {
         const int rl = res >> 1;
         k_mip1<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, s>>>(base, res, mips);
     }
@@ -299,5 +352,12 @@ int lvx_build_mips(const uint32_t *base, int res, double *mips, void *stream) {
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }
+
+int lvx_build_mips(const uint32_t *base, int res, double *mips, void *stream) {
+    if (!base) return LVX_E_ARG;
+    return build_mips_from(base, res, mips, stream);
+}
+
+int lvx_build_mips_upper(int res, double *mips, void *stream) { return build_mips_from(nullptr, res, mips, stream); }
 
 }  // extern "C"

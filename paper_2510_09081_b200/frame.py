@@ -104,6 +104,7 @@ class FrameEngine:
         self.wide = None
         self.nz_bits = None          # per-voxel "occupancy non-zero" bits from the pack pass (level-0 shading mask)
         self._nz_valid = False
+        self._mip1_done = False
         # Accumulate into 64-bit (count << 32 | occ) words and pack afterwards (lvx_voxelize_wide +
         # lvx_pack_wide) instead of the packed 32-bit word with carry repair (lvx_voxelize).  The wide
         # form never needs the atomic's return value, so it compiles to fire-and-forget RED.64: measured
@@ -142,11 +143,11 @@ class FrameEngine:
         n = 1 + 1                                   # stats_reset, upload
         n += 3 if self.order_brick > 0 else 0       # processing order: histogram, scan, scatter
         n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
-        n += 1 + pyramid(2)                         # mips: level 1 from the packed grid, then the rest
+        n += (0 if (self.use_wide and self.res >= 64) else 1) + pyramid(2)   # mips: level 1 (fused into the pack pass at res >= 64), then the rest
         n += (5 if self.strategy == "vcsv" else 1) + pyramid(1)   # solid, super-brick shadow, visibility, march, dilate | occupied; or-mips
         n += 1 + pyramid(1) if self._owned else 0   # tile owners + their OR pyramid
         n += 1                                      # scan
-        n += 3 + 1                                  # cursor init, scatter, order; march table
+        n += 2 + 1                                  # scatter, order (the cursors come from the scan); march table
         n += 1 + pyramid(1) + 1                     # non-empty masks (level 0, the rest), shade
         if self.shading == "demand":
             n += 3                                  # trace_hits, need list, resolve
@@ -220,10 +221,15 @@ class FrameEngine:
                 after_voxelize(self)
             if self.nz_bits is None and self.res >= 32:
                 self.nz_bits = self.torch.empty(self.V // 32, dtype=self.torch.int32, device=self.dev)
-            ops.pack_wide(self.wide, self.base, self.stats, self.nz_bits)
+            if self.res >= 64:     # pack + level 1 of the pyramid in one read of the accumulators
+                ops.pack_wide_mip1(self.wide, self.res, self.base, self.stats, self.nz_bits, self.mips)
+                self._mip1_done = True
+            else:
+                ops.pack_wide(self.wide, self.base, self.stats, self.nz_bits)
             self._nz_valid = self.nz_bits is not None
         else:
             self._nz_valid = False
+            self._mip1_done = False
             ops.clear(self.base)
             ops.clear(self.occ_sat)
             ops.voxelize(self.lines, self.res, self.r_min, self.method, self.base, self.occ_sat, self.stats, b, e)
@@ -232,7 +238,10 @@ class FrameEngine:
                 after_voxelize(self)
 
     def _stage_mips(self):
-        ops.build_mips(self.base, self.res, self.mips)
+        if self._mip1_done:
+            ops.build_mips_upper(self.res, self.mips)
+        else:
+            ops.build_mips(self.base, self.res, self.mips)
 
     def _stage_cull(self, cam):
         if self.strategy == "vcsv":
@@ -265,13 +274,14 @@ class FrameEngine:
 
     def _stage_scan(self):
         flat, _ = self._owner_bits()
-        ops.scan(self.base, None if flat is None else flat[:self.V], self.offsets, self.scan_scratch, self.stats)
+        ops.scan(self.base, None if flat is None else flat[:self.V], self.offsets, self.scan_scratch, self.stats,
+                 cursor=self.cursor)
 
     def _stage_scatter(self):
         rt = ops.footprint_radius(self.lines.r, self.r_min)
         flat, lst = self._owner_bits()
         ops.scatter(self.lines, rt, self.res, self.method, flat, lst,
-                    self.offsets, self.cursor, self.frags, self.stats, tight=self.tight)
+                    self.offsets, self.cursor, self.frags, self.stats, tight=self.tight, cursor_ready=True)
 
     def _stage_shade(self):
         demand = self.shading == "demand"

@@ -167,6 +167,16 @@ def pack_wide(wide, base, stats, nz_bits=None):
     check(lib().lvx_pack_wide(_ptr(wide), wide.numel(), _ptr(base), _ptr(nz_bits), _ptr(stats), _stream()), "lvx_pack_wide")
 
 
+def pack_wide_mip1(wide, res, base, stats, nz_bits, mips):
+    """pack_wide + level 1 of build_mips in one read of the accumulators (res >= 64); then build_mips_upper."""
+    check(lib().lvx_pack_wide_mip1(_ptr(wide), int(res), _ptr(base), _ptr(nz_bits), _ptr(mips), _ptr(stats), _stream()),
+          "lvx_pack_wide_mip1")
+
+
+def build_mips_upper(res, mips):
+    check(lib().lvx_build_mips_upper(int(res), _ptr(mips), _stream()), "lvx_build_mips_upper")
+
+
 def finalize_base(base, occ_sat, stats):
     check(lib().lvx_finalize_base(_ptr(base), _ptr(occ_sat), base.numel(), _ptr(stats), _stream()),
           "lvx_finalize_base")
@@ -209,9 +219,10 @@ def scan_scratch_bytes(n_voxels: int) -> int:
     return int(lib().lvx_scan_scratch_bytes(n_voxels))
 
 
-def scan(base, cull_base, offsets, scratch, stats):
+def scan(base, cull_base, offsets, scratch, stats, cursor=None):
+    """`cursor` (optional, V i32): also written by the scan (pass cursor_ready=True to `scatter`)."""
     check(lib().lvx_scan(_ptr(base), _ptr(cull_base), base.numel(), _ptr(offsets), _ptr(scratch),
-                         _ptr(stats), _stream()), "lvx_scan")
+                         _ptr(stats), _ptr(cursor), _stream()), "lvx_scan")
 
 
 TIGHT_MARGIN = 1e-3   # voxels; see csrc/abuffer.cu "Loose bits"
@@ -245,7 +256,8 @@ def _tight_ptrs(tight):
     return (None, None, None) if tight is None else tight.ptrs()
 
 
-def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, cursor, frags, stats, tight=None):
+def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, cursor, frags, stats, tight=None,
+            cursor_ready=False):
     """`tight` (optional TightIndex with capacity >= frags.numel()) receives the index of the fragments whose
     capsule of radius lines.r can reach into their voxel, for the ray tracer."""
     if tight is not None and tight.capacity < frags.numel():
@@ -254,7 +266,8 @@ def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, c
     check(lib().lvx_scatter(_ptr(lines.verts), _ptr(lines.proc_segs), lines.n_segments, float(rt),
                             float(lines.r) + TIGHT_MARGIN, res,
                             METHODS[method], _ptr(cull_flat), _ptr(vis_list), _ptr(offsets), _ptr(cursor),
-                            _ptr(frags), frags.numel(), tf, ts, tc, _ptr(stats), _stream()), "lvx_scatter")
+                            _ptr(frags), frags.numel(), tf, ts, tc, int(bool(cursor_ready)), _ptr(stats), _stream()),
+          "lvx_scatter")
 
 
 def march_levels(bits_flat, res, march):
