@@ -335,6 +335,9 @@ def run_gpu(args):
         if world > 1:
             dist.destroy_process_group()
         return
+    drop_in = None
+    if world == 1 and not args.no_drop_in:
+        drop_in = time_drop_in(args, lvx, torch, ls, host, out_srgb, out_hit, n_variants, rv)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -384,11 +387,47 @@ def run_gpu(args):
                      "per_stage": stage_roof},
         "clocks": clocks,
     }
+    if os.environ.get("LVX_DEBUG_STATS"):
+        line["raw_stats"] = last.raw_stats
+    if drop_in is not None:
+        line["drop_in"] = drop_in
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args.workload, steps=1, warmup=0)
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def time_drop_in(args, lvx, torch, ls, host, out_srgb, out_hit, n_variants, rv):
+    """The same frames through the reference-shaped entry point (lv/pipeline.py:50-150): `ScenePipeline`
+    with cfg.revoxelize, new vertices per frame via update_vertices (pinned host -> HBM), render_frame()
+    returning an Image that owns its pixels, sRGB + hit ids copied back.  Two host synchronisations and
+    fresh output tensors per frame -- the price of the reference's stage-by-stage contract."""
+    _, res, w, h, strat, mode, alpha = WORKLOADS[args.workload]
+    cfg = lvx.PipelineConfig(res=res, width=w, height=h, strategy=strat, mode=mode, alpha=alpha, light=LIGHT,
+                             r=rv, revoxelize=True)
+    pipe = lvx.ScenePipeline(cfg, lineset_override=ls)
+
+    def frame(i):
+        pipe.update_vertices(host[i % n_variants])
+        img = pipe.render_frame()
+        out_srgb.copy_(img.srgb_dev, non_blocking=True)
+        out_hit.copy_(img.hit_id_dev, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for i in range(args.warmup):
+        frame(i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        frame(args.warmup + i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"api": "ScenePipeline(cfg.revoxelize).update_vertices(pinned host) + render_frame() -> Image, "
+                   "sRGB + hit ids copied to the host", "frames_per_s": round(args.steps / (ms * 1e-3), 3),
+            "ms_per_step": round(ms / args.steps, 4)}
 
 
 def run_tiled(args, lvx, torch, dist, rank, world, local, ls, g, cfg):
@@ -548,7 +587,9 @@ def cpu_baseline(workload, steps, warmup, fraction=None):
 
 
 def reference_package_probe():
-    """Whether the reference's own package could run on this host (it needs numba); recorded, not required."""
+    """Whether the reference's own package can run on this host: it needs numba, and its pip-installed copy
+    under baseline/_ref (git-ignored; `python -m pip install --no-index --no-build-isolation --no-deps --target
+    baseline/_ref <copy of /root/reference/pkg>`, done by __graft_entry__.build() where /root/reference exists)."""
     out = {}
     try:
         import numba
@@ -557,6 +598,54 @@ def reference_package_probe():
         out["numba"] = f"not importable ({type(e).__name__})"
     out["baseline_ref_present"] = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "linevox"))
     return out
+
+
+def time_reference_package(workload):
+    """ONE frame of the workload through the UNMODIFIED reference package (linevox: Python + numba, all host
+    threads) and its own entry point: the line set is written as a .lns file with the reference's writer,
+    `linevox.ScenePipeline(PipelineConfig(input=<file>, ...))` loads, voxelizes, culls, builds, shades and
+    renders it.  frames/s = 1 / (sum of the reference's own five stage timers), its definition of the frame
+    (lv/pipeline.py:68-136; file loading and the per-polyline Python loop of compute_clip_normals are its
+    `load_ms`, reported beside).  JIT compilation happens before, on a tiny scene of the same mode."""
+    info = reference_package_probe()
+    if not info["baseline_ref_present"] or "not importable" in info["numba"] or workload == "c4":
+        info["ran"] = False
+        if workload == "c4":
+            info["why"] = "C4 (512^3, 10 M segments) needs tens of GB and minutes per frame in the reference"
+        return info
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "lvx_numba_cache"))
+    sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+    try:
+        import linevox as lv
+        import numba
+        numba.set_num_threads(min(numba.config.NUMBA_NUM_THREADS, len(os.sched_getaffinity(0))))
+        threads = numba.get_num_threads()
+        _, res, w, h, strat, mode, alpha = WORKLOADS[workload]
+        full, ls, *_ = make_workload(workload)
+        t0 = time.perf_counter()
+        lv.ScenePipeline(lv.PipelineConfig(input="gen:helix?turns=2&verts=60", res=32, width=32, height=32,
+                                           strategy=strat, mode=mode, alpha=alpha, light=LIGHT)).render_frame()
+        jit_s = time.perf_counter() - t0
+        path = os.path.join(tempfile.gettempdir(), f"lvx_{workload}.lns")
+        lv.save_lineset(lv.LineSet(ls.vertices, ls.polyline_offsets, ls.radius), path)
+        cfg = lv.PipelineConfig(input=path, res=res, width=w, height=h, strategy=strat, mode=mode, alpha=alpha,
+                                light=LIGHT, r=radius_of(workload))
+        t0 = time.perf_counter()
+        pipe = lv.ScenePipeline(cfg)          # build_geometry: load + clip normals + fit + voxelize
+        img = pipe.render_frame()
+        wall = time.perf_counter() - t0
+        os.unlink(path)
+        st = pipe.stats
+        stages = {k: round(float(st[k]), 1) for k in ("voxelize_ms", "cull_ms", "abuffer_ms", "shading_ms", "render_ms")}
+        frame_s = sum(stages.values()) * 1e-3
+        info.update(ran=True, kind="reference", threads=threads, jit_warmup_s=round(jit_s, 1),
+                    frames_per_s=round(1.0 / frame_s, 5), frame_seconds=round(frame_s, 2),
+                    wall_seconds_incl_load=round(wall, 2), load_ms=round(float(st["load_ms"]), 1),
+                    stages_ms=stages, fragments=int(st["fragments"]), ray_capsule_tests=int(st["ray_capsule_tests"]),
+                    hits=int((img.hit_id >= 0).sum()))
+    except Exception as e:          # the reference arm must still print its line
+        info.update(ran=False, why=f"{type(e).__name__}: {e}"[:300])
+    return info
 
 
 def run_reference(args):
@@ -575,7 +664,7 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.workload, ls),
         "cpu_baseline": cb,
-        "reference_package": reference_package_probe(),
+        "reference_package": (reference_package_probe() if args.no_ref_package else time_reference_package(args.workload)),
         "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -608,6 +697,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-ref-package", action="store_true", help="--impl reference: do not time the real reference "
+                                                                   "package (baseline/_ref) beside the C port")
+    ap.add_argument("--no-drop-in", action="store_true", help="skip the ScenePipeline (reference-shaped API) timing")
     ap.add_argument("--bundles", type=int, default=0, help="c2/c3/c4 only: number of fibre bundles (25 000 segments "
                                                            "each) instead of the workload's own, for segment-count sweeps")
     ap.add_argument("--pipeline", type=int, default=3, help="frames in flight per GPU (engines on separate streams); "

@@ -471,4 +471,5 @@ class FrameEngine:
             "shaded_voxels": shaded, "shading": self.shading,
             "owned_voxels": int(st[N.ST_OWNED]) if self._owned else int(st[N.ST_VISIBLE]),
         }
+        out.raw_stats = [int(v) for v in st[:N.STATS_WORDS]]     # incl. the -DLVX_COUNT debug counters (words 11..15)
         return out
