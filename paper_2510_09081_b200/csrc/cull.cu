@@ -475,32 +475,53 @@ k_visibility(const uint32_t *__restrict__ bricks, const uint8_t *__restrict__ sb
     }
 }
 
-// Phase B: the literal fine march (lv/culling.py:143-188) decides for the remaining candidates.
+// Phase B: the literal fine march (lv/culling.py:143-188) decides for the remaining candidates, in two
+// launches.  In a frame with many solid voxels most candidates sit inside the solid mass and their walk ends
+// in a blocker within a few steps, while the visible ones walk on for hundreds of steps: taken together a
+// warp runs the long walks with a third of its lanes.  k_march_probe walks only the first ~6 voxels (a
+// "true" of the truncated walk is a "true" of the full one; a "false" decides nothing) and compacts the
+// undecided candidates into a second list; k_march then runs the long walks on full warps.
 __global__ void __launch_bounds__(128)
-k_march(const uint32_t *__restrict__ solid, const uint32_t *__restrict__ bricks, const uint32_t *__restrict__ march_list,
-        int res, double cx, double cy, double cz, uint8_t *__restrict__ vis) {
+k_march_probe(const uint32_t *__restrict__ solid, const uint32_t *__restrict__ march_list, int res, double cx, double cy,
+              double cz, uint32_t *__restrict__ long_list) {
     const int64_t n = (int64_t)*reinterpret_cast<const unsigned long long *>(march_list);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_iter = (n + stride - 1) / stride;
+    for (int64_t it = 0; it < n_iter; it++) {
+        const int64_t e = it * stride + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        bool undecided = false;
+        uint32_t idx = 0;
+        if (e < n) {
+            idx = march_list[LVX_LIST_HDR + e];
+            const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
+            const float dmax = fmaxf(fmaxf(fabsf((float)cx - (x + 0.5f)), fabsf((float)cy - (y + 0.5f))), fabsf((float)cz - (z + 0.5f)));
+            undecided = !(dmax > 0.f && march_blocked(solid, res, x, y, z, cx, cy, cz, 6.0 / (double)dmax));
+            // (blocked: vis[idx] stays 0)
+        }
+        list_append_block(long_list, undecided, idx);
+    }
+}
+
+__global__ void __launch_bounds__(128)
+k_march(const uint32_t *__restrict__ solid, const uint32_t *__restrict__ bricks, const uint32_t *__restrict__ long_list,
+        int res, double cx, double cy, double cz, uint8_t *__restrict__ vis) {
+    const int64_t n = (int64_t)*reinterpret_cast<const unsigned long long *>(long_list);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
-        const uint32_t idx = march_list[LVX_LIST_HDR + e];
+        const uint32_t idx = long_list[LVX_LIST_HDR + e];
         const int x = (int)(idx % res), y = (int)((idx / res) % res), z = (int)(idx / ((uint32_t)res * res));
-        // Most candidates are visible, and their literal walk would run on to the camera or the grid's
+        // Most of these candidates are visible, and their literal walk would run on to the camera or the grid's
         // boundary long after the last place a solid voxel can be.  A brick walk over the whole segment
         // (f32, conservative: flags cover the solid voxels dilated by a voxel) gives the parameter where
         // the segment leaves the last flagged 8^3 brick; two voxels later the literal walk may stop.
         const float ox = x + 0.5f, oy = y + 0.5f, oz = z + 0.5f;
-        const float dmax = fmaxf(fmaxf(fabsf((float)cx - ox), fabsf((float)cy - oy)), fabsf((float)cz - oz));
-        // In a frame with many solid voxels most candidates sit inside the solid mass and their walk ends in a
-        // blocker within a few steps: probe the first ~6 voxels of the literal walk before paying for the brick
-        // walk.  (A "true" of the truncated walk is a "true" of the full one; a "false" decides nothing.)
-        bool blocked = dmax > 0.f && march_blocked(solid, res, x, y, z, cx, cy, cz, 6.0 / (double)dmax);
-        if (!blocked) {
-            const float tl = coarse_last_flagged(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz,
-                                                 (float)cx, (float)cy, (float)cz);
-            if (tl >= 0.0f) {
-                const double t_stop = dmax > 0.f ? (double)tl * 1.0001 + 2.0 / (double)dmax + 1e-4 : 2.0;
-                blocked = march_blocked(solid, res, x, y, z, cx, cy, cz, t_stop);
-            }
+        const float tl = coarse_last_flagged(bricks, (res + LVX_BRICK - 1) / LVX_BRICK, LVX_BRICK, ox, oy, oz,
+                                             (float)cx, (float)cy, (float)cz);
+        bool blocked = false;
+        if (tl >= 0.0f) {
+            const float dmax = fmaxf(fmaxf(fabsf((float)cx - ox), fabsf((float)cy - oy)), fabsf((float)cz - oz));
+            const double t_stop = dmax > 0.f ? (double)tl * 1.0001 + 2.0 / (double)dmax + 1e-4 : 2.0;
+            blocked = march_blocked(solid, res, x, y, z, cx, cy, cz, t_stop);
         }
         vis[idx] = blocked ? 0 : 1;
     }
@@ -759,7 +780,8 @@ int64_t lvx_cull_scratch_words(int res) {
     const int64_t V = (int64_t)res * res * res;
     const int64_t rs = (res + LVX_SUPER - 1) / LVX_SUPER;
     return (V + 31) / 32 + brick_words(res, LVX_BRICK) + brick_words(res, LVX_SUPER)
-           + (LVX_LIST_HDR + LVX_SOLID_CAP) + (rs * rs * rs + 3) / 4 + V    // + solid list, super-brick flags, occupied-voxel list
+           + (LVX_LIST_HDR + LVX_SOLID_CAP) + (rs * rs * rs + 3) / 4 + 1    // + solid list, super-brick flags, alignment
+           + (V + LVX_LIST_HDR)                                             // + occupied-voxel list (later: long-march list)
            + rs * rs * rs * LVX_SB_ROW;                                     // + solid voxels shadowing each super-brick
 }
 
@@ -776,7 +798,8 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     const int rs = (res + LVX_SUPER - 1) / LVX_SUPER;
     uint8_t *sb_flag = reinterpret_cast<uint8_t *>(solid_list + LVX_LIST_HDR + LVX_SOLID_CAP);
     uint32_t *occ_list = solid_list + LVX_LIST_HDR + LVX_SOLID_CAP + (rs * rs * rs + 3) / 4;
-    uint32_t *sb_rows = occ_list + V;
+    if ((occ_list - solid_bits) & 1) occ_list++;      // its first two words become a 64-bit list counter
+    uint32_t *sb_rows = occ_list + V + LVX_LIST_HDR;
     LVX_CUDA(cudaMemsetAsync(vis_tmp, 0, (size_t)V, s));
     k_solid<<<blocks_for(V, SOLID_ITEMS * 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, solid_list, occ_list, stats);
     k_superbrick_shadow<<<(unsigned)(rs * rs * rs), 64, 0, s>>>(solid_list, res, (float)cam_voxel_host[0],
@@ -787,7 +810,10 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
     k_visibility<<<nb, 128, 0, s>>>(bricks, sb_flag, sb_rows, solid_list, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                     cam_voxel_host[2], stats, vis_tmp, vis_list);
-    k_march<<<nb, 128, 0, s>>>(solid_bits, bricks, vis_list, res, cam_voxel_host[0], cam_voxel_host[1],
+    // the occupied list has been consumed: its memory becomes the list of candidates whose walk is long
+    LVX_CUDA(cudaMemsetAsync(occ_list, 0, 8, s));
+    k_march_probe<<<nb, 128, 0, s>>>(solid_bits, vis_list, res, cam_voxel_host[0], cam_voxel_host[1], cam_voxel_host[2], occ_list);
+    k_march<<<nb, 128, 0, s>>>(solid_bits, bricks, occ_list, res, cam_voxel_host[0], cam_voxel_host[1],
                                cam_voxel_host[2], vis_tmp);
     LVX_CUDA(cudaMemsetAsync(vis_list, 0, 8, s));
     k_dilate<<<blocks_for(V / 4, 256), 256, 0, s>>>(base, vis_tmp, res, V, cull_flat, vis_list, stats);
