@@ -124,12 +124,14 @@ class FrameEngine:
         # within 2 % of each other on C2 (256^3), 32 is best on C4 (512^3): res / 16
         import os
         self.order_brick = min(int(os.environ.get("LVX_ORDER_BRICK", str(max(8, self.res // 16)))), self.res)
+        self._order_shard = None
         self._stats_host = self._done = self._side = self._ev_side = self._pending = None
         self._geom_stats = self._geom_ms = None
         # tiled frames (`run(..., tile=rect)`): build the A-buffer only for the voxels the tile's rays can
         # visit (see _stage_owners).  False = replicate the whole build on every rank.
         self.tile_build = True
         self._owned = False
+        self._sharded = False
         self.owner_flat = self.owner_list = None
         self._overlapped = False
 
@@ -142,6 +144,7 @@ class FrameEngine:
             return big + (1 if big < levels - first else 0)
         n = 1 + 1                                   # stats_reset, upload
         n += 3 if self.order_brick > 0 else 0       # processing order: histogram, scan, scatter
+        n += 3 if (self.order_brick > 0 and self._sharded) else 0   # ... and the same for a rank's voxelization shard
         n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
         n += (0 if (self.use_wide and self.res >= 64) else 1) + pyramid(2)   # mips: level 1 (fused into the pack pass at res >= 64), then the rest
         n += (6 if self.strategy == "vcsv" else 1) + pyramid(1)   # solid, super-brick shadow, visibility, march probe, march, dilate | occupied; or-mips
@@ -212,11 +215,21 @@ class FrameEngine:
         accumulation and packing and sums `engine.wide` across ranks (exact: per-field saturation
         comes after the sum, lv/voxelizer.py:490-495); on the packed path it runs on the finished `base`."""
         b, e = (0, self.lines.n_segments) if seg_range is None else seg_range
+        self._sharded = self.use_wide and (b, e) != (0, self.lines.n_segments) and e > b
         if self.use_wide:
             if self.wide is None:
                 self.wide = self.torch.empty(self.V, dtype=self.torch.int64, device=self.dev)
             ops.clear(self.wide)
-            ops.voxelize_wide(self.lines, self.res, self.r_min, self.method, self.wide, self.stats, b, e)
+            shard_order = None
+            if self._order is not None and (b, e) != (0, self.lines.n_segments) and e > b:
+                # a multi-GPU rank's shard of the canonical segment list, grouped by brick like the whole set
+                if self._order_shard is None:
+                    self._order_shard = self.torch.empty_like(self._order)
+                ops.segment_order(self.lines, self.res, self.order_brick, self._order_shard, self._order_scratch,
+                                  seg_range=(b, e))
+                shard_order = self._order_shard
+            ops.voxelize_wide(self.lines, self.res, self.r_min, self.method, self.wide, self.stats, b, e,
+                              shard_order=shard_order)
             if after_voxelize is not None:
                 after_voxelize(self)
             if self.nz_bits is None and self.res >= 32:

@@ -114,8 +114,16 @@ def segment_order_scratch_words(n_seg: int, res: int, brick: int) -> int:
     return int(lib().lvx_segment_order_scratch_words(int(n_seg), int(res), int(brick)))
 
 
-def segment_order(lines: DeviceLines, res: int, brick: int, order, scratch):
-    """Fills `order` (i32, n_segments) with lines.segs grouped by brick and makes it the processing order."""
+def segment_order(lines: DeviceLines, res: int, brick: int, order, scratch, seg_range=None):
+    """Fills `order` (i32, n_segments) with lines.segs grouped by brick and makes it the processing order.
+    With `seg_range` = (b, e) only that shard of `segs` is ordered, into order[:e - b], and the whole-set
+    processing order is left alone (a multi-GPU rank orders its own voxelization shard)."""
+    if seg_range is not None:
+        b, e = seg_range
+        if e > b:
+            check(lib().lvx_segment_order(_ptr(lines.verts), _ptr(lines.segs[b:e]), e - b, int(res), int(brick),
+                                          _ptr(order), _ptr(scratch), _stream()), "lvx_segment_order")
+        return
     check(lib().lvx_segment_order(_ptr(lines.verts), _ptr(lines.segs), lines.n_segments, int(res), int(brick),
                                   _ptr(order), _ptr(scratch), _stream()), "lvx_segment_order")
     lines.order = order
@@ -149,10 +157,15 @@ def voxelize(lines: DeviceLines, res, r_min, method, base, occ_sat, stats, seg_b
           "lvx_voxelize")
 
 
-def voxelize_wide(lines: DeviceLines, res, r_min, method, wide, stats, seg_begin=0, seg_end=None):
+def voxelize_wide(lines: DeviceLines, res, r_min, method, wide, stats, seg_begin=0, seg_end=None, shard_order=None):
+    """`shard_order` (optional i32 tensor): the segments of the shard [seg_begin, seg_end) in the order to process
+    them in (segment_order(..., seg_range=...)); the kernel then walks shard_order[0 : seg_end - seg_begin]."""
     seg_end = lines.n_segments if seg_end is None else seg_end
     r = lines.r
-    check(lib().lvx_voxelize_wide(_ptr(lines.verts), _ptr(lines.normals), _ptr(_shard_segs(lines, seg_begin, seg_end)), seg_begin,
+    segs = _shard_segs(lines, seg_begin, seg_end)
+    if shard_order is not None:
+        segs, seg_begin, seg_end = shard_order, 0, seg_end - seg_begin
+    check(lib().lvx_voxelize_wide(_ptr(lines.verts), _ptr(lines.normals), _ptr(segs), seg_begin,
                                   seg_end, int(lines.use_clip), r, footprint_radius(r, r_min), float(r_min),
                                   res, METHODS[method], _ptr(wide), _ptr(stats), _stream()),
           "lvx_voxelize_wide")

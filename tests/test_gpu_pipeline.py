@@ -435,3 +435,36 @@ def test_fragment_buffer_overflow_is_redone_exactly(lvx, oracle):
     ref0 = oracle.run_frame(ls, g, rw, cam, cfg.light_vector(), strategy="vsv")
     assert again.stats["fragments"] == ref0.abuf.total
     assert np.array_equal(eng.rgb.cpu().numpy(), ref0.image.rgb)
+
+
+@pytest.mark.parametrize("res,r", [(64, 0.3), (128, 1.4), (32, 0.5)])
+def test_engine_fused_pack_and_level1(lvx, oracle, res, r):
+    """FrameEngine packs the 64-bit accumulators and builds pyramid level 1 in one kernel at res >= 64
+    (lvx_pack_wide_mip1), then the upper levels (lvx_build_mips_upper), and lets the scan write the scatter
+    cursors: grid, every pyramid level, the non-zero bits handed to the cone tracer, saturation count and the
+    fragment lists must be what the separate passes / the oracle give."""
+    ls = lvx.generate("grid_diagonals", count=220, length=18.0, domain=22.0)
+    g, rw = lvx.fit_grid(ls, res, radius_voxels=r)
+    cfg = lvx.PipelineConfig(res=res, width=48, height=40, strategy="vcsv")
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, rw, cam, cfg.light_vector(), strategy="vcsv")
+    e = lvx.FrameEngine(res, 48, 40, strategy="vcsv", keep_rgb=True)
+    e.set_topology(ls.polyline_offsets, ls.n_vertices)
+    e.load_vertices(ls.vertices)
+    out = e.run(cam, g, rw)
+    assert e._mip1_done == (res >= 64)
+    base = e.base.cpu().numpy().view(np.uint32).reshape(res, res, res)
+    assert np.array_equal(base, ref.pyramid.base)
+    assert out.stats["saturated"] == ref.pyramid.saturated
+    mips = e.mips.cpu().numpy()
+    off = 0
+    for l, lvl in enumerate(ref.pyramid.occ_levels[1:], 1):
+        n = lvl.size
+        assert np.array_equal(mips[off:off + n], lvl.ravel()), f"pyramid level {l}"
+        off += n
+    nz = np.unpackbits(e.nz_bits.cpu().numpy().view(np.uint8), bitorder="little").astype(bool)
+    assert np.array_equal(nz, (ref.pyramid.base.ravel() & 0xFFFF) != 0)
+    n = out.stats["fragments"]
+    assert n == ref.abuf.total
+    assert np.array_equal(e.frags[:n].cpu().numpy().view(np.uint32), ref.abuf.fragments)
+    assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
