@@ -443,7 +443,7 @@ def test_engine_fused_pack_and_level1(lvx, oracle, res, r):
     (lvx_pack_wide_mip1), then the upper levels (lvx_build_mips_upper), and lets the scan write the scatter
     cursors: grid, every pyramid level, the non-zero bits handed to the cone tracer, saturation count and the
     fragment lists must be what the separate passes / the oracle give."""
-    ls = lvx.generate("grid_diagonals", count=220, length=18.0, domain=22.0)
+    ls = lvx.generate("grid_diagonals", count=220, length=16.0, domain=24.0)
     g, rw = lvx.fit_grid(ls, res, radius_voxels=r)
     cfg = lvx.PipelineConfig(res=res, width=48, height=40, strategy="vcsv")
     cam = lvx.make_camera(cfg, g)
