@@ -189,8 +189,27 @@ def dumps_and_stats():
         json.dump(out, f, indent=1)
 
 
+def lns_files():
+    """Line-set files written by the reference's own writer (lv/lineset.py:191-210), both formats, committed as
+    fixtures: the GPU package's loader must read them to the same arrays and its writer reproduce their bytes.
+    `decimate` (lv/lineset.py:245-263) and `compute_clip_normals` (213-242) of the same set ride along."""
+    ls = lv.generate("random_streamlines", seed=5, polylines=6, verts_per_line=9)
+    ls = lv.LineSet(ls.vertices, ls.polyline_offsets, 0.3125)
+    lv.save_lineset(ls, os.path.join(OUT, "walk6.lns"), "lns-binary")
+    lv.save_lineset(ls, os.path.join(OUT, "walk6_text.lns"), "lns-text")
+    dec = lv.decimate(ls, 3)
+    np.savez_compressed(os.path.join(OUT, "walk6_lns.npz"), vertices=ls.vertices, polyline_offsets=ls.polyline_offsets,
+                        radius=np.float64(ls.radius), dec_vertices=dec.vertices, dec_offsets=dec.polyline_offsets,
+                        clip_normals=lv.compute_clip_normals(ls), segment_vertex_ids=ls.segment_vertex_ids())
+    print("lns", ls.n_polylines, ls.n_vertices, flush=True)
+
+
 if __name__ == "__main__":
     only = sys.argv[1:]
+    if not only or "lns" in only:
+        lns_files()
+    if only == ["lns"]:
+        sys.exit(0)
     if not only or "unit" in only:
         unit_vectors()
     if not only or "dumps" in only:

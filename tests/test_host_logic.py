@@ -140,3 +140,24 @@ def test_bench_config_is_the_same_in_both_arms():
     assert set(c) == {"workload", "segments", "grid", "image", "l2"} and c["segments"] == 10000
     assert "10000 segments" in c["workload"] and "r=0.2" in c["workload"]
     assert "r=0.6" in bench.describe("c2thick", ls)
+
+
+def test_lns_files_written_by_the_reference():
+    """tests/golden/walk6*.lns were written by the reference's save_lineset (make_golden.py lns_files): our
+    loader reads both formats to the reference's arrays, our writer reproduces the files byte for byte, and
+    decimate / segment_vertex_ids agree with the reference on the same set."""
+    import tempfile
+    g = os.path.join(ROOT, "tests", "golden")
+    want = np.load(os.path.join(g, "walk6_lns.npz"))
+    for name, fmt in (("walk6.lns", "lns-binary"), ("walk6_text.lns", "lns-text")):
+        ls = lvx.load_lineset(os.path.join(g, name))          # format sniffed from the first bytes
+        assert ls.vertices.dtype == np.float32 and np.array_equal(ls.vertices, want["vertices"])
+        assert np.array_equal(ls.polyline_offsets, want["polyline_offsets"])
+        assert ls.radius == float(want["radius"])
+        with tempfile.TemporaryDirectory() as d:
+            out = os.path.join(d, "o.lns")
+            lvx.save_lineset(ls, out, fmt)
+            assert open(out, "rb").read() == open(os.path.join(g, name), "rb").read(), f"{fmt} bytes differ"
+    dec = lvx.decimate(ls, 3)
+    assert np.array_equal(dec.vertices, want["dec_vertices"]) and np.array_equal(dec.polyline_offsets, want["dec_offsets"])
+    assert np.array_equal(ls.segment_vertex_ids(), want["segment_vertex_ids"])
