@@ -24,8 +24,15 @@ def scale(name, val, unit):
     if name == "inst_M":
         v *= 1e-6
     return v
+import os
+try:
+    PEAK = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"])
+    PEAK_SRC = "MEASURED_PEAKS.json hbm_gbs"
+except Exception:
+    PEAK, PEAK_SRC = 6650.0, "fallback of B200_PROFILING.md"
 seen, traffic = set(), {}
-print(f"{'kernel':34s}" + "".join(f"{n:>9s}" for n, _ in M))
+print(f"# DRAM GB/s = (dram bytes read + written) / kernel time; frac = that over the HBM peak of {PEAK:.0f} GB/s ({PEAK_SRC})")
+print(f"{'kernel':34s}" + "".join(f"{n:>9s}" for n, _ in M) + f"{'DRAM GB/s':>11s}{'frac':>7s}")
 for r in rows[2:]:
     d = dict(zip(h, r)); u = dict(zip(h, units))
     k = re.sub(r"\(.*", "", d["Kernel Name"]).replace("void ", "").replace("lvx::", "")
@@ -34,7 +41,8 @@ for r in rows[2:]:
         continue
     seen.add(k)
     vals = {n: scale(n, d.get(m, ""), u.get(m, "")) for n, m in M}
-    print(f"{k:34s}" + "".join(f"{vals[n]:9.2f}" for n, _ in M))
+    gbs = (vals["dR_MB"] + vals["dW_MB"]) / max(vals["time_ms"], 1e-9)      # MB / ms = GB/s
+    print(f"{k:34s}" + "".join(f"{vals[n]:9.2f}" for n, _ in M) + f"{gbs:11.1f}{gbs / PEAK:7.3f}")
     traffic[k] = int((vals["dR_MB"] + vals["dW_MB"]) * 1e6)
 if len(sys.argv) > 3:
     path, wl = sys.argv[2], sys.argv[3]
