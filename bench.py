@@ -455,6 +455,9 @@ def run_tiled(args, lvx, torch, dist, rank, world, local, ls, g, cfg):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def strip_work(stage):       # the part of a rank's frame that depends on its strip
+        return sum(stage.get(k, 0.0) for k in ("scan", "scatter", "shade", "trace"))
+
     def frame(tf, i, e2e):
         eng.load_vertices((host if e2e else dev)[i % n_variants])
         g_i, rw_i = eng.fit(radius_voxels=rv)
@@ -468,7 +471,9 @@ def run_tiled(args, lvx, torch, dist, rank, world, local, ls, g, cfg):
 
     def timed(tf, e2e):
         for i in range(args.warmup):
-            frame(tf, i, e2e)
+            r = frame(tf, i, e2e)
+            if world > 1 and not e2e:         # strips follow the measured work of the warm-up frames, then stay put
+                tf.rebalance(strip_work(r.stage_ms))
         barrier()
         stage, last = {}, None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -484,26 +489,40 @@ def run_tiled(args, lvx, torch, dist, rank, world, local, ls, g, cfg):
     keys = ("fragments", "owned_voxels", "visible_voxels", "ray_capsule_tests", "voxels_visited", "shaded_voxels")
     sampler = ClockSampler(local) if rank == 0 else None
     if emu:
-        per_rank = []
-        for r in range(emu):
-            tf = D.TiledFrame(eng, comm=D.EmulatedComm(r, emu))
-            ms, stage, last = timed(tf, False)
-            own = sum(v for k, v in stage.items() if k != "emulated_peers")
-            per_rank.append({"rank": r, "tile": list(tf.tiles[r]), "segments": list(tf.seg_range()),
-                             "own_stage_ms_sum": round(own, 4), "stages_ms": {k: round(v, 4) for k, v in stage.items()},
-                             "stats": {k: last.stats[k] for k in keys}})
+        def one_pass(rows):
+            per_rank = []
+            for r in range(emu):
+                tf = D.TiledFrame(eng, comm=D.EmulatedComm(r, emu))
+                if rows is not None:
+                    tf.set_rows(rows)
+                ms, stage, last = timed(tf, False)
+                own = sum(v for k, v in stage.items() if k != "emulated_peers")
+                per_rank.append({"rank": r, "tile": list(tf.tiles[r]), "segments": list(tf.seg_range()),
+                                 "own_stage_ms_sum": round(own, 4), "strip_work_ms": round(strip_work(stage), 4),
+                                 "stages_ms": {k: round(v, 4) for k, v in stage.items()},
+                                 "stats": {k: last.stats[k] for k in keys}})
+            return per_rank
+        equal = one_pass(None)
+        rows0 = [p["tile"][1] for p in equal] + [h]
+        # strip balancing: what TiledFrame.rebalance does with the all-gathered numbers of the real job
+        rows1 = D.balanced_rows(rows0, [p["strip_work_ms"] for p in equal], h)
+        balanced = one_pass(rows1)
         clocks = sampler.stop()
-        worst = max(p["own_stage_ms_sum"] for p in per_rank)
+        worst_eq = max(p["own_stage_ms_sum"] for p in equal)
+        worst = max(p["own_stage_ms_sum"] for p in balanced)
         line = {
             "metric": "frames/sec (voxelize+cull+build+shade+trace, full rebuild per frame) at 1920x1080",
             "value": round(1e3 / worst, 3), "unit": "frames/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(worst, 4), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": workload_config(args.workload, ls),
             "emulated": {"world": emu, "note": "ONE GPU plays the ranks of a tiled job in turn; value = 1 / (largest per-rank "
-                         "sum of the rank's own stage times); the all-reduce of the accumulators (exchange_bytes per rank) "
+                         "sum of the rank's own stage times) with strips balanced from the strip-dependent stage times "
+                         "of a first pass on equal strips; the all-reduce of the accumulators (exchange_bytes per rank) "
                          "and the gather of the strips are NOT included", "exchange_bytes": 8 * res ** 3,
-                         "ranks": per_rank},
-            "gpu_launches": int((eng.kernel_launches_per_frame() + 3) * args.steps * emu), "clocks": clocks}
+                         "equal_strips": {"rows": rows0, "slowest_rank_ms": round(worst_eq, 4), "ranks": equal},
+                         "balanced_strips": {"rows": rows1, "slowest_rank_ms": round(worst, 4), "ranks": balanced},
+                         "ranks": balanced},
+            "gpu_launches": int((eng.kernel_launches_per_frame() + 3) * args.steps * emu * 2), "clocks": clocks}
         print(json.dumps(line))
         return
 

@@ -29,7 +29,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["shard_bounds", "tile_rects", "frames_for_rank", "widen_packed", "pack_wide",
+__all__ = ["shard_bounds", "tile_rects", "balanced_rows", "frames_for_rank", "widen_packed", "pack_wide",
            "merge_partial_grids", "TiledFrame", "Comm", "TorchComm", "EmulatedComm"]
 
 
@@ -44,6 +44,31 @@ def tile_rects(width: int, height: int, world: int) -> list:
     Strips keep each rank's pixels contiguous in the (H, W) image, so the gather is a concat."""
     ys = np.linspace(0, int(height), int(world) + 1).astype(np.int64)
     return [(0, int(ys[g]), int(width), int(ys[g + 1])) for g in range(int(world))]
+
+
+def balanced_rows(bounds, weights, height: int) -> list:
+    """New strip boundaries (world+1 ascending row indices, 0 .. height) that equalise the work per strip, given
+    the work `weights[r]` measured on the strips `bounds[r] .. bounds[r+1]` of an earlier frame: the work is taken
+    to be spread evenly over a strip's rows (a piecewise-constant density) and the cumulative density is cut
+    into equal parts.  Every strip keeps at least one row.  Deterministic, so all ranks that feed it the same
+    numbers get the same strips."""
+    b = [int(x) for x in bounds]
+    world = len(b) - 1
+    w = [max(float(x), 0.0) for x in weights]
+    total = sum(w)
+    if world < 2 or total <= 0.0 or b[0] != 0 or b[-1] != int(height):
+        return [int(x) for x in np.linspace(0, int(height), world + 1).astype(np.int64)]
+    dens = [w[r] / max(b[r + 1] - b[r], 1) for r in range(world)]
+    cum = np.zeros(int(height) + 1)
+    for r in range(world):
+        cum[b[r] + 1:b[r + 1] + 1] = cum[b[r]] + dens[r] * np.arange(1, b[r + 1] - b[r] + 1)
+    out = [0]
+    for k in range(1, world):
+        row = int(np.searchsorted(cum, total * k / world, side="left"))
+        row = min(max(row, out[-1] + 1), int(height) - (world - k))
+        out.append(row)
+    out.append(int(height))
+    return out
 
 
 def frames_for_rank(n_frames: int, rank: int, world: int) -> range:
@@ -84,6 +109,10 @@ class Comm:
     def barrier(self):
         pass
 
+    def all_gather_value(self, x: float) -> list:
+        """[x of rank 0, x of rank 1, ...] on every rank (host numbers; used once per frame for strip balancing)."""
+        return [float(x)]
+
 
 class TorchComm(Comm):
     """torch.distributed: NCCL over NVLink on GPUs, gloo in the CPU tests."""
@@ -111,6 +140,13 @@ class TorchComm(Comm):
         if self.world > 1:
             self.dist.barrier(group=self.group)
 
+    def all_gather_value(self, x: float) -> list:
+        if self.world == 1:
+            return [float(x)]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, float(x), group=self.group)
+        return [float(v) for v in out]
+
 
 class EmulatedComm(Comm):
     """Rank `rank` of a `world`-rank job played on one device.  The all-reduce of the occupancy
@@ -134,6 +170,13 @@ class EmulatedComm(Comm):
 
     def gather(self, t):
         return [t] if self.rank == 0 else None
+
+    def all_gather_value(self, x: float) -> list:
+        """The ranks of an emulated job run one after the other, so a rank only learns its own number; the caller
+        collects them (bench.py --emulate-world runs a first pass on equal strips for this)."""
+        out = [0.0] * self.world
+        out[self.rank] = float(x)
+        return out
 
 
 def merge_partial_grids(base_i32, group=None, comm=None):
@@ -169,6 +212,29 @@ class TiledFrame:
         self._ev = None
         if getattr(comm, "emulated", False):
             comm.peers = self._voxelize_peers
+
+    def set_rows(self, bounds):
+        """Use the horizontal strips bounds[r] .. bounds[r+1] (world+1 ascending rows, 0 .. height) from now on.
+        Every rank of the job must be given the same bounds."""
+        b = [int(x) for x in bounds]
+        if len(b) != self.world + 1 or b[0] != 0 or b[-1] != self.engine.h or any(b[i + 1] <= b[i] for i in range(self.world)):
+            raise ValueError("strip bounds must be world+1 strictly ascending rows from 0 to the image height")
+        self.tiles = [(0, b[r], self.engine.w, b[r + 1]) for r in range(self.world)]
+
+    def rows(self) -> list:
+        return [t[1] for t in self.tiles] + [self.tiles[-1][3]]
+
+    def rebalance(self, my_work: float):
+        """Strip balancing from measured work: every rank contributes the work of its strip in the frame just
+        rendered (e.g. the milliseconds of its strip-dependent stages: scan + scatter + shade + trace); the
+        numbers are all-gathered (one host number per rank) and the strips of the following frames are cut so
+        that each would have held the same share of it (`balanced_rows`).  Returns the new bounds."""
+        w = self.comm.all_gather_value(my_work)
+        if getattr(self.comm, "emulated", False):
+            return self.rows()                   # one rank's number alone cannot rebalance; see bench.py
+        b = balanced_rows(self.rows(), w, self.engine.h)
+        self.set_rows(b)
+        return b
 
     def seg_range(self):
         b = shard_bounds(self.engine._segs.numel(), self.world)
@@ -232,7 +298,7 @@ class TiledFrame:
         pad_h = torch.zeros((rows, eng.w), dtype=torch.int32, device=eng.srgb.device)
         pad_s[:y1 - y0] = eng.srgb[y0:y1]
         pad_h[:y1 - y0] = eng.hit_id[y0:y1]
-        outs = self.comm.gather(pad_s)
+        outs = self.comm.gather(pad_s)        # (strips may differ in height once they are balanced: padded to the tallest)
         outh = self.comm.gather(pad_h)
         if self.rank != 0:
             return None, None

@@ -183,3 +183,35 @@ def test_tiles_partition_the_image(w, h, world):
 def test_frames_for_rank_partition():
     frames = sorted(f for r in range(8) for f in D.frames_for_rank(100, r, 8))
     assert frames == list(range(100))
+
+
+def test_balanced_rows():
+    rows = [0, 135, 270, 405, 540, 675, 810, 945, 1080]
+    w = [2.0, 3.8, 4.2, 4.4, 4.9, 4.7, 3.2, 1.9]
+    b = D.balanced_rows(rows, w, 1080)
+    assert b[0] == 0 and b[-1] == 1080 and all(b[i + 1] > b[i] for i in range(8))
+    # the work each new strip would have held under the piecewise-constant density is equal to within a row's worth
+    dens = np.repeat(np.array(w) / 135.0, 135)
+    share = [dens[b[i]:b[i + 1]].sum() for i in range(8)]
+    assert max(share) - min(share) <= 2 * dens.max()
+    assert b[1] - b[0] > 135 and b[4] - b[3] < 135          # light strips grow, heavy strips shrink
+    assert D.balanced_rows([0, 540, 1080], [1, 1], 1080) == [0, 540, 1080]
+    assert D.balanced_rows([0, 540, 1080], [0, 0], 1080) == [0, 540, 1080]    # nothing measured: equal strips
+    assert D.balanced_rows([0, 1, 3], [5, 0], 3) == [0, 1, 3]                    # every strip keeps a row
+    assert D.balanced_rows([0, 2, 3], [0, 9], 3) == [0, 2, 3]
+
+
+def test_tiled_frame_set_rows_validation():
+    class E:
+        w, h = 64, 48
+        _segs = torch.arange(10, dtype=torch.int32)
+    tf = D.TiledFrame(E(), comm=D.EmulatedComm(1, 3))
+    assert tf.rows() == [0, 16, 32, 48]
+    tf.set_rows([0, 5, 40, 48])
+    assert tf.tiles[1] == (0, 5, 64, 40) and tf.rows() == [0, 5, 40, 48]
+    for bad in ([0, 5, 48], [0, 5, 5, 48], [1, 5, 40, 48], [0, 5, 40, 47]):
+        with pytest.raises(ValueError):
+            tf.set_rows(bad)
+    assert tf.rebalance(3.0) == [0, 5, 40, 48]        # an emulated rank alone cannot rebalance
+    one = D.TiledFrame(E(), comm=D.Comm())
+    assert one.rebalance(1.0) == [0, 48]

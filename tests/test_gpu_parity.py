@@ -519,6 +519,8 @@ def test_tiled_frame_emulated_ranks_make_the_frame(lvx, oracle, kind, mode):
         e.set_topology(ls.polyline_offsets, ls.n_vertices)
         e.load_vertices(ls.vertices)
         tf = D.TiledFrame(e, comm=D.EmulatedComm(rank, world))
+        if kind == "diag":      # strips of unequal height, as strip balancing produces them
+            tf.set_rows([0, 7, 50, h])
         lo, hi = tf.seg_range()
         assert hi - lo in (ls.n_segments // world, ls.n_segments // world + 1)
         out = tf.run(cam, g, r_world)
@@ -527,7 +529,7 @@ def test_tiled_frame_emulated_ranks_make_the_frame(lvx, oracle, kind, mode):
         assert out.stats["voxels_visited"] == ref.pyramid.visited
         if ref.culling is not None:
             assert np.array_equal(e.cull_flat.cpu().numpy(), ref.culling.flat)
-        assert out.stats["fragments"] < ref.abuf.total
+        assert out.stats["fragments"] <= ref.abuf.total          # (a tall strip may own every visible voxel)
         s, hh = tf.gather_image()
         x0, y0, x1, y1 = tf.tiles[rank]
         if rank == 0:
