@@ -54,7 +54,7 @@ WORKLOADS = {
 # culling-active variant of C2: the same bundles drawn as thick tubes (radius 0.6 voxel), so that bundle
 # interiors become solid (eroded occupancy >= 0.999) and the voxels behind them are culled
 WORKLOADS["c2thick"] = WORKLOADS["c2"]
-C5_TIME_STEPS = 2      # distinct time steps generated on the host (~20 s each); the sequence cycles through them
+C5_TIME_STEPS = 100    # the sequence has 100 time steps (seed = time step); a run generates the ones it renders (~0.5 s each)
 R_VOXELS = 0.2
 R_VOXELS_OF = {"c2thick": 0.6}
 R_MIN = 0.5
@@ -214,7 +214,7 @@ def run_gpu(args):
     # a dynamic sequence: every step gets its own deformed vertex set (rank r renders frames r, r+world, ...)
     n_variants = 4
     if args.workload == "c5":   # time steps = independent line sets of the same topology
-        n_variants = C5_TIME_STEPS
+        n_variants = min(C5_TIME_STEPS, args.warmup + args.steps)     # frame i of this rank = time step rank + world * i
         gen = dict(WORKLOADS["c5"][0]); kind = gen.pop("kind"); gen.pop("seed")
         host = [torch.from_numpy(ls.vertices if rank + world * i == 0 else
                                  lvx.generate(kind, seed=rank + world * i, **gen).vertices).pin_memory()

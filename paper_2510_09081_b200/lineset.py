@@ -125,15 +125,49 @@ def _walk(rng, n_verts, lo, hi, seg_length, curl):
     return out
 
 
+def _walks_vectorised(rng, polylines, n_verts, lo, hi, seg_length, curl):
+    """All polylines' walks advanced together, one vertex per step.  The random numbers are drawn polyline by
+    polyline in `_walk`'s order (uniform start, then a normal triple per vertex: a Generator's stream does not
+    depend on how a request is batched) and every arithmetic step is `_walk`'s, element for element; the vector
+    norms go through a batched matmul, which rounds like the `x.dot(x)` inside np.linalg.norm (an explicit
+    x0*x0 + x1*x1 + x2*x2 does not).  The caller checks the first polylines against `_walk` itself."""
+    p = np.empty((polylines, 3))
+    nrm = np.empty((polylines, n_verts, 3))
+    for i in range(polylines):
+        p[i] = rng.uniform(lo, hi, size=3)
+        nrm[i] = rng.normal(size=(n_verts, 3))
+
+    def unit(v):
+        return v / np.sqrt(np.matmul(v[:, None, :], v[:, :, None]).reshape(-1, 1))
+
+    d = unit(nrm[:, 0])
+    out = np.empty((polylines, n_verts, 3))
+    out[:, 0] = p
+    for j in range(1, n_verts):
+        d = unit(d + curl * nrm[:, j])
+        p = p + seg_length * d
+        bad = (p < lo) | (p > hi)
+        d = np.where(bad, -d, d)
+        p = np.where(bad, np.clip(p, lo, hi), p)
+        out[:, j] = p
+    return out.reshape(-1, 3)
+
+
 def _random_streamlines(polylines=50, verts_per_line=30, seg_length=1.0, domain=32.0,
                         radius=0.25, curl=0.6, seed=0):
     if polylines < 1 or verts_per_line < 2 or seg_length <= 0 or radius <= 0:
         raise LineSetError("bad random_streamlines parameters")
-    rng = np.random.default_rng(seed)
     lo, hi = 0.2 * domain, 0.8 * domain
+    off = np.arange(polylines + 1, dtype=np.int64) * verts_per_line
+    if polylines >= 64:      # large sets (C5's time steps: 20 000 polylines): ~40x faster than walk by walk
+        v = _walks_vectorised(np.random.default_rng(seed), polylines, verts_per_line, lo, hi, seg_length, curl)
+        rng = np.random.default_rng(seed)
+        head = np.concatenate([_walk(rng, verts_per_line, lo, hi, seg_length, curl) for _ in range(2)])
+        if np.array_equal(v[:head.shape[0]], head):      # bit for bit the reference's walk on this platform
+            return LineSet(v.astype(np.float32), off, radius)
+    rng = np.random.default_rng(seed)
     v = np.concatenate([_walk(rng, verts_per_line, lo, hi, seg_length, curl)
                         for _ in range(polylines)])
-    off = np.arange(polylines + 1, dtype=np.int64) * verts_per_line
     return LineSet(v.astype(np.float32), off, radius)
 
 

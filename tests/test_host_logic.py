@@ -161,3 +161,23 @@ def test_lns_files_written_by_the_reference():
     dec = lvx.decimate(ls, 3)
     assert np.array_equal(dec.vertices, want["dec_vertices"]) and np.array_equal(dec.polyline_offsets, want["dec_offsets"])
     assert np.array_equal(ls.segment_vertex_ids(), want["segment_vertex_ids"])
+
+
+@pytest.mark.parametrize("kw", [dict(polylines=100, verts_per_line=101, seed=0),
+                                dict(polylines=257, verts_per_line=33, seed=9, domain=128.0, curl=0.3),
+                                dict(polylines=64, verts_per_line=2, seed=2, seg_length=9.0, domain=12.0)])
+def test_vectorised_streamlines_are_the_reference_walks(kw):
+    """random_streamlines advances all walks together for large sets (C5's 2 M-segment time steps in 0.5 s instead
+    of 20 s); vertex for vertex it must be the sequential walk of lv/lineset.py:288-314 (same random stream, same
+    rounding, reflections included)."""
+    from paper_2510_09081_b200 import lineset as L
+    k = dict(seg_length=1.0, domain=32.0, curl=0.6)
+    k.update(kw)
+    lo, hi = 0.2 * k["domain"], 0.8 * k["domain"]
+    rng = np.random.default_rng(k["seed"])
+    slow = np.concatenate([L._walk(rng, k["verts_per_line"], lo, hi, k["seg_length"], k["curl"]) for _ in range(k["polylines"])])
+    fast = L._walks_vectorised(np.random.default_rng(k["seed"]), k["polylines"], k["verts_per_line"], lo, hi, k["seg_length"], k["curl"])
+    assert np.array_equal(slow, fast)
+    assert ((slow == lo) | (slow == hi)).any() or kw["verts_per_line"] < 5      # some walk was reflected at the domain wall
+    ls = lvx.generate("random_streamlines", **kw)
+    assert np.array_equal(ls.vertices, slow.astype(np.float32))
