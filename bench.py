@@ -33,7 +33,6 @@ import socket
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
