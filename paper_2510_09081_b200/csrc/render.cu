@@ -386,9 +386,12 @@ struct PairQueues {
 // hold entry e and evaluate candidate subset `sub` (see ray_capsule); the callee merges the pair.
 // Written as one loop with a single call site per stage: the stages are large (stage C inlines the
 // f64 intersection routine), and every extra inlined copy costs instruction-cache capacity.
-template <int M, class F>
+// `last_ord()`: the highest ordinal this lane's ray still needs (opaque: the ordinal of the best hit found so
+// far -- stage C of its early pairs has usually run by the time stage A reaches its later voxels; n_ord - 1 when
+// every ordinal is needed).  Ordinals beyond it are not queued at all.
+template <int M, class F, class G>
 __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S, int n_ord, int lane, uint32_t lt_mask,
-                                          float R2f, F &&stage_c) {
+                                          float R2f, F &&stage_c, G &&last_ord) {
     uint32_t qa = 0, qb = 0;
     // stage-A cursor of this lane: ordinal m, next global index g of its range, entries left, index in the range
     int m = -1;
@@ -447,6 +450,7 @@ __device__ __forceinline__ void run_pairs(const RenderArgs &A, PairQueues<M> &S,
         do {    // (tight loop: this is the most frequent step of the whole kernel)
             if (left == 0 && m < n_ord) {
                 m++;
+                if (m > last_ord()) m = n_ord;          // a hit in an earlier voxel: the later ones cannot matter
                 if (m < n_ord) {
                     g = S.fo[m][lane]; left = S.tn[m][lane]; idx = 0;
                     tag = ((uint32_t)m << 21) | ((uint32_t)lane << 16);
@@ -747,7 +751,7 @@ k_render_opaque_coop(const RenderArgs A) {
                 }
             }
             __syncwarp();
-        });
+        }, [&]() { return cur_t >= 0.0 ? (int)(cur_ms >> 16) : Mr - 1; });
         if (active) {
             // tests the reference would have run: every voxel up to and including the one with the hit
             const int m_end = cur_t >= 0.0 ? (int)(cur_ms >> 16) : Mr - 1;
@@ -1024,7 +1028,7 @@ k_render_transparent_coop(const RenderArgs A) {
 #endif
             __syncwarp();
             if (hl_n + 32 > HL_CAP || fin) drain();
-        });
+        }, [&]() { return M - 1; });
         // ---- consume the ordinals in order (lv/raytracer.py:543-544, 608-637): fix the blend
         // weights now, queue the colours
         bool going = active;       // false once this lane's ray has stopped consuming this round
