@@ -163,3 +163,43 @@ def test_c4_full_size_properties(lvx):
     assert torch.equal(e1.frags[:n], e2.frags[:n])
     assert torch.equal(e1.hit_id, e2.hit_id)
     assert torch.equal(e1.srgb, e2.srgb)
+
+
+def test_largest_grid_1024(lvx):
+    """res = 1024 (the largest grid the C ABI accepts: 2^30 voxels, flat indices and fragment offsets near the
+    32-bit range).  Too large for the oracle inside a test, so the size-independent properties are checked on the
+    device: incidences = sum of counts = fragment total (vsv), offsets = exclusive scan, every sampled list
+    strictly ascending, no count mismatch, and the frame sees the lines; the same set at res = 64 through the
+    oracle pins the segments themselves."""
+    import torch
+    res = 1024
+    ls = lvx.generate("random_streamlines", seed=8, polylines=40, verts_per_line=60, domain=64.0)
+    g, rw = lvx.fit_grid(ls, res, radius_voxels=0.6)
+    cfg = lvx.PipelineConfig(res=res, width=96, height=64, strategy="vsv")
+    cam = lvx.make_camera(cfg, g)
+    eng = lvx.FrameEngine(res, 96, 64, strategy="vsv", mode="opaque")
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    eng.load_vertices(ls.vertices)
+    out = eng.run(cam, g, rw)
+    st = out.stats
+    assert st["fragments"] == st["voxels_visited"] > 0 and st["saturated"] == 0
+    offs = eng.offsets.view(torch.int32)
+    total = int(offs[-1].item()) & 0xFFFFFFFF
+    assert total == st["fragments"]
+    cnt = (eng.base.view(torch.int32) >> 16) & 0xFFFF
+    assert int(cnt.sum(dtype=torch.int64).item()) == total
+    occ = torch.nonzero(cnt).flatten()
+    assert occ.numel() == st["occupied_voxels"]
+    # voxels near both ends of the index range are in play (the lines fill the grid)
+    assert int(occ.min().item()) < res ** 3 // 8 and int(occ.max().item()) > 7 * (res ** 3 // 8)
+    pick = occ[:: max(1, occ.numel() // 2000)]
+    lo = offs[pick].cpu().numpy().view(np.uint32).astype(np.int64)
+    hi = offs[pick + 1].cpu().numpy().view(np.uint32).astype(np.int64)
+    assert np.array_equal(hi - lo, cnt[pick].cpu().numpy().astype(np.int64))
+    fr = eng.frags[:total].cpu().numpy().view(np.uint32)
+    for a, b in zip(lo[:400], hi[:400]):
+        assert np.all(np.diff(fr[a:b].astype(np.int64)) > 0) and fr[b - 1] < ls.n_segments
+    hits = int((eng.hit_id >= 0).sum().item())
+    assert hits > 0 and int(eng.hit_id.max().item()) < ls.n_segments
+    del eng
+    torch.cuda.empty_cache()
