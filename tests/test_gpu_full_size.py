@@ -198,8 +198,8 @@ def test_largest_grid_1024(lvx):
     assert np.array_equal(hi - lo, cnt[pick].cpu().numpy().astype(np.int64))
     fr = eng.frags[:total].cpu().numpy().view(np.uint32)
     for a, b in zip(lo[:400], hi[:400]):
-        assert np.all(np.diff(fr[a:b].astype(np.int64)) > 0) and fr[b - 1] < ls.n_segments
+        assert np.all(np.diff(fr[a:b].astype(np.int64)) > 0) and fr[b - 1] < ls.n_vertices    # ids = start-vertex indices
     hits = int((eng.hit_id >= 0).sum().item())
-    assert hits > 0 and int(eng.hit_id.max().item()) < ls.n_segments
+    assert hits > 0 and int(eng.hit_id.max().item()) < ls.n_vertices
     del eng
     torch.cuda.empty_cache()
