@@ -645,3 +645,40 @@ def test_launch_count_is_what_the_engine_claims(lvx, res, strategy, mode):
     if not names:
         pytest.skip("the profiler recorded no device activity")
     assert len(names) == eng.kernel_launches_per_frame(), sorted(names)
+
+
+@pytest.mark.parametrize("r", [0.3, 1.7])
+def test_zero_length_segments_through_the_engine(lvx, oracle, r):
+    """Repeated vertices (zero-length segments take the AABB traversal, lv/voxelizer.py:155-156) mixed with
+    ordinary ones, some of them at the grid boundary: the row-pooled scatter's state machine has its own form
+    of that branch (RowGen box mode), so grid, lists and image are compared with the oracle."""
+    rng = np.random.default_rng(17)
+    polys, off = [], [0]
+    for _ in range(40):
+        n = int(rng.integers(3, 9))
+        p = rng.uniform(2.0, 29.0, size=(n, 3))
+        for k in rng.choice(n - 1, size=max(1, n // 3), replace=False):
+            p[k + 1] = p[k]                      # a zero-length segment
+        polys.append(p)
+        off.append(off[-1] + n)
+    polys.append(np.array([[0.2, 0.3, 31.6], [0.2, 0.3, 31.6], [0.2, 0.3, 31.6]]))   # all in one corner voxel
+    off.append(off[-1] + 3)
+    v = np.concatenate(polys).astype(np.float32)
+    v[-3:] += np.array([[0, 0, 0], [0, 0, 0], [0.4, 0.0, -0.3]], np.float32)          # (not fully degenerate)
+    ls = lvx.LineSet(v, np.array(off, dtype=np.int64), 0.25)
+    res = 32
+    g = lvx.GridDesc(res, np.zeros(3), 1.0)
+    r_world = r
+    cfg = lvx.PipelineConfig(res=res, width=80, height=60, strategy="vcsv")
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vcsv")
+    e = lvx.FrameEngine(res, 80, 60, strategy="vcsv", keep_rgb=True)
+    e.set_topology(ls.polyline_offsets, ls.n_vertices)
+    e.load_vertices(ls.vertices)
+    out = e.run(cam, g, r_world)
+    assert np.array_equal(e.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
+    n = out.stats["fragments"]
+    assert n == ref.abuf.total and out.stats["voxels_visited"] == ref.pyramid.visited
+    assert np.array_equal(e.frags[:n].cpu().numpy().view(np.uint32), ref.abuf.fragments)
+    assert np.array_equal(e.hit_id.cpu().numpy(), ref.image.hit_id)
+    assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
