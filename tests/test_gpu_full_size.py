@@ -203,3 +203,37 @@ def test_largest_grid_1024(lvx):
     assert hits > 0 and int(eng.hit_id.max().item()) < ls.n_vertices
     del eng
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("strategy,mode,alpha,frames", [("vcsv", "opaque", 1.0, 40), ("vsv", "transparent", 0.3, 12)])
+def test_run_to_run_determinism_at_full_size(lvx, c2_lines, strategy, mode, alpha, frames):
+    """lv `t/test_acceptance.py:249-266` (byte determinism across worker counts and runs), GPU form: the build
+    uses atomics whose order differs from run to run, the outputs may not.  The same C2 / C3 frame is rendered
+    many times on two engines (different buffers, brick-order permutations and tile schedules every time);
+    position-weighted checksums of grid, culling pyramid, offsets, the whole fragment array, the tight index
+    counts, hit ids and sRGB bytes are formed on the device and must never change."""
+    import torch
+    ls, g, rw = c2_lines
+    res, w, h = 256, 1920, 1080
+    cfg = lvx.PipelineConfig(res=res, width=w, height=h, strategy=strategy, mode=mode, alpha=alpha)
+    cam = lvx.make_camera(cfg, g)
+
+    def digest(t, n=None):
+        v = (t.reshape(-1) if n is None else t.reshape(-1)[:n]).to(torch.int64)
+        k = torch.arange(1, v.numel() + 1, device=v.device, dtype=torch.int64)
+        return int(((v * ((k * 2654435761) & 0xFFFFFFF)).sum() & 0x7FFFFFFFFFFFFFFF).item())
+
+    engines = [lvx.FrameEngine(res, w, h, strategy=strategy, mode=mode, alpha=alpha) for _ in range(2)]
+    for e in engines:
+        e.set_topology(ls.polyline_offsets, ls.n_vertices)
+    want = None
+    for i in range(frames):
+        e = engines[i & 1]
+        e.load_vertices(ls.vertices)
+        out = e.run(cam, g, rw)
+        n = out.stats["fragments"]
+        got = (out.stats["voxels_visited"], n, out.stats["ray_capsule_tests"], digest(e.base), digest(e.cull_flat),
+               digest(e.offsets), digest(e.frags, n), digest(e.tight.cnt * (e.march == 255)), digest(e.hit_id), digest(e.srgb))
+        if want is None:
+            want = got
+        assert got == want, f"frame {i} differs from frame 0"
