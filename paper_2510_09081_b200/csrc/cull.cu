@@ -33,8 +33,7 @@ __device__ __forceinline__ bool q_solid(const uint32_t *__restrict__ base, int r
 constexpr int SOLID_ITEMS = 4;
 __global__ void __launch_bounds__(256)
 k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restrict__ solid,
-        uint32_t *__restrict__ bricks, uint32_t *__restrict__ solid_list, uint32_t *__restrict__ occ_list,
-        uint64_t *__restrict__ stats) {
+        uint32_t *__restrict__ solid_list, uint32_t *__restrict__ occ_list, uint64_t *__restrict__ stats) {
     __shared__ uint32_t s_warp[8];
     __shared__ unsigned long long s_base;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -56,28 +55,6 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
             s = q_solid(base, res, x - 1, y, z) && q_solid(base, res, x + 1, y, z) &&
                 q_solid(base, res, x, y - 1, z) && q_solid(base, res, x, y + 1, z) &&
                 q_solid(base, res, x, y, z - 1) && q_solid(base, res, x, y, z + 1);
-            if (s) {
-                // flag every brick that overlaps this solid voxel dilated by one voxel, at both brick sizes.
-                // In a frame with many solid voxels most flags are already set: look before the atomic
-                // (a stale zero only costs a redundant atomicOr).
-                uint32_t *bits = bricks;
-#pragma unroll
-                for (int lvl = 0; lvl < 2; lvl++) {
-                    const int B = lvl == 0 ? LVX_BRICK : LVX_SUPER;
-                    const int rb = (res + B - 1) / B;
-                    const int bx0 = max(x - 1, 0) / B, bx1 = min(x + 1, res - 1) / B;
-                    const int by0 = max(y - 1, 0) / B, by1 = min(y + 1, res - 1) / B;
-                    const int bz0 = max(z - 1, 0) / B, bz1 = min(z + 1, res - 1) / B;
-                    for (int bz = bz0; bz <= bz1; bz++)
-                        for (int by = by0; by <= by1; by++)
-                            for (int bx = bx0; bx <= bx1; bx++) {
-                                const int bi = bx + rb * (by + rb * bz);
-                                const uint32_t bit = 1u << (bi & 31);
-                                if (!(*reinterpret_cast<volatile uint32_t *>(&bits[bi >> 5]) & bit)) atomicOr(&bits[bi >> 5], bit);
-                            }
-                    bits += brick_words(res, B);
-                }
-            }
         }
         const uint32_t m = __ballot_sync(0xffffffffu, s);
         if (lane == 0 && idx < V) {
@@ -131,6 +108,55 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
     }
 }
 
+// Brick flags from the finished solid bits.  An 8^3 brick is flagged when it overlaps a solid voxel dilated by
+// one voxel, i.e. when a solid bit is set in the brick grown by a voxel on every side; a 32^3 super-brick
+// overlaps such a dilated voxel exactly when one of its 8^3 bricks does.  One thread per brick: 10 x 10 rows of
+// 10 bits.  (Round 1 had every solid voxel set its bricks' flags with atomics from k_solid: in a frame full
+// of solid voxels that was most of that kernel's time.)  Nothing is solid -> the flags stay as cleared.
+__global__ void __launch_bounds__(128)
+k_brick_flags(const uint32_t *__restrict__ solid, int res, const uint64_t *__restrict__ stats, uint32_t *__restrict__ flags) {
+    if (stats[LVX_ST_SOLID] == 0) return;
+    const int rb = (res + LVX_BRICK - 1) / LVX_BRICK;
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    bool any = false;
+    if (b < rb * rb * rb) {
+        const int bx = b % rb, by = (b / rb) % rb, bz = b / (rb * rb);
+        const int x0 = max(bx * LVX_BRICK - 1, 0), x1 = min(bx * LVX_BRICK + LVX_BRICK, res - 1);
+        const int y0 = max(by * LVX_BRICK - 1, 0), y1 = min(by * LVX_BRICK + LVX_BRICK, res - 1);
+        const int z0 = max(bz * LVX_BRICK - 1, 0), z1 = min(bz * LVX_BRICK + LVX_BRICK, res - 1);
+        for (int z = z0; z <= z1 && !any; z++)
+            for (int y = y0; y <= y1 && !any; y++) {
+                const int64_t i0 = x0 + (int64_t)res * (y + (int64_t)res * z), i1 = i0 + (x1 - x0);   // bits i0 .. i1 of the row
+                const int64_t w0 = i0 >> 5, w1 = i1 >> 5;
+                const uint32_t lo = 0xffffffffu << (i0 & 31), hi = 0xffffffffu >> (31 - (i1 & 31));
+                if (w0 == w1) any = (solid[w0] & lo & hi) != 0;
+                else any = (solid[w0] & lo) != 0 || (solid[w1] & hi) != 0;               // (at most 10 bits: two words)
+            }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, any);
+    if ((threadIdx.x & 31) == 0 && b < ((rb * rb * rb + 31) & ~31)) flags[b >> 5] = m;
+}
+
+__global__ void __launch_bounds__(128)
+k_super_flags(const uint32_t *__restrict__ flags, int res, const uint64_t *__restrict__ stats, uint32_t *__restrict__ sflags) {
+    if (stats[LVX_ST_SOLID] == 0) return;
+    const int rb = (res + LVX_BRICK - 1) / LVX_BRICK, rs = (res + LVX_SUPER - 1) / LVX_SUPER;
+    constexpr int K = LVX_SUPER / LVX_BRICK;
+    const int sb = blockIdx.x * blockDim.x + threadIdx.x;
+    bool any = false;
+    if (sb < rs * rs * rs) {
+        const int sx = sb % rs, sy = (sb / rs) % rs, sz = sb / (rs * rs);
+        for (int z = sz * K; z < min(sz * K + K, rb) && !any; z++)
+            for (int y = sy * K; y < min(sy * K + K, rb) && !any; y++)
+                for (int x = sx * K; x < min(sx * K + K, rb); x++) {
+                    const int bi = x + rb * (y + rb * z);
+                    if ((flags[bi >> 5] >> (bi & 31)) & 1u) { any = true; break; }
+                }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, any);
+    if ((threadIdx.x & 31) == 0 && sb < ((rs * rs * rs + 31) & ~31)) sflags[sb >> 5] = m;
+}
+
 // lv/culling.py:143-188, literally: Amanatides-Woo from the voxel centre to the camera point.
 // `t_stop`: a parameter beyond which the caller has PROVED that the walk cannot meet a solid voxel (see
 // coarse_last_flagged); there the reference's loop can only run on to one of its `return False` exits.
@@ -147,16 +173,23 @@ __device__ __forceinline__ bool march_blocked(const uint32_t *__restrict__ solid
     const double tdx = dx != 0.0 ? fabs(1.0 / dx) : big;
     const double tdy = dy != 0.0 ? fabs(1.0 / dy) : big;
     const double tdz = dz != 0.0 ? fabs(1.0 / dz) : big;
+    // The reference's loop leaves with "not blocked" on four conditions (reached the camera: t >= 1; left the
+    // grid; entered the camera's own voxel; here also t > t_stop) before it looks at the voxel, and their order
+    // among themselves does not matter.  t >= 1 or t > t_stop  <=>  t > min(t_stop, pred(1)); only the coordinate
+    // that was stepped can leave the grid (the walk starts inside it); the camera's voxel is one flat index.
+    const double t_lim = fmin(t_stop, 0x1.fffffffffffffp-1);
+    const uint32_t ures = (uint32_t)res;
+    const bool cam_in = (uint32_t)ex < ures && (uint32_t)ey < ures && (uint32_t)ez < ures;
+    const uint32_t cam_idx = cam_in ? (uint32_t)ex + ures * ((uint32_t)ey + ures * (uint32_t)ez) : 0xffffffffu;   // (V <= 2^30)
+    uint32_t idx = (uint32_t)x + ures * ((uint32_t)y + ures * (uint32_t)z);
+    const uint32_t stx = (uint32_t)sx, sty = (uint32_t)(sy * res), stz = (uint32_t)(sz * res * res);
     for (;;) {
         double t;
-        if (tmx <= tmy && tmx <= tmz) { x += sx; t = tmx; tmx += tdx; }
-        else if (tmy <= tmz) { y += sy; t = tmy; tmy += tdy; }
-        else { z += sz; t = tmz; tmz += tdz; }
-        if (t >= 1.0) return false;                                               // reached the camera
-        if (t > t_stop) return false;                                             // nothing solid from here on
-        if (x < 0 || y < 0 || z < 0 || x >= res || y >= res || z >= res) return false;  // left the grid
-        if (x == ex && y == ey && z == ez) return false;                          // camera's own voxel
-        const int64_t idx = x + (int64_t)res * (y + (int64_t)res * z);
+        uint32_t c;                                                                  // the coordinate just stepped
+        if (tmx <= tmy && tmx <= tmz) { x += sx; c = (uint32_t)x; idx += stx; t = tmx; tmx += tdx; }
+        else if (tmy <= tmz) { y += sy; c = (uint32_t)y; idx += sty; t = tmy; tmy += tdy; }
+        else { z += sz; c = (uint32_t)z; idx += stz; t = tmz; tmz += tdz; }
+        if (t > t_lim || c >= ures || idx == cam_idx) return false;
         if ((solid[idx >> 5] >> (idx & 31)) & 1u) return true;
     }
 }
@@ -801,7 +834,12 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     if ((occ_list - solid_bits) & 1) occ_list++;      // its first two words become a 64-bit list counter
     uint32_t *sb_rows = occ_list + V + LVX_LIST_HDR;
     LVX_CUDA(cudaMemsetAsync(vis_tmp, 0, (size_t)V, s));
-    k_solid<<<blocks_for(V, SOLID_ITEMS * 256), 256, 0, s>>>(base, res, V, solid_bits, bricks, solid_list, occ_list, stats);
+    k_solid<<<blocks_for(V, SOLID_ITEMS * 256), 256, 0, s>>>(base, res, V, solid_bits, solid_list, occ_list, stats);
+    {
+        const int rb = (res + LVX_BRICK - 1) / LVX_BRICK;
+        k_brick_flags<<<blocks_for(((int64_t)rb * rb * rb + 31) & ~31LL, 128), 128, 0, s>>>(solid_bits, res, stats, bricks);
+        k_super_flags<<<blocks_for(((int64_t)rs * rs * rs + 31) & ~31LL, 128), 128, 0, s>>>(bricks, res, stats, bricks + brick_words(res, LVX_BRICK));
+    }
     k_superbrick_shadow<<<(unsigned)(rs * rs * rs), 64, 0, s>>>(solid_list, res, (float)cam_voxel_host[0],
                                                                           (float)cam_voxel_host[1], (float)cam_voxel_host[2], sb_flag, sb_rows);
     unsigned nb = 148 * 16;

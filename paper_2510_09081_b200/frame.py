@@ -147,7 +147,7 @@ class FrameEngine:
         n += 3 if (self.order_brick > 0 and self._sharded) else 0   # ... and the same for a rank's voxelization shard
         n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
         n += (0 if (self.use_wide and self.res >= 64) else 1) + pyramid(2)   # mips: level 1 (fused into the pack pass at res >= 64), then the rest
-        n += (6 if self.strategy == "vcsv" else 1) + pyramid(1)   # solid, super-brick shadow, visibility, march probe, march, dilate | occupied; or-mips
+        n += (8 if self.strategy == "vcsv" else 1) + pyramid(1)   # solid, brick flags, super-brick flags, super-brick shadow, visibility, march probe, march, dilate | occupied; or-mips
         n += 1 + pyramid(1) if self._owned else 0   # tile owners + their OR pyramid
         n += 1                                      # scan
         n += 2 + 1                                  # scatter, order (the cursors come from the scan); march table
