@@ -52,7 +52,8 @@ enum {
     LVX_ST_OCC_SAT = 11,     /* voxels whose 16-bit occupancy sum saturated */
     LVX_ST_TILE_CURSOR = 12, /* scratch: pixel-tile queue of the persistent trace kernels (reset by every launch) */
     LVX_ST_OWNED = 13,       /* voxels a screen tile owns (lvx_tile_owners) */
-    LVX_STATS_WORDS = 16
+    LVX_ST_BRICK_PAIRS = 16, /* (segment, brick) pairs lvx_build_lists needs; > its pair_capacity: nothing was built, redo */
+    LVX_STATS_WORDS = 24
 };
 
 typedef struct lvx_camera {
@@ -193,6 +194,22 @@ int lvx_scatter(const double *verts, const int32_t *segs, int64_t n_seg, double 
                 const uint32_t *offsets, uint32_t *cursor, uint32_t *frags, int64_t frag_capacity,
                 uint32_t *tight_frags, uint16_t *tight_slot, uint16_t *tight_cnt /* may be NULL */,
                 int cursor_ready, uint64_t *stats, void *stream);
+
+/* The same second traversal for the capsule method (method 1), without per-incidence global atomics and without
+ * an ordering pass (csrc/bricks.cu): the segments are binned into 8^3-voxel bricks, one CTA per brick sorts the
+ * brick's segment ids and builds the lists of its voxels in ascending order in shared memory.  Same `frags` as
+ * lvx_scatter bit for bit (the reference's array, lv/abuffer.py:313-317); the tight index may list a few more
+ * fragments (cube grown by r_tight in the maximum norm instead of the Euclidean one), it stays conservative.
+ * res >= 8.  scratch: lvx_brick_scratch_words(res, pair_capacity) u32; pair_capacity = (segment, brick) pairs the
+ * scratch can hold (a segment overlaps ~3-5 bricks).  stats[LVX_ST_BRICK_PAIRS] receives the number needed: if
+ * it exceeds pair_capacity nothing was built and the call must be repeated with a larger scratch.  No cursor, no
+ * vis_list. */
+int64_t lvx_brick_scratch_words(int res, int64_t pair_capacity);
+int lvx_build_lists(const double *verts, const int32_t *segs, int64_t n_seg, double rt, double r_tight, int res,
+                    const uint8_t *cull_flat /* NULL = no culling */, const uint32_t *offsets,
+                    uint32_t *frags, int64_t frag_capacity,
+                    uint32_t *tight_frags, uint16_t *tight_slot, uint16_t *tight_cnt /* may be NULL */,
+                    uint32_t *scratch, int64_t pair_capacity, uint64_t *stats, void *stream);
 
 /* ---- shading: lv/shading.py:72-155 _trilinear/_cone_trace/_shading_kernel, 170-185.
  * dirs_host: n_dirs*3 unit vectors (lv/shading.py:32-40); light_host: unit light direction.

@@ -17,7 +17,8 @@ LIB_PATH = os.environ.get("LVX_LIB") or os.path.join(_HERE, "liblvx_b200.so")
 ST_VISITED, ST_SATURATED, ST_NEED_WIDE, ST_SOLID, ST_FRAG_TOTAL, ST_MISMATCH, ST_RAY_TESTS, \
     ST_LONG_LISTS, ST_DEGENERATE, ST_VISIBLE, ST_OCCUPIED, ST_OCC_SAT = range(12)
 ST_OWNED = 13
-STATS_WORDS = 16
+ST_BRICK_PAIRS = 16
+STATS_WORDS = 24
 
 
 class lvx_camera(C.Structure):
@@ -65,6 +66,8 @@ SIGNATURES = {
     "lvx_segment_order_scratch_words": (_L, [_L, _I, _I]),
     "lvx_segment_order": (_I, [_P, _P, _L, _I, _I, _P, _P, _P]),
     "lvx_scatter": (_I, [_P, _P, _L, _D, _D, _I, _I, _P, _P, _P, _P, _P, _L, _P, _P, _P, _I, _P, _P]),
+    "lvx_brick_scratch_words": (_L, [_I, _L]),
+    "lvx_build_lists": (_I, [_P, _P, _L, _D, _D, _I, _P, _P, _P, _L, _P, _P, _P, _P, _L, _P, _P]),
     "lvx_march_levels": (_I, [_P, _I, _P, _P]),
     "lvx_shade_scratch_bytes": (_L, [_L]),
     "lvx_shade": (_I, [_P, _P, _I, _P, _P, _I, _D, _P, _D, _P, _P, _I, _P, _P, _P]),

@@ -108,11 +108,22 @@ def _second_pass(ls, cn, g, pyramid, culling, method, r_world):
     rt = ops.footprint_radius(lines.r, pyramid.r_min)
     frags = torch.empty(max(table.total, 1), dtype=torch.int32, device=dev)
     tight = ops.TightIndex(frags.numel(), res ** 3, dev)
-    cursor = torch.empty(res ** 3, dtype=torch.int32, device=dev)
-    owners = culling if culling is not None else occupied_bits(pyramid)   # voxels that own fragments
-    ops.scatter(lines, rt, res, method, None if culling is None else culling.flat_dev, owners.list_dev,
-                table.offsets_dev, cursor, frags, stats, tight=tight)
-    st = stats.cpu().numpy()
+    flat = None if culling is None else culling.flat_dev
+    if ops.brick_lists_supported(method, res):     # capsule traversal: per-brick build, no atomics per incidence
+        pairs = 6 * lines.n_segments + 1024
+        while True:
+            scratch = ops.BrickScratch(res, pairs, dev)
+            ops.build_lists(lines, rt, res, flat, table.offsets_dev, frags, stats, scratch, tight=tight)
+            st = stats.cpu().numpy()
+            if int(st[N.ST_BRICK_PAIRS]) <= pairs:
+                break
+            pairs = int(st[N.ST_BRICK_PAIRS])
+    else:
+        cursor = torch.empty(res ** 3, dtype=torch.int32, device=dev)
+        owners = culling if culling is not None else occupied_bits(pyramid)   # voxels that own fragments
+        ops.scatter(lines, rt, res, method, flat, owners.list_dev,
+                    table.offsets_dev, cursor, frags, stats, tight=tight)
+        st = stats.cpu().numpy()
     if pyramid.saturated == 0 and st[N.ST_MISMATCH]:
         raise ABufferError("fragment count mismatch between passes (nondeterministic traversal?)")
     inc = table.total      # every scanned slot was written exactly once when there is no mismatch

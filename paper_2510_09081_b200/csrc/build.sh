@@ -7,5 +7,5 @@ NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 OUT=${LVX_OUT:-../liblvx_b200.so}
 $NVCC -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=c++17 \
       -Xcompiler -fPIC -shared ${LVX_NVCC_EXTRA} \
-      upload.cu voxelize.cu cull.cu abuffer.cu shade.cu render.cu -o $OUT
+      upload.cu voxelize.cu cull.cu abuffer.cu bricks.cu shade.cu render.cu -o $OUT
 echo "built $(realpath $OUT)"

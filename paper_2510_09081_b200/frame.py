@@ -48,7 +48,7 @@ class FrameEngine:
     def __init__(self, res: int, width: int, height: int, strategy="vcsv", mode="opaque", alpha=1.0, k=8,
                  method="capsule", r_min=0.5, light=(-0.5, -0.3, -0.8), clip=True, keep_rgb=False,
                  early_termination=True, background=(0.1, 0.1, 0.12), device=None, frag_capacity=0,
-                 shading="auto"):
+                 shading="auto", builder=None):
         torch = N.require_cuda()
         if strategy not in ("vsv", "vcsv"):
             raise ValueError("strategy must be vsv or vcsv")
@@ -134,6 +134,9 @@ class FrameEngine:
         self._sharded = False
         self.owner_flat = self.owner_list = None
         self._overlapped = False
+        # A-buffer build through per-brick segment lists (csrc/bricks.cu): opt-in (builder="bricks"), capsule traversal only
+        self._bricks = ops.brick_lists_supported(method, self.res, builder)
+        self._brick_scratch = None
 
     def kernel_launches_per_frame(self) -> int:
         """Number of lvx kernels one `run` enqueues (csrc/*.cu), for bench.py's `gpu_launches`."""
@@ -150,7 +153,7 @@ class FrameEngine:
         n += (8 if self.strategy == "vcsv" else 1) + pyramid(1)   # solid, brick flags, super-brick flags, super-brick shadow, visibility, march probe, march, dilate | occupied; or-mips
         n += 1 + pyramid(1) if self._owned else 0   # tile owners + their OR pyramid
         n += 1                                      # scan
-        n += 2 + 1                                  # scatter, order (the cursors come from the scan); march table
+        n += (4 if self._bricks else 2) + 1         # bin count, alloc, fill, brick build | scatter, order (cursors from the scan); march table
         n += 1 + pyramid(1) + 1                     # non-empty masks (level 0, the rest), shade
         if self.shading == "demand":
             n += 3                                  # trace_hits, need list, resolve
@@ -288,11 +291,17 @@ class FrameEngine:
     def _stage_scan(self):
         flat, _ = self._owner_bits()
         ops.scan(self.base, None if flat is None else flat[:self.V], self.offsets, self.scan_scratch, self.stats,
-                 cursor=self.cursor)
+                 cursor=None if self._bricks else self.cursor)
 
     def _stage_scatter(self):
         rt = ops.footprint_radius(self.lines.r, self.r_min)
         flat, lst = self._owner_bits()
+        if self._bricks:
+            if self._brick_scratch is None:
+                self._ensure_pairs(6 * self.lines.n_segments + 1024)
+            ops.build_lists(self.lines, rt, self.res, flat, self.offsets, self.frags, self.stats,
+                            self._brick_scratch, tight=self.tight)
+            return
         ops.scatter(self.lines, rt, self.res, self.method, flat, lst,
                     self.offsets, self.cursor, self.frags, self.stats, tight=self.tight, cursor_ready=True)
 
@@ -327,6 +336,11 @@ class FrameEngine:
             cap = min(int(need * 1.25) + 1024, limit)      # head-room never pushes a valid total over the limit
             self.frags = self.torch.empty(cap, dtype=self.torch.int32, device=self.dev)
             self.tight = ops.TightIndex(cap, self.V, self.dev)
+
+    def _ensure_pairs(self, need: int):
+        if self._brick_scratch is None or need > self._brick_scratch.capacity:
+            self._brick_scratch = None
+            self._brick_scratch = ops.BrickScratch(self.res, int(need * 1.25) + 1024, self.dev)
 
     def run(self, cam, grid: GridDesc, r_world: float, tile=None, seg_range=None, after_voxelize=None,
             geometry=True):
@@ -447,8 +461,11 @@ class FrameEngine:
                 self.submit(*self._pending)
                 continue
             total = int(st[N.ST_FRAG_TOTAL])
-            if total > self.frags.numel():
+            pairs = int(st[N.ST_BRICK_PAIRS]) if self._bricks else 0
+            if total > self.frags.numel() or (self._bricks and pairs > self._brick_scratch.capacity):
                 self._ensure_capacity(total)
+                if self._bricks:
+                    self._ensure_pairs(pairs)
                 self.submit(*self._pending)
                 continue
             break

@@ -283,6 +283,42 @@ def scatter(lines: DeviceLines, rt, res, method, cull_flat, vis_list, offsets, c
           "lvx_scatter")
 
 
+BRICK = 8     # csrc/bricks.cu
+
+
+def brick_lists_supported(method, res, builder=None) -> bool:
+    """The brick-binned build (lvx_build_lists, csrc/bricks.cu) covers the capsule traversal on grids of at least
+    one brick.  It is the OPT-IN builder (`builder="bricks"` / LVX_BUILDER=bricks): same fragments bit for bit, but
+    measured slower than the scatter + ordering passes on one B200, which stay the default."""
+    import os
+    builder = builder or os.environ.get("LVX_BUILDER", "scatter")
+    if builder not in ("scatter", "bricks"):
+        raise ValueError(f"unknown A-buffer builder {builder!r}")
+    return builder == "bricks" and method == "capsule" and res >= BRICK
+
+
+class BrickScratch:
+    """Scratch of lvx_build_lists: per-brick counters and the (segment, brick) pair array."""
+
+    def __init__(self, res: int, pair_capacity: int, device):
+        import torch
+        self.res, self.capacity = int(res), int(pair_capacity)
+        self.words = torch.empty(int(lib().lvx_brick_scratch_words(self.res, self.capacity)), dtype=torch.int32,
+                                 device=device)
+
+
+def build_lists(lines: DeviceLines, rt, res, cull_flat, offsets, frags, stats, scratch: BrickScratch, tight=None):
+    """lv/abuffer.py:195-255, 281-328 through per-brick segment lists (csrc/bricks.cu).  The caller checks
+    stats[ST_BRICK_PAIRS] <= scratch.capacity (else nothing was built: grow the scratch and call again)."""
+    if tight is not None and tight.capacity < frags.numel():
+        raise ValueError("tight index too small for the fragment buffer")
+    tf, ts, tc = _tight_ptrs(tight)
+    check(lib().lvx_build_lists(_ptr(lines.verts), _ptr(lines.proc_segs), lines.n_segments, float(rt),
+                                float(lines.r) + TIGHT_MARGIN, res, _ptr(cull_flat), _ptr(offsets),
+                                _ptr(frags), frags.numel(), tf, ts, tc, _ptr(scratch.words), scratch.capacity,
+                                _ptr(stats), _stream()), "lvx_build_lists")
+
+
 def march_levels(bits_flat, res, march):
     check(lib().lvx_march_levels(_ptr(bits_flat), res, _ptr(march), _stream()), "lvx_march_levels")
 
