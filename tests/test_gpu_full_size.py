@@ -237,3 +237,40 @@ def test_run_to_run_determinism_at_full_size(lvx, c2_lines, strategy, mode, alph
         if want is None:
             want = got
         assert got == want, f"frame {i} differs from frame 0"
+
+
+def test_bench_frame_deformed_and_refitted_vs_oracle(lvx, oracle, c2_lines):
+    """The frame bench.py actually times: a DEFORMED variant of the C2 set (bench.deform, frame t = 3), the grid
+    re-fitted from the device AABB of the new vertices (FrameEngine.fit) and the orbit camera rebuilt from it --
+    grid, lists, hit ids and colours against the oracle run on the same deformed line set."""
+    import bench
+    ls, g, _ = c2_lines
+    verts = bench.deform(ls.vertices, 3, g.voxel_size)
+    ls_t = lvx.LineSet(verts, ls.polyline_offsets, ls.radius)
+    cfg = lvx.PipelineConfig(res=256, width=1920, height=1080, strategy="vcsv", mode="opaque", light=bench.LIGHT)
+    eng = lvx.FrameEngine(256, 1920, 1080, strategy="vcsv", mode="opaque", keep_rgb=True, light=cfg.light_vector())
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    eng.load_vertices(verts)
+    g_t, rw_t = eng.fit(radius_voxels=bench.R_VOXELS)
+    g_h, rw_h = lvx.fit_grid(ls_t, 256, radius_voxels=bench.R_VOXELS)
+    assert g_t.voxel_size == g_h.voxel_size and np.array_equal(g_t.world_min, g_h.world_min) and rw_t == rw_h
+    assert not np.array_equal(g_t.world_min, g.world_min) or g_t.voxel_size != g.voxel_size   # the fit did change
+    cam = lvx.make_camera(cfg, g_t)
+    out = eng.run(cam, g_t, rw_t)
+    ref = oracle.run_frame(ls_t, g_t, rw_t, cam, cfg.light_vector(), strategy="vcsv", mode="opaque")
+    _check_build(eng, out, ref, 256)
+    _check_image(eng, out, ref)
+
+
+def test_c2thick_full_size_vs_oracle(lvx, oracle, c2_lines):
+    """bench.py's culling-active workload at full size (C2 drawn with a radius of 0.6 voxel: ~750 k solid voxels,
+    three quarters of the occupied voxels culled): culling pyramid, culled lists and image against the oracle."""
+    ls, _, _ = c2_lines
+    g, r_world = lvx.fit_grid(ls, 256, radius_voxels=0.6)
+    cfg = lvx.PipelineConfig(res=256, width=1920, height=1080, strategy="vcsv", mode="opaque", light="-0.5,-0.3,-0.8")
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vcsv", mode="opaque")
+    eng, out = _engine_frame(lvx, ls, g, r_world, cam, "vcsv", "opaque", 1.0)
+    assert out.stats["solid_voxels"] > 500_000 and out.stats["culled_fraction"] > 0.5
+    _check_build(eng, out, ref, 256)
+    _check_image(eng, out, ref)
