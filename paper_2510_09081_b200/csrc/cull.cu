@@ -110,31 +110,31 @@ k_solid(const uint32_t *__restrict__ base, int res, int64_t V, uint32_t *__restr
 
 // Brick flags from the finished solid bits.  An 8^3 brick is flagged when it overlaps a solid voxel dilated by
 // one voxel, i.e. when a solid bit is set in the brick grown by a voxel on every side; a 32^3 super-brick
-// overlaps such a dilated voxel exactly when one of its 8^3 bricks does.  One thread per brick: 10 x 10 rows of
+// overlaps such a dilated voxel exactly when one of its 8^3 bricks does.  One warp per brick: 10 x 10 rows of
 // 10 bits.  (Round 1 had every solid voxel set its bricks' flags with atomics from k_solid: in a frame full
 // of solid voxels that was most of that kernel's time.)  Nothing is solid -> the flags stay as cleared.
 __global__ void __launch_bounds__(128)
 k_brick_flags(const uint32_t *__restrict__ solid, int res, const uint64_t *__restrict__ stats, uint32_t *__restrict__ flags) {
     if (stats[LVX_ST_SOLID] == 0) return;
+    // one warp per brick, the (up to) 10 x 10 rows spread over its lanes; the flag words were cleared by the caller
     const int rb = (res + LVX_BRICK - 1) / LVX_BRICK;
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (b >= rb * rb * rb) return;
+    const int bx = b % rb, by = (b / rb) % rb, bz = b / (rb * rb);
+    const int x0 = max(bx * LVX_BRICK - 1, 0), x1 = min(bx * LVX_BRICK + LVX_BRICK, res - 1);
+    const int y0 = max(by * LVX_BRICK - 1, 0), y1 = min(by * LVX_BRICK + LVX_BRICK, res - 1);
+    const int z0 = max(bz * LVX_BRICK - 1, 0), z1 = min(bz * LVX_BRICK + LVX_BRICK, res - 1);
+    const int ny = y1 - y0 + 1, n_rows = ny * (z1 - z0 + 1);
     bool any = false;
-    if (b < rb * rb * rb) {
-        const int bx = b % rb, by = (b / rb) % rb, bz = b / (rb * rb);
-        const int x0 = max(bx * LVX_BRICK - 1, 0), x1 = min(bx * LVX_BRICK + LVX_BRICK, res - 1);
-        const int y0 = max(by * LVX_BRICK - 1, 0), y1 = min(by * LVX_BRICK + LVX_BRICK, res - 1);
-        const int z0 = max(bz * LVX_BRICK - 1, 0), z1 = min(bz * LVX_BRICK + LVX_BRICK, res - 1);
-        for (int z = z0; z <= z1 && !any; z++)
-            for (int y = y0; y <= y1 && !any; y++) {
-                const int64_t i0 = x0 + (int64_t)res * (y + (int64_t)res * z), i1 = i0 + (x1 - x0);   // bits i0 .. i1 of the row
-                const int64_t w0 = i0 >> 5, w1 = i1 >> 5;
-                const uint32_t lo = 0xffffffffu << (i0 & 31), hi = 0xffffffffu >> (31 - (i1 & 31));
-                if (w0 == w1) any = (solid[w0] & lo & hi) != 0;
-                else any = (solid[w0] & lo) != 0 || (solid[w1] & hi) != 0;               // (at most 10 bits: two words)
-            }
+    for (int r = lane; r < n_rows; r += 32) {
+        const int y = y0 + r % ny, z = z0 + r / ny;
+        const int64_t i0 = x0 + (int64_t)res * (y + (int64_t)res * z), i1 = i0 + (x1 - x0);   // bits i0 .. i1 of the row
+        const int64_t w0 = i0 >> 5, w1 = i1 >> 5;
+        const uint32_t lo = 0xffffffffu << (i0 & 31), hi = 0xffffffffu >> (31 - (i1 & 31));
+        if (w0 == w1) any |= (solid[w0] & lo & hi) != 0;
+        else any |= (solid[w0] & lo) != 0 || (solid[w1] & hi) != 0;                  // (at most 10 bits: two words)
     }
-    const uint32_t m = __ballot_sync(0xffffffffu, any);
-    if ((threadIdx.x & 31) == 0 && b < ((rb * rb * rb + 31) & ~31)) flags[b >> 5] = m;
+    if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(&flags[b >> 5], 1u << (b & 31));
 }
 
 __global__ void __launch_bounds__(128)
@@ -720,6 +720,79 @@ k_ormip(const uint8_t *__restrict__ src, int rsrc, uint8_t *__restrict__ out) {
 // ancestors at levels 1..l are all clear).  One load per DDA step instead of a walk up the pyramid.
 // One thread per 4 x-adjacent voxels (they share every ancestor from level 2 up).
 struct MarchOffsets { uint32_t off[16]; };
+
+// the four march bytes of voxels x0 .. x0 + 3 (bits b), which share every ancestor from level 2 up
+__device__ __forceinline__ uchar4 march_four(const uint8_t *__restrict__ flat, const MarchOffsets &O, int res, int n_levels,
+                                             uint32_t x0, uint32_t y, uint32_t z, uchar4 b) {
+    uchar4 out = make_uchar4(255, 255, 255, 255);
+    if (b.x && b.y && b.z && b.w) return out;
+    int up = 0;          // result for a voxel whose level-1 parent is clear
+    uint8_t p1a = 1, p1b = 1;
+    if (n_levels > 1) {
+        const uint32_t r1 = (uint32_t)res >> 1;
+        const uint32_t i1 = O.off[1] + (x0 >> 1) + r1 * ((y >> 1) + r1 * (z >> 1));
+        p1a = flat[i1]; p1b = flat[i1 + 1];
+        if (!(p1a && p1b)) {
+            // In an OR pyramid a set node has set ancestors only, so "ancestors 1..l all clear" holds
+            // for l up to the highest clear ancestor: all levels are loaded at once (independent
+            // loads, one round trip) and the clear ones counted, instead of a dependent walk upwards.
+            uint32_t clear = 0;
+#pragma unroll
+            for (int nl = 2; nl < 11; nl++) {     // res <= 1024: at most 11 levels
+                if (nl < n_levels) {
+                    const uint32_t rl = (uint32_t)res >> nl;
+                    if (flat[O.off[nl] + (x0 >> nl) + rl * ((y >> nl) + rl * (z >> nl))] == 0)
+                        clear |= 1u << nl;
+                }
+            }
+            up = __ffs(~(clear | 3u)) - 2;        // the level below the first set ancestor (>= 1)
+        }
+    }
+    const uint8_t la = p1a ? 0 : (uint8_t)up, lb = p1b ? 0 : (uint8_t)up;
+    if (!b.x) out.x = la;
+    if (!b.y) out.y = la;
+    if (!b.z) out.z = lb;
+    if (!b.w) out.w = lb;
+    return out;
+}
+
+// One thread per 16 x-adjacent voxels (res >= 16), which share every ancestor from level 4 up.  Most of a volume
+// lies under clear 16^3 nodes: there the 16 bytes are one value -- the highest level whose ancestors are all
+// clear -- and one 128-bit store; the other runs go through march_four four voxels at a time.
+__global__ void __launch_bounds__(256)
+k_march_levels16(const uint8_t *__restrict__ flat, const MarchOffsets O, int res, int n_levels, int64_t n16,
+                 uint8_t *__restrict__ skip) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= n16) return;
+    const uint32_t r16 = (uint32_t)res >> 4;
+    const uint32_t x0 = (uint32_t)(g % r16) << 4, y = (uint32_t)((g / r16) % res), z = (uint32_t)(g / ((int64_t)r16 * res));
+    const uint4 w = *reinterpret_cast<const uint4 *>(flat + (x0 + (int64_t)res * (y + (int64_t)res * z)));
+    const uint32_t r4l = (uint32_t)res >> 4;
+    if (flat[O.off[4] + (x0 >> 4) + r4l * ((y >> 4) + r4l * (z >> 4))] == 0) {
+        uint32_t clear = 0;
+#pragma unroll
+        for (int nl = 5; nl < 11; nl++) {
+            if (nl < n_levels) {
+                const uint32_t rl = (uint32_t)res >> nl;
+                if (flat[O.off[nl] + (x0 >> nl) + rl * ((y >> nl) + rl * (z >> nl))] == 0) clear |= 1u << nl;
+            }
+        }
+        const uint32_t up = (uint32_t)(__ffs(~(clear | 31u)) - 2);       // levels 1..4 are clear under a clear level-4 node
+        const uint32_t v = up * 0x01010101u;
+        *reinterpret_cast<uint4 *>(skip + 16 * g) = make_uint4(v, v, v, v);
+        return;
+    }
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const uchar4 b = make_uchar4(ws[q] & 0xFF, (ws[q] >> 8) & 0xFF, (ws[q] >> 16) & 0xFF, ws[q] >> 24);
+        const uchar4 r = march_four(flat, O, res, n_levels, x0 + 4 * q, y, z, b);
+        o[q] = (uint32_t)r.x | (uint32_t)r.y << 8 | (uint32_t)r.z << 16 | (uint32_t)r.w << 24;
+    }
+    *reinterpret_cast<uint4 *>(skip + 16 * g) = make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 __global__ void __launch_bounds__(256)
 k_march_levels(const uint8_t *__restrict__ flat, const MarchOffsets O, int res, int n_levels, int64_t n4,
                uint8_t *__restrict__ skip) {
@@ -728,37 +801,7 @@ k_march_levels(const uint8_t *__restrict__ flat, const MarchOffsets O, int res, 
     const int r4 = res >> 2;
     const int x0 = (int)(g % r4) << 2, y = (int)((g / r4) % res), z = (int)(g / ((int64_t)r4 * res));
     const uchar4 b = *reinterpret_cast<const uchar4 *>(flat + (x0 + (int64_t)res * (y + (int64_t)res * z)));
-    uchar4 out = make_uchar4(255, 255, 255, 255);
-    if (!(b.x && b.y && b.z && b.w)) {
-        int up = 0;          // result for a voxel whose level-1 parent is clear
-        uint8_t p1a = 1, p1b = 1;
-        if (n_levels > 1) {
-            const uint32_t r1 = (uint32_t)res >> 1;
-            const uint32_t i1 = O.off[1] + ((uint32_t)x0 >> 1) + r1 * (((uint32_t)y >> 1) + r1 * ((uint32_t)z >> 1));
-            p1a = flat[i1]; p1b = flat[i1 + 1];
-            if (!(p1a && p1b)) {
-                // In an OR pyramid a set node has set ancestors only, so "ancestors 1..l all clear" holds
-                // for l up to the highest clear ancestor: all levels are loaded at once (independent
-                // loads, one round trip) and the clear ones counted, instead of a dependent walk upwards.
-                uint32_t clear = 0;
-#pragma unroll
-                for (int nl = 2; nl < 11; nl++) {     // res <= 1024: at most 11 levels
-                    if (nl < n_levels) {
-                        const uint32_t rl = (uint32_t)res >> nl;
-                        if (flat[O.off[nl] + ((uint32_t)x0 >> nl) + rl * (((uint32_t)y >> nl) + rl * ((uint32_t)z >> nl))] == 0)
-                            clear |= 1u << nl;
-                    }
-                }
-                up = __ffs(~(clear | 3u)) - 2;        // the level below the first set ancestor (>= 1)
-            }
-        }
-        const uint8_t la = p1a ? 0 : (uint8_t)up, lb = p1b ? 0 : (uint8_t)up;
-        if (!b.x) out.x = la;
-        if (!b.y) out.y = la;
-        if (!b.z) out.z = lb;
-        if (!b.w) out.w = lb;
-    }
-    *reinterpret_cast<uchar4 *>(skip + 4 * g) = out;
+    *reinterpret_cast<uchar4 *>(skip + 4 * g) = march_four(flat, O, res, n_levels, (uint32_t)x0, (uint32_t)y, (uint32_t)z, b);
 }
 
 // The top of the OR pyramid (levels of <= 16^3 nodes) in one launch: a single CTA, level after level.
@@ -837,7 +880,7 @@ int lvx_cull(const uint32_t *base, int res, const double *cam_voxel_host, uint32
     k_solid<<<blocks_for(V, SOLID_ITEMS * 256), 256, 0, s>>>(base, res, V, solid_bits, solid_list, occ_list, stats);
     {
         const int rb = (res + LVX_BRICK - 1) / LVX_BRICK;
-        k_brick_flags<<<blocks_for(((int64_t)rb * rb * rb + 31) & ~31LL, 128), 128, 0, s>>>(solid_bits, res, stats, bricks);
+        k_brick_flags<<<blocks_for((int64_t)rb * rb * rb * 32, 128), 128, 0, s>>>(solid_bits, res, stats, bricks);
         k_super_flags<<<blocks_for(((int64_t)rs * rs * rs + 31) & ~31LL, 128), 128, 0, s>>>(bricks, res, stats, bricks + brick_words(res, LVX_BRICK));
     }
     k_superbrick_shadow<<<(unsigned)(rs * rs * rs), 64, 0, s>>>(solid_list, res, (float)cam_voxel_host[0],
@@ -904,7 +947,8 @@ int lvx_march_levels(const uint8_t *bits_flat, int res, uint8_t *march, void *st
     MarchOffsets O;
     for (int l = 0; l < 16; l++) O.off[l] = l < L.n_levels ? (uint32_t)L.off[l] : 0;
     const int64_t n4 = L.off[1] / 4;
-    k_march_levels<<<blocks_for(n4, 256), 256, 0, (cudaStream_t)stream>>>(bits_flat, O, res, L.n_levels, n4, march);
+    if (res >= 32) k_march_levels16<<<blocks_for(n4 / 4, 256), 256, 0, (cudaStream_t)stream>>>(bits_flat, O, res, L.n_levels, n4 / 4, march);
+    else k_march_levels<<<blocks_for(n4, 256), 256, 0, (cudaStream_t)stream>>>(bits_flat, O, res, L.n_levels, n4, march);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }
