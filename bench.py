@@ -548,9 +548,12 @@ def run_tiled(args, lvx, torch, dist, rank, world, local, ls, g, cfg):
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args.workload, ls),
-            "run": {"multi_gpu": "tiled: segment-sharded voxelize + all-reduce of the 64-bit accumulators + per-rank "
+            "run": {"multi_gpu": "tiled: segment-sharded voxelize + all-reduce of the occupancy grid (packed words or 64-bit accumulators) + per-rank "
                                  "screen strip (tile-restricted build) + gather on rank 0", "frames_in_flight": 1},
-            "exchange": {"all_reduce_bytes_per_rank": xb, "all_reduce_ms_max": round(xms, 4),
+            "exchange": {"all_reduce_bytes_per_rank": xb, "kind": tf.exchange_kind if world > 1 else None,
+                         "note": "packed = 4-byte words after a 16-byte pre-check (no field of the merged grid can overflow), "
+                                 "wide = the 8-byte accumulators; all_reduce_ms includes the pre-check and the pack pass",
+                         "all_reduce_ms_max": round(xms, 4),
                          "bus_gbs": round(2 * (world - 1) / world * xb / (xms * 1e-3) / 1e9, 1) if xms > 0 else None,
                          "gather_bytes": int(out_srgb.numel() + out_hit.numel() * 4)},
             "ranks": ranks,

@@ -120,6 +120,11 @@ int lvx_voxelize_wide(const double *verts, const double *normals, const int32_t 
                       int res, int method, uint64_t *wide, uint64_t *stats, void *stream);
 /* packed (+occ_sat) -> wide, so that per-GPU partial grids can be all-reduced with a plain sum */
 int lvx_widen(const uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, uint64_t *wide, void *stream);
+/* out2 (device, 2 x u64) = {largest count, largest occupancy sum} of the accumulators.  Multi-GPU exchange: the
+ * sums of these maxima over the ranks bound every field of the merged grid; while both stay below 65536 the ranks
+ * can all-reduce the PACKED words (lvx_pack_wide, 4 bytes per voxel: no field can carry into the other or saturate)
+ * instead of the accumulators (8 bytes per voxel), and lvx_widen the sum back. */
+int lvx_wide_field_max(const uint64_t *wide, int64_t n_voxels, uint64_t *out2, void *stream);
 /* wide -> packed with per-field saturation (lv/voxelizer.py:493-495); adds to LVX_ST_SATURATED */
 int lvx_pack_wide(const uint64_t *wide, int64_t n_voxels, uint32_t *base,
                   uint32_t *nz_bits /* may be NULL; n_voxels/32 u32: bit = occupancy field non-zero, for lvx_shade */,

@@ -117,6 +117,33 @@ k_widen(const uint32_t *__restrict__ base, const uint32_t *__restrict__ occ_sat,
     wide[i] = ((unsigned long long)(w >> 16) << 32) | lo;
 }
 
+// Largest count and largest occupancy sum of a rank's accumulators (multi-GPU exchange: the sums of these maxima
+// over the ranks bound every field of the merged grid; below 2^16 the packed 4-byte words can be summed instead
+// of the 8-byte accumulators).  Four accumulators per thread (two 128-bit loads), grid-stride.
+__global__ void __launch_bounds__(256)
+k_wide_field_max(const unsigned long long *__restrict__ wide, int64_t n, unsigned long long *__restrict__ out2) {
+    unsigned long long mc = 0, mo = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
+        if (i + 3 < n) {
+            const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(wide + i), b = *reinterpret_cast<const ulonglong2 *>(wide + i + 2);
+            mc = max(max(mc, a.x >> 32), max(max(a.y >> 32, b.x >> 32), b.y >> 32));
+            mo = max(max(mo, a.x & 0xFFFFFFFFull), max(max(a.y & 0xFFFFFFFFull, b.x & 0xFFFFFFFFull), b.y & 0xFFFFFFFFull));
+        } else {
+            for (int64_t j = i; j < n; j++) { mc = max(mc, wide[j] >> 32); mo = max(mo, wide[j] & 0xFFFFFFFFull); }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mc = max(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+        mo = max(mo, __shfl_xor_sync(0xffffffffu, mo, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (mc) atomicMax(&out2[0], mc);
+        if (mo) atomicMax(&out2[1], mo);
+    }
+}
+
 __global__ void __launch_bounds__(256)
 k_pack_wide(const unsigned long long *__restrict__ wide, int64_t n, uint32_t *__restrict__ base,
             uint32_t *__restrict__ nz_bits, uint64_t *__restrict__ stats) {
@@ -299,6 +326,17 @@ int lvx_voxelize_wide(const double *verts, const double *normals, const int32_t 
 int lvx_widen(const uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, uint64_t *wide, void *stream) {
     k_widen<<<blocks_for(n_voxels, 256), 256, 0, (cudaStream_t)stream>>>(base, occ_sat, n_voxels,
                                                                         (unsigned long long *)wide);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_wide_field_max(const uint64_t *wide, int64_t n_voxels, uint64_t *out2, void *stream) {
+    if (!wide || !out2 || n_voxels <= 0 || (reinterpret_cast<uintptr_t>(wide) & 15)) return LVX_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    LVX_CUDA(cudaMemsetAsync(out2, 0, 16, s));
+    unsigned nb = blocks_for((n_voxels + 3) / 4, 256);
+    if (nb > 148 * 8) nb = 148 * 8;
+    k_wide_field_max<<<nb, 256, 0, s>>>((const unsigned long long *)wide, n_voxels, (unsigned long long *)out2);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -30,6 +30,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["shard_bounds", "tile_rects", "balanced_rows", "frames_for_rank", "widen_packed", "pack_wide",
+           "field_bounds", "exchange_accumulators",
            "merge_partial_grids", "TiledFrame", "Comm", "TorchComm", "EmulatedComm"]
 
 
@@ -179,6 +180,56 @@ class EmulatedComm(Comm):
         return out
 
 
+FIELD_LIMIT = 1 << 16      # a 16-bit field of the packed word
+
+
+def field_bounds(wide_i64):
+    """int64[2] = {largest count, largest occupancy sum} of a rank's accumulators `(count << 32) | occ sum`
+    (device kernel on CUDA tensors; torch ops on the CPU tensors of the gloo tests)."""
+    import torch
+    if wide_i64.is_cuda:
+        from . import ops
+        out = torch.empty(2, dtype=torch.int64, device=wide_i64.device)
+        ops.wide_field_max(wide_i64, out)
+        return out
+    return torch.stack([(wide_i64 >> 32).max(), (wide_i64 & 0xFFFFFFFF).max()])
+
+
+def exchange_accumulators(wide_i64, comm, packed_scratch=None, stats=None, widen_back=True):
+    """The exchange step of a segment-sharded voxelization.  Returns (bytes every rank contributed, "packed" | "wide").
+
+    The accumulators are 8 bytes per voxel.  Every rank first contributes the two maxima of its own fields to a
+    16-byte all-reduce: their sums over the ranks bound every field of the merged grid, and while both bounds stay
+    below 2^16 no packed field can carry into its neighbour or saturate -- the ranks then all-reduce the PACKED
+    words (4 bytes per voxel, a plain integer sum).  Otherwise the accumulators themselves are
+    summed.  All ranks see the same bounds, so they take the same branch; reading them is the one host
+    synchronisation of the step (the collective synchronises the ranks anyway).
+
+    "wide": `wide_i64` holds the sum over all ranks.  "packed": `packed_scratch` (CUDA; V int32) holds the merged
+    PACKED grid, which is final -- nothing saturates below the bounds, so it is what packing the merged
+    accumulators would give -- and, with `widen_back`, `wide_i64` holds the merged accumulators as well."""
+    import torch
+    n = wide_i64.numel()
+    bounds = field_bounds(wide_i64)
+    comm.all_reduce_sum(bounds)
+    if bool((bounds < FIELD_LIMIT).all().item()):
+        if wide_i64.is_cuda:
+            from . import ops
+            packed = packed_scratch if packed_scratch is not None else torch.empty(n, dtype=torch.int32, device=wide_i64.device)
+            st = stats if stats is not None else ops.new_stats(wide_i64.device)
+            ops.pack_wide(wide_i64, packed, st)              # (no field reaches 2^16: nothing saturates here)
+            comm.all_reduce_sum(packed)                      # int32 wraps like the u32 bit patterns it carries
+            if widen_back:
+                ops.widen(packed, None, wide_i64)
+        else:
+            packed, _ = pack_wide(wide_i64)
+            comm.all_reduce_sum(packed)
+            wide_i64.copy_(widen_packed(packed))
+        return 4 * n, "packed"
+    comm.all_reduce_sum(wide_i64)
+    return 8 * n, "wide"
+
+
 def merge_partial_grids(base_i32, group=None, comm=None):
     """All-reduce the per-rank packed grids exactly.  `base_i32`: this rank's finalized packed grid
     (int32 bit patterns, any device).  Returns (merged packed int32 grid, total visited)."""
@@ -209,6 +260,8 @@ class TiledFrame:
         self.tiles = tile_rects(engine.w, engine.h, self.world)
         self.exchange_ms = None
         self.exchange_bytes = 0
+        self.exchange_kind = None        # "packed" (4 B per voxel) | "wide" (8 B per voxel), see exchange_accumulators
+        self.packed_exchange = True
         self._ev = None
         if getattr(comm, "emulated", False):
             comm.peers = self._voxelize_peers
@@ -253,13 +306,22 @@ class TiledFrame:
     def _merge(self, eng):
         import torch
         timed = eng.stats.is_cuda
+        base_final = False
         if timed:
             if self._ev is None:
                 self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             self._ev[0].record()
         if eng.use_wide:     # the engine's 64-bit accumulators are sum-reducible as they are; it packs afterwards
-            self.exchange_bytes = eng.wide.numel() * 8
-            self.comm.all_reduce_sum(eng.wide)
+            if self.packed_exchange and not getattr(self.comm, "emulated", False):
+                # packed 4-byte words when a 16-byte pre-check proves that no field can overflow (exchange_accumulators)
+                final = eng.stats.is_cuda and getattr(eng, "base", None) is not None     # a FrameEngine: its `base` receives the merged grid
+                self.exchange_bytes, self.exchange_kind = exchange_accumulators(
+                    eng.wide, self.comm, packed_scratch=eng.base if final else None,
+                    stats=eng.stats if eng.stats.is_cuda else None, widen_back=not final)
+                base_final = final and self.exchange_kind == "packed"
+            else:
+                self.exchange_bytes, self.exchange_kind = eng.wide.numel() * 8, "wide"
+                self.comm.all_reduce_sum(eng.wide)
         else:
             self.exchange_bytes = eng.base.numel() * 8
             merged, _ = merge_partial_grids(eng.base, comm=self.comm)
@@ -269,6 +331,7 @@ class TiledFrame:
             self.comm.all_reduce_sum(eng.stats[N.ST_VISITED:N.ST_VISITED + 1])
         if timed:
             self._ev[1].record()
+        return "base_final" if base_final else None       # the engine then skips its pack pass (FrameEngine._stage_voxelize)
 
     def run(self, cam, grid, r_world):
         """This rank's part of the frame.  Returns the engine's FrameResult; its `stage_ms` gets an

@@ -132,6 +132,7 @@ class FrameEngine:
         self.tile_build = True
         self._owned = False
         self._sharded = False
+        self._base_final = False
         self.owner_flat = self.owner_list = None
         self._overlapped = False
         # A-buffer build through per-brick segment lists (csrc/bricks.cu): opt-in (builder="bricks"), capsule traversal only
@@ -149,7 +150,8 @@ class FrameEngine:
         n += 3 if self.order_brick > 0 else 0       # processing order: histogram, scan, scatter
         n += 3 if (self.order_brick > 0 and self._sharded) else 0   # ... and the same for a rank's voxelization shard
         n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
-        n += (0 if (self.use_wide and self.res >= 64) else 1) + pyramid(2)   # mips: level 1 (fused into the pack pass at res >= 64), then the rest
+        n += 1 if self._base_final else 0           # multi-GPU packed exchange: field maxima, pack (no saturation), no fused level 1
+        n += (0 if (self.use_wide and self.res >= 64 and not self._base_final) else 1) + pyramid(2)   # mips: level 1 (fused into the pack pass at res >= 64), then the rest
         n += (8 if self.strategy == "vcsv" else 1) + pyramid(1)   # solid, brick flags, super-brick flags, super-brick shadow, visibility, march probe, march, dilate | occupied; or-mips
         n += 1 + pyramid(1) if self._owned else 0   # tile owners + their OR pyramid
         n += 1                                      # scan
@@ -233,8 +235,14 @@ class FrameEngine:
                 shard_order = self._order_shard
             ops.voxelize_wide(self.lines, self.res, self.r_min, self.method, self.wide, self.stats, b, e,
                               shard_order=shard_order)
-            if after_voxelize is not None:
-                after_voxelize(self)
+            if after_voxelize is not None and after_voxelize(self) == "base_final":
+                # the multi-GPU exchange summed PACKED words (no field could overflow): `base` is the merged,
+                # final grid already -- no pack pass; level 1 and the non-empty bits come from `base`
+                self._nz_valid = False
+                self._mip1_done = False
+                self._base_final = True
+                return
+            self._base_final = False
             if self.nz_bits is None and self.res >= 32:
                 self.nz_bits = self.torch.empty(self.V // 32, dtype=self.torch.int32, device=self.dev)
             if self.res >= 64:     # pack + level 1 of the pyramid in one read of the accumulators

@@ -175,6 +175,11 @@ def widen(base, occ_sat, wide):
     check(lib().lvx_widen(_ptr(base), _ptr(occ_sat), base.numel(), _ptr(wide), _stream()), "lvx_widen")
 
 
+def wide_field_max(wide, out2):
+    """out2 (device int64[2]) = {largest count, largest occupancy sum} of the 64-bit accumulators."""
+    check(lib().lvx_wide_field_max(_ptr(wide), wide.numel(), _ptr(out2), _stream()), "lvx_wide_field_max")
+
+
 def pack_wide(wide, base, stats, nz_bits=None):
     """`nz_bits` (optional i32, V/32): receives one bit per voxel "occupancy non-zero" for `shade`."""
     check(lib().lvx_pack_wide(_ptr(wide), wide.numel(), _ptr(base), _ptr(nz_bits), _ptr(stats), _stream()), "lvx_pack_wide")

@@ -103,7 +103,9 @@ def _tiled_worker(rank, world, port, scene_name, out_dir):
         srgb, hit = tf.gather_image()
         ref = orc.run_frame(sc.ls, sc.g, sc.r_world, sc.cam, sc.light, strategy=sc.strategy, mode=sc.mode,
                             alpha=sc.alpha, k=sc.k)
-        ok = out.stats["voxels_visited"] == ref.pyramid.visited and tf.exchange_bytes == 8 * sc.g.resolution ** 3
+        ok = out.stats["voxels_visited"] == ref.pyramid.visited
+        # thin lines: the 16-byte pre-check lets the ranks exchange the packed words (4 bytes per voxel)
+        ok = ok and tf.exchange_kind == "packed" and tf.exchange_bytes == 4 * sc.g.resolution ** 3
         ok = ok and 0 <= lo < hi <= sc.ls.n_segments
         if rank == 0:
             ok = ok and np.array_equal(srgb.numpy(), ref.image.srgb) and np.array_equal(hit.numpy(), ref.image.hit_id)
@@ -123,6 +125,50 @@ def test_tiled_frame_runs_and_gathers_over_gloo(scene, tmp_path, oracle):
     r = [np.load(tmp_path / f"tiled{k}.npy") for k in range(world)]
     assert all(x[0] for x in r)
     assert r[0][1] == 0 and r[0][2] == r[1][1] and r[1][2] > r[1][1]      # the shards tile [0, n)
+
+
+class PeerComm(D.Comm):
+    """A 2-rank job seen from rank 0: all_reduce_sum adds what a peer holding `peer_wide` would contribute to
+    whichever of the three buffers of exchange_accumulators is being reduced."""
+    rank, world = 0, 2
+
+    def __init__(self, peer_wide):
+        self.peer, self.reduced = peer_wide, []
+
+    def all_reduce_sum(self, t):
+        if t.numel() == 2 and t.dtype == torch.int64:
+            t += D.field_bounds(self.peer).to(t.device); self.reduced.append("bounds")
+        elif t.dtype == torch.int32:
+            t += D.pack_wide(self.peer.cpu())[0].to(t.device); self.reduced.append("packed")
+        else:
+            t += self.peer; self.reduced.append("wide")
+
+
+def test_exchange_accumulators_packed_when_no_field_can_overflow():
+    """The multi-GPU exchange: packed 4-byte words while the summed per-rank maxima stay below 2^16,
+    else the 8-byte accumulators -- the merged accumulators are the plain sum either way."""
+    g = torch.Generator().manual_seed(3)
+    cnt_a = torch.randint(0, 300, (4096,), generator=g); occ_a = torch.randint(0, 30000, (4096,), generator=g)
+    cnt_b = torch.randint(0, 300, (4096,), generator=g); occ_b = torch.randint(0, 30000, (4096,), generator=g)
+    a = (cnt_a << 32) | occ_a
+    b = (cnt_b << 32) | occ_b
+    mine = a.clone()
+    comm = PeerComm(b)
+    nbytes, kind = D.exchange_accumulators(mine, comm)
+    assert (nbytes, kind) == (4 * 4096, "packed") and comm.reduced == ["bounds", "packed"]
+    assert torch.equal(mine, a + b)
+    # one voxel whose occupancy sums COULD reach 2^16 (40000 here, 30000 somewhere on the peer): the bound fails
+    a2 = a.clone(); a2[7] = (5 << 32) | 40000
+    mine = a2.clone()
+    comm = PeerComm(b)
+    nbytes, kind = D.exchange_accumulators(mine, comm)
+    assert (nbytes, kind) == (8 * 4096, "wide") and comm.reduced == ["bounds", "wide"]
+    assert torch.equal(mine, a2 + b)
+    # counts near the field limit: 40000 + 299 < 65536 is fine, and the packed words then have their top bit set
+    a3 = a.clone(); a3[11] = (40000 << 32) | 17
+    mine = a3.clone()
+    nbytes, kind = D.exchange_accumulators(mine, PeerComm(b))
+    assert kind == "packed" and torch.equal(mine, a3 + b)
 
 
 def test_emulated_comm_contract():

@@ -468,3 +468,131 @@ def test_engine_fused_pack_and_level1(lvx, oracle, res, r):
     assert n == ref.abuf.total
     assert np.array_equal(e.frags[:n].cpu().numpy().view(np.uint32), ref.abuf.fragments)
     assert np.array_equal(e.rgb.cpu().numpy(), ref.image.rgb)
+
+
+def test_packed_exchange_of_two_shards_equals_the_whole_grid(lvx, oracle):
+    """Multi-GPU exchange on the device (distributed.exchange_accumulators): the accumulators of two
+    segment shards, merged through the 16-byte pre-check + PACKED 4-byte words (lvx_wide_field_max, lvx_pack_wide,
+    int32 sum, lvx_widen), equal the accumulators of the whole set; a set whose fields can overflow takes the
+    8-byte path; the packed base of the merged grid is the oracle's."""
+    import torch
+    from paper_2510_09081_b200 import distributed as D, ops
+    ls = lvx.generate("random_streamlines", seed=8, polylines=80, verts_per_line=60)
+    res = 64
+    dev = torch.device("cuda")
+
+    class Peer(D.Comm):
+        rank, world = 0, 2
+
+        def __init__(self, peer):
+            self.peer, self.reduced = peer, []
+
+        def all_reduce_sum(self, t):
+            if t.numel() == 2 and t.dtype == torch.int64:
+                t += D.field_bounds(self.peer); self.reduced.append("bounds")
+            elif t.dtype == torch.int32:
+                p = torch.empty_like(t)
+                ops.pack_wide(self.peer, p, ops.new_stats(dev))
+                t += p; self.reduced.append("packed")
+            else:
+                t += self.peer; self.reduced.append("wide")
+
+    dense = lvx.generate("random_streamlines", seed=9, polylines=600, verts_per_line=60, domain=16.0)
+    for ls, rv, want in ((ls, 0.3, "packed"), (dense, 3.0, "wide")):   # thin lines | a crowd of fat tubes (occupancy sums beyond 2^16)
+        g, r_world = lvx.fit_grid(ls, res, radius_voxels=rv)
+        eng = lvx.FrameEngine(res, 64, 48, strategy="vsv")
+        eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+        eng.load_vertices(ls.vertices)
+        eng._prepare_host()
+        ops.stats_reset(eng.stats)
+        eng._stage_upload(g, r_world)
+        n = eng.lines.n_segments
+        b = D.shard_bounds(n, 2)
+        V = res ** 3
+        parts = []
+        for r in range(2):
+            w = torch.zeros(V, dtype=torch.int64, device=dev)
+            ops.voxelize_wide(eng.lines, res, eng.r_min, eng.method, w, eng.stats, int(b[r]), int(b[r + 1]))
+            parts.append(w)
+        whole = torch.zeros(V, dtype=torch.int64, device=dev)
+        ops.voxelize_wide(eng.lines, res, eng.r_min, eng.method, whole, eng.stats, 0, n)
+        bounds = D.field_bounds(whole).cpu().numpy()
+        assert bounds[0] == int((whole >> 32).max().item()) and bounds[1] == int((whole & 0xFFFFFFFF).max().item())
+        assert (bounds[1] >= 65536) == (want == "wide")
+        mine = parts[0].clone()
+        comm = Peer(parts[1])
+        nbytes, kind = D.exchange_accumulators(mine, comm, packed_scratch=torch.empty(V, dtype=torch.int32, device=dev), stats=eng.stats)
+        assert kind == want and nbytes == (4 if want == "packed" else 8) * V and comm.reduced == ["bounds", want]
+        assert torch.equal(mine, whole)
+        base = torch.empty(V, dtype=torch.int32, device=dev)
+        ops.pack_wide(mine, base, ops.new_stats(dev))
+        ref = oracle.voxelize(ls, oracle.compute_clip_normals(ls), g, r_world=r_world)
+        assert np.array_equal(base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.base)
+
+
+@pytest.mark.parametrize("rank", [0, 1])
+def test_tiled_frame_with_packed_exchange_on_the_engine(lvx, oracle, rank):
+    """TiledFrame.run on the real FrameEngine as one rank of a 2-rank job whose peer is played by a Comm that adds
+    what the other rank would contribute to each of the three collectives (bounds, packed words, incidence count):
+    the exchange takes the packed 4-byte path, the engine skips its pack pass (`base` arrives final), and grid,
+    lists and the rank's strip of the image are the oracle's."""
+    import torch
+    from paper_2510_09081_b200 import distributed as D, ops
+    ls = lvx.generate("random_streamlines", seed=12, polylines=70, verts_per_line=50)
+    res = 64
+    g, r_world = lvx.fit_grid(ls, res, radius_voxels=0.3)
+    cfg = lvx.PipelineConfig(res=res, width=96, height=64, strategy="vcsv")
+    cam = lvx.make_camera(cfg, g)
+    ref = oracle.run_frame(ls, g, r_world, cam, cfg.light_vector(), strategy="vcsv")
+    eng = lvx.FrameEngine(res, 96, 64, strategy="vcsv", keep_rgb=True)
+    eng.set_topology(ls.polyline_offsets, ls.n_vertices)
+    eng.load_vertices(ls.vertices)
+
+    class PeerComm(D.Comm):
+        world = 2
+
+        def __init__(self, rank):
+            self.rank, self.kinds, self._peer = rank, [], None
+
+        def peer_wide(self):
+            if self._peer is None:        # the other rank's shard, voxelized here (its incidences go to eng.stats too)
+                b = D.shard_bounds(eng.lines.n_segments, 2)
+                o = 1 - self.rank
+                self._peer = torch.zeros(eng.V, dtype=torch.int64, device=eng.dev)
+                ops.voxelize_wide(eng.lines, res, eng.r_min, eng.method, self._peer, eng.stats, int(b[o]), int(b[o + 1]))
+            return self._peer
+
+        def all_reduce_sum(self, t):
+            if t.dtype == torch.int32:
+                p = torch.empty_like(t)
+                ops.pack_wide(self.peer_wide(), p, ops.new_stats(eng.dev))
+                t += p; self.kinds.append("packed")
+            elif t.numel() == 2:
+                t += D.field_bounds(self.peer_wide()); self.kinds.append("bounds")
+            elif t.numel() == 1:
+                self.kinds.append("count")            # (added by peer_wide's voxelization above)
+            else:
+                t += self.peer_wide(); self.kinds.append("wide")
+
+        def gather(self, t):
+            return [t] if self.rank == 0 else None
+
+    comm = PeerComm(rank)
+    tf = D.TiledFrame(eng, comm=comm)
+    out = tf.run(cam, g, r_world)
+    assert tf.exchange_kind == "packed" and tf.exchange_bytes == 4 * res ** 3 and comm.kinds == ["bounds", "packed", "count"]
+    assert eng._base_final
+    assert np.array_equal(eng.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
+    assert out.stats["voxels_visited"] == ref.pyramid.visited
+    assert np.array_equal(eng.cull_flat.cpu().numpy(), ref.culling.flat)
+    x0, y0, x1, y1 = tf.tiles[rank]
+    assert np.array_equal(eng.hit_id.cpu().numpy()[y0:y1, x0:x1], ref.image.hit_id[y0:y1, x0:x1])
+    assert np.array_equal(eng.rgb.cpu().numpy()[y0:y1, x0:x1], ref.image.rgb[y0:y1, x0:x1])
+    # the same rank with the packed exchange switched off: the 8-byte path, the same frame
+    comm2 = PeerComm(rank)
+    tf2 = D.TiledFrame(eng, comm=comm2)
+    tf2.packed_exchange = False
+    tf2.run(cam, g, r_world)
+    assert tf2.exchange_kind == "wide" and comm2.kinds == ["wide", "count"] and not eng._base_final
+    assert np.array_equal(eng.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
+    assert np.array_equal(eng.hit_id.cpu().numpy()[y0:y1, x0:x1], ref.image.hit_id[y0:y1, x0:x1])
