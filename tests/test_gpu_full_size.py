@@ -121,8 +121,8 @@ def test_c4_full_size_properties(lvx):
     cam = lvx.make_camera(cfg, g)
     V = res ** 3
 
-    def frame(order_brick, wide):
-        e = lvx.FrameEngine(res, w, h, strategy="vcsv", mode="opaque")
+    def frame(order_brick, wide, builder=None):
+        e = lvx.FrameEngine(res, w, h, strategy="vcsv", mode="opaque", builder=builder)
         if order_brick is not None:
             e.order_brick = order_brick
         e.use_wide = wide
@@ -163,6 +163,15 @@ def test_c4_full_size_properties(lvx):
     assert torch.equal(e1.frags[:n], e2.frags[:n])
     assert torch.equal(e1.hit_id, e2.hit_id)
     assert torch.equal(e1.srgb, e2.srgb)
+    del e2
+    torch.cuda.empty_cache()
+    # the opt-in brick builder (csrc/bricks.cu) at this size: 262 144 bricks, 43 M (segment, brick) pairs, the same
+    # 922 M fragments in the same places and the same image
+    e3, o3 = frame(None, True, builder="bricks")
+    assert o3.stats["fragments"] == n and o3.stats["ray_capsule_tests"] == o1.stats["ray_capsule_tests"]
+    assert torch.equal(e1.frags[:n], e3.frags[:n])
+    assert torch.equal(e1.hit_id, e3.hit_id)
+    assert torch.equal(e1.srgb, e3.srgb)
 
 
 def test_largest_grid_1024(lvx):
