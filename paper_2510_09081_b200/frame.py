@@ -3,7 +3,7 @@
 
 It is what `ScenePipeline` and `bench.py` run.  All buffers are allocated once and reused;
 every stage is enqueued on the current CUDA stream with a CUDA event between stages; the only
-host synchronisation is the read-back of the 128-byte stats block (and of the image, when the
+host synchronisation is the read-back of the 192-byte stats block (and of the image, when the
 caller asks for it) at the end of the frame.  The fragment buffer is sized from the previous
 frame's total with head-room; if a frame overflows it (or trips the 16-bit count fallback) the
 affected stages are re-run -- exactness is never traded for the fast path.
