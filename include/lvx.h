@@ -124,7 +124,13 @@ int lvx_widen(const uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, u
  * sums of these maxima over the ranks bound every field of the merged grid; while both stay below 65536 the ranks
  * can all-reduce the PACKED words (lvx_pack_wide, 4 bytes per voxel: no field can carry into the other or saturate)
  * instead of the accumulators (8 bytes per voxel), and lvx_widen the sum back. */
-int lvx_wide_field_max(const uint64_t *wide, int64_t n_voxels, uint64_t *out2, void *stream);
+int lvx_wide_field_max(const uint64_t *wide, int64_t n_voxels, uint64_t *out2,
+                       uint32_t *packed /* may be NULL; n_voxels u32: also receives the packed words, same pass */,
+                       void *stream);
+/* level 1 of the pyramid (at the start of `mips`, as lvx_build_mips writes it) and the "occupancy non-zero" bits
+ * from a PACKED grid -- lvx_pack_wide_mip1 without the pack, for a grid that arrives packed (the merged grid of a
+ * packed multi-GPU exchange).  res >= 64; follow with lvx_build_mips_upper. */
+int lvx_base_mip1(const uint32_t *base, int res, uint32_t *nz_bits /* may be NULL */, double *mips, void *stream);
 /* wide -> packed with per-field saturation (lv/voxelizer.py:493-495); adds to LVX_ST_SATURATED */
 int lvx_pack_wide(const uint64_t *wide, int64_t n_voxels, uint32_t *base,
                   uint32_t *nz_bits /* may be NULL; n_voxels/32 u32: bit = occupancy field non-zero, for lvx_shade */,

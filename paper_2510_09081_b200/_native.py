@@ -50,7 +50,8 @@ SIGNATURES = {
     "lvx_voxelize": (_I, [_P, _P, _P, _L, _L, _I, _D, _D, _D, _I, _I, _P, _P, _P, _P]),
     "lvx_voxelize_wide": (_I, [_P, _P, _P, _L, _L, _I, _D, _D, _D, _I, _I, _P, _P, _P]),
     "lvx_widen": (_I, [_P, _P, _L, _P, _P]),
-    "lvx_wide_field_max": (_I, [_P, _L, _P, _P]),
+    "lvx_wide_field_max": (_I, [_P, _L, _P, _P, _P]),
+    "lvx_base_mip1": (_I, [_P, _I, _P, _P, _P]),
     "lvx_pack_wide": (_I, [_P, _L, _P, _P, _P, _P]),
     "lvx_pack_wide_mip1": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "lvx_finalize_base": (_I, [_P, _P, _L, _P, _P]),

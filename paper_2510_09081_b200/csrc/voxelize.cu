@@ -121,16 +121,27 @@ k_widen(const uint32_t *__restrict__ base, const uint32_t *__restrict__ occ_sat,
 // over the ranks bound every field of the merged grid; below 2^16 the packed 4-byte words can be summed instead
 // of the 8-byte accumulators).  Four accumulators per thread (two 128-bit loads), grid-stride.
 __global__ void __launch_bounds__(256)
-k_wide_field_max(const unsigned long long *__restrict__ wide, int64_t n, unsigned long long *__restrict__ out2) {
+k_wide_field_max(const unsigned long long *__restrict__ wide, int64_t n, unsigned long long *__restrict__ out2,
+                 uint32_t *__restrict__ packed) {
+    // `packed` (optional): the packed words (count << 16 | occ, fields clamped) are written in the same pass -- the
+    // exchange needs them exactly when the maxima allow the packed path, and one read of the accumulators serves both
     unsigned long long mc = 0, mo = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+    auto pk = [](unsigned long long w) {
+        const unsigned long long c = w >> 32, o = w & 0xFFFFFFFFull;
+        return (uint32_t)((min(c, 0xFFFFull) << 16) | min(o, 0xFFFFull));
+    };
     for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < n; i += stride) {
         if (i + 3 < n) {
             const ulonglong2 a = *reinterpret_cast<const ulonglong2 *>(wide + i), b = *reinterpret_cast<const ulonglong2 *>(wide + i + 2);
             mc = max(max(mc, a.x >> 32), max(max(a.y >> 32, b.x >> 32), b.y >> 32));
             mo = max(max(mo, a.x & 0xFFFFFFFFull), max(max(a.y & 0xFFFFFFFFull, b.x & 0xFFFFFFFFull), b.y & 0xFFFFFFFFull));
+            if (packed) *reinterpret_cast<uint4 *>(packed + i) = make_uint4(pk(a.x), pk(a.y), pk(b.x), pk(b.y));
         } else {
-            for (int64_t j = i; j < n; j++) { mc = max(mc, wide[j] >> 32); mo = max(mo, wide[j] & 0xFFFFFFFFull); }
+            for (int64_t j = i; j < n; j++) {
+                mc = max(mc, wide[j] >> 32); mo = max(mo, wide[j] & 0xFFFFFFFFull);
+                if (packed) packed[j] = pk(wide[j]);
+            }
         }
     }
 #pragma unroll
@@ -217,6 +228,28 @@ k_pack_mip1(const ulonglong2 *__restrict__ wide2, int res, uint32_t *__restrict_
 __device__ __forceinline__ double occ0(uint32_t w) {
     const uint32_t q = min(w & 0xFFFFu, 4096u);      // lv/voxelizer.py:496
     return (double)q * (1.0 / 4096.0);
+}
+
+// Level 1 of the pyramid and the "occupancy non-zero" bits from a PACKED grid (the merged grid of a packed multi-GPU
+// exchange): k_pack_mip1 without the pack.  One thread per level-1 cell, 8-byte loads of x-adjacent children.
+__global__ void __launch_bounds__(256)
+k_base_mip1(const uint32_t *__restrict__ base, int res, uint32_t *__restrict__ nz_bits, double *__restrict__ mip1) {
+    const int rl = res >> 1;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;    // rl^3 is a multiple of the block size
+    const int lane = threadIdx.x & 31;
+    const int x = (int)(i % rl), y = (int)((i / rl) % rl), z = (int)(i / ((int64_t)rl * rl));
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int64_t v = 2 * x + (int64_t)res * ((2 * y + (k & 1)) + (int64_t)res * (2 * z + (k >> 1)));
+        const uint2 w = *reinterpret_cast<const uint2 *>(base + v);
+        const uint32_t o0 = w.x & 0xFFFFu, o1 = w.y & 0xFFFFu;
+        s += min(o0, 4096u) + min(o1, 4096u);                               // lv/voxelizer.py:496
+        const uint32_t be = __ballot_sync(0xffffffffu, o0 != 0), bo = __ballot_sync(0xffffffffu, o1 != 0);
+        if (nz_bits && (lane & 15) == 0)
+            nz_bits[v >> 5] = spread16((be >> lane) & 0xFFFFu) | (spread16((bo >> lane) & 0xFFFFu) << 1);
+    }
+    mip1[i] = (double)s * (1.0 / 32768.0);   // (sum / 4096) / 8, exact
 }
 
 // level 1 from the packed base: one thread per parent, 8-byte loads of x-adjacent children
@@ -330,13 +363,22 @@ int lvx_widen(const uint32_t *base, const uint32_t *occ_sat, int64_t n_voxels, u
     return LVX_OK;
 }
 
-int lvx_wide_field_max(const uint64_t *wide, int64_t n_voxels, uint64_t *out2, void *stream) {
-    if (!wide || !out2 || n_voxels <= 0 || (reinterpret_cast<uintptr_t>(wide) & 15)) return LVX_E_ARG;
+int lvx_wide_field_max(const uint64_t *wide, int64_t n_voxels, uint64_t *out2, uint32_t *packed, void *stream) {
+    if (!wide || !out2 || n_voxels <= 0 || (reinterpret_cast<uintptr_t>(wide) & 15) || (reinterpret_cast<uintptr_t>(packed) & 15))
+        return LVX_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     LVX_CUDA(cudaMemsetAsync(out2, 0, 16, s));
     unsigned nb = blocks_for((n_voxels + 3) / 4, 256);
     if (nb > 148 * 8) nb = 148 * 8;
-    k_wide_field_max<<<nb, 256, 0, s>>>((const unsigned long long *)wide, n_voxels, (unsigned long long *)out2);
+    k_wide_field_max<<<nb, 256, 0, s>>>((const unsigned long long *)wide, n_voxels, (unsigned long long *)out2, packed);
+    LVX_LAUNCH_CHECK();
+    return LVX_OK;
+}
+
+int lvx_base_mip1(const uint32_t *base, int res, uint32_t *nz_bits, double *mips, void *stream) {
+    if (!pow2(res) || res < 64 || !base || !mips) return LVX_E_ARG;
+    const int rl = res >> 1;
+    k_base_mip1<<<blocks_for((int64_t)rl * rl * rl, 256), 256, 0, (cudaStream_t)stream>>>(base, res, nz_bits, mips);
     LVX_LAUNCH_CHECK();
     return LVX_OK;
 }

@@ -183,19 +183,20 @@ class EmulatedComm(Comm):
 FIELD_LIMIT = 1 << 16      # a 16-bit field of the packed word
 
 
-def field_bounds(wide_i64):
+def field_bounds(wide_i64, packed_out=None):
     """int64[2] = {largest count, largest occupancy sum} of a rank's accumulators `(count << 32) | occ sum`
-    (device kernel on CUDA tensors; torch ops on the CPU tensors of the gloo tests)."""
+    (device kernel on CUDA tensors; torch ops on the CPU tensors of the gloo tests).  `packed_out` (CUDA, V int32):
+    the packed words are written in the same pass over the accumulators."""
     import torch
     if wide_i64.is_cuda:
         from . import ops
         out = torch.empty(2, dtype=torch.int64, device=wide_i64.device)
-        ops.wide_field_max(wide_i64, out)
+        ops.wide_field_max(wide_i64, out, packed_out)
         return out
     return torch.stack([(wide_i64 >> 32).max(), (wide_i64 & 0xFFFFFFFF).max()])
 
 
-def exchange_accumulators(wide_i64, comm, packed_scratch=None, stats=None, widen_back=True):
+def exchange_accumulators(wide_i64, comm, packed_scratch=None, widen_back=True):
     """The exchange step of a segment-sharded voxelization.  Returns (bytes every rank contributed, "packed" | "wide").
 
     The accumulators are 8 bytes per voxel.  Every rank first contributes the two maxima of its own fields to a
@@ -210,14 +211,14 @@ def exchange_accumulators(wide_i64, comm, packed_scratch=None, stats=None, widen
     accumulators would give -- and, with `widen_back`, `wide_i64` holds the merged accumulators as well."""
     import torch
     n = wide_i64.numel()
-    bounds = field_bounds(wide_i64)
+    packed = None
+    if wide_i64.is_cuda:     # the packed words come out of the same pass as the maxima (unused if the bounds fail)
+        packed = packed_scratch if packed_scratch is not None else torch.empty(n, dtype=torch.int32, device=wide_i64.device)
+    bounds = field_bounds(wide_i64, packed)
     comm.all_reduce_sum(bounds)
     if bool((bounds < FIELD_LIMIT).all().item()):
         if wide_i64.is_cuda:
             from . import ops
-            packed = packed_scratch if packed_scratch is not None else torch.empty(n, dtype=torch.int32, device=wide_i64.device)
-            st = stats if stats is not None else ops.new_stats(wide_i64.device)
-            ops.pack_wide(wide_i64, packed, st)              # (no field reaches 2^16: nothing saturates here)
             comm.all_reduce_sum(packed)                      # int32 wraps like the u32 bit patterns it carries
             if widen_back:
                 ops.widen(packed, None, wide_i64)
@@ -309,19 +310,28 @@ class TiledFrame:
         base_final = False
         if timed:
             if self._ev is None:
-                self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                self._ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             self._ev[0].record()
+            self._ev[2].record()
         if eng.use_wide:     # the engine's 64-bit accumulators are sum-reducible as they are; it packs afterwards
             if self.packed_exchange and not getattr(self.comm, "emulated", False):
                 # packed 4-byte words when a 16-byte pre-check proves that no field can overflow (exchange_accumulators)
                 final = eng.stats.is_cuda and getattr(eng, "base", None) is not None     # a FrameEngine: its `base` receives the merged grid
                 self.exchange_bytes, self.exchange_kind = exchange_accumulators(
-                    eng.wide, self.comm, packed_scratch=eng.base if final else None,
-                    stats=eng.stats if eng.stats.is_cuda else None, widen_back=not final)
+                    eng.wide, self.comm, packed_scratch=eng.base if final else None, widen_back=not final)
                 base_final = final and self.exchange_kind == "packed"
             else:
                 self.exchange_bytes, self.exchange_kind = eng.wide.numel() * 8, "wide"
                 self.comm.all_reduce_sum(eng.wide)
+                if (self.packed_exchange and getattr(self.comm, "emulated", False) and eng.stats.is_cuda
+                        and getattr(eng, "base", None) is not None):
+                    # Emulation: the peers' shards were voxelized into `wide` above (that time is reported apart).
+                    # What THIS rank does locally on the packed path -- the field maxima, the pack pass, an engine
+                    # that takes `base` as final -- is run here as in the real job, so that the emulated per-rank
+                    # times include it.  (The bounds are taken on the merged grid: at most the real job's.)
+                    self._ev[2].record()
+                    if bool((field_bounds(eng.wide, eng.base) < FIELD_LIMIT).all().item()):
+                        self.exchange_bytes, self.exchange_kind, base_final = eng.wide.numel() * 4, "packed", True
         else:
             self.exchange_bytes = eng.base.numel() * 8
             merged, _ = merge_partial_grids(eng.base, comm=self.comm)
@@ -341,9 +351,12 @@ class TiledFrame:
                       after_voxelize=self._merge if self.world > 1 else None)
         self.exchange_ms = None
         if self.world > 1 and self._ev is not None:
-            ms = self._ev[0].elapsed_time(self._ev[1])
+            emulated = getattr(self.comm, "emulated", False)
+            # emulation: up to event 2 the peers' shards were voxelized here (not this rank's work); what follows it
+            # -- the local passes of the packed exchange -- stays in "voxelize"
+            ms = self._ev[0].elapsed_time(self._ev[2] if (emulated and self.exchange_kind == "packed") else self._ev[1])
             out.stage_ms["voxelize"] = max(0.0, out.stage_ms["voxelize"] - ms)
-            if getattr(self.comm, "emulated", False):     # the peers' shards voxelized here: not this rank's work
+            if emulated:
                 out.stage_ms["emulated_peers"] = ms
             else:
                 out.stage_ms["exchange"] = self.exchange_ms = ms

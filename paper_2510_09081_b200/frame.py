@@ -150,8 +150,8 @@ class FrameEngine:
         n += 3 if self.order_brick > 0 else 0       # processing order: histogram, scan, scatter
         n += 3 if (self.order_brick > 0 and self._sharded) else 0   # ... and the same for a rank's voxelization shard
         n += 2 if not self.use_wide else 2          # voxelize + finalize | voxelize_wide + pack_wide
-        n += 1 if self._base_final else 0           # multi-GPU packed exchange: field maxima, pack (no saturation), no fused level 1
-        n += (0 if (self.use_wide and self.res >= 64 and not self._base_final) else 1) + pyramid(2)   # mips: level 1 (fused into the pack pass at res >= 64), then the rest
+        n += 1 if (self._base_final and self.res >= 64) else 0   # multi-GPU packed exchange: field maxima + pack, then level 1 + non-empty bits from the merged grid (instead of one fused pack pass)
+        n += (0 if (self.use_wide and self.res >= 64) else 1) + pyramid(2)   # mips: level 1 (fused into the pack pass at res >= 64), then the rest
         n += (8 if self.strategy == "vcsv" else 1) + pyramid(1)   # solid, brick flags, super-brick flags, super-brick shadow, visibility, march probe, march, dilate | occupied; or-mips
         n += 1 + pyramid(1) if self._owned else 0   # tile owners + their OR pyramid
         n += 1                                      # scan
@@ -238,9 +238,16 @@ class FrameEngine:
             if after_voxelize is not None and after_voxelize(self) == "base_final":
                 # the multi-GPU exchange summed PACKED words (no field could overflow): `base` is the merged,
                 # final grid already -- no pack pass; level 1 and the non-empty bits come from `base`
-                self._nz_valid = False
-                self._mip1_done = False
                 self._base_final = True
+                if self.res >= 64:     # level 1 + the non-empty bits in one read of the merged grid
+                    if self.nz_bits is None:
+                        self.nz_bits = self.torch.empty(self.V // 32, dtype=self.torch.int32, device=self.dev)
+                    ops.base_mip1(self.base, self.res, self.nz_bits, self.mips)
+                    self._nz_valid = True
+                    self._mip1_done = True
+                else:
+                    self._nz_valid = False
+                    self._mip1_done = False
                 return
             self._base_final = False
             if self.nz_bits is None and self.res >= 32:

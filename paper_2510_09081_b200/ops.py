@@ -175,9 +175,15 @@ def widen(base, occ_sat, wide):
     check(lib().lvx_widen(_ptr(base), _ptr(occ_sat), base.numel(), _ptr(wide), _stream()), "lvx_widen")
 
 
-def wide_field_max(wide, out2):
-    """out2 (device int64[2]) = {largest count, largest occupancy sum} of the 64-bit accumulators."""
-    check(lib().lvx_wide_field_max(_ptr(wide), wide.numel(), _ptr(out2), _stream()), "lvx_wide_field_max")
+def wide_field_max(wide, out2, packed=None):
+    """out2 (device int64[2]) = {largest count, largest occupancy sum} of the 64-bit accumulators; `packed`
+    (optional, V int32) receives the packed words in the same pass."""
+    check(lib().lvx_wide_field_max(_ptr(wide), wide.numel(), _ptr(out2), _ptr(packed), _stream()), "lvx_wide_field_max")
+
+
+def base_mip1(base, res, nz_bits, mips):
+    """Level 1 of the pyramid + the non-zero bits from a packed grid (res >= 64); then build_mips_upper."""
+    check(lib().lvx_base_mip1(_ptr(base), int(res), _ptr(nz_bits), _ptr(mips), _stream()), "lvx_base_mip1")
 
 
 def pack_wide(wide, base, stats, nz_bits=None):

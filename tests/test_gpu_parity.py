@@ -524,7 +524,9 @@ def test_tiled_frame_emulated_ranks_make_the_frame(lvx, oracle, kind, mode):
         lo, hi = tf.seg_range()
         assert hi - lo in (ls.n_segments // world, ls.n_segments // world + 1)
         out = tf.run(cam, g, r_world)
-        assert tf.exchange_ms is None and tf.exchange_bytes == 8 * res ** 3
+        # thin lines: the packed exchange (4 bytes per voxel, `base` arrives final); `diag` saturates a field: 8 bytes
+        assert tf.exchange_kind == ("wide" if kind == "diag" else "packed") and e._base_final == (kind != "diag")
+        assert tf.exchange_ms is None and tf.exchange_bytes == (8 if kind == "diag" else 4) * res ** 3
         assert np.array_equal(e.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
         assert out.stats["voxels_visited"] == ref.pyramid.visited
         if ref.culling is not None:

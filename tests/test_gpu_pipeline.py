@@ -521,7 +521,7 @@ def test_packed_exchange_of_two_shards_equals_the_whole_grid(lvx, oracle):
         assert (bounds[1] >= 65536) == (want == "wide")
         mine = parts[0].clone()
         comm = Peer(parts[1])
-        nbytes, kind = D.exchange_accumulators(mine, comm, packed_scratch=torch.empty(V, dtype=torch.int32, device=dev), stats=eng.stats)
+        nbytes, kind = D.exchange_accumulators(mine, comm, packed_scratch=torch.empty(V, dtype=torch.int32, device=dev))
         assert kind == want and nbytes == (4 if want == "packed" else 8) * V and comm.reduced == ["bounds", want]
         assert torch.equal(mine, whole)
         base = torch.empty(V, dtype=torch.int32, device=dev)
