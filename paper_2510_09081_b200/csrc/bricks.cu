@@ -12,17 +12,17 @@
 //   2. k_bin_alloc    every brick reserves a range of the pair array (warp-aggregated allocator);
 //   3. k_bin<fill>    the segments write their ids into the ranges;
 //   4. k_brick_build  one WARP per brick.  It sorts the brick's segment ids (a few hundred; shared
-//                     memory) and takes them 32 at a time in ascending order, one per lane.  A lane runs
-//                     its segment's traversal RESTRICTED TO THE BRICK (the slabs of lv/voxelizer.py:180-206
-//                     are random-access, see brick_slabs) and ORs every slab -- an axis-aligned box of
-//                     cells one cell thick -- into its PRIVATE 512-bit map of the brick (16 words in
-//                     shared memory, column `lane`: no atomics, no bank conflicts).  The warp then
-//                     transposes the 32 x 32 bit matrix of every non-empty word with five shuffle stages:
-//                     lane b now holds, for voxel 32 w + b, the mask of the lanes (= segments) that visit
-//                     it, and appends them to the voxel's list bit by bit: ascending lane = ascending
-//                     segment id, so every list comes out in the reference's order (lv/abuffer.py:313-317)
-//                     by construction.  The tight index (see abuffer.cu) is written in the same sweep
-//                     from a second map.
+//                     memory) and takes them 32 at a time in ascending order, one per lane.  A lane PLANS
+//                     its segment's traversal restricted to the brick (the slabs of lv/voxelizer.py:180-206
+//                     are random-access, see SlabPlan / slab_at); the slabs of all 32 segments are pooled and
+//                     worked off 32 at a time, each -- an axis-aligned box of cells one cell thick -- ORed
+//                     into its owner's 512-bit map of the brick (16 words in shared memory, column
+//                     `owner`).  The warp then transposes the 32 x 32 bit matrix of every non-empty word
+//                     with five shuffle stages: lane b now holds, for voxel 32 w + b, the mask of the lanes
+//                     (= segments) that visit it, and appends them to the voxel's list bit by bit:
+//                     ascending lane = ascending segment id, so every list comes out in the reference's
+//                     order (lv/abuffer.py:313-317) by construction.  The tight index (see abuffer.cu) is
+//                     written in the same sweep from a second map, filled row by row (rows pooled too).
 //
 // (A first version -- one 256-thread CTA per brick, lanes setting their bit of per-voxel masks with
 // shared-memory atomicOr cell by cell, then one thread per voxel emitting -- was slower than scatter + order:
@@ -138,28 +138,35 @@ k_bin_alloc(int64_t nb, BrickScratch S) {
 // T1 = min(t_max, floor(t_min + 1)); every later one starts at an integer t0 = c (its cell index) < t_max, ends
 // at min(t_max, c + 1), and its entry point p0 is the previous slab's p1 = e + s * (t0 - t_min) -- the same
 // expression on the same operands.  So the slabs of one brick are computed directly.
-// (SlabWalk::next is the body of the reference's while loop, entered at the brick's first slab; it has ONE call
-// site, so the 32 lanes of a warp step their slabs in lockstep.)
-struct SlabWalk {
-    double t_min, t_max, e1, e2, s1, s2, r1, r2, t0;
-    int lo_j, hi_j, lo_k, hi_k, c_end, ci, a0, a1, a2;
-    bool box, done;
+// SlabPlan = what a lane knows about its segment's slabs inside the brick: the constants of the traversal, where the
+// walk enters the brick (t_start) and where its first slab there ends (T1), and how many slabs follow.  Slab q is
+// computed from these alone (slab_at), by ANY lane: the slabs of the warp's 32 segments are pooled and worked off 32
+// at a time, because a pair has anything from 1 to 8 of them and a lane-per-segment loop runs at a quarter of the
+// warp's width.
+struct SlabPlan {
+    double t_min, t_max, e1, e2, s1, s2, r1, r2, t_start, T1;
+    int lo_j, hi_j, lo_k, hi_k;     // minor ranges, grid coordinates, already clamped to the brick
+    int c0;                         // box traversal: first slab
+    int code;                       // a0 | a1 << 2 | a2 << 4 | box << 6
+    int n_slab;
 
     __device__ __forceinline__ void init(const d3 &a, const d3 &b, double r, int res, int bx0, int by0, int bz0) {
         const d3 d{b.x - a.x, b.y - a.y, b.z - a.z};
-        box = d.x == 0.0 && d.y == 0.0 && d.z == 0.0;
-        done = false;
+        const bool box = d.x == 0.0 && d.y == 0.0 && d.z == 0.0;
+        t_min = t_max = e1 = e2 = s1 = s2 = r1 = r2 = t_start = T1 = 0.0;
+        c0 = 0; n_slab = 0;
         if (box) {      // lv/voxelizer.py:116-140 (zero-length segment): slabs along z, rows along x, fixed ranges
-            a0 = 2; a1 = 1; a2 = 0;
+            code = 2 | (1 << 2) | (0 << 4) | (1 << 6);
             lo_k = max((int)floor(fmin(a.x, b.x) - r), bx0); hi_k = min((int)floor(fmax(a.x, b.x) + r), min(res, bx0 + BR) - 1);
             lo_j = max((int)floor(fmin(a.y, b.y) - r), by0); hi_j = min((int)floor(fmax(a.y, b.y) + r), min(res, by0 + BR) - 1);
-            ci = max((int)floor(fmin(a.z, b.z) - r), bz0);
-            c_end = min((int)floor(fmax(a.z, b.z) + r), min(res, bz0 + BR) - 1) + 1;
-            if (hi_k < lo_k || hi_j < lo_j) done = true;
-            t_min = t_max = e1 = e2 = s1 = s2 = r1 = r2 = t0 = 0.0;
+            c0 = max((int)floor(fmin(a.z, b.z) - r), bz0);
+            const int c_end = min((int)floor(fmax(a.z, b.z) + r), min(res, bz0 + BR) - 1) + 1;
+            if (hi_k >= lo_k && hi_j >= lo_j) n_slab = max(c_end - c0, 0);
             return;
         }
+        int a0, a1, a2;
         rank3(fabs(d.x), fabs(d.y), fabs(d.z), a0, a1, a2);
+        code = a0 | (a1 << 2) | (a2 << 4);
         double d0 = sel(d, a0), d1 = sel(d, a1), d2 = sel(d, a2);
         double v0_0 = sel(a, a0), v0_1 = sel(a, a1), v0_2 = sel(a, a2);
         double v1_0 = sel(b, a0), v1_1 = sel(b, a1), v1_2 = sel(b, a2);
@@ -181,51 +188,52 @@ struct SlabWalk {
         const int B2 = a2 == 0 ? bx0 : (a2 == 1 ? by0 : bz0);
         lo_j = max((int)floor(fmin(v0_1, v1_1) - r), B1); hi_j = min((int)floor(fmax(v0_1, v1_1) + r), min(res, B1 + BR) - 1);
         lo_k = max((int)floor(fmin(v0_2, v1_2) - r), B2); hi_k = min((int)floor(fmax(v0_2, v1_2) + r), min(res, B2 + BR) - 1);
-        c_end = min(res, B0 + BR);                                                 // slabs B0 .. c_end - 1
-        ci = 0;
-        if (hi_j < lo_j || hi_k < lo_k) { done = true; return; }
+        const int c_end = min(res, B0 + BR);                                       // slabs B0 .. c_end - 1
+        if (hi_j < lo_j || hi_k < lo_k) return;
         // enter the walk at the brick: at t_min if the first slab is not below the brick, else at the first integer
-        // t0 >= B0 the walk reaches (T1, T1 + 1, ...: every slab after the first starts at an integer)
-        t0 = t_min;
+        // t0 >= B0 the walk reaches (every slab after the first starts at an integer)
+        t_start = t_min;
         if (floor(t_min) < (double)B0) {
-            const double T1 = fmin(t_max, floor(t_min + 1.0));
-            t0 = T1 < t_max ? fmax(T1, (double)B0) : t_max;
+            const double T1r = fmin(t_max, floor(t_min + 1.0));
+            t_start = T1r < t_max ? fmax(T1r, (double)B0) : t_max;
         }
-    }
-    // the next slab inside the brick: cells [lo, hi] per axis (grid coordinates); false = no more
-    __device__ __forceinline__ bool next(int lo[3], int hi[3]) {
-        for (;;) {
-            if (done) return false;
-            int j_min, j_max, k_min, k_max, c;
-            if (box) {
-                if (ci >= c_end) { done = true; return false; }
-                c = ci++;
-                j_min = lo_j; j_max = hi_j; k_min = lo_k; k_max = hi_k;
-            } else {
-                if (!(t0 < t_max)) { done = true; return false; }
-                const double c_f = floor(t0);
-                if (!(c_f < (double)c_end)) { done = true; return false; }
-                c = (int)c_f;
-                const double t1 = fmin(t_max, floor(t0 + 1.0));
-                const double dt0 = t0 - t_min, dt = t1 - t_min;
-                const double p0_1 = e1 + s1 * dt0, p0_2 = e2 + s2 * dt0;       // (= e1, e2 at t0 = t_min)
-                const double p1_1 = e1 + s1 * dt, p1_2 = e2 + s2 * dt;
-                j_min = max((int)floor(fmin(p0_1, p1_1) - r1), lo_j);
-                j_max = min((int)floor(fmax(p0_1, p1_1) + r1), hi_j);
-                k_min = max((int)floor(fmin(p0_2, p1_2) - r2), lo_k);
-                k_max = min((int)floor(fmax(p0_2, p1_2) + r2), hi_k);
-                t0 = t1;
-            }
-            if (k_max < k_min || j_max < j_min) continue;
-#pragma unroll
-            for (int ax = 0; ax < 3; ax++) {
-                lo[ax] = ax == a0 ? c : (ax == a1 ? j_min : k_min);
-                hi[ax] = ax == a0 ? c : (ax == a1 ? j_max : k_max);
-            }
-            return true;
-        }
+        if (!(t_start < t_max) || !(floor(t_start) < (double)c_end)) return;
+        T1 = fmin(t_max, floor(t_start + 1.0));                                    // end of the first slab in the brick
+        n_slab = 1;
+        if (T1 < t_max) n_slab += max(min((int)ceil(t_max), c_end) - (int)T1, 0);  // then one per integer T1, T1 + 1, ... < t_max
     }
 };
+
+// Slab q of a plan (its fields passed one by one: they come out of shuffles): cells [lo, hi] per axis, grid
+// coordinates; false = the slab holds no cell of the brick.  The body of the reference's while loop.
+__device__ __forceinline__ bool slab_at(int q, double t_min, double t_max, double e1, double e2, double s1, double s2,
+                                        double r1, double r2, double t_start, double T1, int lo_j, int hi_j, int lo_k,
+                                        int hi_k, int c0, int code, int lo[3], int hi[3]) {
+    int j_min, j_max, k_min, k_max, c;
+    if (code >> 6) {
+        c = c0 + q;
+        j_min = lo_j; j_max = hi_j; k_min = lo_k; k_max = hi_k;
+    } else {
+        const double t0 = q == 0 ? t_start : T1 + (double)(q - 1);
+        c = (int)floor(t0);
+        const double t1 = fmin(t_max, floor(t0 + 1.0));
+        const double dt0 = t0 - t_min, dt = t1 - t_min;
+        const double p0_1 = e1 + s1 * dt0, p0_2 = e2 + s2 * dt0;       // (= e1, e2 at t0 = t_min)
+        const double p1_1 = e1 + s1 * dt, p1_2 = e2 + s2 * dt;
+        j_min = max((int)floor(fmin(p0_1, p1_1) - r1), lo_j);
+        j_max = min((int)floor(fmax(p0_1, p1_1) + r1), hi_j);
+        k_min = max((int)floor(fmin(p0_2, p1_2) - r2), lo_k);
+        k_max = min((int)floor(fmax(p0_2, p1_2) + r2), hi_k);
+    }
+    if (k_max < k_min || j_max < j_min) return false;
+    const int a0 = code & 3, a1 = (code >> 2) & 3;
+#pragma unroll
+    for (int ax = 0; ax < 3; ax++) {
+        lo[ax] = ax == a0 ? c : (ax == a1 ? j_min : k_min);
+        hi[ax] = ax == a0 ? c : (ax == a1 ? j_max : k_max);
+    }
+    return true;
+}
 
 // Cells u in [u_lo, u_hi] of the row (cx, cy, cz) + u * e_axis (cell centres, in the segment's f32 frame) whose
 // cube grown by h - 0.5 in the maximum norm is met by the segment; u_lo > u_hi = none.
@@ -343,22 +351,33 @@ k_brick_build(const double *__restrict__ verts, double rt, float r_tight, int re
     // ---- the voxels of this lane (bit `lane` of every word): list bounds
     const int vx = bx0 + (lane & 7), vy_lo = by0 + (lane >> 3);
     bool any = false;
-#pragma unroll 4
-    for (int w = 0; w < BM_WORDS; w++) {
-        const int y = vy_lo + 4 * (w & 1), z = bz0 + (w >> 1);
-        uint32_t b = 0, nv = 0;
-        if (vx < res && y < res && z < res) {
-            const uint32_t idx = (uint32_t)vx + (uint32_t)res * ((uint32_t)y + (uint32_t)res * (uint32_t)z);
-            b = offsets[idx];
-            const uint32_t e = offsets[idx + 1];
-            nv = e - b;
-            if ((int64_t)e > cap) {                   // never touch memory past the buffer: the frame is redone with a
-                nv = 0;                               // larger one, but the tracer of THIS frame still runs
-                if (T.cnt) T.cnt[idx] = 0;
+    {
+        // all 32 loads of the lane in flight together (the walk up the brick is a chain of dependent phases run by
+        // ~20 warps per SM: 7 % of its stall samples sat on these loads when they went out four at a time)
+        uint32_t bb[BM_WORDS], ee[BM_WORDS];
+#pragma unroll
+        for (int w = 0; w < BM_WORDS; w++) {
+            const int y = vy_lo + 4 * (w & 1), z = bz0 + (w >> 1);
+            bb[w] = 0; ee[w] = 0;
+            if (vx < res && y < res && z < res) {
+                const uint32_t idx = (uint32_t)vx + (uint32_t)res * ((uint32_t)y + (uint32_t)res * (uint32_t)z);
+                bb[w] = offsets[idx];
+                ee[w] = offsets[idx + 1];
             }
         }
-        s_base[w][lane] = b; s_nv[w][lane] = (uint16_t)nv; s_k[w][lane] = 0; s_tk[w][lane] = 0;
-        any |= nv != 0;
+#pragma unroll
+        for (int w = 0; w < BM_WORDS; w++) {
+            uint32_t nv = ee[w] - bb[w];
+            if ((int64_t)ee[w] > cap) {               // never touch memory past the buffer: the frame is redone with a
+                nv = 0;                               // larger one, but the tracer of THIS frame still runs
+                if (T.cnt) {
+                    const int y = vy_lo + 4 * (w & 1), z = bz0 + (w >> 1);
+                    T.cnt[(uint32_t)vx + (uint32_t)res * ((uint32_t)y + (uint32_t)res * (uint32_t)z)] = 0;
+                }
+            }
+            s_base[w][lane] = bb[w]; s_nv[w][lane] = (uint16_t)nv; s_k[w][lane] = 0; s_tk[w][lane] = 0;
+            any |= nv != 0;
+        }
     }
     if (!__any_sync(0xffffffffu, any)) return;       // nothing in this brick owns a fragment (culled / other tile)
 
@@ -395,34 +414,77 @@ k_brick_build(const double *__restrict__ verts, double rt, float r_tight, int re
         const uint32_t me = c0 + lane;
         const uint32_t id = me < n ? ids[me] : 0xffffffffu;
         s_ids[lane] = id;
-        // ---- one segment per lane: its slabs inside the brick -> the lane's bit map of all cells; the slabs are
-        // kept (20 bits each) for the tight test
+        if (me + 32 < n) {                            // the next chunk's end points: asked for a whole chunk ahead
+            const uint32_t nid = ids[me + 32];
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(verts + 3 * (int64_t)nid));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(verts + 3 * (int64_t)nid + 5));
+        }
+        // ---- the slabs of the 32 segments, pooled: every lane plans its own segment, then the warp works the slabs
+        // off 32 at a time whoever's they are.  A slab is ORed into its OWNER's bit map of all cells and kept
+        // (20 bits) for the tight test.
         SegBox sb;
         uint32_t n_rows = 0;
         {
             d3 a{0, 0, 0}, b{0, 0, 0};
             if (me < n) { a = ld3(verts + 3 * (int64_t)id); b = ld3(verts + 3 * (int64_t)id + 3); }
             sb = make_segbox(a, b, bx0, by0, bz0);
-            SlabWalk walk;
-            walk.init(a, b, rt, res, bx0, by0, bz0);
-            if (me >= n) walk.done = true;
-            int lo[3], hi[3], ns = 0;
-            while (walk.next(lo, hi)) {
-                const int x0 = lo[0] - bx0, x1 = hi[0] - bx0, y0 = lo[1] - by0, y1 = hi[1] - by0, z0 = lo[2] - bz0, z1 = hi[2] - bz0;
-                uint32_t w_lo, w_hi;
-                layer_bits(x0, x1, y0, y1, w_lo, w_hi);
-                for (int z = z0; z <= z1; z++) {
-                    if (w_lo) s_bm[0][2 * z][lane] |= w_lo;
-                    if (w_hi) s_bm[0][2 * z + 1][lane] |= w_hi;
+            SlabPlan P;
+            P.init(a, b, rt, res, bx0, by0, bz0);
+            if (me >= n) P.n_slab = 0;
+            uint32_t incl_s = (uint32_t)P.n_slab;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl_s, o);
+                if (lane >= o) incl_s += v;
+            }
+            const uint32_t total_s = __shfl_sync(0xffffffffu, incl_s, 31);
+            for (uint32_t g0 = 0; g0 < total_s; g0 += 32) {
+                const uint32_t g = g0 + lane;
+                int o = 0;                                        // owner = number of lanes whose slabs end at or before g
+#pragma unroll
+                for (int step = 16; step; step >>= 1) {
+                    const uint32_t v = __shfl_sync(0xffffffffu, incl_s, o + step - 1);
+                    if (v <= g) o += step;
                 }
-                // rows of the slab = the reference's innermost loops, along a2: one per cell of the two other axes
-                const int axis = walk.a2;
-                const int ex = axis == 0 ? 1 : x1 - x0 + 1, ey = axis == 1 ? 1 : y1 - y0 + 1, ez = axis == 2 ? 1 : z1 - z0 + 1;
-                n_rows += ex * ey * ez;
-                s_slab[ns][lane] = (uint32_t)x0 | (uint32_t)x1 << 3 | (uint32_t)y0 << 6 | (uint32_t)y1 << 9 | (uint32_t)z0 << 12 |
-                                   (uint32_t)z1 << 15 | (uint32_t)axis << 18;
-                s_cum[ns][lane] = (uint8_t)n_rows;
-                ns++;
+                const bool valid = g < total_s;
+                o = min(o, 31);
+                const uint32_t o_incl = __shfl_sync(0xffffffffu, incl_s, o);
+                const int o_n = __shfl_sync(0xffffffffu, P.n_slab, o);
+                const double t_min = __shfl_sync(0xffffffffu, P.t_min, o), t_max = __shfl_sync(0xffffffffu, P.t_max, o);
+                const double e1 = __shfl_sync(0xffffffffu, P.e1, o), e2 = __shfl_sync(0xffffffffu, P.e2, o);
+                const double s1 = __shfl_sync(0xffffffffu, P.s1, o), s2 = __shfl_sync(0xffffffffu, P.s2, o);
+                const double r1 = __shfl_sync(0xffffffffu, P.r1, o), r2 = __shfl_sync(0xffffffffu, P.r2, o);
+                const double t_start = __shfl_sync(0xffffffffu, P.t_start, o), T1 = __shfl_sync(0xffffffffu, P.T1, o);
+                const int lo_j = __shfl_sync(0xffffffffu, P.lo_j, o), hi_j = __shfl_sync(0xffffffffu, P.hi_j, o);
+                const int lo_k = __shfl_sync(0xffffffffu, P.lo_k, o), hi_k = __shfl_sync(0xffffffffu, P.hi_k, o);
+                const int c0 = __shfl_sync(0xffffffffu, P.c0, o), code = __shfl_sync(0xffffffffu, P.code, o);
+                if (valid) {
+                    const int q = (int)(g - (o_incl - (uint32_t)o_n));
+                    int lo[3], hi[3];
+                    uint32_t desc = 0, rows = 0;
+                    if (slab_at(q, t_min, t_max, e1, e2, s1, s2, r1, r2, t_start, T1, lo_j, hi_j, lo_k, hi_k, c0, code, lo, hi)) {
+                        const int x0 = lo[0] - bx0, x1 = hi[0] - bx0, y0 = lo[1] - by0, y1 = hi[1] - by0, z0 = lo[2] - bz0, z1 = hi[2] - bz0;
+                        uint32_t w_lo, w_hi;
+                        layer_bits(x0, x1, y0, y1, w_lo, w_hi);
+                        for (int z = z0; z <= z1; z++) {
+                            if (w_lo) atomicOr(&s_bm[0][2 * z][o], w_lo);
+                            if (w_hi) atomicOr(&s_bm[0][2 * z + 1][o], w_hi);
+                        }
+                        // rows of the slab = the reference's innermost loops, along a2: one per cell of the two other axes
+                        const int axis = (code >> 4) & 3;
+                        const int ex = axis == 0 ? 1 : x1 - x0 + 1, ey = axis == 1 ? 1 : y1 - y0 + 1, ez = axis == 2 ? 1 : z1 - z0 + 1;
+                        rows = (uint32_t)(ex * ey * ez);
+                        desc = (uint32_t)x0 | (uint32_t)x1 << 3 | (uint32_t)y0 << 6 | (uint32_t)y1 << 9 | (uint32_t)z0 << 12 |
+                               (uint32_t)z1 << 15 | (uint32_t)axis << 18;
+                    }
+                    s_slab[q][o] = desc;
+                    s_cum[q][o] = (uint8_t)rows;
+                }
+            }
+            __syncwarp();
+            for (int q = 0; q < P.n_slab; q++) {                  // running row counts of this lane's slabs
+                n_rows += s_cum[q][lane];
+                s_cum[q][lane] = (uint8_t)n_rows;
             }
         }
         __syncwarp();

@@ -137,7 +137,7 @@ def test_pair_scratch_grows(lvx, oracle):
 @pytest.mark.parametrize("r", [0.3, 1.7])
 def test_zero_length_and_boundary_segments(lvx, oracle, r):
     """Zero-length segments (box traversal, lv/voxelizer.py:155-156) and segments at the grid boundary through
-    SlabWalk's box mode."""
+    the box mode of SlabPlan / slab_at."""
     rng = np.random.default_rng(17)
     polys, off = [], [0]
     for _ in range(40):
