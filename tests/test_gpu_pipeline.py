@@ -596,3 +596,35 @@ def test_tiled_frame_with_packed_exchange_on_the_engine(lvx, oracle, rank):
     assert tf2.exchange_kind == "wide" and comm2.kinds == ["wide", "count"] and not eng._base_final
     assert np.array_equal(eng.base.cpu().numpy().view(np.uint32).reshape(res, res, res), ref.pyramid.base)
     assert np.array_equal(eng.hit_id.cpu().numpy()[y0:y1, x0:x1], ref.image.hit_id[y0:y1, x0:x1])
+
+
+def test_base_mip1_equals_the_fused_pack_pass(lvx):
+    """lvx_base_mip1 (level 1 of the pyramid + non-empty bits from a PACKED grid, used after a packed multi-GPU
+    exchange) against lvx_pack_wide_mip1 on the same accumulators; lvx_wide_field_max's packed words against
+    lvx_pack_wide's."""
+    import torch
+    from paper_2510_09081_b200 import ops
+    res = 64
+    V = res ** 3
+    dev = torch.device("cuda")
+    g = torch.Generator(device="cpu").manual_seed(5)
+    cnt = torch.randint(0, 70000, (V,), generator=g)          # some counts and sums beyond the 16-bit fields
+    occ = torch.randint(0, 90000, (V,), generator=g) * (torch.rand(V, generator=g) < 0.3)
+    wide = ((cnt << 32) | occ).to(dev)
+    n_mip = int(ops.level_offsets(res)[-1]) - V
+    base_a = torch.empty(V, dtype=torch.int32, device=dev); nz_a = torch.zeros(V // 32, dtype=torch.int32, device=dev)
+    mips_a = torch.zeros(n_mip, dtype=torch.float64, device=dev)
+    ops.pack_wide_mip1(wide, res, base_a, ops.new_stats(dev), nz_a, mips_a)
+    out2 = torch.empty(2, dtype=torch.int64, device=dev)
+    base_b = torch.empty(V, dtype=torch.int32, device=dev)
+    ops.wide_field_max(wide, out2, base_b)
+    assert out2.tolist() == [int(cnt.max()), int(occ.max())]
+    assert torch.equal(base_a, base_b)
+    base_c = torch.empty(V, dtype=torch.int32, device=dev)
+    ops.pack_wide(wide, base_c, ops.new_stats(dev))
+    assert torch.equal(base_a, base_c)
+    nz_b = torch.zeros(V // 32, dtype=torch.int32, device=dev); mips_b = torch.zeros(n_mip, dtype=torch.float64, device=dev)
+    ops.base_mip1(base_b, res, nz_b, mips_b)
+    n1 = (res // 2) ** 3
+    assert torch.equal(nz_a, nz_b)
+    assert torch.equal(mips_a[:n1], mips_b[:n1])
